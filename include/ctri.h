@@ -1,0 +1,194 @@
+/*
+ * ctri.h -- C ABI of the B200-native batched cyclic tridiagonal solver.
+ *
+ * The library solves A x = b for every batch column of a 3D right-layout
+ * grid (third index contiguous, "right memory layout is used,
+ * where the third index maps to contiguous memory"), A the cyclic (or
+ * acyclic) tridiagonal matrix with constant bands (l, d, u) =
+ * (A[i,i-1], A[i,i], A[i,i+1]); cyclic corners A[0,N-1] = l, A[N-1,0] = u.
+ * The benchmark matrix is B[1/3, 1, 1/3] (P:5).
+ *
+ * The solve direction is sharded over `nparts` ranks (one GPU each), rank i
+ * owning global rows [i*n, (i+1)*n), n = N/nparts (P:5 "the domain is
+ * decomposed equally along the solving direction").  Local row 0 of every
+ * slab is the interface unknown x~_i, rows 1..n-1 the interior x_i
+ * (Eqs. system1/system2; reading R1).  Per solve the
+ * library runs the paper's method (Sec. "Parallel linear solver"):
+ *   (a1) y_i = D_i^{-1} b_i on every column (Eq. yi; per-partition PCR),
+ *   (a2) b^_i = b~_i - L~_i y_{i-1} - U~_i y_i (Eq. bi_hat), one exchange i -> i+1,
+ *   (a3) cyclic PCR on the reduced system A^ x~ = b^ in log2(nparts) pairwise
+ *        stages with partners i +- 2^k,
+ *   (a4) x_i = y_i - S_i x~_i - R_i x~_{i+1} (Eq. xi_app), one exchange i+1 -> i.
+ * Everything that does not depend on b (S_i, R_i, L^, D^, U^, the per-stage
+ * reduction coefficients) is pre-factorised at plan creation.
+ *
+ * Conventions for every entry point:
+ *  - Return a ctri_status; no exception crosses the ABI.  On failure a
+ *    thread-local detail string is available from ctri_last_error().
+ *  - Device pointers are CUDA device addresses on the current device, fp64,
+ *    16-byte aligned, holding the LOCAL slab in right layout with local dims
+ *    = global dims except dims[solve_dim] = N/nparts.  The caller owns them.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Solves are
+ *    asynchronous and stream ordered; with nparts > 1 they are collective:
+ *    every rank calls with the same plan parameters in the same order.
+ */
+#ifndef CTRI_H
+#define CTRI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CTRI_ABI_VERSION 1
+
+typedef struct ctri_plan_s* ctri_plan;
+typedef struct CUstream_st* ctri_stream; /* == cudaStream_t */
+
+typedef enum ctri_status {
+  CTRI_OK = 0,
+  CTRI_ERR_INVALID_ARG = 1,     /* bad pointer, dims, solve_dim, rank, alignment */
+  CTRI_ERR_UNSUPPORTED = 2,     /* e.g. cyclic with non-power-of-two nparts (detach/reattach not built) */
+  CTRI_ERR_SINGULAR = 3,        /* plan-time pivot guard: |pivot| < 1e-13 * max|band| */
+  CTRI_ERR_PARTITION_TOO_SMALL = 4, /* n = N/nparts < 3 or N not divisible by nparts */
+  CTRI_ERR_CUDA = 5,            /* a CUDA runtime call or kernel launch failed */
+  CTRI_ERR_NCCL = 6,            /* an NCCL call failed */
+  CTRI_ERR_OOM = 7              /* device or pinned-host allocation failed */
+} ctri_status;
+
+/* Plan flags (bitwise OR). */
+#define CTRI_FLAG_FULL_BACKSUB   (1u << 0) /* (a4) on every interior row instead of the window W (R15) */
+#define CTRI_FLAG_GENERIC_LOCAL  (1u << 1) /* force the column-serial local-solve kernel (testing) */
+#define CTRI_FLAG_TIMING         (1u << 2) /* record per-phase CUDA events; read with ctri_get_stats */
+#define CTRI_FLAG_DERIV          (1u << 3) /* allocate halo planes so ctri_deriv may be called */
+
+#define CTRI_MAX_STAGES 16
+
+typedef struct ctri_stats {
+  int64_t global_dims[3];
+  int32_t solve_dim, nparts, rank, cyclic;
+  int64_t n_local;              /* rows of the local slab along solve_dim */
+  int64_t m_batch;              /* batch columns = product of the two other dims */
+  int32_t local_kernel;         /* 0 = column-serial, 1 = cluster-tile (strided axis), 2 = cluster-tile (contiguous axis) */
+  int32_t rows_per_thread;      /* K of the tile kernel (0 for column-serial) */
+  int32_t cluster_size;         /* CTAs cooperating on one column tile */
+  int32_t tile_columns;         /* batch columns per tile */
+  int32_t chunk_heads;          /* Q: on-chip reduced-system rows per column */
+  int32_t window_rows;          /* W: rows per slab end touched by (a4); n-1 means all rows */
+  int32_t pcr_stages;           /* q = log2(nparts) distributed PCR stages */
+  int32_t comm_rounds;          /* dependent exchange rounds per solve: 2 + q (nparts > 1) */
+  int32_t sends_per_solve;      /* messages sent by this rank per solve: 2q + 1 */
+  int64_t bytes_sent_per_solve; /* 8 m * sends */
+  int32_t launches_per_solve;   /* kernels this library launches per ctri_solve */
+  uint64_t solves;              /* ctri_solve calls on this plan */
+  /* Per-phase device times of the LAST solve in microseconds (CTRI_FLAG_TIMING; else -1).
+     ctri_get_stats synchronises the plan's events. */
+  float t_total_us, t_local_us, t_yexchange_us, t_bhat_us;
+  float t_stage_us[CTRI_MAX_STAGES]; /* exchange + update of PCR stage k */
+  float t_xexchange_us, t_backsub_us;
+} ctri_stats;
+
+/* Human-readable status name; never NULL. */
+const char* ctri_status_string(ctri_status s);
+
+/* Detail of the last failure on the calling thread ("" if none). */
+const char* ctri_last_error(void);
+
+/* ABI version (CTRI_ABI_VERSION) -- lets the binding check it loaded the right library. */
+int ctri_abi_version(void);
+
+/* Fill `out` (128 bytes) with a fresh NCCL unique id.  Rank 0 calls this and
+ * broadcasts the bytes (the Python binding uses torch.distributed) before
+ * every rank calls ctri_plan_create. */
+ctri_status ctri_get_unique_id(void* out128);
+
+/* Create a plan (pre-factorisation) for this rank.
+ *   global_dims  [3] global grid dims, right layout.
+ *   solve_dim    0, 1 or 2: index along which every column is solved.
+ *   nparts       partitions of the solve direction == ranks; rank in [0, nparts).
+ *   bands        {l, d, u}; constant along the solve direction.
+ *   cyclic       1 periodic (the paper's benchmark), 0 acyclic.
+ *   nccl_unique_id  128-byte ncclUniqueId shared by all ranks; NULL iff nparts == 1.
+ *   flags        CTRI_FLAG_*.
+ *   stream       stream used for the table uploads during create.
+ * Errors: INVALID_ARG, PARTITION_TOO_SMALL, UNSUPPORTED (cyclic with non-power-of-two
+ * nparts), SINGULAR (pivot guard), CUDA, NCCL, OOM.  On error *out is NULL.
+ * The plan owns its device tables, plane buffers, events and NCCL communicator. */
+ctri_status ctri_plan_create(ctri_plan* out, const int64_t global_dims[3], int solve_dim,
+                             int nparts, int rank, const double bands[3], int cyclic,
+                             const void* nccl_unique_id, uint32_t flags, ctri_stream stream);
+
+/* TEST-ONLY in-process "loopback" group: create `nparts` plans on the current
+ * device (ranks 0..nparts-1) whose exchanges are device-to-device copies
+ * instead of NCCL messages.  Solve them together with ctri_solve_loopback.
+ * `plans` receives nparts handles; destroy each with ctri_plan_destroy. */
+ctri_status ctri_plan_create_loopback(ctri_plan* plans, int nparts, const int64_t global_dims[3],
+                                      int solve_dim, const double bands[3], int cyclic,
+                                      uint32_t flags, ctri_stream stream);
+
+/* Solve on device buffers: x = A^{-1} b for the local slab.  x == b (in place) is
+ * allowed; partial overlap is not.  Asynchronous, stream ordered, collective.
+ * Errors: INVALID_ARG (NULL/misaligned), CUDA, NCCL. */
+ctri_status ctri_solve(ctri_plan plan, const double* b, double* x, ctri_stream stream);
+
+/* Solve a loopback group: b[r], x[r] are rank r's slabs (device pointers). */
+ctri_status ctri_solve_loopback(const ctri_plan* plans, int nparts, const double* const* b,
+                                double* const* x, ctri_stream stream);
+
+/* End-to-end solve from HOST memory: copies b_host to the device, solves and copies
+ * the result back into x_host, all on `stream` (pinned host memory gives
+ * asynchronous DMA; pageable memory works but blocks).  The plan allocates its
+ * device staging slab on first use.  Returns after enqueuing; synchronise the
+ * stream before reading x_host. */
+ctri_status ctri_solve_host(ctri_plan plan, const double* b_host, double* x_host,
+                            ctri_stream stream);
+
+/* Compact first derivative along solve_dim:
+ *   rhs_j = a (f_{j+1}-f_{j-1})/(2h) + bc (f_{j+2}-f_{j-2})/(4h)  (periodic, halo from
+ *   ranks i-1 / i+1), then df = A^{-1} rhs with this plan's bands.
+ * Requires a cyclic plan created with CTRI_FLAG_DERIV and n >= 2.  f and df must not
+ * overlap.  Asynchronous, stream ordered, collective. */
+ctri_status ctri_deriv(ctri_plan plan, const double* f, double* df, double a, double bc,
+                       double h, ctri_stream stream);
+
+/* TEST-ONLY: ctri_deriv for a loopback group (f[r], df[r] are rank r's slabs). */
+ctri_status ctri_deriv_loopback(const ctri_plan* plans, int nparts, const double* const* f,
+                                double* const* df, double a, double bc, double h,
+                                ctri_stream stream);
+
+/* Copy the plan's configuration, counters and (with CTRI_FLAG_TIMING) last-solve
+ * phase times into *out.  Synchronises the plan's timing events. */
+ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out);
+
+/* Release everything the plan owns (including its NCCL communicator).  NULL is a no-op. */
+ctri_status ctri_plan_destroy(ctri_plan plan);
+
+/* ---- Host-only pre-factorisation queries (no device needed; used by the CPU tests) ---- */
+
+/* Partition tables of one slab of n rows:
+ *   S, R       [n-1] each: D S = l e_0, D R = u e_{n-2} (Eqs. Si, Ri), D the acyclic
+ *              (n-1)x(n-1) interior block; NULL to skip.
+ *   hat        [3]: {L^, D^, U^} of Eqs. Li_hat, Di_hat, Ui_hat; NULL to skip.
+ *   window     rows per slab end that (a4) touches (R15); NULL to skip.
+ * Errors: INVALID_ARG, PARTITION_TOO_SMALL, SINGULAR. */
+ctri_status ctri_factor_query(int64_t n, const double bands[3], double* S, double* R,
+                              double* hat, int* window);
+
+/* Reduction coefficients of PCR on a P-row (block size 1) tridiagonal system with
+ * row coefficients L[c] (on row c-1), D[c], U[c] (on row c+1); cyclic wraps indices,
+ * acyclic ignores L[0] and U[P-1].  Stage k (stride s = 2^k), row c:
+ *     b[c] <- b[c] - alpha[k*P+c] * b[c-s] - gamma[k*P+c] * b[c+s]
+ * and after the last stage x[c] = inv[c] * b[c] (the cyclic wrap folded into the
+ * diagonal, R3).  *stages = log2 P (cyclic; P must be a power of two) or
+ * ceil(log2 P) (acyclic).  alpha/gamma hold stages*P entries (CTRI_MAX_STAGES*P suffices).
+ * Errors: INVALID_ARG, UNSUPPORTED (cyclic non-power-of-two), SINGULAR. */
+ctri_status ctri_pcr_coefficients(int P, int cyclic, const double* L, const double* D,
+                                  const double* U, double* alpha, double* gamma, double* inv,
+                                  int* stages);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CTRI_H */

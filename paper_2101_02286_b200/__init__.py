@@ -1,0 +1,15 @@
+"""B200-native batched cyclic tridiagonal solver (arXiv 2101.02286 hot path).
+
+The product is the C-ABI library ``libctri.so`` (``include/ctri.h``); this
+package is its thin binding.  ``ctri.load()`` raises if the library is not
+built -- there is no CPU fallback.
+"""
+from .ctri import (CTRI_FLAG_DERIV, CTRI_FLAG_FULL_BACKSUB, CTRI_FLAG_GENERIC_LOCAL,  # noqa: F401
+                   CTRI_FLAG_TIMING, CtriError, LoopbackGroup, Plan, ctri_deriv,
+                   ctri_deriv_loopback, ctri_factor_query, ctri_get_stats, ctri_get_unique_id,
+                   ctri_pcr_coefficients, ctri_plan_create, ctri_plan_create_loopback,
+                   ctri_plan_destroy, ctri_solve, ctri_solve_host, ctri_solve_loopback, load,
+                   local_shape)
+
+__all__ = [n for n in dir() if n.startswith(("ctri_", "CTRI_")) or n in
+           ("Plan", "LoopbackGroup", "CtriError", "load", "local_shape")]

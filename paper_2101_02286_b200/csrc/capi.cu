@@ -1,0 +1,591 @@
+// capi.cu -- implementation of include/ctri.h: plan creation (pre-factorisation),
+// the per-solve phase sequence (a1)-(a4) with NCCL (or test-only loopback) exchanges,
+// the compact-derivative entry point and the statistics / host-query functions.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace ctri;
+
+namespace {
+thread_local std::string g_err;
+
+ctri_status fail(ctri_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(e_ == cudaErrorMemoryAllocation ? CTRI_ERR_OOM : CTRI_ERR_CUDA,         \
+                  std::string(#expr) + ": " + cudaGetErrorString(e_));                    \
+  } while (0)
+
+#define NCCL_TRY(expr)                                                                    \
+  do {                                                                                    \
+    ncclResult_t r_ = (expr);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      return fail(CTRI_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_));     \
+  } while (0)
+
+#define TRY(expr)                      \
+  do {                                 \
+    ctri_status s_ = (expr);           \
+    if (s_ != CTRI_OK) return s_;      \
+  } while (0)
+
+// timing event slots
+enum { EV_START = 0, EV_LOCAL, EV_YX, EV_BHAT, EV_STAGE0, EV_XX = EV_STAGE0 + CTRI_MAX_STAGES,
+       EV_BACK, EV_COUNT };
+
+ctri_status upload(double** dst, const std::vector<double>& src, cudaStream_t s) {
+  CUDA_TRY(cudaMalloc(dst, std::max<size_t>(1, src.size()) * sizeof(double)));
+  if (!src.empty())
+    CUDA_TRY(cudaMemcpyAsync(*dst, src.data(), src.size() * sizeof(double),
+                             cudaMemcpyHostToDevice, s));
+  return CTRI_OK;
+}
+
+ctri_status alloc_plane(double** p, int64_t count) {
+  CUDA_TRY(cudaMalloc(p, std::max<int64_t>(1, count) * sizeof(double)));
+  CUDA_TRY(cudaMemset(*p, 0, std::max<int64_t>(1, count) * sizeof(double)));
+  return CTRI_OK;
+}
+
+void free_plan(Plan* P) {
+  if (!P) return;
+  double* bufs[] = {P->d_cp,    P->d_inv_den, P->d_S,      P->d_R,       P->yf,      P->yl,
+                    P->bt,      P->yl_prev,   P->bh,       P->recv_m,    P->recv_p,  P->xt,
+                    P->xt_next, P->halo_lo,   P->halo_hi,  P->send_lo,   P->send_hi, P->tile.d_pcr,
+                    P->d_stage_b, P->d_stage_x};
+  for (double* b : bufs)
+    if (b) cudaFree(b);
+  for (cudaEvent_t e : P->ev) cudaEventDestroy(e);
+  if (P->comm) ncclCommDestroy(P->comm);
+  delete P;
+}
+
+bool has_left(const Plan& P) { return P.cyclic || P.rank > 0; }
+bool has_right(const Plan& P) { return P.cyclic || P.rank < P.p - 1; }
+int wrap(const Plan& P, int r) { return ((r % P.p) + P.p) % P.p; }
+
+// Common plan set-up (no communicator).
+ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, const double bands[3],
+                      int cyclic, uint32_t flags, cudaStream_t s) {
+  if (!gd || !bands) return fail(CTRI_ERR_INVALID_ARG, "NULL dims or bands");
+  if (sd < 0 || sd > 2) return fail(CTRI_ERR_INVALID_ARG, "solve_dim must be 0, 1 or 2");
+  for (int k = 0; k < 3; ++k)
+    if (gd[k] < 1) return fail(CTRI_ERR_INVALID_ARG, "global dims must be >= 1");
+  if (p < 1 || rank < 0 || rank >= p) return fail(CTRI_ERR_INVALID_ARG, "bad nparts/rank");
+  for (int k = 0; k < 3; ++k)
+    if (!std::isfinite(bands[k])) return fail(CTRI_ERR_INVALID_ARG, "bands must be finite");
+  if (gd[sd] % p != 0)
+    return fail(CTRI_ERR_PARTITION_TOO_SMALL, "N is not divisible by nparts (equal split, P:5)");
+  const int64_t n = gd[sd] / p;
+  if (n < 3) return fail(CTRI_ERR_PARTITION_TOO_SMALL, "n = N/nparts < 3 (N_i = n-1 >= 2r)");
+  if (cyclic && !is_pow2(p))
+    return fail(CTRI_ERR_UNSUPPORTED,
+                "cyclic solve with non-power-of-two nparts needs detach/reattach (P:271), not built");
+  std::memcpy(P->gdims, gd, sizeof(P->gdims));
+  P->sd = sd;
+  P->p = p;
+  P->rank = rank;
+  P->cyclic = cyclic ? 1 : 0;
+  P->flags = flags;
+  P->bands = Bands{bands[0], bands[1], bands[2]};
+  P->lay.n = n;
+  P->lay.outer = 1;
+  P->lay.inner = 1;
+  for (int k = 0; k < sd; ++k) P->lay.outer *= gd[k];
+  for (int k = sd + 1; k < 3; ++k) P->lay.inner *= gd[k];
+  CUDA_TRY(cudaGetDevice(&P->device));
+  CUDA_TRY(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device));
+
+  // ---- pre-factorisation ----
+  FactorError fe;
+  if (!partition_factor(n - 1, P->bands, &P->part, &fe)) return fail((ctri_status)fe.code, fe.detail);
+  const Partition& pt = P->part;
+  const int64_t last = n - 2;
+  std::vector<double> L(p), D(p), U(p);
+  for (int i = 0; i < p; ++i) {
+    const bool lft = cyclic || i > 0, rgt = cyclic || i < p - 1;
+    L[i] = lft ? -P->bands.l * pt.S[last] : 0.0;                                 // Eq. Li_hat
+    D[i] = P->bands.d - (lft ? P->bands.l * pt.R[last] : 0.0) - P->bands.u * pt.S[0];  // Eq. Di_hat
+    U[i] = rgt ? -P->bands.u * pt.R[0] : 0.0;                                    // Eq. Ui_hat
+  }
+  if (!pcr_factor(p, cyclic != 0, L, D, U, pivot_threshold(P->bands), &P->gpcr, &fe))
+    return fail((ctri_status)fe.code, fe.detail);
+  if (P->gpcr.stages > CTRI_MAX_STAGES) return fail(CTRI_ERR_UNSUPPORTED, "too many PCR stages");
+  P->inv_closure = P->gpcr.inv[0];
+  P->window = backsub_window(pt);
+
+  // ---- device tables ----
+  TRY(upload(&P->d_S, pt.S, s));
+  TRY(upload(&P->d_R, pt.R, s));
+  const int64_t m = P->lay.m();
+  std::string why;
+  if (tile_configure(*P, &why)) {
+    P->local_kernel = 1;
+    std::vector<double> t;
+    t.insert(t.end(), P->tile.pcr.alpha.begin(), P->tile.pcr.alpha.end());
+    t.insert(t.end(), P->tile.pcr.gamma.begin(), P->tile.pcr.gamma.end());
+    t.insert(t.end(), P->tile.pcr.inv.begin(), P->tile.pcr.inv.end());
+    TRY(upload(&P->tile.d_pcr, t, s));
+  } else {
+    P->local_kernel = 0;
+    TRY(upload(&P->d_cp, pt.th.cp, s));
+    TRY(upload(&P->d_inv_den, pt.th.inv_den, s));
+  }
+  if (p > 1) {
+    double** planes[] = {&P->yf, &P->yl, &P->bt, &P->yl_prev, &P->bh, &P->recv_m, &P->recv_p,
+                         &P->xt, &P->xt_next};
+    for (double** pl : planes) TRY(alloc_plane(pl, m));
+  }
+  if (flags & CTRI_FLAG_DERIV) {
+    if (!cyclic) return fail(CTRI_ERR_INVALID_ARG, "CTRI_FLAG_DERIV needs a cyclic plan");
+    TRY(alloc_plane(&P->halo_lo, 2 * m));
+    TRY(alloc_plane(&P->halo_hi, 2 * m));
+    TRY(alloc_plane(&P->send_lo, 2 * m));
+    TRY(alloc_plane(&P->send_hi, 2 * m));
+  }
+  if (flags & CTRI_FLAG_TIMING) {
+    P->ev.resize(EV_COUNT);
+    for (auto& e : P->ev) CUDA_TRY(cudaEventCreate(&e));
+  }
+  // launches per solve
+  int launches = 1;
+  if (p > 1) launches += 1 /*bhat*/ + P->gpcr.stages + 1 /*backsub*/;
+  P->launches_per_solve = launches;
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return CTRI_OK;
+}
+
+// ---------------- exchanges ----------------
+struct Xfer {
+  int send_to;        // -1: none
+  const double* sbuf;
+  int recv_from;      // -1: none
+  double* rbuf;
+  int64_t count;
+};
+
+// NCCL: one group per round (all of this rank's sends and receives of the round).
+ctri_status exchange_nccl(Plan& P, const std::vector<Xfer>& xs, cudaStream_t s) {
+  NCCL_TRY(ncclGroupStart());
+  for (const Xfer& x : xs) {
+    if (x.send_to >= 0) NCCL_TRY(ncclSend(x.sbuf, (size_t)x.count, ncclDouble, x.send_to, P.comm, s));
+    if (x.recv_from >= 0)
+      NCCL_TRY(ncclRecv(x.rbuf, (size_t)x.count, ncclDouble, x.recv_from, P.comm, s));
+  }
+  NCCL_TRY(ncclGroupEnd());
+  return CTRI_OK;
+}
+
+// Per-rank transfer lists of each round (shared by NCCL and loopback).
+std::vector<Xfer> round_y(Plan& P) {  // y_{i-1}[last]: i -> i+1
+  Xfer x{has_right(P) ? wrap(P, P.rank + 1) : -1, P.yl, has_left(P) ? wrap(P, P.rank - 1) : -1,
+         P.yl_prev, P.lay.m()};
+  return {x};
+}
+std::vector<Xfer> round_stage(Plan& P, int k) {  // b^ with partners i -+ 2^k
+  const int s = 1 << k;
+  const int64_t m = P.lay.m();
+  int lm = P.rank - s, lp = P.rank + s;
+  if (P.cyclic) {
+    lm = wrap(P, lm);
+    lp = wrap(P, lp);
+  } else {
+    if (lm < 0) lm = -1;
+    if (lp >= P.p) lp = -1;
+  }
+  if (lm >= 0 && lm == lp) return {Xfer{lp, P.bh, lm, P.recv_m, m}};  // s = p/2: single partner
+  std::vector<Xfer> v;
+  // order: send to i+s / recv from i-s, then send to i-s / recv from i+s
+  v.push_back(Xfer{lp, P.bh, lm, P.recv_m, m});
+  v.push_back(Xfer{lm, P.bh, lp, P.recv_p, m});
+  return v;
+}
+std::vector<Xfer> round_x(Plan& P) {  // x~_{i+1}: i+1 -> i
+  Xfer x{has_left(P) ? wrap(P, P.rank - 1) : -1, P.xt, has_right(P) ? wrap(P, P.rank + 1) : -1,
+         P.xt_next, P.lay.m()};
+  return {x};
+}
+std::vector<Xfer> round_halo(Plan& P) {
+  const int64_t m2 = 2 * P.lay.m();
+  return {Xfer{wrap(P, P.rank - 1), P.send_lo, wrap(P, P.rank + 1), P.halo_hi, m2},
+          Xfer{wrap(P, P.rank + 1), P.send_hi, wrap(P, P.rank - 1), P.halo_lo, m2}};
+}
+
+// Loopback: for each rank r and each of its receives, copy from the sender's buffer.  The
+// sender's buffer is identified by matching the sender's own transfer list.
+template <typename RoundFn>
+ctri_status exchange_loopback(std::vector<Plan*>& G, RoundFn fn, cudaStream_t s) {
+  const int p = (int)G.size();
+  std::vector<std::vector<Xfer>> lists(p);
+  for (int r = 0; r < p; ++r) lists[r] = fn(*G[r]);
+  for (int r = 0; r < p; ++r) {
+    // receives of rank r are matched in order with sends of the peer addressed to r
+    std::vector<int> used(p, 0);
+    for (const Xfer& x : lists[r]) {
+      if (x.recv_from < 0) continue;
+      const int q = x.recv_from;
+      int seen = 0;
+      const double* src = nullptr;
+      for (const Xfer& y : lists[q]) {
+        if (y.send_to == r) {
+          if (seen == used[q]) { src = y.sbuf; break; }
+          ++seen;
+        }
+      }
+      if (!src) return fail(CTRI_ERR_INVALID_ARG, "loopback: unmatched receive");
+      ++used[q];
+      CUDA_TRY(cudaMemcpyAsync(x.rbuf, src, x.count * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  return CTRI_OK;
+}
+
+void record(Plan& P, int slot, cudaStream_t s) {
+  if (!P.ev.empty()) cudaEventRecord(P.ev[slot], s);
+}
+
+ctri_status local_phase(Plan& P, const double* b, double* x, cudaStream_t s) {
+  cudaError_t e = (P.local_kernel == 1) ? launch_tile(P, b, x, s) : launch_local_generic(P, b, x, s);
+  if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("local solve launch: ") + cudaGetErrorString(e));
+  return CTRI_OK;
+}
+
+ctri_status stage_kernel(Plan& P, int k, cudaStream_t s) {
+  const bool last = (k == P.gpcr.stages - 1);
+  // single-partner stage: both couplings read recv_m
+  double* saved = P.recv_p;
+  std::vector<Xfer> r = round_stage(P, k);
+  if (r.size() == 1) P.recv_p = P.recv_m;
+  cudaError_t e = launch_pcr_stage(P, k, last, s);
+  P.recv_p = saved;
+  if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("pcr stage: ") + cudaGetErrorString(e));
+  return CTRI_OK;
+}
+
+// The whole solve for a set of co-scheduled plans: one plan (NCCL) or a loopback group.
+ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* const* x,
+                        cudaStream_t s) {
+  const bool nccl = !G[0]->loopback;
+  Plan& P0 = *G[0];
+  for (size_t r = 0; r < G.size(); ++r) {
+    if (!b[r] || !x[r]) return fail(CTRI_ERR_INVALID_ARG, "NULL b or x");
+    if (((uintptr_t)b[r] | (uintptr_t)x[r]) & 15)
+      return fail(CTRI_ERR_INVALID_ARG, "b and x must be 16-byte aligned");
+  }
+  for (Plan* P : G) P->solves++;
+  record(P0, EV_START, s);
+  for (size_t r = 0; r < G.size(); ++r) TRY(local_phase(*G[r], b[r], x[r], s));
+  record(P0, EV_LOCAL, s);
+  if (P0.p == 1) return CTRI_OK;
+  // (a2) neighbour exchange of y_{i-1}[last] and b^ assembly
+  if (nccl) TRY(exchange_nccl(P0, round_y(P0), s));
+  else TRY(exchange_loopback(G, [](Plan& P) { return round_y(P); }, s));
+  record(P0, EV_YX, s);
+  for (Plan* P : G) {
+    cudaError_t e = launch_bhat(*P, s);
+    if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, cudaGetErrorString(e));
+  }
+  record(P0, EV_BHAT, s);
+  // (a3) distributed PCR stages
+  for (int k = 0; k < P0.gpcr.stages; ++k) {
+    if (nccl) TRY(exchange_nccl(P0, round_stage(P0, k), s));
+    else TRY(exchange_loopback(G, [k](Plan& P) { return round_stage(P, k); }, s));
+    for (Plan* P : G) TRY(stage_kernel(*P, k, s));
+    record(P0, EV_STAGE0 + k, s);
+  }
+  // (a4) x~_{i+1} exchange and back-substitution
+  if (nccl) TRY(exchange_nccl(P0, round_x(P0), s));
+  else TRY(exchange_loopback(G, [](Plan& P) { return round_x(P); }, s));
+  record(P0, EV_XX, s);
+  for (size_t r = 0; r < G.size(); ++r) {
+    cudaError_t e = launch_backsub(*G[r], x[r], s);
+    if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, cudaGetErrorString(e));
+  }
+  record(P0, EV_BACK, s);
+  for (Plan* P : G) P->timed_valid = !P->ev.empty();
+  return CTRI_OK;
+}
+
+ctri_status deriv_group(std::vector<Plan*>& G, const double* const* f, double* const* df,
+                        double a, double bc, double h, cudaStream_t s) {
+  for (size_t r = 0; r < G.size(); ++r) {
+    Plan& P = *G[r];
+    if (!(P.flags & CTRI_FLAG_DERIV)) return fail(CTRI_ERR_INVALID_ARG, "plan lacks CTRI_FLAG_DERIV");
+    if (!f[r] || !df[r] || f[r] == df[r]) return fail(CTRI_ERR_INVALID_ARG, "f/df NULL or aliased");
+    if (h == 0.0 || !std::isfinite(h)) return fail(CTRI_ERR_INVALID_ARG, "bad h");
+  }
+  if (G[0]->p > 1) {
+    for (size_t r = 0; r < G.size(); ++r) {
+      cudaError_t e = launch_pack_halo(*G[r], f[r], s);
+      if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, cudaGetErrorString(e));
+    }
+    if (!G[0]->loopback) TRY(exchange_nccl(*G[0], round_halo(*G[0]), s));
+    else TRY(exchange_loopback(G, [](Plan& P) { return round_halo(P); }, s));
+  }
+  for (size_t r = 0; r < G.size(); ++r) {
+    cudaError_t e = launch_stencil(*G[r], f[r], df[r], a, bc, h, s);
+    if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, cudaGetErrorString(e));
+  }
+  return solve_group(G, df, df, s);
+}
+
+float elapsed(const Plan& P, int a, int b) {
+  float ms = -1.f;
+  if (cudaEventElapsedTime(&ms, P.ev[a], P.ev[b]) != cudaSuccess) {
+    cudaGetLastError();
+    return -1.f;
+  }
+  return ms * 1000.f;
+}
+}  // namespace
+
+// ====================================== ABI =============================================
+extern "C" {
+
+const char* ctri_status_string(ctri_status s) {
+  switch (s) {
+    case CTRI_OK: return "CTRI_OK";
+    case CTRI_ERR_INVALID_ARG: return "CTRI_ERR_INVALID_ARG";
+    case CTRI_ERR_UNSUPPORTED: return "CTRI_ERR_UNSUPPORTED";
+    case CTRI_ERR_SINGULAR: return "CTRI_ERR_SINGULAR";
+    case CTRI_ERR_PARTITION_TOO_SMALL: return "CTRI_ERR_PARTITION_TOO_SMALL";
+    case CTRI_ERR_CUDA: return "CTRI_ERR_CUDA";
+    case CTRI_ERR_NCCL: return "CTRI_ERR_NCCL";
+    case CTRI_ERR_OOM: return "CTRI_ERR_OOM";
+  }
+  return "CTRI_ERR_UNKNOWN";
+}
+
+const char* ctri_last_error(void) { return g_err.c_str(); }
+
+int ctri_abi_version(void) { return CTRI_ABI_VERSION; }
+
+ctri_status ctri_get_unique_id(void* out128) {
+  if (!out128) return fail(CTRI_ERR_INVALID_ARG, "NULL out");
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  std::memcpy(out128, &id, sizeof(id));
+  return CTRI_OK;
+}
+
+ctri_status ctri_plan_create(ctri_plan* out, const int64_t global_dims[3], int solve_dim,
+                             int nparts, int rank, const double bands[3], int cyclic,
+                             const void* nccl_unique_id, uint32_t flags, ctri_stream stream) {
+  if (!out) return fail(CTRI_ERR_INVALID_ARG, "NULL out");
+  *out = nullptr;
+  if (nparts > 1 && !nccl_unique_id)
+    return fail(CTRI_ERR_INVALID_ARG, "nparts > 1 needs an NCCL unique id");
+  std::unique_ptr<Plan, void (*)(Plan*)> P(new Plan(), free_plan);
+  ctri_status st = plan_init(P.get(), global_dims, solve_dim, nparts, rank, bands, cyclic, flags,
+                             (cudaStream_t)stream);
+  if (st != CTRI_OK) return st;
+  if (nparts > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    NCCL_TRY(ncclCommInitRank(&P->comm, nparts, id, rank));
+  }
+  *out = reinterpret_cast<ctri_plan>(P.release());
+  return CTRI_OK;
+}
+
+ctri_status ctri_plan_create_loopback(ctri_plan* plans, int nparts, const int64_t global_dims[3],
+                                      int solve_dim, const double bands[3], int cyclic,
+                                      uint32_t flags, ctri_stream stream) {
+  if (!plans || nparts < 1) return fail(CTRI_ERR_INVALID_ARG, "bad plans/nparts");
+  std::vector<Plan*> made;
+  for (int r = 0; r < nparts; ++r) {
+    Plan* P = new Plan();
+    P->loopback = true;
+    ctri_status st = plan_init(P, global_dims, solve_dim, nparts, r, bands, cyclic, flags,
+                               (cudaStream_t)stream);
+    if (st != CTRI_OK) {
+      free_plan(P);
+      for (Plan* q : made) free_plan(q);
+      return st;
+    }
+    made.push_back(P);
+  }
+  for (int r = 0; r < nparts; ++r) {
+    made[r]->group = made;
+    plans[r] = reinterpret_cast<ctri_plan>(made[r]);
+  }
+  return CTRI_OK;
+}
+
+ctri_status ctri_solve(ctri_plan plan, const double* b, double* x, ctri_stream stream) {
+  if (!plan) return fail(CTRI_ERR_INVALID_ARG, "NULL plan");
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  if (P->loopback && P->p > 1) return fail(CTRI_ERR_INVALID_ARG, "loopback plan: use ctri_solve_loopback");
+  std::vector<Plan*> G{P};
+  return solve_group(G, &b, &x, (cudaStream_t)stream);
+}
+
+ctri_status ctri_solve_loopback(const ctri_plan* plans, int nparts, const double* const* b,
+                                double* const* x, ctri_stream stream) {
+  if (!plans || !b || !x || nparts < 1) return fail(CTRI_ERR_INVALID_ARG, "NULL arguments");
+  std::vector<Plan*> G(nparts);
+  for (int r = 0; r < nparts; ++r) {
+    G[r] = reinterpret_cast<Plan*>(plans[r]);
+    if (!G[r] || G[r]->rank != r || G[r]->p != nparts || !G[r]->loopback)
+      return fail(CTRI_ERR_INVALID_ARG, "plans must be one loopback group in rank order");
+  }
+  return solve_group(G, b, x, (cudaStream_t)stream);
+}
+
+ctri_status ctri_solve_host(ctri_plan plan, const double* b_host, double* x_host,
+                            ctri_stream stream) {
+  if (!plan || !b_host || !x_host) return fail(CTRI_ERR_INVALID_ARG, "NULL argument");
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  const size_t bytes = (size_t)P->lay.elems() * sizeof(double);
+  if (!P->d_stage_b) {
+    CUDA_TRY(cudaMalloc(&P->d_stage_b, bytes));
+    CUDA_TRY(cudaMalloc(&P->d_stage_x, bytes));
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemcpyAsync(P->d_stage_b, b_host, bytes, cudaMemcpyHostToDevice, s));
+  TRY(ctri_solve(plan, P->d_stage_b, P->d_stage_x, stream));
+  CUDA_TRY(cudaMemcpyAsync(x_host, P->d_stage_x, bytes, cudaMemcpyDeviceToHost, s));
+  return CTRI_OK;
+}
+
+ctri_status ctri_deriv(ctri_plan plan, const double* f, double* df, double a, double bc, double h,
+                       ctri_stream stream) {
+  if (!plan) return fail(CTRI_ERR_INVALID_ARG, "NULL plan");
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  std::vector<Plan*> G{P};
+  if (P->loopback && P->p > 1) return fail(CTRI_ERR_INVALID_ARG, "loopback plan: use ctri_deriv_loopback");
+  return deriv_group(G, &f, &df, a, bc, h, (cudaStream_t)stream);
+}
+
+ctri_status ctri_deriv_loopback(const ctri_plan* plans, int nparts, const double* const* f,
+                                double* const* df, double a, double bc, double h,
+                                ctri_stream stream) {
+  if (!plans || !f || !df || nparts < 1) return fail(CTRI_ERR_INVALID_ARG, "NULL arguments");
+  std::vector<Plan*> G(nparts);
+  for (int r = 0; r < nparts; ++r) {
+    G[r] = reinterpret_cast<Plan*>(plans[r]);
+    if (!G[r] || G[r]->rank != r || G[r]->p != nparts || !G[r]->loopback)
+      return fail(CTRI_ERR_INVALID_ARG, "plans must be one loopback group in rank order");
+  }
+  return deriv_group(G, f, df, a, bc, h, (cudaStream_t)stream);
+}
+
+ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
+  if (!plan || !out) return fail(CTRI_ERR_INVALID_ARG, "NULL argument");
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  std::memset(out, 0, sizeof(*out));
+  std::memcpy(out->global_dims, P->gdims, sizeof(P->gdims));
+  out->solve_dim = P->sd;
+  out->nparts = P->p;
+  out->rank = P->rank;
+  out->cyclic = P->cyclic;
+  out->n_local = P->lay.n;
+  out->m_batch = P->lay.m();
+  out->local_kernel = P->local_kernel;
+  out->rows_per_thread = P->local_kernel ? P->tile.K : 0;
+  out->cluster_size = P->local_kernel ? P->tile.G : 1;
+  out->tile_columns = P->local_kernel ? kTileCols : 1;
+  out->chunk_heads = P->local_kernel ? P->tile.Q : 1;
+  const bool full = (P->flags & CTRI_FLAG_FULL_BACKSUB) || (2 * P->window >= P->lay.n - 1);
+  out->window_rows = (int32_t)(full ? P->lay.n - 1 : P->window);
+  out->pcr_stages = P->gpcr.stages;
+  if (P->p > 1) {
+    out->comm_rounds = 2 + P->gpcr.stages;
+    int sends = (has_right(*P) ? 1 : 0) + (has_left(*P) ? 1 : 0);
+    for (int k = 0; k < P->gpcr.stages; ++k)
+      for (const Xfer& x : round_stage(*P, k)) sends += (x.send_to >= 0);
+    out->sends_per_solve = sends;
+    out->bytes_sent_per_solve = (int64_t)sends * 8 * P->lay.m();
+  }
+  out->launches_per_solve = P->launches_per_solve;
+  out->solves = P->solves;
+  float* ts[] = {&out->t_total_us, &out->t_local_us, &out->t_yexchange_us, &out->t_bhat_us,
+                 &out->t_xexchange_us, &out->t_backsub_us};
+  for (float* t : ts) *t = -1.f;
+  for (int k = 0; k < CTRI_MAX_STAGES; ++k) out->t_stage_us[k] = -1.f;
+  if (P->timed_valid || (!P->ev.empty() && P->solves > 0)) {
+    CUDA_TRY(cudaEventSynchronize(P->ev[P->p > 1 ? EV_BACK : EV_LOCAL]));
+    out->t_local_us = elapsed(*P, EV_START, EV_LOCAL);
+    if (P->p > 1) {
+      out->t_yexchange_us = elapsed(*P, EV_LOCAL, EV_YX);
+      out->t_bhat_us = elapsed(*P, EV_YX, EV_BHAT);
+      int prev = EV_BHAT;
+      for (int k = 0; k < P->gpcr.stages; ++k) {
+        out->t_stage_us[k] = elapsed(*P, prev, EV_STAGE0 + k);
+        prev = EV_STAGE0 + k;
+      }
+      out->t_xexchange_us = elapsed(*P, prev, EV_XX);
+      out->t_backsub_us = elapsed(*P, EV_XX, EV_BACK);
+      out->t_total_us = elapsed(*P, EV_START, EV_BACK);
+    } else {
+      out->t_total_us = out->t_local_us;
+    }
+  }
+  return CTRI_OK;
+}
+
+ctri_status ctri_plan_destroy(ctri_plan plan) {
+  if (!plan) return CTRI_OK;
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  // detach from a loopback group
+  for (Plan* q : P->group)
+    if (q != P)
+      for (auto& g : q->group)
+        if (g == P) g = nullptr;
+  free_plan(P);
+  return CTRI_OK;
+}
+
+ctri_status ctri_factor_query(int64_t n, const double bands[3], double* S, double* R, double* hat,
+                              int* window) {
+  if (!bands) return fail(CTRI_ERR_INVALID_ARG, "NULL bands");
+  if (n < 3) return fail(CTRI_ERR_PARTITION_TOO_SMALL, "n < 3");
+  Partition pt;
+  FactorError fe;
+  if (!partition_factor(n - 1, Bands{bands[0], bands[1], bands[2]}, &pt, &fe))
+    return fail((ctri_status)fe.code, fe.detail);
+  if (S) std::memcpy(S, pt.S.data(), sizeof(double) * (n - 1));
+  if (R) std::memcpy(R, pt.R.data(), sizeof(double) * (n - 1));
+  if (hat) {
+    hat[0] = pt.Lh;
+    hat[1] = pt.Dh;
+    hat[2] = pt.Uh;
+  }
+  if (window) *window = (int)backsub_window(pt);
+  return CTRI_OK;
+}
+
+ctri_status ctri_pcr_coefficients(int P, int cyclic, const double* L, const double* D,
+                                  const double* U, double* alpha, double* gamma, double* inv,
+                                  int* stages) {
+  if (P < 1 || !L || !D || !U || !inv || !stages) return fail(CTRI_ERR_INVALID_ARG, "bad arguments");
+  PcrTables t;
+  FactorError fe;
+  double mx = 0;
+  for (int c = 0; c < P; ++c) mx = std::max(mx, std::max(std::fabs(D[c]), std::max(std::fabs(L[c]), std::fabs(U[c]))));
+  if (!pcr_factor(P, cyclic != 0, std::vector<double>(L, L + P), std::vector<double>(D, D + P),
+                  std::vector<double>(U, U + P), 1e-13 * mx, &t, &fe))
+    return fail((ctri_status)fe.code, fe.detail);
+  *stages = t.stages;
+  if (alpha) std::memcpy(alpha, t.alpha.data(), sizeof(double) * t.alpha.size());
+  if (gamma) std::memcpy(gamma, t.gamma.data(), sizeof(double) * t.gamma.size());
+  std::memcpy(inv, t.inv.data(), sizeof(double) * P);
+  return CTRI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,67 @@
+// factor.h -- host fp64 pre-factorisation ("the construction of
+// L^, D^, U^ and D_i does not require the right-hand-side ... the original
+// matrix can be pre-factorized").  Pure host code, no CUDA.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace ctri {
+
+struct Bands {
+  double l, d, u;  // A[i,i-1], A[i,i], A[i,i+1]
+};
+
+// Outcome of a factorisation step: 0 ok, else a ctri_status value.
+struct FactorError {
+  int code = 0;
+  std::string detail;
+};
+
+// Pivot guard: |pivot| < 1e-13 * max|band| trips CTRI_ERR_SINGULAR.
+double pivot_threshold(const Bands& b);
+
+// Thomas factors of the acyclic N x N block with constant bands:
+//   den[0] = d, den[k] = d - l*cp[k-1], cp[k] = u/den[k].
+// Forward:  g_k = (r_k - l g_{k-1}) * inv_den[k];  backward: y_k = g_k - cp[k] y_{k+1}.
+struct Thomas {
+  std::vector<double> cp, inv_den;
+};
+bool thomas_factor(int64_t N, const Bands& b, Thomas* out, FactorError* err);
+// Solve in place with the factors (host, one column).
+void thomas_solve(const Thomas& t, const Bands& b, std::vector<double>& r);
+
+// Partition tables of a block of N interior rows (Eqs. Si, Ri):
+//   S = D^{-1}(l e_0), R = D^{-1}(u e_{N-1});
+// reduced-row coefficients (Eqs. Li_hat, Di_hat, Ui_hat) for uniform partitions:
+//   L^ = -l S[N-1], D^ = d - l R[N-1] - u S[0], U^ = -u R[0].
+struct Partition {
+  Thomas th;
+  std::vector<double> S, R;
+  double Lh = 0, Dh = 0, Uh = 0;
+};
+bool partition_factor(int64_t N, const Bands& b, Partition* out, FactorError* err);
+
+// Rows per slab end where |S[k]| or |R[k]| exceeds 2^-64 (reading R15);
+// returns N if the two windows would overlap (then every row is touched).
+int64_t backsub_window(const Partition& p);
+
+// PCR reduction coefficients on a P-row tridiagonal system with per-row
+// (L, D, U), cyclic (P a power of two, last stage folds the wrapped couplings
+// into the diagonal) or acyclic.  alpha/gamma are stage-major [stages][P].
+struct PcrTables {
+  int P = 0, stages = 0;
+  bool cyclic = true;
+  std::vector<double> alpha, gamma, inv;
+};
+bool pcr_factor(int P, bool cyclic, const std::vector<double>& L, const std::vector<double>& D,
+                const std::vector<double>& U, double guard, PcrTables* out, FactorError* err);
+
+inline bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+inline int ilog2(int64_t v) {
+  int q = 0;
+  while ((int64_t(1) << q) < v) ++q;
+  return q;
+}
+
+}  // namespace ctri

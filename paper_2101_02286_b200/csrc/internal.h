@@ -1,0 +1,127 @@
+// internal.h -- plan object and kernel launcher declarations (not part of the ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/ctri.h"
+#include "factor.h"
+
+namespace ctri {
+
+// Fixed tile geometry of the cluster-tile local solve (kernels.cu).
+constexpr int kTileCols = 16;     // batch columns per tile: one 128-byte line per row
+constexpr int kTileThreads = 512; // threads per CTA; one (column, chunk) per thread
+constexpr int kTileChunksPerCta = kTileThreads / kTileCols;  // 32
+constexpr int kMaxCluster = 8;
+
+// Layout of a local slab viewed as (outer, n, inner): element (o, r, c) at (o*n + r)*inner + c.
+struct Layout {
+  int64_t outer = 1, n = 0, inner = 1;
+  int64_t m() const { return outer * inner; }
+  int64_t elems() const { return outer * n * inner; }
+};
+
+// Parameters of the cluster-tile kernel that live in the kernel's constant bank.
+template <int K>
+struct TileConsts {
+  double l, u;
+  double inv_den[K > 1 ? K - 1 : 1];  // Thomas on the (K-1)-row chunk interior
+  double cp[K > 1 ? K - 1 : 1];
+  double S[K > 1 ? K - 1 : 1];        // chunk-level S_K = D_K^{-1} l e_0
+  double R[K > 1 ? K - 1 : 1];        // chunk-level R_K = D_K^{-1} u e_last
+};
+
+struct TileArgs {
+  const double* b;
+  double* x;
+  Layout lay;
+  int64_t tiles_per_outer, num_tiles;
+  int Q;            // chunk heads per column (n / K)
+  int G;            // cluster size
+  int rows_per_cta; // n / G
+  int stages;       // log2 Q
+  int mode;         // 0: complete cyclic solve (p = 1); 1: y_D = D_i^{-1} b_i + planes (p >= 2);
+                    // 2: complete acyclic solve (p = 1)
+  const double* pcr_alpha;  // [stages][Q]
+  const double* pcr_gamma;  // [stages][Q]
+  const double* pcr_inv;    // [Q]
+  double* plane_yf;  // mode 1: y_D at interior row 1
+  double* plane_yl;  // mode 1: y_D at row n-1
+  double* plane_bt;  // mode 1: b at row 0 (b~_i)
+};
+
+struct TileConfig {
+  bool ok = false;
+  int K = 0, G = 0, Q = 0;
+  int smem_bytes = 0;
+  int grid = 0;  // CTAs launched (multiple of G)
+  std::vector<double> consts;  // serialized TileConsts<K> (l, u, then 4 tables of K-1)
+  PcrTables pcr;
+  double* d_pcr = nullptr;     // device: alpha | gamma | inv
+};
+
+struct Plan {
+  // configuration
+  int64_t gdims[3] = {0, 0, 0};
+  int sd = 0, p = 1, rank = 0, cyclic = 1;
+  uint32_t flags = 0;
+  Bands bands{};
+  Layout lay;           // local slab
+  int device = 0;
+  int num_sms = 0;
+  bool loopback = false;
+
+  // host tables
+  Partition part;       // GPU-level S_i, R_i, L^, D^, U^ (p >= 2); (n-1)-row interior
+  PcrTables gpcr;       // GPU-level PCR over the p reduced rows
+  int64_t window = 0;   // rows per end for (a4)
+  double inv_closure = 0;  // p = 1 generic path: 1/(L^ + D^ + U^)
+
+  // device tables
+  double* d_cp = nullptr;       // generic local solve Thomas factors (n-1)
+  double* d_inv_den = nullptr;
+  double* d_S = nullptr;        // GPU-level S_i, R_i (n-1)
+  double* d_R = nullptr;
+
+  // planes (m doubles each)
+  double *yf = nullptr, *yl = nullptr, *bt = nullptr, *yl_prev = nullptr, *bh = nullptr,
+         *recv_m = nullptr, *recv_p = nullptr, *xt = nullptr, *xt_next = nullptr;
+  // derivative halos: [2][m] each
+  double *halo_lo = nullptr, *halo_hi = nullptr, *send_lo = nullptr, *send_hi = nullptr;
+
+  // local-solve kernel selection
+  int local_kernel = 0;  // 0 generic, 1 tile (strided axis)
+  TileConfig tile;
+
+  // e2e staging
+  double* d_stage_b = nullptr;
+  double* d_stage_x = nullptr;
+
+  // comm
+  ncclComm_t comm = nullptr;
+  std::vector<Plan*> group;  // loopback peers (index = rank)
+
+  // stats
+  uint64_t solves = 0;
+  std::vector<cudaEvent_t> ev;  // timing events
+  bool timed_valid = false;
+  int launches_per_solve = 0;
+};
+
+// kernels.cu launchers (return cudaError_t of the launch)
+cudaError_t launch_local_generic(const Plan& P, const double* b, double* x, cudaStream_t s);
+cudaError_t launch_bhat(const Plan& P, cudaStream_t s);
+cudaError_t launch_pcr_stage(const Plan& P, int k, bool last, cudaStream_t s);
+cudaError_t launch_backsub(const Plan& P, double* x, cudaStream_t s);
+cudaError_t launch_pack_halo(const Plan& P, const double* f, cudaStream_t s);
+cudaError_t launch_stencil(const Plan& P, const double* f, double* rhs, double a, double bc,
+                           double h, cudaStream_t s);
+bool tile_configure(Plan& P, std::string* why);
+cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t s);
+
+}  // namespace ctri

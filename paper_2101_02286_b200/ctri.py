@@ -1,0 +1,361 @@
+"""Thin ctypes binding of ``include/ctri.h`` (argument marshalling only).
+
+Every step of the solve runs inside ``libctri.so`` (sm_100a kernels + NCCL).
+This module converts torch tensors / numpy arrays to pointers, checks status
+codes and raises :class:`CtriError`.  There is no CPU fallback: if the
+extension is missing the import fails loudly.
+
+Function names mirror the C ABI (``ctri_plan_create``, ``ctri_solve`` ...);
+:class:`Plan` and :class:`LoopbackGroup` are small conveniences over them.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libctri.so")
+
+CTRI_FLAG_FULL_BACKSUB = 1 << 0
+CTRI_FLAG_GENERIC_LOCAL = 1 << 1
+CTRI_FLAG_TIMING = 1 << 2
+CTRI_FLAG_DERIV = 1 << 3
+CTRI_MAX_STAGES = 16
+ABI_VERSION = 1
+
+STATUS = {0: "CTRI_OK", 1: "CTRI_ERR_INVALID_ARG", 2: "CTRI_ERR_UNSUPPORTED", 3: "CTRI_ERR_SINGULAR",
+          4: "CTRI_ERR_PARTITION_TOO_SMALL", 5: "CTRI_ERR_CUDA", 6: "CTRI_ERR_NCCL",
+          7: "CTRI_ERR_OOM"}
+
+# Every symbol include/ctri.h declares (checked by tests/test_abi.py).
+ABI_SYMBOLS = ("ctri_status_string", "ctri_last_error", "ctri_abi_version", "ctri_get_unique_id",
+               "ctri_plan_create", "ctri_plan_create_loopback", "ctri_solve", "ctri_solve_loopback",
+               "ctri_solve_host", "ctri_deriv", "ctri_deriv_loopback", "ctri_get_stats",
+               "ctri_plan_destroy", "ctri_factor_query", "ctri_pcr_coefficients")
+
+
+class CtriError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        self.status = status
+        self.name = STATUS.get(status, f"status {status}")
+        super().__init__(f"{where}: {self.name}: {detail}")
+
+
+class ctri_stats(ctypes.Structure):
+    _fields_ = [("global_dims", ctypes.c_int64 * 3),
+                ("solve_dim", ctypes.c_int32), ("nparts", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("cyclic", ctypes.c_int32),
+                ("n_local", ctypes.c_int64), ("m_batch", ctypes.c_int64),
+                ("local_kernel", ctypes.c_int32), ("rows_per_thread", ctypes.c_int32),
+                ("cluster_size", ctypes.c_int32), ("tile_columns", ctypes.c_int32),
+                ("chunk_heads", ctypes.c_int32), ("window_rows", ctypes.c_int32),
+                ("pcr_stages", ctypes.c_int32), ("comm_rounds", ctypes.c_int32),
+                ("sends_per_solve", ctypes.c_int32),
+                ("bytes_sent_per_solve", ctypes.c_int64),
+                ("launches_per_solve", ctypes.c_int32),
+                ("solves", ctypes.c_uint64),
+                ("t_total_us", ctypes.c_float), ("t_local_us", ctypes.c_float),
+                ("t_yexchange_us", ctypes.c_float), ("t_bhat_us", ctypes.c_float),
+                ("t_stage_us", ctypes.c_float * CTRI_MAX_STAGES),
+                ("t_xexchange_us", ctypes.c_float), ("t_backsub_us", ctypes.c_float)]
+
+    def as_dict(self):
+        d = {}
+        for name, _ in self._fields_:
+            v = getattr(self, name)
+            if hasattr(v, "__len__"):
+                v = list(v)
+            d[name] = v
+        d["t_stage_us"] = d["t_stage_us"][: max(0, self.pcr_stages)]
+        return d
+
+
+_lib = None
+
+
+def load(build_if_missing: bool = False):
+    """Load libctri.so (raises if it is missing; optionally builds it first)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        if build_if_missing:
+            from . import build as _b
+            _b.build()
+        else:
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2101_02286_b200.build`")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    dp = ctypes.POINTER(ctypes.c_double)
+    st = ctypes.c_int
+    sig = {
+        "ctri_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+        "ctri_last_error": (ctypes.c_char_p, []),
+        "ctri_abi_version": (ctypes.c_int, []),
+        "ctri_get_unique_id": (st, [P]),
+        "ctri_plan_create": (st, [ctypes.POINTER(P), i64p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                  dp, ctypes.c_int, P, ctypes.c_uint32, P]),
+        "ctri_plan_create_loopback": (st, [ctypes.POINTER(P), ctypes.c_int, i64p, ctypes.c_int, dp,
+                                           ctypes.c_int, ctypes.c_uint32, P]),
+        "ctri_solve": (st, [P, P, P, P]),
+        "ctri_solve_loopback": (st, [ctypes.POINTER(P), ctypes.c_int, ctypes.POINTER(P),
+                                     ctypes.POINTER(P), P]),
+        "ctri_solve_host": (st, [P, P, P, P]),
+        "ctri_deriv": (st, [P, P, P, ctypes.c_double, ctypes.c_double, ctypes.c_double, P]),
+        "ctri_deriv_loopback": (st, [ctypes.POINTER(P), ctypes.c_int, ctypes.POINTER(P),
+                                     ctypes.POINTER(P), ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_double, P]),
+        "ctri_get_stats": (st, [P, ctypes.POINTER(ctri_stats)]),
+        "ctri_plan_destroy": (st, [P]),
+        "ctri_factor_query": (st, [ctypes.c_int64, dp, dp, dp, dp, ctypes.POINTER(ctypes.c_int)]),
+        "ctri_pcr_coefficients": (st, [ctypes.c_int, ctypes.c_int, dp, dp, dp, dp, dp, dp,
+                                       ctypes.POINTER(ctypes.c_int)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.ctri_abi_version() != ABI_VERSION:
+        raise ImportError("libctri.so ABI version mismatch; rebuild")
+    _lib = lib
+    return lib
+
+
+def _check(status: int, where: str):
+    if status != 0:
+        detail = load().ctri_last_error().decode(errors="replace")
+        raise CtriError(status, where, detail)
+
+
+def _ptr(t) -> int:
+    """Device/host address of a torch tensor, numpy array or int."""
+    if t is None:
+        return 0
+    if isinstance(t, int):
+        return t
+    if isinstance(t, np.ndarray):
+        if not t.flags["C_CONTIGUOUS"] or t.dtype != np.float64:
+            raise ValueError("numpy buffers must be C-contiguous float64")
+        return t.ctypes.data
+    # torch tensor
+    if not t.is_contiguous() or str(t.dtype) != "torch.float64":
+        raise ValueError("tensors must be contiguous float64")
+    return t.data_ptr()
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _dbl3(v):
+    return (ctypes.c_double * 3)(*[float(x) for x in v])
+
+
+# ---------------------------------------------------------------- raw ABI (same names)
+def ctri_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load().ctri_get_unique_id(buf), "ctri_get_unique_id")
+    return buf.raw
+
+
+def ctri_plan_create(global_dims, solve_dim, nparts=1, rank=0, bands=(1 / 3, 1.0, 1 / 3), cyclic=True,
+                     unique_id: bytes | None = None, flags: int = 0, stream=None) -> int:
+    h = ctypes.c_void_p()
+    dims = (ctypes.c_int64 * 3)(*[int(d) for d in global_dims])
+    uid = ctypes.create_string_buffer(unique_id, 128) if unique_id is not None else None
+    _check(load().ctri_plan_create(ctypes.byref(h), dims, int(solve_dim), int(nparts), int(rank),
+                                   _dbl3(bands), int(bool(cyclic)), uid, int(flags),
+                                   _stream_ptr(stream)), "ctri_plan_create")
+    return h.value
+
+
+def ctri_plan_create_loopback(global_dims, solve_dim, nparts, bands=(1 / 3, 1.0, 1 / 3), cyclic=True,
+                              flags: int = 0, stream=None) -> list[int]:
+    hs = (ctypes.c_void_p * nparts)()
+    dims = (ctypes.c_int64 * 3)(*[int(d) for d in global_dims])
+    _check(load().ctri_plan_create_loopback(hs, int(nparts), dims, int(solve_dim), _dbl3(bands),
+                                            int(bool(cyclic)), int(flags), _stream_ptr(stream)),
+           "ctri_plan_create_loopback")
+    return [hs[i] for i in range(nparts)]
+
+
+def ctri_solve(plan: int, b, x, stream=None):
+    _check(load().ctri_solve(plan, _ptr(b), _ptr(x), _stream_ptr(stream)), "ctri_solve")
+
+
+def ctri_solve_loopback(plans, bs, xs, stream=None):
+    n = len(plans)
+    hp = (ctypes.c_void_p * n)(*plans)
+    bp = (ctypes.c_void_p * n)(*[_ptr(b) for b in bs])
+    xp = (ctypes.c_void_p * n)(*[_ptr(x) for x in xs])
+    _check(load().ctri_solve_loopback(hp, n, bp, xp, _stream_ptr(stream)), "ctri_solve_loopback")
+
+
+def ctri_solve_host(plan: int, b_host, x_host, stream=None):
+    _check(load().ctri_solve_host(plan, _ptr(b_host), _ptr(x_host), _stream_ptr(stream)),
+           "ctri_solve_host")
+
+
+def ctri_deriv(plan: int, f, df, a=14 / 9, bc=1 / 9, h=None, stream=None, n_global=None):
+    _check(load().ctri_deriv(plan, _ptr(f), _ptr(df), float(a), float(bc), float(h),
+                             _stream_ptr(stream)), "ctri_deriv")
+
+
+def ctri_deriv_loopback(plans, fs, dfs, a, bc, h, stream=None):
+    n = len(plans)
+    hp = (ctypes.c_void_p * n)(*plans)
+    fp = (ctypes.c_void_p * n)(*[_ptr(f) for f in fs])
+    dp = (ctypes.c_void_p * n)(*[_ptr(d) for d in dfs])
+    _check(load().ctri_deriv_loopback(hp, n, fp, dp, float(a), float(bc), float(h),
+                                      _stream_ptr(stream)), "ctri_deriv_loopback")
+
+
+def ctri_get_stats(plan: int) -> dict:
+    s = ctri_stats()
+    _check(load().ctri_get_stats(plan, ctypes.byref(s)), "ctri_get_stats")
+    return s.as_dict()
+
+
+def ctri_plan_destroy(plan: int):
+    _check(load().ctri_plan_destroy(plan), "ctri_plan_destroy")
+
+
+def ctri_factor_query(n: int, bands=(1 / 3, 1.0, 1 / 3)):
+    """Host-only: S, R (n-1 each), (L^, D^, U^) and the back-substitution window W."""
+    S = np.zeros(max(1, n - 1))
+    R = np.zeros(max(1, n - 1))
+    hat = np.zeros(3)
+    w = ctypes.c_int()
+    dp = ctypes.POINTER(ctypes.c_double)
+    _check(load().ctri_factor_query(int(n), _dbl3(bands), S.ctypes.data_as(dp), R.ctypes.data_as(dp),
+                                    hat.ctypes.data_as(dp), ctypes.byref(w)), "ctri_factor_query")
+    return S, R, tuple(hat), w.value
+
+
+def ctri_pcr_coefficients(L, D, U, cyclic=True):
+    """Host-only: PCR multipliers alpha/gamma [stages][P] and the final inverse diagonal."""
+    L = np.ascontiguousarray(L, dtype=np.float64)
+    D = np.ascontiguousarray(D, dtype=np.float64)
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    P = len(D)
+    a = np.zeros(CTRI_MAX_STAGES * P)
+    g = np.zeros(CTRI_MAX_STAGES * P)
+    inv = np.zeros(P)
+    stages = ctypes.c_int()
+    dp = ctypes.POINTER(ctypes.c_double)
+    _check(load().ctri_pcr_coefficients(P, int(bool(cyclic)), L.ctypes.data_as(dp),
+                                        D.ctypes.data_as(dp), U.ctypes.data_as(dp),
+                                        a.ctypes.data_as(dp), g.ctypes.data_as(dp),
+                                        inv.ctypes.data_as(dp), ctypes.byref(stages)),
+           "ctri_pcr_coefficients")
+    q = stages.value
+    return a[: q * P].reshape(q, P), g[: q * P].reshape(q, P), inv
+
+
+# ---------------------------------------------------------------- conveniences
+def local_shape(global_dims, solve_dim, nparts):
+    s = list(global_dims)
+    s[solve_dim] //= nparts
+    return tuple(s)
+
+
+class Plan:
+    """One rank's plan.  With nparts > 1 pass the shared NCCL ``unique_id``
+    (see :func:`paper_2101_02286_b200.dist.plan_from_process_group`)."""
+
+    def __init__(self, global_dims, solve_dim=0, nparts=1, rank=0, bands=(1 / 3, 1.0, 1 / 3),
+                 cyclic=True, unique_id=None, flags=0, stream=None):
+        self.global_dims = tuple(int(d) for d in global_dims)
+        self.solve_dim = int(solve_dim)
+        self.nparts = int(nparts)
+        self.rank = int(rank)
+        self.handle = ctri_plan_create(global_dims, solve_dim, nparts, rank, bands, cyclic,
+                                       unique_id, flags, stream)
+
+    @property
+    def local_shape(self):
+        return local_shape(self.global_dims, self.solve_dim, self.nparts)
+
+    def solve(self, b, x=None, stream=None):
+        if x is None:
+            x = b
+        ctri_solve(self.handle, b, x, stream)
+        return x
+
+    def solve_host(self, b_host, x_host, stream=None):
+        ctri_solve_host(self.handle, b_host, x_host, stream)
+        return x_host
+
+    def deriv(self, f, df, a=14 / 9, bc=1 / 9, h=None, stream=None):
+        if h is None:
+            import math
+            h = 2 * math.pi / self.global_dims[self.solve_dim]
+        ctri_deriv(self.handle, f, df, a, bc, h, stream)
+        return df
+
+    def stats(self) -> dict:
+        return ctri_get_stats(self.handle)
+
+    def close(self):
+        if self.handle:
+            ctri_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+class LoopbackGroup:
+    """TEST-ONLY: nparts ranks on one device, exchanges as device copies."""
+
+    def __init__(self, global_dims, solve_dim, nparts, bands=(1 / 3, 1.0, 1 / 3), cyclic=True,
+                 flags=0, stream=None):
+        self.global_dims = tuple(int(d) for d in global_dims)
+        self.solve_dim = int(solve_dim)
+        self.nparts = int(nparts)
+        self.handles = ctri_plan_create_loopback(global_dims, solve_dim, nparts, bands, cyclic, flags,
+                                                 stream)
+
+    @property
+    def local_shape(self):
+        return local_shape(self.global_dims, self.solve_dim, self.nparts)
+
+    def solve(self, bs, xs, stream=None):
+        ctri_solve_loopback(self.handles, bs, xs, stream)
+
+    def deriv(self, fs, dfs, a=14 / 9, bc=1 / 9, h=None, stream=None):
+        if h is None:
+            import math
+            h = 2 * math.pi / self.global_dims[self.solve_dim]
+        ctri_deriv_loopback(self.handles, fs, dfs, a, bc, h, stream)
+
+    def stats(self, rank=0):
+        return ctri_get_stats(self.handles[rank])
+
+    def close(self):
+        for h in self.handles or []:
+            ctri_plan_destroy(h)
+        self.handles = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

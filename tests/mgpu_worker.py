@@ -1,0 +1,71 @@
+"""torchrun worker for tests/test_multi_gpu.py: the NCCL path of ctri_solve / ctri_deriv on
+p = WORLD_SIZE GPUs, gathered to rank 0 and compared with the CPU oracle."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+import oracle
+import workloads
+from helpers import rel_err, residual
+from paper_2101_02286_b200 import CTRI_FLAG_DERIV, CTRI_FLAG_TIMING
+from paper_2101_02286_b200 import dist as pdist
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    results = {}
+    cases = [((64 * world, 8, 16), 0, (1 / 3, 1.0, 1 / 3), True),
+             ((1024, 4, 32), 0, (0.45, 1.0, 0.45), True),
+             ((256 * world, 2, 48), 0, (0.2, 1.1, 0.4), True),
+             ((8, 128 * world, 32), 1, (1 / 3, 1.0, 1 / 3), True),
+             ((4, 6, 64 * world), 2, (1 / 3, 1.0, 1 / 3), True),
+             ((96 * world, 3, 16), 0, (0.2, 1.1, 0.4), False)]
+    for idx, (dims, sd, bands, cyc) in enumerate(cases):
+        b = workloads.uniform(dims, 6 + idx)
+        plan = pdist.plan_from_process_group(dims, sd, bands, cyc, flags=CTRI_FLAG_TIMING)
+        bl = torch.from_numpy(workloads.slab(b, sd, world, rank)).to(dev)
+        xl = torch.empty_like(bl)
+        plan.solve(bl, xl)
+        torch.cuda.synchronize()
+        st = plan.stats()
+        x = pdist.gather_to_rank0(xl, sd)
+        plan.close()
+        if rank == 0:
+            xn = x.cpu().numpy()
+            ref = oracle.cyclic_solve(b, sd, bands) if cyc else oracle.acyclic_solve(b, sd, bands)
+            results[f"case{idx}"] = {"err": rel_err(xn, ref, sd),
+                                     "res": residual(xn, b, sd, bands, cyc),
+                                     "stages": st["pcr_stages"], "sends": st["sends_per_solve"],
+                                     "kernel": st["local_kernel"]}
+    # compact derivative over NCCL (halo exchange)
+    dims = (128 * world, 4, 16)
+    f = workloads.cfg5_field(dims, 0, 5, kappas=(1, 5, 13))
+    plan = pdist.plan_from_process_group(dims, 0, flags=CTRI_FLAG_DERIV)
+    fl = torch.from_numpy(workloads.slab(f, 0, world, rank)).to(dev)
+    dl = torch.empty_like(fl)
+    plan.deriv(fl, dl)
+    torch.cuda.synchronize()
+    d = pdist.gather_to_rank0(dl, 0)
+    plan.close()
+    if rank == 0:
+        results["deriv"] = {"err": rel_err(d.cpu().numpy(), oracle.deriv(f, 0), 0)}
+        print("RESULTS " + json.dumps(results), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,250 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle on cuda:0.
+
+Metric (R11): max over columns of max_j|x - x_oracle| / max_j|x_oracle| <= 1e-12 and
+residual ||Ax - b||_inf/||b||_inf <= 1e-13 (BASELINE.json north_star).  Multi-partition runs use
+the test-only loopback group (all ranks on one GPU, exchanges as device copies); the NCCL path
+is covered by tests/test_multi_gpu.py.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from helpers import TOL_REL, TOL_RES, gpu_solve, rel_err, residual
+
+pytestmark = pytest.mark.gpu
+
+SYM = (1 / 3, 1.0, 1 / 3)
+NONSYM = (0.2, 1.1, 0.4)
+
+
+def check(b, sd, p=1, bands=SYM, cyclic=True, flags=0, inplace=False, tol=TOL_REL):
+    x, st = gpu_solve(b, sd, p, bands, cyclic, flags, inplace, return_stats=True)
+    ref = oracle.cyclic_solve(b, sd, bands) if cyclic else oracle.acyclic_solve(b, sd, bands)
+    err = rel_err(x, ref, sd)
+    res = residual(x, b, sd, bands, cyclic)
+    assert err <= tol, (err, st)
+    assert res <= max(TOL_RES, tol / 10), (res, st)
+    return x, st
+
+
+def test_cfg1_tile_and_generic():
+    from paper_2101_02286_b200 import CTRI_FLAG_GENERIC_LOCAL
+    dims, sd = workloads.config("cfg1")
+    b = workloads.uniform(dims, workloads.SEEDS["cfg1"])
+    _, st = check(b, sd)
+    assert st["local_kernel"] == 1 and st["rows_per_thread"] == 2
+    _, st = check(b, sd, flags=CTRI_FLAG_GENERIC_LOCAL)
+    assert st["local_kernel"] == 0
+
+
+@pytest.mark.parametrize("shape,sd,kernel", [
+    ((128, 16, 16), 0, 1),      # K=4, G=1
+    ((96, 4, 20), 0, 0),        # n = 96: not K*G*32 -> column-serial
+    ((256, 3, 40), 0, 1),       # ragged batch: inner = 120 (7.5 tiles)
+    ((8, 512, 32), 1, 1),       # solve along index 1 (strided 2 KiB rows)
+    ((4, 6, 256), 2, 0),        # contiguous solve axis -> column-serial
+    ((1024, 2, 16), 0, 1),      # K=32, G=1
+    ((2048, 1, 32), 0, 1),      # K=32, G=2 (cluster, DSMEM)
+    ((8192, 1, 16), 0, 1),      # K=32, G=8: the benchmark column length
+    ((5, 3, 4), 0, 0),          # tiny odd N
+])
+def test_shapes_single_gpu(shape, sd, kernel):
+    b = workloads.uniform(shape, 6)
+    _, st = check(b, sd)
+    assert st["local_kernel"] == kernel, st
+
+
+@pytest.mark.parametrize("bands", [NONSYM, (-0.3, 1.0, 0.25), (0.45, 1.0, 0.45), (0.499, 1.0, 0.499)])
+@pytest.mark.parametrize("cyclic", [True, False])
+def test_bands_single_gpu(bands, cyclic):
+    b = workloads.uniform((512, 4, 32), 6)
+    tol = 1e-12 if bands[0] < 0.49 else 1e-11  # cond(A) ~ 1000 at alpha = 0.499 (oracle's error)
+    check(b, 0, 1, bands, cyclic, tol=tol)
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+@pytest.mark.parametrize("shape", [(64, 8, 8), (1024, 4, 32)])
+@pytest.mark.parametrize("bands", [SYM, NONSYM, (0.45, 1.0, 0.45), (0.499, 1.0, 0.499)])
+def test_loopback_partitions(p, shape, bands):
+    """Multi-partition path (a1)-(a4), incl. alpha -> 1/2 where the reduced coupling is large."""
+    b = workloads.uniform(shape, 6)
+    tol = 1e-12 if bands[0] < 0.49 else 1e-11
+    x, st = check(b, 0, p, bands, tol=tol)
+    assert st["pcr_stages"] == int(math.log2(p))
+    assert st["comm_rounds"] == 2 + int(math.log2(p))
+    assert st["sends_per_solve"] == 2 * int(math.log2(p)) + 1
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 5, 8])
+def test_loopback_acyclic(p):
+    b = workloads.uniform((p * 32, 4, 16), 6)
+    check(b, 0, p, NONSYM, cyclic=False)
+
+
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+@pytest.mark.parametrize("alpha", [1 / 3, 0.45])
+def test_green_function_partition_edges(p, alpha):
+    """b = e_r at partition edges: the closed-form periodic Green's function."""
+    N = 256
+    n = N // p
+    lam = (-1 + math.sqrt(1 - 4 * alpha ** 2)) / (2 * alpha)
+    for r in sorted({0, n - 1, n % N, (n + 1) % N, N - 1}):
+        b = workloads.delta((N, 2, 16), 0, r)
+        x = gpu_solve(b, 0, p, (alpha, 1.0, alpha))
+        dl = (np.arange(N) - r) % N
+        g = (lam ** dl + lam ** (N - dl)) / (math.sqrt(1 - 4 * alpha ** 2) * (1 - lam ** N))
+        assert np.max(np.abs(x - g[:, None, None])) < 5e-15, (p, r)
+
+
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+def test_fourier_modes(p):
+    N = 512
+    for k in (0, 1, 7, 255, 256):
+        b = workloads.fourier_mode((N, 2, 16), 0, k)
+        x = gpu_solve(b, 0, p)
+        expect = b / (1 + 2 / 3 * math.cos(2 * math.pi * k / N))
+        assert np.max(np.abs(x - expect)) < 1e-14, (p, k)
+
+
+def test_p_independence():
+    b = workloads.uniform((1024, 2, 16), 6)
+    xs = [gpu_solve(b, 0, p) for p in (1, 2, 4, 8)]
+    for x in xs[1:]:
+        assert np.max(np.abs(x - xs[0])) < 2e-15
+
+
+def test_window_equals_full_backsub():
+    from paper_2101_02286_b200 import CTRI_FLAG_FULL_BACKSUB
+    b = workloads.uniform((4096, 2, 32), 6)
+    xw, st = gpu_solve(b, 0, 4, return_stats=True)
+    assert st["window_rows"] == 46
+    xf, st = gpu_solve(b, 0, 4, flags=CTRI_FLAG_FULL_BACKSUB, return_stats=True)
+    assert st["window_rows"] == 1023
+    assert np.max(np.abs(xw - xf)) <= 2.0 ** -60 * np.max(np.abs(xf))
+
+
+def test_inplace_and_determinism():
+    b = workloads.uniform((2048, 2, 48), 6)
+    x1 = gpu_solve(b, 0)
+    x2 = gpu_solve(b, 0)
+    assert np.array_equal(x1, x2)
+    x3 = gpu_solve(b, 0, inplace=True)
+    assert np.array_equal(x1, x3)
+    x4 = gpu_solve(b, 0, p=2, inplace=True)
+    assert rel_err(x4, x1, 0) < 1e-14
+
+
+def test_direction_permutation():
+    """Solving along index 1 and 2 of permuted copies gives the permuted index-0 result."""
+    b0 = workloads.uniform((512, 8, 32), 2)
+    x0 = gpu_solve(b0, 0)
+    b1 = np.ascontiguousarray(np.transpose(b0, (1, 0, 2)))
+    x1 = gpu_solve(b1, 1)
+    b2 = np.ascontiguousarray(np.transpose(b0, (1, 2, 0)))
+    x2 = gpu_solve(b2, 2)
+    assert rel_err(np.transpose(x1, (1, 0, 2)), x0, 0) < 1e-14
+    assert rel_err(np.transpose(x2, (2, 0, 1)), x0, 0) < 1e-14
+
+
+@pytest.mark.parametrize("p", [1, 2, 4])
+def test_deriv_matches_oracle_and_wavenumber(p):
+    import torch
+
+    from paper_2101_02286_b200 import CTRI_FLAG_DERIV, ctri
+    N = 1024
+    shape = (N, 2, 16)
+    f = workloads.cfg5_field(shape, 0, 5)
+    ref = oracle.deriv(f, 0)
+    dev = torch.device("cuda:0")
+    fs = [torch.from_numpy(workloads.slab(f, 0, p, r)).to(dev) for r in range(p)]
+    ds = [torch.empty_like(t) for t in fs]
+    if p == 1:
+        plan = ctri.Plan(shape, 0, 1, 0, flags=CTRI_FLAG_DERIV)
+        plan.deriv(fs[0], ds[0])
+        torch.cuda.synchronize()
+        plan.close()
+    else:
+        g = ctri.LoopbackGroup(shape, 0, p, flags=CTRI_FLAG_DERIV)
+        g.deriv(fs, ds)
+        torch.cuda.synchronize()
+        g.close()
+    df = workloads.assemble([t.cpu().numpy() for t in ds], 0)
+    assert rel_err(df, ref, 0) < 1e-12
+    # closed form: sum_k A_k k'(kappa) cos(kappa x + phi)
+    amps, ph = workloads.cfg5_modes(shape, 0, 5)
+    h = 2 * math.pi / N
+    x = (2 * math.pi * np.arange(N) / N)[:, None, None]
+    expect = np.zeros(shape)
+    for q, kap in enumerate(workloads.CFG5_KAPPAS):
+        kp = (14 / 9 * math.sin(kap * h) + 1 / 18 * math.sin(2 * kap * h)) / (1 + 2 / 3 * math.cos(kap * h)) / h
+        expect += amps[q][None] * kp * np.cos(kap * x + ph[q][None])
+    assert np.max(np.abs(df - expect)) < 1e-9 * np.max(np.abs(expect))
+
+
+def test_solve_host_e2e():
+    import torch
+
+    from paper_2101_02286_b200 import ctri
+    shape = (1024, 4, 32)
+    b = workloads.uniform(shape, 6)
+    bh = torch.from_numpy(b).pin_memory()
+    xh = torch.empty_like(bh).pin_memory()
+    plan = ctri.Plan(shape, 0)
+    plan.solve_host(bh, xh)
+    torch.cuda.synchronize()
+    plan.close()
+    assert rel_err(xh.numpy(), oracle.cyclic_solve(b, 0), 0) < TOL_REL
+
+
+def test_errors():
+    import torch
+
+    from paper_2101_02286_b200 import CtriError, ctri
+    with pytest.raises(CtriError) as e:
+        ctri.LoopbackGroup((96, 2, 16), 0, 3)  # cyclic, non-power-of-two p
+    assert e.value.name == "CTRI_ERR_UNSUPPORTED"
+    with pytest.raises(CtriError) as e:
+        ctri.Plan((100, 2, 16), 0, 1, 0, bands=(1.0, 0.0, 1.0))
+    assert e.value.name == "CTRI_ERR_SINGULAR"
+    with pytest.raises(CtriError) as e:
+        ctri.LoopbackGroup((10, 2, 16), 0, 4)
+    assert e.value.name == "CTRI_ERR_PARTITION_TOO_SMALL"
+    plan = ctri.Plan((64, 2, 16), 0)
+    b = torch.zeros(64 * 32 + 1, dtype=torch.float64, device="cuda")
+    with pytest.raises(CtriError) as e:
+        ctri.ctri_solve(plan.handle, b.data_ptr() + 8, b.data_ptr() + 8)
+    assert e.value.name == "CTRI_ERR_INVALID_ARG"
+    plan.close()
+
+
+def test_cfg2_full_size_sampled():
+    """BASELINE configuration (8192 x 256^2, index 0, p = 1), same launch as bench.py:
+    oracle on sampled columns + residual over the whole grid."""
+    import torch
+
+    from paper_2101_02286_b200 import ctri
+    dims, sd = workloads.config("cfg2")
+    dev = torch.device("cuda:0")
+    b = workloads.device_uniform(dims, 2, dev)
+    x = torch.empty_like(b)
+    plan = ctri.Plan(dims, sd)
+    plan.solve(b, x)
+    torch.cuda.synchronize()
+    st = plan.stats()
+    plan.close()
+    assert st["local_kernel"] == 1 and st["cluster_size"] == 8
+    rng = np.random.default_rng(0)
+    cols = rng.choice(dims[1] * dims[2], size=256, replace=False)
+    cols = np.sort(np.r_[cols, [0, 15, 16, 65535]])
+    bs = b.reshape(dims[0], -1)[:, cols].cpu().numpy()
+    xs = x.reshape(dims[0], -1)[:, cols].cpu().numpy()
+    ref = oracle.cyclic_solve(bs.reshape(dims[0], -1, 1), 0).reshape(dims[0], -1)
+    assert rel_err(xs[:, :, None], ref[:, :, None], 0) < TOL_REL
+    # residual over the full grid (band matvec with torch on the device, as a check only)
+    a = 1 / 3
+    r = a * torch.roll(x, 1, 0) + x + a * torch.roll(x, -1, 0) - b
+    res = (r.abs().amax(0) / b.abs().amax(0)).max().item()
+    assert res < TOL_RES

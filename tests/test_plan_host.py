@@ -1,0 +1,172 @@
+"""Host pre-factorisation tables against dense linear algebra.
+
+The plan's fp64 tables are host C++ (paper_2101_02286_b200/csrc/factor.cpp);
+here they are checked without a GPU against dense inverses, the dense Schur
+complement of the permuted system (block-LU reading), the paper's
+stage counts and the golden PCR step of tests/golden/pcr_reduced_p4.txt.
+"""
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import paper_2101_02286_b200 as pk
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+BANDS = [(1 / 3, 1.0, 1 / 3), (0.2, 1.1, 0.4), (-0.3, 1.0, 0.25), (0.45, 1.0, 0.45)]
+
+
+def dense_acyclic(N, bands):
+    l, d, u = bands
+    return np.diag(np.full(N, d)) + np.diag(np.full(N - 1, l), -1) + np.diag(np.full(N - 1, u), 1)
+
+
+def dense_cyclic(N, bands):
+    l, d, u = bands
+    A = np.zeros((N, N))
+    for i in range(N):
+        A[i, i] += d
+        A[i, (i - 1) % N] += l
+        A[i, (i + 1) % N] += u
+    return A
+
+
+@pytest.mark.parametrize("bands", BANDS)
+@pytest.mark.parametrize("n", [3, 4, 8, 33, 256])
+def test_S_R_vs_dense_inverse(bands, n):
+    """Eqs. Si, Ri: D S = L (= l e_0), D R = U (= u e_last) with D the (n-1)-row interior block."""
+    S, R, hat, w = pk.ctri_factor_query(n, bands)
+    l, d, u = bands
+    Dinv = np.linalg.inv(dense_acyclic(n - 1, bands))
+    assert np.max(np.abs(S - l * Dinv[:, 0])) < 1e-15
+    assert np.max(np.abs(R - u * Dinv[:, -1])) < 1e-15
+    # Eqs. Li_hat, Di_hat, Ui_hat
+    assert hat[0] == pytest.approx(-l * S[-1], abs=1e-18)
+    assert hat[1] == pytest.approx(d - l * R[-1] - u * S[0], abs=1e-15)
+    assert hat[2] == pytest.approx(-u * R[0], abs=1e-18)
+
+
+def test_symmetric_limits_and_persymmetry():
+    a = 1 / 3
+    S, R, hat, w = pk.ctri_factor_query(8192)
+    lam = (-1 + math.sqrt(1 - 4 * a * a)) / (2 * a)
+    assert S[0] == pytest.approx(abs(lam), abs=1e-16)  # S[0] -> |lambda|
+    assert hat[1] == pytest.approx(math.sqrt(1 - 4 * a * a), abs=1e-15)  # D^ -> sqrt(5)/3
+    assert np.max(np.abs(S - R[::-1])) < 1e-16  # persymmetry S[k] = R[N-1-k]
+    assert hat[0] == 0.0 and hat[2] == 0.0  # S underflows to exactly 0 for N_i >~ 774
+    for n, expect in ((8, -3.38e-4), (32, -3.1e-14), (256, -7.4e-108)):
+        _, _, h, _ = pk.ctri_factor_query(n)
+        assert h[0] == pytest.approx(expect, rel=0.02), (n, h[0])
+
+
+def test_window():
+    """W = rows per end with |S| or |R| > 2^-64 (R15): 46 at alpha = 1/3."""
+    for n in (256, 1024, 8192):
+        assert pk.ctri_factor_query(n)[3] == 46
+    S, R, _, w = pk.ctri_factor_query(1024)
+    tau = 2.0 ** -64
+    inner = np.r_[np.zeros(w, bool), np.ones(1023 - 2 * w, bool), np.zeros(w, bool)]
+    assert np.all(np.abs(S[inner]) <= tau) and np.all(np.abs(R[inner]) <= tau)
+    assert abs(S[w - 1]) > tau
+    # alpha -> 1/2 widens the window to every row at small n
+    assert pk.ctri_factor_query(64, (0.499, 1, 0.499))[3] == 63
+
+
+def schur_reduced(N, p, bands, cyclic=True):
+    """Dense Schur complement of the interface unknowns (rows i*n) -- block-LU reading P:254."""
+    A = dense_cyclic(N, bands) if cyclic else dense_acyclic(N, bands)
+    n = N // p
+    I = [i * n for i in range(p)]
+    J = [r for r in range(N) if r % n]
+    AII = A[np.ix_(I, I)]
+    AIJ = A[np.ix_(I, J)]
+    AJI = A[np.ix_(J, I)]
+    AJJ = A[np.ix_(J, J)]
+    return AII - AIJ @ np.linalg.solve(AJJ, AJI)
+
+
+@pytest.mark.parametrize("bands", BANDS)
+@pytest.mark.parametrize("p,n", [(2, 8), (4, 8), (8, 4), (4, 33)])
+def test_reduced_system_is_schur_complement(bands, p, n):
+    """Eq. sub-system: the reduced system equals the dense Schur complement, cyclic wrap included."""
+    _, _, (Lh, Dh, Uh), _ = pk.ctri_factor_query(n, bands)
+    Ah = np.zeros((p, p))
+    for i in range(p):
+        Ah[i, i] += Dh
+        Ah[i, (i - 1) % p] += Lh
+        Ah[i, (i + 1) % p] += Uh
+    Sc = schur_reduced(n * p, p, bands)
+    assert np.max(np.abs(Ah - Sc)) < 1e-14
+
+
+def apply_pcr(alpha, gamma, inv, b, cyclic=True):
+    """Apply the PCR multipliers to a RHS (P:84 step structure), for checking the tables."""
+    q, P = alpha.shape if alpha.size else (0, len(inv))
+    b = np.array(b, dtype=np.float64)
+    for k in range(q):
+        s = 1 << k
+        nb = b.copy()
+        for c in range(P):
+            lm, lp = c - s, c + s
+            vm = b[lm % P] if (cyclic or lm >= 0) else 0.0
+            vp = b[lp % P] if (cyclic or lp < P) else 0.0
+            nb[c] = b[c] - alpha[k, c] * vm - gamma[k, c] * vp
+        b = nb
+    return b * inv
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8, 16, 64])
+def test_cyclic_pcr_tables_vs_dense(P):
+    rng = np.random.default_rng(P)
+    L = rng.uniform(-0.4, 0.4, P)
+    U = rng.uniform(-0.4, 0.4, P)
+    D = rng.uniform(1.0, 1.3, P)
+    a, g, inv = pk.ctri_pcr_coefficients(L, D, U, cyclic=True)
+    assert a.shape[0] == int(math.log2(P))  # floor(log2 p) stages
+    A = np.zeros((P, P))
+    for c in range(P):
+        A[c, c] += D[c]
+        A[c, (c - 1) % P] += L[c]
+        A[c, (c + 1) % P] += U[c]
+    for _ in range(3):
+        b = rng.uniform(-1, 1, P)
+        x = apply_pcr(a, g, inv, b, True)
+        assert np.max(np.abs(x - np.linalg.solve(A, b))) < 1e-14
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 5, 7, 8, 13])
+def test_acyclic_pcr_tables_vs_dense(P):
+    rng = np.random.default_rng(100 + P)
+    L = rng.uniform(-0.4, 0.4, P)
+    U = rng.uniform(-0.4, 0.4, P)
+    D = rng.uniform(1.0, 1.3, P)
+    a, g, inv = pk.ctri_pcr_coefficients(L, D, U, cyclic=False)
+    assert a.shape[0] == (math.ceil(math.log2(P)) if P > 1 else 0)  # ceil(log2 p)
+    A = np.diag(D) + np.diag(L[1:], -1) + np.diag(U[:-1], 1)
+    b = rng.uniform(-1, 1, P)
+    assert np.max(np.abs(apply_pcr(a, g, inv, b, False) - np.linalg.solve(A, b))) < 1e-14
+
+
+def test_golden_pcr_step_p4():
+    """tests/golden/pcr_reduced_p4.txt (fold reading R3)."""
+    gold = {}
+    for line in open(os.path.join(GOLDEN, "pcr_reduced_p4.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        k, num, den = line.split()
+        gold[k] = Fraction(int(num), int(den))
+    a, g, inv = pk.ctri_pcr_coefficients([1 / 3] * 4, [1.0] * 4, [1 / 3] * 4, cyclic=True)
+    assert a.shape == (2, 4)
+    # stage 0: alpha = gamma = 1/3 -> new diagonal 1 - 2/9 = 7/9, new off-diagonal -1/9
+    assert np.allclose(a[0], 1 / 3) and np.allclose(g[0], 1 / 3)
+    d0 = 1 - a[0, 0] / 3 - g[0, 0] / 3
+    off0 = -a[0, 0] / 3
+    assert d0 == pytest.approx(float(gold["stage0_diag"]), abs=1e-15)
+    assert off0 == pytest.approx(float(gold["stage0_off"]), abs=1e-15)
+    # stage 1: alpha = off0 / d0 = -1/7; fold gives 5/7
+    assert a[1, 0] == pytest.approx(float(gold["stage0_off"] / gold["stage0_diag"]), abs=1e-15)
+    assert 1 / inv[0] == pytest.approx(float(gold["fold_diag"]), abs=1e-15)
+    x = apply_pcr(a, g, inv, np.ones(4))
+    assert np.allclose(x, float(gold["x"]), rtol=0, atol=1e-15)
