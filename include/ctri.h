@@ -88,6 +88,8 @@ typedef struct ctri_stats {
   float t_total_us, t_local_us, t_yexchange_us, t_bhat_us;
   float t_stage_us[CTRI_MAX_STAGES]; /* exchange + update of PCR stage k */
   float t_xexchange_us, t_backsub_us;
+  int32_t tile_variant;         /* cluster-tile variant index (columns/threads/ring depth), -1 if none */
+  int32_t tile_stages;          /* TMA shared-memory ring depth of the tile kernel */
 } ctri_stats;
 
 /* Human-readable status name; never NULL. */

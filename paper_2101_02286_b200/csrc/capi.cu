@@ -499,7 +499,9 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
   out->local_kernel = P->local_kernel;
   out->rows_per_thread = P->local_kernel ? P->tile.K : 0;
   out->cluster_size = P->local_kernel ? P->tile.G : 1;
-  out->tile_columns = P->local_kernel ? kTileCols : 1;
+  out->tile_columns = P->local_kernel ? P->tile.C : 1;
+  out->tile_variant = P->local_kernel ? P->tile.variant : -1;
+  out->tile_stages = P->local_kernel ? P->tile.STAGES : 0;
   out->chunk_heads = P->local_kernel ? P->tile.Q : 1;
   const bool full = (P->flags & CTRI_FLAG_FULL_BACKSUB) || (2 * P->window >= P->lay.n - 1);
   out->window_rows = (int32_t)(full ? P->lay.n - 1 : P->window);
@@ -544,7 +546,7 @@ ctri_status ctri_plan_destroy(ctri_plan plan) {
   Plan* P = reinterpret_cast<Plan*>(plan);
   // detach from a loopback group
   for (Plan* q : P->group)
-    if (q != P)
+    if (q && q != P)
       for (auto& g : q->group)
         if (g == P) g = nullptr;
   free_plan(P);

@@ -13,11 +13,8 @@
 
 namespace ctri {
 
-// Fixed tile geometry of the cluster-tile local solve (kernels.cu).
-constexpr int kTileCols = 16;     // batch columns per tile: one 128-byte line per row
-constexpr int kTileThreads = 512; // threads per CTA; one (column, chunk) per thread
-constexpr int kTileChunksPerCta = kTileThreads / kTileCols;  // 32
-constexpr int kMaxCluster = 8;
+constexpr int kMaxCluster = 8;               // portable thread-block cluster size
+constexpr int kMaxClusterNonPortable = 16;  // opt-in (cudaFuncAttributeNonPortableClusterSizeAllowed)
 
 // Layout of a local slab viewed as (outer, n, inner): element (o, r, c) at (o*n + r)*inner + c.
 struct Layout {
@@ -31,6 +28,7 @@ template <int K>
 struct TileConsts {
   double l, u;
   double inv_den[K > 1 ? K - 1 : 1];  // Thomas on the (K-1)-row chunk interior
+  double mlid[K > 1 ? K - 1 : 1];     // -l * inv_den
   double cp[K > 1 ? K - 1 : 1];
   double S[K > 1 ? K - 1 : 1];        // chunk-level S_K = D_K^{-1} l e_0
   double R[K > 1 ? K - 1 : 1];        // chunk-level R_K = D_K^{-1} u e_last
@@ -47,6 +45,7 @@ struct TileArgs {
   int stages;       // log2 Q
   int mode;         // 0: complete cyclic solve (p = 1); 1: y_D = D_i^{-1} b_i + planes (p >= 2);
                     // 2: complete acyclic solve (p = 1)
+  int rows_box;     // TMA box rows (<= 256)
   const double* pcr_alpha;  // [stages][Q]
   const double* pcr_gamma;  // [stages][Q]
   const double* pcr_inv;    // [Q]
@@ -57,6 +56,8 @@ struct TileArgs {
 
 struct TileConfig {
   bool ok = false;
+  int variant = 0;  // index into the tile variant table (tile.cu)
+  int C = 0, NT = 0, STAGES = 0, MINB = 0;  // columns per tile, threads, smem ring depth, CTAs/SM
   int K = 0, G = 0, Q = 0;
   int smem_bytes = 0;
   int grid = 0;  // CTAs launched (multiple of G)
@@ -122,6 +123,7 @@ cudaError_t launch_pack_halo(const Plan& P, const double* f, cudaStream_t s);
 cudaError_t launch_stencil(const Plan& P, const double* f, double* rhs, double a, double bc,
                            double h, cudaStream_t s);
 bool tile_configure(Plan& P, std::string* why);
+const char* tile_variant_name(int v);
 cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t s);
 
 }  // namespace ctri

@@ -1,0 +1,508 @@
+// tile.cu -- the hot kernel: cluster-tile local solve of (a1) for a strided solve axis.
+//
+// PAPER.md P:317 solves D_i y_i = b_i "on the shared memory" by generalized PCR; here the
+// same partition method (Eqs. system1/system2, xi, Li_hat..bi_hat, xi_app) is
+// applied hierarchically ON CHIP (R16):
+//   * a column of the slab (n rows, fixed batch index) is cut into Q = n/K chunks of K rows;
+//     the first row of each chunk is its head (the chunk-level interface unknown, like x~_i),
+//     the other K-1 rows its interior;
+//   * each thread holds one chunk of one column in registers and eliminates the interior
+//     with plan-time Thomas factors (the register leaf: y_c = D_K^{-1} b_c, Eq. yi);
+//   * the Q heads of a column form a tridiagonal system with RHS b^_c = b~_c - l y_{c-1}[last]
+//     - u y_c[first] (Eq. bi_hat) and plan-time coefficients (Eqs. Li_hat..Ui_hat at chunk
+//     level), solved by PCR in shared memory of the CTA owning that column; the Q
+//     chunks of a column live in the G CTAs of a thread-block cluster and reach the owner
+//     through distributed shared memory;
+//   * each chunk is back-substituted, x_c = y_c - S_K x~_c - R_K x~_{c+1} (Eq. xi_app), and
+//     stored.
+// The batch is streamed in column tiles of C columns: TMA (cp.async.bulk.tensor) moves tile
+// t+STAGES into a shared-memory ring while tile t is computed from registers, so HBM sees
+// one read of b and one write of x: 16 B per grid point.
+//
+// mode 0: nparts = 1 cyclic (complete solve; the head system is cyclic)
+// mode 1: nparts > 1: y_D = D_i^{-1} b_i on rows 1..n-1 (row 0 is the GPU interface, decoupled
+//         as a dummy head), plus the planes y_D[1], y_D[n-1], b[0] for (a2)
+// mode 2: nparts = 1 acyclic (complete solve)
+// mode 3: measurement only (CTRI_TILE_COPY_ONLY): x = b through the same TMA ring and stores
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace ctri {
+
+template <int K, int C, int NT, int STAGES, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+    k_tile(const __grid_constant__ CUtensorMap tmap, const TileArgs A, const TileConsts<K> T) {
+  static_assert(K >= 4 && NT % C == 0 && (C == 4 || C == 8 || C == 16), "tile geometry");
+  constexpr int CPC = NT / C;             // chunks per CTA
+  constexpr int ROWS = CPC * K;           // rows per CTA
+  constexpr int PRD = 16 / C;             // rows sharing the 32 smem banks (128 B)
+  static_assert(K % PRD == 0, "K must be a multiple of the bank period");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int Q = A.Q;
+  const int stages = A.stages;
+  double* ring = reinterpret_cast<double*>(smem_raw);
+  double* ex_bt = ring + (size_t)STAGES * ROWS * C;  // owner: b~ of every head it owns
+  double* ex_yf = ex_bt + NT;                        // owner: y_c[first]
+  double* ex_yl = ex_yf + NT;                        // owner: y_c[last]
+  double* pb0 = ex_yl + NT;                          // owner: PCR ping-pong
+  double* pb1 = pb0 + NT;
+  double* rx_a = pb1 + NT;                           // holder: x~_c of its chunk
+  double* rx_b = rx_a + NT;                          // holder: x~_{c+1}
+  double* s_alpha = rx_b + NT;                       // PCR multipliers [stages][Q]
+  double* s_gamma = s_alpha + (size_t)stages * Q;
+  double* s_inv = s_gamma + (size_t)stages * Q;      // [Q]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(s_inv + Q);  // [STAGES] ring, ex, rx
+  uint64_t* mbar_ex = mbar + STAGES;
+  uint64_t* mbar_rx = mbar_ex + 1;
+
+  const int tid = threadIdx.x;
+  const int j = tid % C;   // column within the tile
+  const int cl = tid / C;  // chunk within this CTA
+  const int G = A.G;
+  const uint32_t g = (G > 1) ? dev::cluster_ctarank() : 0u;
+  const int c = (int)g * CPC + cl;  // chunk index within the column (0..Q-1)
+  const int cpo = C / G;            // columns owned per CTA
+  const uint32_t owner = (uint32_t)(j / cpo);
+  const int slot = (j % cpo) * Q + c;
+  const int oj = tid / Q, oc = tid - (tid / Q) * Q;  // reduced row owned by this thread
+  const int prev_row = oj * Q + ((oc - 1) & (Q - 1));
+  const int ocol = (int)g * cpo + oj;                // tile column of the owned row
+  // rotation of the smem row reads so that the PRD groups of a warp hit disjoint banks
+  const int rot = ((tid & 31) / C) % PRD;
+
+  for (int i = tid; i < stages * Q; i += NT) {
+    s_alpha[i] = A.pcr_alpha[i];
+    s_gamma[i] = A.pcr_gamma[i];
+  }
+  for (int i = tid; i < Q; i += NT) s_inv[i] = A.pcr_inv[i];
+  if (tid < STAGES) dev::mbar_init(dev::smem_u32(mbar + tid), 1);
+  if (tid == STAGES) dev::mbar_init(dev::smem_u32(mbar_ex), 1);
+  if (tid == STAGES + 1) dev::mbar_init(dev::smem_u32(mbar_rx), 1);
+  if (tid == 0) dev::fence_mbar_init();
+  __syncthreads();
+  if (G > 1) dev::cluster_sync();  // barriers initialised cluster-wide before any st.async
+
+  const uint32_t ncl = (G > 1) ? dev::ncluster_x() : gridDim.x;
+  const int64_t first = (G > 1) ? (int64_t)dev::cluster_id_x() : (int64_t)blockIdx.x;
+  constexpr uint32_t kTileBytes = (uint32_t)ROWS * C * (uint32_t)sizeof(double);
+  const int boxr = A.rows_box;
+  const int row0 = (int)g * ROWS;
+  const uint64_t pol = dev::policy_evict_first();
+
+  auto issue = [&](int64_t t, int s) {
+    const int o = (int)(t / A.tiles_per_outer);
+    const int col0 = (int)(t - (int64_t)o * A.tiles_per_outer) * C;
+    const uint32_t bar = dev::smem_u32(mbar + s);
+    double* dst = ring + (size_t)s * ROWS * C;
+    dev::fence_proxy_async();
+    dev::mbar_expect_tx(bar, kTileBytes);
+    for (int r = 0; r < ROWS; r += boxr)
+      dev::tma_load_3d(dev::smem_u32(dst + (size_t)r * C), &tmap, col0, row0 + r, o, bar, pol);
+  };
+
+  // remote addresses: my (b~, y_first, y_last) -> owner; my x~ -> holders of chunks oc, oc-1
+  uint32_t r_bt = dev::smem_u32(ex_bt + slot), r_yf = dev::smem_u32(ex_yf + slot),
+           r_yl = dev::smem_u32(ex_yl + slot), r_exbar = dev::smem_u32(mbar_ex);
+  const int ha = oc / CPC, ta = (oc % CPC) * C + ocol;          // holder of chunk oc
+  const int ocm = (oc - 1) & (Q - 1);
+  const int hb = ocm / CPC, tb = (ocm % CPC) * C + ocol;        // holder of chunk oc-1
+  uint32_t r_xa = dev::smem_u32(rx_a + ta), r_xb = dev::smem_u32(rx_b + tb),
+           r_rxa = dev::smem_u32(mbar_rx), r_rxb = dev::smem_u32(mbar_rx);
+  if (G > 1) {
+    r_bt = dev::mapa(r_bt, owner);
+    r_yf = dev::mapa(r_yf, owner);
+    r_yl = dev::mapa(r_yl, owner);
+    r_exbar = dev::mapa(r_exbar, owner);
+    r_xa = dev::mapa(r_xa, (uint32_t)ha);
+    r_rxa = dev::mapa(r_rxa, (uint32_t)ha);
+    r_xb = dev::mapa(r_xb, (uint32_t)hb);
+    r_rxb = dev::mapa(r_rxb, (uint32_t)hb);
+  }
+
+  if (tid == 0)
+    for (int s = 0; s < STAGES; ++s)
+      if (first + (int64_t)s * ncl < A.num_tiles) issue(first + (int64_t)s * ncl, s);
+
+  int it = 0;
+  for (int64_t t = first; t < A.num_tiles; t += ncl, ++it) {
+    const int s = it % STAGES;
+    const int64_t o = t / A.tiles_per_outer;
+    const int64_t col = (t - o * A.tiles_per_outer) * C + j;
+    if (tid == 0 && A.mode != 3) {  // arm this tile's exchange barriers (remote bytes may race ahead)
+      dev::mbar_expect_tx(dev::smem_u32(mbar_ex), (uint32_t)NT * 3u * 8u);
+      dev::mbar_expect_tx(dev::smem_u32(mbar_rx), (uint32_t)NT * 2u * 8u);
+    }
+    dev::mbar_wait(dev::smem_u32(mbar + s), (uint32_t)(it / STAGES) & 1u);
+    const double* tile = ring + (size_t)s * ROWS * C;
+    double v[K];
+#pragma unroll
+    for (int k = 0; k < K; k += PRD) {
+      double a[PRD];
+#pragma unroll
+      for (int i = 0; i < PRD; ++i) a[i] = tile[(cl * K + k + ((i + rot) % PRD)) * C + j];
+#pragma unroll
+      for (int m = 0; m < PRD; ++m) {  // a[i] holds row k + (i + rot) % PRD
+        double r = a[0];
+#pragma unroll
+        for (int i = 1; i < PRD; ++i)
+          if ((i + rot) % PRD == m) r = a[i];
+        v[k + m] = r;
+      }
+    }
+    __syncthreads();  // every thread has its chunk in registers: stage s is free
+    if (tid == 0 && t + (int64_t)STAGES * ncl < A.num_tiles) issue(t + (int64_t)STAGES * ncl, s);
+    if (A.mode == 3) {  // measurement only: the same TMA/store pipeline without the solve
+      if (col < A.lay.inner) {
+        double* xp = A.x + (o * A.lay.n + (int64_t)c * K) * A.lay.inner + col;
+#pragma unroll
+        for (int k = 0; k < K; ++k) dev::st_global_cs(xp + (int64_t)k * A.lay.inner, v[k]);
+      }
+      continue;
+    }
+
+    // ---- chunk interior solve (rows 1..K-1), Thomas with plan-time factors (Eq. yi) ----
+    const double btv = v[0];
+    {
+      double gg = v[1] * T.inv_den[0];
+      v[1] = gg;
+#pragma unroll
+      for (int k = 2; k < K; ++k) {
+        gg = fma(T.mlid[k - 1], gg, v[k] * T.inv_den[k - 1]);  // (v_k - l g_{k-1}) / den_k
+        v[k] = gg;
+      }
+#pragma unroll
+      for (int k = K - 2; k >= 1; --k) v[k] = fma(-T.cp[k - 1], v[k + 1], v[k]);
+    }
+    // ---- (b~_c, y_c[first], y_c[last]) -> owner CTA, completing on its exchange barrier ----
+    dev::st_async_f64(r_bt, btv, r_exbar);
+    dev::st_async_f64(r_yf, v[1], r_exbar);
+    dev::st_async_f64(r_yl, v[K - 1], r_exbar);
+    // ---- owner: head system b^_c (Eq. bi_hat at chunk level), then PCR stages ----
+    {
+      dev::mbar_wait(dev::smem_u32(mbar_ex), (uint32_t)it & 1u);
+      const double lt = (A.mode == 2 && oc == 0) ? 0.0 : T.l * ex_yl[prev_row];  // acyclic top
+      double bh = ex_bt[tid] - lt - T.u * ex_yf[tid];
+      if (A.mode == 1 && oc == 0) bh = 0.0;  // slab row 0 is the GPU interface, not in D_i
+      double* cur = pb0;
+      double* nxt = pb1;
+      for (int k = 0; k < stages; ++k) {
+        cur[tid] = bh;
+        __syncthreads();
+        const int sh = 1 << k;
+        const double vm = cur[oj * Q + ((oc - sh) & (Q - 1))];
+        const double vp = cur[oj * Q + ((oc + sh) & (Q - 1))];
+        bh = bh - s_alpha[k * Q + oc] * vm - s_gamma[k * Q + oc] * vp;
+        double* tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+      }
+      const double xt = bh * s_inv[oc];
+      // x~_oc -> x_a of chunk oc's holder and x_b of chunk oc-1's holder
+      dev::st_async_f64(r_xa, xt, r_rxa);
+      dev::st_async_f64(r_xb, xt, r_rxb);
+    }
+    dev::mbar_wait(dev::smem_u32(mbar_rx), (uint32_t)it & 1u);
+    const double xa = rx_a[tid];
+    const double xb = (A.mode != 0 && c == Q - 1) ? 0.0 : rx_b[tid];  // x~_{i+1} outside D_i / acyclic end
+    // ---- chunk back-substitution, Eq. xi_app at chunk level ----
+    v[0] = (A.mode == 1 && c == 0) ? btv : xa;  // mode 1: slab row 0 keeps b~ (scratch)
+#pragma unroll
+    for (int k = 1; k < K; ++k) v[k] = v[k] - T.S[k - 1] * xa - T.R[k - 1] * xb;
+    if (col < A.lay.inner) {
+      double* xp = A.x + (o * A.lay.n + (int64_t)c * K) * A.lay.inner + col;
+#pragma unroll
+      for (int k = 0; k < K; ++k) dev::st_global_cs(xp + (int64_t)k * A.lay.inner, v[k]);
+      if (A.mode == 1) {
+        const int64_t pj = o * A.lay.inner + col;
+        if (c == 0) {
+          A.plane_yf[pj] = v[1];
+          A.plane_bt[pj] = btv;
+        }
+        if (c == Q - 1) A.plane_yl[pj] = v[K - 1];
+      }
+    }
+  }
+  if (G > 1) dev::cluster_sync();  // no CTA exits while peers may still address its smem
+}
+
+// ------------------------------------------------------------------------------------------
+// variants: (C columns per tile, NT threads, STAGES smem ring depth, MINB CTAs per SM)
+// ------------------------------------------------------------------------------------------
+struct Variant {
+  const char* name;
+  int C, NT, STAGES, MINB;
+};
+static const Variant kVariants[] = {
+    {"c16t512s1", 16, 512, 1, 1},
+    {"c8t512s1", 8, 512, 1, 1},
+    {"c4t512s1", 4, 512, 1, 1},
+    {"c8t256s1", 8, 256, 1, 2},
+    {"c16t256s1", 16, 256, 1, 2},
+};
+static constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+
+template <int K>
+static void fill_consts(const TileConfig& tc, TileConsts<K>* T) {
+  const double* c = tc.consts.data();
+  T->l = c[0];
+  T->u = c[1];
+  const int n1 = K - 1;
+  for (int k = 0; k < n1; ++k) {
+    T->inv_den[k] = c[2 + k];
+    T->mlid[k] = -c[0] * c[2 + k];
+    T->cp[k] = c[2 + n1 + k];
+    T->S[k] = c[2 + 2 * n1 + k];
+    T->R[k] = c[2 + 3 * n1 + k];
+  }
+}
+
+template <int K, int C, int NT, int S, int M>
+static cudaError_t launch_one(const TileConfig& tc, const CUtensorMap& map, const TileArgs& A,
+                              cudaStream_t s, bool configure_only) {
+  auto fn = k_tile<K, C, NT, S, M>;
+  if (configure_only) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc.smem_bytes);
+    return e;
+  }
+  TileConsts<K> T;
+  fill_consts<K>(tc, &T);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tc.grid, 1, 1);
+  cfg.blockDim = dim3(NT, 1, 1);
+  cfg.dynamicSmemBytes = tc.smem_bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = tc.G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, map, A, T);
+}
+
+template <int K, int C, int NT, int S, int M>
+static const void* fn_ptr() {
+  return reinterpret_cast<const void*>(&k_tile<K, C, NT, S, M>);
+}
+
+template <int C, int NT, int S, int M>
+static cudaError_t dispatch_k(const TileConfig& tc, const CUtensorMap& map, const TileArgs& A,
+                              cudaStream_t s, bool cfg_only, const void** fp) {
+  switch (tc.K) {
+#define CTRI_K(KK)                                                       \
+  case KK:                                                               \
+    if (fp) *fp = fn_ptr<KK, C, NT, S, M>();                              \
+    return fp ? cudaSuccess : launch_one<KK, C, NT, S, M>(tc, map, A, s, cfg_only);
+    CTRI_K(4) CTRI_K(8) CTRI_K(16) CTRI_K(32)
+#undef CTRI_K
+  }
+  return cudaErrorInvalidValue;
+}
+
+static cudaError_t dispatch(const TileConfig& tc, const CUtensorMap& map, const TileArgs& A,
+                            cudaStream_t s, bool cfg_only, const void** fp = nullptr) {
+  switch (tc.variant) {
+    case 0: return dispatch_k<16, 512, 1, 1>(tc, map, A, s, cfg_only, fp);
+    case 1: return dispatch_k<8, 512, 1, 1>(tc, map, A, s, cfg_only, fp);
+    case 2: return dispatch_k<4, 512, 1, 1>(tc, map, A, s, cfg_only, fp);
+    case 3: return dispatch_k<8, 256, 1, 2>(tc, map, A, s, cfg_only, fp);
+    case 4: return dispatch_k<16, 256, 1, 2>(tc, map, A, s, cfg_only, fp);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// Preference order when CTRI_TILE_VARIANT is not set: the first variant whose geometry fits n.
+static const int kPreference[] = {4, 0, 1, 3, 2};
+
+static int forced_variant() {
+  const char* e = std::getenv("CTRI_TILE_VARIANT");  // experiment knob (bench sweeps)
+  if (e)
+    for (int v = 0; v < kNumVariants; ++v)
+      if (!std::strcmp(e, kVariants[v].name)) return v;
+  return -1;
+}
+
+const char* tile_variant_name(int v) { return (v >= 0 && v < kNumVariants) ? kVariants[v].name : "?"; }
+
+static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
+  TileConfig& tc = P.tile;
+  tc = TileConfig();
+  const Layout& L = P.lay;
+  const Variant& V = kVariants[vi];
+  if (L.inner < V.C || (L.inner % 2) != 0) { *why = "contiguous or narrow solve axis"; return false; }
+  if (L.outer > ((int64_t)1 << 30) || L.inner > ((int64_t)1 << 31) || L.n > ((int64_t)1 << 31)) {
+    *why = "dims too large for TMA coordinates";
+    return false;
+  }
+  const int cpc = V.NT / V.C;
+  if (L.n % cpc != 0) { *why = "n not a multiple of chunks per CTA"; return false; }
+  const int64_t kg = L.n / cpc;  // K * G
+  int K = 0, G = 0;
+  for (int k : {32, 16, 8, 4}) {
+    if (kg % k) continue;
+    const int64_t g = kg / k;
+    if (g >= 1 && g <= kMaxClusterNonPortable && (g & (g - 1)) == 0 && V.C % g == 0) {
+      K = k;
+      G = (int)g;
+      break;
+    }
+  }
+  if (!K) { *why = "n not expressible as K*G*chunks (K<=32, G<=8)"; return false; }
+  tc.variant = (int)(&V - kVariants);
+  tc.C = V.C;
+  tc.NT = V.NT;
+  tc.STAGES = V.STAGES;
+  tc.MINB = V.MINB;
+  const int Q = cpc * G;
+  // chunk-level tables (Eqs. Si, Ri, Li_hat..Ui_hat on the (K-1)-row chunk interior)
+  Partition cp;
+  FactorError fe;
+  if (!partition_factor(K - 1, P.bands, &cp, &fe)) { *why = "chunk factor: " + fe.detail; return false; }
+  tc.consts.clear();
+  tc.consts.push_back(P.bands.l);
+  tc.consts.push_back(P.bands.u);
+  for (int k = 0; k < K - 1; ++k) tc.consts.push_back(cp.th.inv_den[k]);
+  for (int k = 0; k < K - 1; ++k) tc.consts.push_back(cp.th.cp[k]);
+  for (int k = 0; k < K - 1; ++k) tc.consts.push_back(cp.S[k]);
+  for (int k = 0; k < K - 1; ++k) tc.consts.push_back(cp.R[k]);
+  std::vector<double> Lr(Q, cp.Lh), Dr(Q, cp.Dh), Ur(Q, cp.Uh);
+  const bool cyc = (P.p == 1 && P.cyclic);
+  if (P.p > 1) {  // dummy decoupled row 0 (the GPU interface), acyclic over the other heads
+    Lr[0] = 0.0; Dr[0] = 1.0; Ur[0] = 0.0;
+    Lr[1] = 0.0;
+    Ur[Q - 1] = 0.0;
+  } else if (!cyc) {  // p = 1 acyclic: head 0 has no chunk above it
+    Lr[0] = 0.0;
+    Dr[0] = P.bands.d - P.bands.u * cp.S[0];
+    Ur[Q - 1] = 0.0;
+  }
+  if (!pcr_factor(Q, cyc, Lr, Dr, Ur, pivot_threshold(P.bands), &tc.pcr, &fe)) {
+    *why = "chunk PCR factor: " + fe.detail;
+    return false;
+  }
+  tc.K = K;
+  tc.G = G;
+  tc.Q = Q;
+  const int rows_cta = cpc * K;
+  tc.smem_bytes = (int)(sizeof(double) * ((size_t)V.STAGES * rows_cta * V.C + 7 * (size_t)V.NT +
+                                          (2 * (size_t)tc.pcr.stages + 1) * Q) +
+                        8 * (V.STAGES + 2));
+  const void* fn = nullptr;
+  CUtensorMap dummy;
+  TileArgs dA;
+  dispatch(tc, dummy, dA, 0, true, &fn);
+  if (!fn || cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc.smem_bytes) !=
+                 cudaSuccess) {
+    cudaGetLastError();
+    *why = "cudaFuncSetAttribute(smem) failed";
+    return false;
+  }
+  if (G > kMaxCluster &&
+      cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    cudaGetLastError();
+    *why = "non-portable cluster size refused";
+    return false;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G, 1, 1);
+  cfg.blockDim = dim3(V.NT, 1, 1);
+  cfg.dynamicSmemBytes = tc.smem_bytes;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) != cudaSuccess || nclusters < 1) {
+    cudaGetLastError();
+    *why = "cluster occupancy query failed";
+    return false;
+  }
+  const int64_t tiles_per_outer = (L.inner + V.C - 1) / V.C;
+  const int64_t num_tiles = L.outer * tiles_per_outer;
+  const int64_t ncl = std::min<int64_t>(nclusters, num_tiles);
+  tc.grid = (int)(ncl * G);
+  tc.ok = true;
+  return true;
+}
+
+bool tile_configure(Plan& P, std::string* why) {
+  if (P.flags & CTRI_FLAG_GENERIC_LOCAL) { *why = "forced generic"; return false; }
+  const int f = forced_variant();
+  if (f >= 0) return tile_configure_variant(P, f, why);
+  for (int vi : kPreference)
+    if (tile_configure_variant(P, vi, why)) return true;
+  return false;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t s) {
+  const TileConfig& tc = P.tile;
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  const Layout& L = P.lay;
+  const int rows_cta = (tc.NT / tc.C) * tc.K;
+  CUtensorMap map;
+  cuuint64_t gdim[3] = {(cuuint64_t)L.inner, (cuuint64_t)L.n, (cuuint64_t)L.outer};
+  cuuint64_t gstride[2] = {(cuuint64_t)L.inner * 8, (cuuint64_t)(L.n * L.inner * 8)};
+  cuuint32_t box[3] = {(cuuint32_t)tc.C, (cuuint32_t)std::min(rows_cta, 256), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUtensorMapL2promotion prom = CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  if (const char* e = std::getenv("CTRI_TMA_L2_PROMOTION")) {  // measurement knob
+    if (!std::strcmp(e, "64")) prom = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    if (!std::strcmp(e, "128")) prom = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    if (!std::strcmp(e, "256")) prom = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+  CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(b), gdim, gstride,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, prom,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  TileArgs A;
+  A.b = b;
+  A.x = x;
+  A.lay = L;
+  A.tiles_per_outer = (L.inner + tc.C - 1) / tc.C;
+  A.num_tiles = L.outer * A.tiles_per_outer;
+  A.Q = tc.Q;
+  A.G = tc.G;
+  A.rows_per_cta = rows_cta;
+  A.rows_box = std::min(rows_cta, 256);
+  A.stages = tc.pcr.stages;
+  A.mode = (P.p > 1) ? 1 : (P.cyclic ? 0 : 2);
+  if (std::getenv("CTRI_TILE_COPY_ONLY")) A.mode = 3;  // measurement knob: memory ceiling
+  A.pcr_alpha = tc.d_pcr;
+  A.pcr_gamma = tc.d_pcr + (size_t)tc.pcr.stages * tc.Q;
+  A.pcr_inv = tc.d_pcr + (size_t)2 * tc.pcr.stages * tc.Q;
+  A.plane_yf = P.yf;
+  A.plane_yl = P.yl;
+  A.plane_bt = P.bt;
+  return dispatch(tc, map, A, s, false);
+}
+
+}  // namespace ctri

@@ -59,7 +59,8 @@ class ctri_stats(ctypes.Structure):
                 ("t_total_us", ctypes.c_float), ("t_local_us", ctypes.c_float),
                 ("t_yexchange_us", ctypes.c_float), ("t_bhat_us", ctypes.c_float),
                 ("t_stage_us", ctypes.c_float * CTRI_MAX_STAGES),
-                ("t_xexchange_us", ctypes.c_float), ("t_backsub_us", ctypes.c_float)]
+                ("t_xexchange_us", ctypes.c_float), ("t_backsub_us", ctypes.c_float),
+                ("tile_variant", ctypes.c_int32), ("tile_stages", ctypes.c_int32)]
 
     def as_dict(self):
         d = {}
