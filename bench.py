@@ -366,8 +366,13 @@ def main():
                 "cpu_baseline": cpu,
                 "e2e": e2e,
                 "gpu_launches": launches,
-                "comm_us": {"y_exchange": yx, "stages": stage_us, "x_exchange": xx,
-                            "backsub_kernel": back} if p > 1 else None,
+                "comm_us": ({"fused_reduced_kernel_us": back,
+                             "note": "device-initiated (a2)-(a4): LL P2P stores over NVLink + "
+                                     "windowed back-substitution, one kernel; includes waiting "
+                                     "for the slowest peer's local solve"}
+                            if st["reduced_path"] == 1 else
+                            {"y_exchange": yx, "stages": stage_us, "x_exchange": xx,
+                             "backsub_kernel": back}) if p > 1 else None,
                 "clocks": sampler.summary() if sampler else None}
         print(json.dumps(line), flush=True)
     plan.close()

@@ -63,6 +63,8 @@ typedef enum ctri_status {
 #define CTRI_FLAG_GENERIC_LOCAL  (1u << 1) /* force the column-serial local-solve kernel (testing) */
 #define CTRI_FLAG_TIMING         (1u << 2) /* record per-phase CUDA events; read with ctri_get_stats */
 #define CTRI_FLAG_DERIV          (1u << 3) /* allocate halo planes so ctri_deriv may be called */
+#define CTRI_FLAG_NCCL_ROUNDS    (1u << 4) /* nparts > 1: host-issued NCCL rounds instead of the fused
+                                              device-initiated P2P reduced phase */
 
 #define CTRI_MAX_STAGES 16
 
@@ -90,6 +92,9 @@ typedef struct ctri_stats {
   float t_xexchange_us, t_backsub_us;
   int32_t tile_variant;         /* cluster-tile variant index (columns/threads/ring depth), -1 if none */
   int32_t tile_stages;          /* TMA shared-memory ring depth of the tile kernel */
+  int32_t reduced_path;         /* nparts > 1: 0 = NCCL rounds, 1 = fused P2P kernel (t_backsub_us
+                                   then times the whole fused (a2)-(a4) kernel) */
+  int32_t device_error;         /* nonzero: a P2P wait hit its deadline (peer missing) */
 } ctri_stats;
 
 /* Human-readable status name; never NULL. */

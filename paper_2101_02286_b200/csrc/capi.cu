@@ -4,7 +4,10 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -70,6 +73,11 @@ void free_plan(Plan* P) {
   for (double* b : bufs)
     if (b) cudaFree(b);
   for (cudaEvent_t e : P->ev) cudaEventDestroy(e);
+  for (size_t r = 0; r < P->peer_alloc.size(); ++r)
+    if (r < P->peer_ipc.size() && P->peer_ipc[r] && P->peer_alloc[r]) cudaIpcCloseMemHandle(P->peer_alloc[r]);
+  if (P->mbox_alloc) cudaFree(P->mbox_alloc);
+  if (P->d_err) cudaFree(P->d_err);
+  if (P->d_trace) cudaFree(P->d_trace);
   if (P->comm) ncclCommDestroy(P->comm);
   delete P;
 }
@@ -150,6 +158,17 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
                          &P->xt, &P->xt_next};
     for (double** pl : planes) TRY(alloc_plane(pl, m));
   }
+  if (p > 1 && p <= kMaxP2PRanks && !(flags & CTRI_FLAG_NCCL_ROUNDS)) {
+    // fused device-initiated reduced phase: double-buffered mailbox + epoch flags
+    const int q = P->gpcr.stages;
+    P->p2p_nslices = p2p_slices(m, P->loopback ? p : 1, P->num_sms);
+    P->mbox_bytes = sizeof(unsigned long long) * p2p_mailbox_words(m, q);
+    CUDA_TRY(cudaMalloc(&P->mbox_alloc, P->mbox_bytes));
+    CUDA_TRY(cudaMemsetAsync(P->mbox_alloc, 0, P->mbox_bytes, s));
+    CUDA_TRY(cudaMalloc(&P->d_err, sizeof(int)));
+    CUDA_TRY(cudaMemsetAsync(P->d_err, 0, sizeof(int), s));
+    P->p2p = true;
+  }
   if (flags & CTRI_FLAG_DERIV) {
     if (!cyclic) return fail(CTRI_ERR_INVALID_ARG, "CTRI_FLAG_DERIV needs a cyclic plan");
     TRY(alloc_plane(&P->halo_lo, 2 * m));
@@ -163,10 +182,59 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   }
   // launches per solve
   int launches = 1;
-  if (p > 1) launches += 1 /*bhat*/ + P->gpcr.stages + 1 /*backsub*/;
+  if (p > 1) launches += P->p2p ? 1 : 1 /*bhat*/ + P->gpcr.stages + 1 /*backsub*/;
   P->launches_per_solve = launches;
   CUDA_TRY(cudaStreamSynchronize(s));
   return CTRI_OK;
+}
+
+// Map every peer's mailbox: CUDA IPC handles all-gathered over the plan's NCCL communicator.
+// The all-gather is issued after this rank zeroed its mailbox (same stream), so when it
+// completes every rank's flags are initialised.
+ctri_status p2p_connect_ipc(Plan* P, cudaStream_t s) {
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, P->mbox_alloc));
+  char* d_h = nullptr;
+  CUDA_TRY(cudaMalloc(&d_h, sizeof(h) * P->p));
+  std::vector<char> all(sizeof(h) * P->p);
+  ctri_status st = CTRI_OK;
+  do {
+    if (cudaMemcpyAsync(d_h + sizeof(h) * P->rank, &h, sizeof(h), cudaMemcpyHostToDevice, s) != cudaSuccess) { st = fail(CTRI_ERR_CUDA, "ipc handle upload"); break; }
+    if (ncclAllGather(d_h + sizeof(h) * P->rank, d_h, sizeof(h), ncclChar, P->comm, s) != ncclSuccess) { st = fail(CTRI_ERR_NCCL, "ipc handle all-gather"); break; }
+    if (cudaMemcpyAsync(all.data(), d_h, all.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) { st = fail(CTRI_ERR_CUDA, "ipc handle download"); break; }
+  } while (0);
+  cudaFree(d_h);
+  if (st != CTRI_OK) return st;
+  P->peer_alloc.assign(P->p, nullptr);
+  P->peer_ipc.assign(P->p, false);
+  for (int r = 0; r < P->p; ++r) {
+    if (r == P->rank) { P->peer_alloc[r] = P->mbox_alloc; continue; }
+    cudaIpcMemHandle_t hr;
+    std::memcpy(&hr, all.data() + sizeof(h) * r, sizeof(h));
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, hr, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    P->peer_alloc[r] = ptr;
+    P->peer_ipc[r] = true;
+  }
+  return CTRI_OK;
+}
+
+void p2p_fill_rank(const Plan& P, double* x, P2PRank* R) {
+  const int q = P.gpcr.stages;
+  R->rank = P.rank;
+  R->x = x;
+  R->yf = P.yf;
+  R->yl = P.yl;
+  R->bt = P.bt;
+  R->mbox = reinterpret_cast<unsigned long long*>(P.mbox_alloc);
+  for (int r = 0; r < kMaxP2PRanks; ++r) R->peer_mbox[r] = nullptr;
+  for (int r = 0; r < P.p; ++r) R->peer_mbox[r] = reinterpret_cast<unsigned long long*>(P.peer_alloc[r]);
+  for (int k = 0; k < CTRI_MAX_STAGES; ++k) {
+    R->alpha[k] = k < q ? P.gpcr.alpha[(size_t)k * P.p + P.rank] : 0.0;
+    R->gamma[k] = k < q ? P.gpcr.gamma[(size_t)k * P.p + P.rank] : 0.0;
+  }
+  R->inv = P.gpcr.inv[P.rank];
 }
 
 // ---------------- exchanges ----------------
@@ -291,6 +359,53 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
   for (size_t r = 0; r < G.size(); ++r) TRY(local_phase(*G[r], b[r], x[r], s));
   record(P0, EV_LOCAL, s);
   if (P0.p == 1) return CTRI_OK;
+  if (P0.p2p) {  // fused device-initiated (a2)-(a4)
+    P2PArgs A;
+    std::memset(&A, 0, sizeof(A));
+    A.p = P0.p;
+    A.q = P0.gpcr.stages;
+    A.cyclic = P0.cyclic;
+    A.nslices = P0.p2p_nslices;
+    A.m = P0.lay.m();
+    A.slice_cols = (A.m + A.nslices - 1) / A.nslices;
+    A.full = ((P0.flags & CTRI_FLAG_FULL_BACKSUB) || (2 * P0.window >= P0.lay.n - 1)) ? 1 : 0;
+    A.W = P0.window;
+    A.lay = P0.lay;
+    A.l = P0.bands.l;
+    A.u = P0.bands.u;
+    A.S = P0.d_S;
+    A.R = P0.d_R;
+    const unsigned long long ep = ++P0.epoch;
+    for (Plan* P : G) P->epoch = ep;
+    A.epoch = ep;
+    A.err = P0.d_err;
+    const int grid = A.nslices * (int)G.size();
+    if (std::getenv("CTRI_P2P_TRACE") && !P0.d_trace)
+      CUDA_TRY(cudaMalloc(&P0.d_trace, sizeof(unsigned long long) * 8 * grid));
+    A.trace = P0.d_trace;
+    for (size_t r = 0; r < G.size(); ++r) p2p_fill_rank(*G[r], x[r], &A.rk[r]);
+    cudaError_t e = launch_reduced_p2p(A, (int)G.size(), s);
+    if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("p2p reduced kernel: ") + cudaGetErrorString(e));
+    if (P0.d_trace) {  // measurement only: per-phase durations across CTAs
+      std::vector<unsigned long long> t(8 * (size_t)grid);
+      CUDA_TRY(cudaMemcpyAsync(t.data(), P0.d_trace, t.size() * 8, cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      unsigned long long t0 = ~0ull;
+      for (int b = 0; b < grid; ++b) t0 = std::min(t0, t[8 * b]);
+      std::fprintf(stderr, "[p2p trace rank %d epoch %llu]", P0.rank, (unsigned long long)ep);
+      const char* nm[6] = {"start", "y_sent", "y_recv", "stages", "x_recv", "end"};
+      for (int k = 0; k < 6; ++k) {
+        std::vector<double> v;
+        for (int b = 0; b < grid; ++b) v.push_back((t[8 * b + k] - t0) * 1e-3);
+        std::sort(v.begin(), v.end());
+        std::fprintf(stderr, " %s %.1f/%.1f/%.1f", nm[k], v.front(), v[v.size() / 2], v.back());
+      }
+      std::fprintf(stderr, " us\n");
+    }
+    record(P0, EV_BACK, s);
+    for (Plan* P : G) P->timed_valid = !P->ev.empty();
+    return CTRI_OK;
+  }
   // (a2) neighbour exchange of y_{i-1}[last] and b^ assembly
   if (nccl) TRY(exchange_nccl(P0, round_y(P0), s));
   else TRY(exchange_loopback(G, [](Plan& P) { return round_y(P); }, s));
@@ -398,6 +513,10 @@ ctri_status ctri_plan_create(ctri_plan* out, const int64_t global_dims[3], int s
     ncclUniqueId id;
     std::memcpy(&id, nccl_unique_id, sizeof(id));
     NCCL_TRY(ncclCommInitRank(&P->comm, nparts, id, rank));
+    if (P->p2p) {
+      ctri_status cs = p2p_connect_ipc(P.get(), (cudaStream_t)stream);
+      if (cs != CTRI_OK) return cs;
+    }
   }
   *out = reinterpret_cast<ctri_plan>(P.release());
   return CTRI_OK;
@@ -422,6 +541,11 @@ ctri_status ctri_plan_create_loopback(ctri_plan* plans, int nparts, const int64_
   }
   for (int r = 0; r < nparts; ++r) {
     made[r]->group = made;
+    if (made[r]->p2p) {
+      made[r]->peer_alloc.assign(nparts, nullptr);
+      made[r]->peer_ipc.assign(nparts, false);
+      for (int q = 0; q < nparts; ++q) made[r]->peer_alloc[q] = made[q]->mbox_alloc;
+    }
     plans[r] = reinterpret_cast<ctri_plan>(made[r]);
   }
   return CTRI_OK;
@@ -502,6 +626,9 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
   out->tile_columns = P->local_kernel ? P->tile.C : 1;
   out->tile_variant = P->local_kernel ? P->tile.variant : -1;
   out->tile_stages = P->local_kernel ? P->tile.STAGES : 0;
+  out->reduced_path = (P->p > 1 && P->p2p) ? 1 : 0;
+  out->device_error = 0;
+  if (P->d_err) CUDA_TRY(cudaMemcpy(&out->device_error, P->d_err, sizeof(int), cudaMemcpyDeviceToHost));
   out->chunk_heads = P->local_kernel ? P->tile.Q : 1;
   const bool full = (P->flags & CTRI_FLAG_FULL_BACKSUB) || (2 * P->window >= P->lay.n - 1);
   out->window_rows = (int32_t)(full ? P->lay.n - 1 : P->window);
@@ -523,7 +650,10 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
   if (P->timed_valid || (!P->ev.empty() && P->solves > 0)) {
     CUDA_TRY(cudaEventSynchronize(P->ev[P->p > 1 ? EV_BACK : EV_LOCAL]));
     out->t_local_us = elapsed(*P, EV_START, EV_LOCAL);
-    if (P->p > 1) {
+    if (P->p > 1 && P->p2p) {
+      out->t_backsub_us = elapsed(*P, EV_LOCAL, EV_BACK);  // the whole fused (a2)-(a4) kernel
+      out->t_total_us = elapsed(*P, EV_START, EV_BACK);
+    } else if (P->p > 1) {
       out->t_yexchange_us = elapsed(*P, EV_LOCAL, EV_YX);
       out->t_bhat_us = elapsed(*P, EV_YX, EV_BHAT);
       int prev = EV_BHAT;

@@ -66,6 +66,31 @@ struct TileConfig {
   double* d_pcr = nullptr;     // device: alpha | gamma | inv
 };
 
+// ---- fused device-initiated reduced phase (p2p.cu) ----
+constexpr int kMaxP2PRanks = 8;
+struct P2PRank {
+  int rank;
+  double* x;
+  const double *yf, *yl, *bt;
+  unsigned long long* mbox;      // own mailbox of LL words (2 epoch copies)
+  unsigned long long* peer_mbox[kMaxP2PRanks];  // every rank's mailbox as addressable here
+  double alpha[CTRI_MAX_STAGES], gamma[CTRI_MAX_STAGES], inv;
+};
+struct P2PArgs {
+  int p, q, cyclic, nslices, full;
+  int64_t slice_cols, m, W;
+  Layout lay;
+  double l, u;
+  const double *S, *R;
+  unsigned long long epoch;
+  int* err;
+  unsigned long long* trace;  // measurement only (CTRI_P2P_TRACE): [grid][8] globaltimer stamps
+  P2PRank rk[kMaxP2PRanks];
+};
+cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s);
+int p2p_slices(int64_t m, int nranks_launch, int num_sms);
+size_t p2p_mailbox_words(int64_t m, int q);
+
 struct Plan {
   // configuration
   int64_t gdims[3] = {0, 0, 0};
@@ -102,6 +127,17 @@ struct Plan {
   // e2e staging
   double* d_stage_b = nullptr;
   double* d_stage_x = nullptr;
+
+  // fused P2P reduced phase
+  bool p2p = false;
+  int p2p_nslices = 0;
+  void* mbox_alloc = nullptr;          // own LL mailbox (cudaMalloc, IPC-exported)
+  size_t mbox_bytes = 0;
+  std::vector<void*> peer_alloc;       // peer allocations as mapped here (IPC) or direct
+  std::vector<bool> peer_ipc;          // opened with cudaIpcOpenMemHandle
+  int* d_err = nullptr;                // device error word (p2p deadline)
+  unsigned long long* d_trace = nullptr;  // CTRI_P2P_TRACE stamps
+  unsigned long long epoch = 0;
 
   // comm
   ncclComm_t comm = nullptr;

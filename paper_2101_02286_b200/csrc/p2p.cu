@@ -1,0 +1,227 @@
+// p2p.cu -- fused, device-initiated reduced phase (a2)-(a4) for nparts > 1.
+//
+// One kernel per solve replaces the host-issued NCCL rounds.  For its batch columns every
+// thread
+//   (a2) stores y_D[n-1] into the right neighbour's mailbox and forms
+//        b^_i = b~_i - l y_{i-1}[last] - u y_i[first]                    (Eq. bi_hat)
+//   (a3) runs the log2 p cyclic PCR stages: stores b^ into the mailboxes of ranks i +- 2^k,
+//        waits for theirs, b^ <- b^ - alpha b^_{i-s} - gamma b^_{i+s}
+//        and x~ = b^ / (L+D+U) after the fold (R3)
+//   (a4) stores x~_i into the left neighbour's mailbox, waits for x~_{i+1} and applies
+//        x_i = y_i - S_i x~_i - R_i x~_{i+1} on the window rows          (Eq. xi_app)
+//
+// Messages are "LL" words: each fp64 travels as two 8-byte words {32-bit half, 32-bit epoch}
+// written with one 16-byte store over NVLink into CUDA-IPC-mapped peer memory.  An 8-byte
+// word is single-copy atomic, so a receiver that sees the current epoch in both words has
+// the value: no fences, no flags, no CTA barriers -- each thread polls only its own columns
+// in its own (local) mailbox.  Mailboxes are double-buffered by epoch parity, so a word for
+// solve e+1 never overwrites one of solve e that may still be unread.  Every wait has a
+// deadline (%globaltimer), after which the kernel records an error and returns.
+//
+// Loopback test mode (all ranks on one GPU) launches every rank's CTAs in ONE cooperative
+// grid, so no two kernels wait on each other.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "internal.h"
+
+namespace ctri {
+
+namespace {
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+constexpr int kP2PThreads = 256;
+constexpr int kMaxCpt = 8;  // columns per thread
+
+// LL send: value + epoch tag as two 8-byte words in one 16-byte store (peer memory).
+__device__ __forceinline__ void ll_send(unsigned long long* dst, double v, uint32_t ep) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+  const unsigned long long w0 = ((unsigned long long)ep << 32) | (bits & 0xffffffffull);
+  const unsigned long long w1 = ((unsigned long long)ep << 32) | (bits >> 32);
+  asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(dst), "l"(w0), "l"(w1)
+               : "memory");
+}
+
+// LL receive: spin on the local word pair until both halves carry `ep` (false on deadline).
+__device__ __forceinline__ bool ll_recv(const unsigned long long* src, uint32_t ep,
+                                        unsigned long long deadline, double* out) {
+  unsigned long long w0, w1;
+  int spins = 0;
+  while (true) {
+    asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(src)
+                 : "memory");
+    if ((uint32_t)(w0 >> 32) == ep && (uint32_t)(w1 >> 32) == ep) break;
+    if (++spins == 64) {
+      spins = 0;
+      if (globaltimer() > deadline) return false;
+    }
+  }
+  *out = __longlong_as_double((long long)((w1 << 32) | (w0 & 0xffffffffull)));
+  return true;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kP2PThreads, 2)
+    k_reduced_p2p(const P2PArgs A) {
+  const int r_local = blockIdx.x / A.nslices;
+  const int slice = blockIdx.x - r_local * A.nslices;
+  const P2PRank& R = A.rk[r_local];
+  const int p = A.p, q = A.q, rank = R.rank;
+  const int64_t m = A.m;
+  const int64_t c0 = (int64_t)slice * A.slice_cols;
+  const int64_t c1 = std::min<int64_t>(m, c0 + A.slice_cols);
+  const uint32_t ep = (uint32_t)A.epoch;
+  const unsigned long long deadline = globaltimer() + 20ull * 1000000000ull;  // 20 s
+  // mailbox copy (epoch parity): [y: 2m][stage k, slot 0/1: 2m each][x: 2m] 64-bit words
+  const int64_t per_copy = (int64_t)(2 + 2 * q) * 2 * m;
+  const int64_t copy_off = (int64_t)(ep & 1u) * per_copy;
+  const int64_t OFF_Y = 0, OFF_X = (int64_t)(1 + 2 * q) * 2 * m;
+  auto OFF_S = [&](int k, int slot) -> int64_t { return (int64_t)(1 + 2 * k + slot) * 2 * m; };
+  const bool cyc = A.cyclic != 0;
+  const int right = cyc ? (rank + 1) % p : (rank + 1 < p ? rank + 1 : -1);
+  const int left = cyc ? (rank + p - 1) % p : (rank > 0 ? rank - 1 : -1);
+  unsigned long long* const mine = R.mbox + copy_off;
+
+  unsigned long long* tr = A.trace ? A.trace + (size_t)blockIdx.x * 8 : nullptr;
+  auto stamp = [&](int k) {
+    if (tr && threadIdx.x == 0) tr[k] = globaltimer();
+  };
+  stamp(0);
+  double bh[kMaxCpt];
+  int64_t col[kMaxCpt];
+  int nc = 0;
+  for (int64_t j = c0 + threadIdx.x; j < c1 && nc < kMaxCpt; j += kP2PThreads) col[nc++] = j;
+  bool ok = true;
+
+  // ---- (a2) y_i[last] -> right neighbour; b^ ----
+  if (right >= 0) {
+    unsigned long long* dst = R.peer_mbox[right] + copy_off + OFF_Y;
+    for (int i = 0; i < nc; ++i) ll_send(dst + 2 * col[i], R.yl[col[i]], ep);
+  }
+  stamp(1);
+  for (int i = 0; i < nc; ++i) {
+    const int64_t j = col[i];
+    double ylp = 0.0;
+    if (left >= 0) ok = ok && ll_recv(mine + OFF_Y + 2 * j, ep, deadline, &ylp);
+    bh[i] = R.bt[j] - A.l * ylp - A.u * R.yf[j];
+  }
+  stamp(2);
+  // ---- (a3) PCR stages over the p reduced rows ----
+  for (int k = 0; k < q && ok; ++k) {
+    const int s = 1 << k;
+    int lm = rank - s, lp = rank + s;
+    if (cyc) {
+      lm = ((lm % p) + p) % p;
+      lp = lp % p;
+    } else {
+      if (lm < 0) lm = -1;
+      if (lp >= p) lp = -1;
+    }
+    const bool single = (lm >= 0 && lm == lp);
+    // my b^ is the "from i-s" message (slot 0) of rank lp and the "from i+s" one (slot 1) of lm
+    if (lp >= 0) {
+      unsigned long long* dst = R.peer_mbox[lp] + copy_off + OFF_S(k, 0);
+      for (int i = 0; i < nc; ++i) ll_send(dst + 2 * col[i], bh[i], ep);
+    }
+    if (lm >= 0 && !single) {
+      unsigned long long* dst = R.peer_mbox[lm] + copy_off + OFF_S(k, 1);
+      for (int i = 0; i < nc; ++i) ll_send(dst + 2 * col[i], bh[i], ep);
+    }
+    const double a = R.alpha[k], g = R.gamma[k];
+    for (int i = 0; i < nc && ok; ++i) {
+      const int64_t j = col[i];
+      double vm = 0.0, vp = 0.0;
+      if (lm >= 0) ok = ok && ll_recv(mine + OFF_S(k, 0) + 2 * j, ep, deadline, &vm);
+      if (lp >= 0) {
+        if (single) vp = vm;
+        else ok = ok && ll_recv(mine + OFF_S(k, 1) + 2 * j, ep, deadline, &vp);
+      }
+      bh[i] = bh[i] - a * vm - g * vp;
+    }
+  }
+  stamp(3);
+  for (int i = 0; i < nc; ++i) bh[i] *= R.inv;  // x~_i
+  // ---- (a4) x~_i -> left neighbour; back-substitution on the window ----
+  if (ok && left >= 0) {
+    unsigned long long* dst = R.peer_mbox[left] + copy_off + OFF_X;
+    for (int i = 0; i < nc; ++i) ll_send(dst + 2 * col[i], bh[i], ep);
+  }
+  double xb[kMaxCpt];
+  for (int i = 0; i < nc && ok; ++i) {
+    xb[i] = 0.0;
+    if (right >= 0) ok = ok && ll_recv(mine + OFF_X + 2 * col[i], ep, deadline, &xb[i]);
+  }
+  if (!ok) {
+    atomicExch(A.err, 1);
+    return;
+  }
+  stamp(4);
+  const int64_t n = A.lay.n, inner = A.lay.inner;
+  const int64_t rows = A.full ? n - 1 : 2 * A.W;  // interior rows touched
+  for (int i = 0; i < nc; ++i) {
+    const int64_t j = col[i];
+    const double xa = bh[i], xn = xb[i];
+    const int64_t o = j / inner, c = j - o * inner;
+    double* xc = R.x + o * n * inner + c;
+    xc[0] = xa;
+    // 8 independent loads in flight per column, then the updates (memory-level parallelism)
+    for (int64_t r0 = 0; r0 < rows; r0 += 8) {
+      double v[8];
+      int64_t rr[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t ry = r0 + u;
+        rr[u] = A.full ? ry + 1 : (ry < A.W ? ry + 1 : n - 2 * A.W + ry);
+        if (ry < rows) v[u] = xc[rr[u] * inner];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (r0 + u < rows) {
+          const int64_t r = rr[u];
+          xc[r * inner] = v[u] - A.S[r - 1] * xa - A.R[r - 1] * xn;
+        }
+      }
+    }
+  }
+  if (tr) {
+    __syncthreads();
+    stamp(5);
+  }
+}
+
+cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(A.nslices * nranks_launch), 1, 1);
+  cfg.blockDim = dim3(kP2PThreads, 1, 1);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (they wait on each other)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = nranks_launch > 1 ? 1 : 0;  // one rank per launch: the grid fits anyway
+  return cudaLaunchKernelEx(&cfg, k_reduced_p2p, A);
+}
+
+int p2p_slices(int64_t m, int nranks_launch, int num_sms) {
+  // one wave: <= resident CTAs in total, <= kMaxCpt columns per thread
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_reduced_p2p, kP2PThreads, 0) !=
+          cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  const int64_t cap = std::max<int64_t>(1, (int64_t)per_sm * num_sms / nranks_launch);
+  int64_t ns = std::min<int64_t>(cap, (m + kP2PThreads - 1) / kP2PThreads);
+  while ((m + ns - 1) / ns > (int64_t)kP2PThreads * kMaxCpt) ++ns;
+  return (int)std::max<int64_t>(1, ns);
+}
+
+size_t p2p_mailbox_words(int64_t m, int q) { return (size_t)2 * (2 + 2 * q) * 2 * (size_t)m; }
+
+}  // namespace ctri

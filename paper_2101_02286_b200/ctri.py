@@ -22,6 +22,7 @@ CTRI_FLAG_FULL_BACKSUB = 1 << 0
 CTRI_FLAG_GENERIC_LOCAL = 1 << 1
 CTRI_FLAG_TIMING = 1 << 2
 CTRI_FLAG_DERIV = 1 << 3
+CTRI_FLAG_NCCL_ROUNDS = 1 << 4
 CTRI_MAX_STAGES = 16
 ABI_VERSION = 1
 
@@ -60,7 +61,8 @@ class ctri_stats(ctypes.Structure):
                 ("t_yexchange_us", ctypes.c_float), ("t_bhat_us", ctypes.c_float),
                 ("t_stage_us", ctypes.c_float * CTRI_MAX_STAGES),
                 ("t_xexchange_us", ctypes.c_float), ("t_backsub_us", ctypes.c_float),
-                ("tile_variant", ctypes.c_int32), ("tile_stages", ctypes.c_int32)]
+                ("tile_variant", ctypes.c_int32), ("tile_stages", ctypes.c_int32),
+                ("reduced_path", ctypes.c_int32), ("device_error", ctypes.c_int32)]
 
     def as_dict(self):
         d = {}

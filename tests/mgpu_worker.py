@@ -15,7 +15,7 @@ import torch.distributed as dist
 import oracle
 import workloads
 from helpers import rel_err, residual
-from paper_2101_02286_b200 import CTRI_FLAG_DERIV, CTRI_FLAG_TIMING
+from paper_2101_02286_b200 import CTRI_FLAG_DERIV, CTRI_FLAG_NCCL_ROUNDS, CTRI_FLAG_TIMING
 from paper_2101_02286_b200 import dist as pdist
 
 
@@ -33,9 +33,10 @@ def main():
              ((8, 128 * world, 32), 1, (1 / 3, 1.0, 1 / 3), True),
              ((4, 6, 64 * world), 2, (1 / 3, 1.0, 1 / 3), True),
              ((96 * world, 3, 16), 0, (0.2, 1.1, 0.4), False)]
-    for idx, (dims, sd, bands, cyc) in enumerate(cases):
+    runs = [(c, fl) for c in cases for fl in (0, CTRI_FLAG_NCCL_ROUNDS)]
+    for idx, ((dims, sd, bands, cyc), fl) in enumerate(runs):
         b = workloads.uniform(dims, 6 + idx)
-        plan = pdist.plan_from_process_group(dims, sd, bands, cyc, flags=CTRI_FLAG_TIMING)
+        plan = pdist.plan_from_process_group(dims, sd, bands, cyc, flags=CTRI_FLAG_TIMING | fl)
         bl = torch.from_numpy(workloads.slab(b, sd, world, rank)).to(dev)
         xl = torch.empty_like(bl)
         plan.solve(bl, xl)
@@ -49,7 +50,8 @@ def main():
             results[f"case{idx}"] = {"err": rel_err(xn, ref, sd),
                                      "res": residual(xn, b, sd, bands, cyc),
                                      "stages": st["pcr_stages"], "sends": st["sends_per_solve"],
-                                     "kernel": st["local_kernel"]}
+                                     "kernel": st["local_kernel"], "path": st["reduced_path"],
+                                     "device_error": st["device_error"]}
     # compact derivative over NCCL (halo exchange)
     dims = (128 * world, 4, 16)
     f = workloads.cfg5_field(dims, 0, 5, kappas=(1, 5, 13))

@@ -30,3 +30,4 @@ def test_nccl_partitions(world):
         assert v["err"] < 1e-12, (k, v)
         if "res" in v:
             assert v["res"] < 1e-13, (k, v)
+            assert v["device_error"] == 0, (k, v)
