@@ -345,8 +345,10 @@ def main():
         step_gbs = bytes_local / (ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": load_traffic(args.config, p),
-                "kernel": "k_tile<%d> (cluster %d)" % (st["rows_per_thread"], st["cluster_size"])
-                if st["local_kernel"] == 1 else "k_local_generic",
+                "kernel": ("k_tile<%d>%s (cluster %d)" % (st["rows_per_thread"],
+                                                          " contiguous-axis" if st["local_kernel"] == 2 else "",
+                                                          st["cluster_size"])
+                           if st["local_kernel"] in (1, 2) else "k_local_generic"),
                 "algorithmic_bytes_per_launch": bytes_local, "launch_us": t_local,
                 "peak_source": peak_src}
         cpu = None if args.no_cpu_baseline else cpu_oracle_sample(args.config)

@@ -142,7 +142,7 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   const int64_t m = P->lay.m();
   std::string why;
   if (tile_configure(*P, &why)) {
-    P->local_kernel = 1;
+    P->local_kernel = P->tile.contig ? 2 : 1;
     std::vector<double> t;
     t.insert(t.end(), P->tile.pcr.alpha.begin(), P->tile.pcr.alpha.end());
     t.insert(t.end(), P->tile.pcr.gamma.begin(), P->tile.pcr.gamma.end());
@@ -327,7 +327,7 @@ void record(Plan& P, int slot, cudaStream_t s) {
 }
 
 ctri_status local_phase(Plan& P, const double* b, double* x, cudaStream_t s) {
-  cudaError_t e = (P.local_kernel == 1) ? launch_tile(P, b, x, s) : launch_local_generic(P, b, x, s);
+  cudaError_t e = (P.local_kernel >= 1) ? launch_tile(P, b, x, s) : launch_local_generic(P, b, x, s);
   if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("local solve launch: ") + cudaGetErrorString(e));
   return CTRI_OK;
 }

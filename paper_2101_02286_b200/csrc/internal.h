@@ -58,6 +58,7 @@ struct TileConfig {
   bool ok = false;
   int variant = 0;  // index into the tile variant table (tile.cu)
   int C = 0, NT = 0, STAGES = 0, MINB = 0;  // columns per tile, threads, smem ring depth, CTAs/SM
+  bool contig = false;                      // contiguous solve axis variant
   int K = 0, G = 0, Q = 0;
   int smem_bytes = 0;
   int grid = 0;  // CTAs launched (multiple of G)

@@ -36,19 +36,24 @@
 
 namespace ctri {
 
-template <int K, int C, int NT, int STAGES, int MINB>
+template <int K, int C, int NT, int STAGES, int MINB, bool CONTIG>
 __global__ void __launch_bounds__(NT, MINB)
     k_tile(const __grid_constant__ CUtensorMap tmap, const TileArgs A, const TileConsts<K> T) {
   static_assert(K >= 4 && NT % C == 0 && (C == 4 || C == 8 || C == 16), "tile geometry");
+  static_assert(!CONTIG || (NT / C == 32 && STAGES == 1), "contiguous axis: 32 chunks per CTA");
   constexpr int CPC = NT / C;             // chunks per CTA
   constexpr int ROWS = CPC * K;           // rows per CTA
-  constexpr int PRD = 16 / C;             // rows sharing the 32 smem banks (128 B)
+  // strided axis: rows of C columns (C*8 bytes) share the 32 banks with PRD-1 other rows;
+  // contiguous axis: chunks are (K+2)*8 bytes apart, half-warps rotate by one row
+  constexpr int PRD = CONTIG ? 2 : 16 / C;
+  constexpr int CSTRIDE = K + 2;          // contiguous axis: padded chunk stride (doubles)
+  constexpr int RING = CONTIG ? C * CPC * CSTRIDE : ROWS * C;  // doubles per ring stage
   static_assert(K % PRD == 0, "K must be a multiple of the bank period");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int Q = A.Q;
   const int stages = A.stages;
   double* ring = reinterpret_cast<double*>(smem_raw);
-  double* ex_bt = ring + (size_t)STAGES * ROWS * C;  // owner: b~ of every head it owns
+  double* ex_bt = ring + (size_t)STAGES * RING;       // owner: b~ of every head it owns
   double* ex_yf = ex_bt + NT;                        // owner: y_c[first]
   double* ex_yl = ex_yf + NT;                        // owner: y_c[last]
   double* pb0 = ex_yl + NT;                          // owner: PCR ping-pong
@@ -63,8 +68,10 @@ __global__ void __launch_bounds__(NT, MINB)
   uint64_t* mbar_rx = mbar_ex + 1;
 
   const int tid = threadIdx.x;
-  const int j = tid % C;   // column within the tile
-  const int cl = tid / C;  // chunk within this CTA
+  // strided axis: lanes run over the C columns of a tile row (coalesced rows);
+  // contiguous axis: lanes run over the 32 chunks of one column, warps over columns
+  const int j = CONTIG ? tid / 32 : tid % C;   // column within the tile
+  const int cl = CONTIG ? tid % 32 : tid / C;  // chunk within this CTA
   const int G = A.G;
   const uint32_t g = (G > 1) ? dev::cluster_ctarank() : 0u;
   const int c = (int)g * CPC + cl;  // chunk index within the column (0..Q-1)
@@ -75,7 +82,7 @@ __global__ void __launch_bounds__(NT, MINB)
   const int prev_row = oj * Q + ((oc - 1) & (Q - 1));
   const int ocol = (int)g * cpo + oj;                // tile column of the owned row
   // rotation of the smem row reads so that the PRD groups of a warp hit disjoint banks
-  const int rot = ((tid & 31) / C) % PRD;
+  const int rot = CONTIG ? ((tid & 31) >> 4) : ((tid & 31) / C) % PRD;
 
   for (int i = tid; i < stages * Q; i += NT) {
     s_alpha[i] = A.pcr_alpha[i];
@@ -100,7 +107,7 @@ __global__ void __launch_bounds__(NT, MINB)
     const int o = (int)(t / A.tiles_per_outer);
     const int col0 = (int)(t - (int64_t)o * A.tiles_per_outer) * C;
     const uint32_t bar = dev::smem_u32(mbar + s);
-    double* dst = ring + (size_t)s * ROWS * C;
+    double* dst = ring + (size_t)s * RING;
     dev::fence_proxy_async();
     dev::mbar_expect_tx(bar, kTileBytes);
     for (int r = 0; r < ROWS; r += boxr)
@@ -110,9 +117,11 @@ __global__ void __launch_bounds__(NT, MINB)
   // remote addresses: my (b~, y_first, y_last) -> owner; my x~ -> holders of chunks oc, oc-1
   uint32_t r_bt = dev::smem_u32(ex_bt + slot), r_yf = dev::smem_u32(ex_yf + slot),
            r_yl = dev::smem_u32(ex_yl + slot), r_exbar = dev::smem_u32(mbar_ex);
-  const int ha = oc / CPC, ta = (oc % CPC) * C + ocol;          // holder of chunk oc
+  // holder thread of (column ocol, chunk cc): strided tid = cl*C + j, contiguous tid = j*32 + cl
+  auto holder_tid = [&](int cc) { return CONTIG ? ocol * 32 + (cc % CPC) : (cc % CPC) * C + ocol; };
+  const int ha = oc / CPC, ta = holder_tid(oc);                 // holder of chunk oc
   const int ocm = (oc - 1) & (Q - 1);
-  const int hb = ocm / CPC, tb = (ocm % CPC) * C + ocol;        // holder of chunk oc-1
+  const int hb = ocm / CPC, tb = holder_tid(ocm);               // holder of chunk oc-1
   uint32_t r_xa = dev::smem_u32(rx_a + ta), r_xb = dev::smem_u32(rx_b + tb),
            r_rxa = dev::smem_u32(mbar_rx), r_rxb = dev::smem_u32(mbar_rx);
   if (G > 1) {
@@ -126,27 +135,51 @@ __global__ void __launch_bounds__(NT, MINB)
     r_rxb = dev::mapa(r_rxb, (uint32_t)hb);
   }
 
-  if (tid == 0)
+  // contiguous axis: every thread copies 16-byte row pairs of the tile into the padded ring
+  auto issue_contig = [&](int64_t t) {
+    const int64_t gc0 = t * C;
+    for (int i = tid; i < C * (ROWS / 2); i += NT) {
+      const int jj = i / (ROWS / 2), pc = i - jj * (ROWS / 2);  // column, row pair
+      const int64_t gc = gc0 + jj;
+      const int r = 2 * pc;
+      double* d = ring + (size_t)jj * CPC * CSTRIDE + (r / K) * CSTRIDE + (r % K);
+      if (gc < A.lay.outer) dev::cp_async_16(dev::smem_u32(d), A.b + gc * A.lay.n + row0 + r);
+    }
+    dev::cp_async_commit();
+  };
+  if (CONTIG) {
+    if (first < A.num_tiles) issue_contig(first);
+  } else if (tid == 0) {
     for (int s = 0; s < STAGES; ++s)
       if (first + (int64_t)s * ncl < A.num_tiles) issue(first + (int64_t)s * ncl, s);
+  }
 
   int it = 0;
   for (int64_t t = first; t < A.num_tiles; t += ncl, ++it) {
     const int s = it % STAGES;
-    const int64_t o = t / A.tiles_per_outer;
-    const int64_t col = (t - o * A.tiles_per_outer) * C + j;
+    // global column: strided axis (o, col) with col < inner; contiguous axis column = o
+    const int64_t o = CONTIG ? t * C + j : t / A.tiles_per_outer;
+    const int64_t col = CONTIG ? 0 : (t - o * A.tiles_per_outer) * C + j;
     if (tid == 0 && A.mode != 3) {  // arm this tile's exchange barriers (remote bytes may race ahead)
       dev::mbar_expect_tx(dev::smem_u32(mbar_ex), (uint32_t)NT * 3u * 8u);
       dev::mbar_expect_tx(dev::smem_u32(mbar_rx), (uint32_t)NT * 2u * 8u);
     }
-    dev::mbar_wait(dev::smem_u32(mbar + s), (uint32_t)(it / STAGES) & 1u);
-    const double* tile = ring + (size_t)s * ROWS * C;
+    if (CONTIG) {
+      dev::cp_async_wait_all();
+      __syncthreads();
+    } else {
+      dev::mbar_wait(dev::smem_u32(mbar + s), (uint32_t)(it / STAGES) & 1u);
+    }
+    const double* tile = ring + (size_t)s * RING;
     double v[K];
 #pragma unroll
     for (int k = 0; k < K; k += PRD) {
       double a[PRD];
 #pragma unroll
-      for (int i = 0; i < PRD; ++i) a[i] = tile[(cl * K + k + ((i + rot) % PRD)) * C + j];
+      for (int i = 0; i < PRD; ++i) {
+        const int kk = k + ((i + rot) % PRD);
+        a[i] = CONTIG ? tile[(j * CPC + cl) * CSTRIDE + kk] : tile[(cl * K + kk) * C + j];
+      }
 #pragma unroll
       for (int m = 0; m < PRD; ++m) {  // a[i] holds row k + (i + rot) % PRD
         double r = a[0];
@@ -157,13 +190,25 @@ __global__ void __launch_bounds__(NT, MINB)
       }
     }
     __syncthreads();  // every thread has its chunk in registers: stage s is free
-    if (tid == 0 && t + (int64_t)STAGES * ncl < A.num_tiles) issue(t + (int64_t)STAGES * ncl, s);
-    if (A.mode == 3) {  // measurement only: the same TMA/store pipeline without the solve
-      if (col < A.lay.inner) {
-        double* xp = A.x + (o * A.lay.n + (int64_t)c * K) * A.lay.inner + col;
+    if (CONTIG) {
+      if (t + ncl < A.num_tiles) issue_contig(t + ncl);
+    } else if (tid == 0 && t + (int64_t)STAGES * ncl < A.num_tiles) {
+      issue(t + (int64_t)STAGES * ncl, s);
+    }
+    const bool valid = CONTIG ? (o < A.lay.outer) : (col < A.lay.inner);
+    auto store_chunk = [&]() {
+      if (!valid) return;
+      double* xp = A.x + (o * A.lay.n + (int64_t)c * K) * A.lay.inner + col;
+      if (CONTIG) {
+#pragma unroll
+        for (int k = 0; k < K; k += 4) dev::st_global_cs_v4(xp + k, v[k], v[k + 1], v[k + 2], v[k + 3]);
+      } else {
 #pragma unroll
         for (int k = 0; k < K; ++k) dev::st_global_cs(xp + (int64_t)k * A.lay.inner, v[k]);
       }
+    };
+    if (A.mode == 3) {  // measurement only: the same load/store pipeline without the solve
+      store_chunk();
       continue;
     }
 
@@ -215,10 +260,8 @@ __global__ void __launch_bounds__(NT, MINB)
     v[0] = (A.mode == 1 && c == 0) ? btv : xa;  // mode 1: slab row 0 keeps b~ (scratch)
 #pragma unroll
     for (int k = 1; k < K; ++k) v[k] = v[k] - T.S[k - 1] * xa - T.R[k - 1] * xb;
-    if (col < A.lay.inner) {
-      double* xp = A.x + (o * A.lay.n + (int64_t)c * K) * A.lay.inner + col;
-#pragma unroll
-      for (int k = 0; k < K; ++k) dev::st_global_cs(xp + (int64_t)k * A.lay.inner, v[k]);
+    store_chunk();
+    if (valid) {
       if (A.mode == 1) {
         const int64_t pj = o * A.lay.inner + col;
         if (c == 0) {
@@ -238,13 +281,16 @@ __global__ void __launch_bounds__(NT, MINB)
 struct Variant {
   const char* name;
   int C, NT, STAGES, MINB;
+  bool contig;  // contiguous solve axis (inner == 1): cp.async into a padded ring
 };
 static const Variant kVariants[] = {
-    {"c16t512s1", 16, 512, 1, 1},
-    {"c8t512s1", 8, 512, 1, 1},
-    {"c4t512s1", 4, 512, 1, 1},
-    {"c8t256s1", 8, 256, 1, 2},
-    {"c16t256s1", 16, 256, 1, 2},
+    {"c16t512s1", 16, 512, 1, 1, false},
+    {"c8t512s1", 8, 512, 1, 1, false},
+    {"c4t512s1", 4, 512, 1, 1, false},
+    {"c8t256s1", 8, 256, 1, 2, false},
+    {"c16t256s1", 16, 256, 1, 2, false},
+    {"c16t512s1_contig", 16, 512, 1, 1, true},
+    {"c8t256s1_contig", 8, 256, 1, 2, true},
 };
 static constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -263,10 +309,10 @@ static void fill_consts(const TileConfig& tc, TileConsts<K>* T) {
   }
 }
 
-template <int K, int C, int NT, int S, int M>
+template <int K, int C, int NT, int S, int M, bool CG>
 static cudaError_t launch_one(const TileConfig& tc, const CUtensorMap& map, const TileArgs& A,
                               cudaStream_t s, bool configure_only) {
-  auto fn = k_tile<K, C, NT, S, M>;
+  auto fn = k_tile<K, C, NT, S, M, CG>;
   if (configure_only) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc.smem_bytes);
     return e;
@@ -288,19 +334,19 @@ static cudaError_t launch_one(const TileConfig& tc, const CUtensorMap& map, cons
   return cudaLaunchKernelEx(&cfg, fn, map, A, T);
 }
 
-template <int K, int C, int NT, int S, int M>
+template <int K, int C, int NT, int S, int M, bool CG>
 static const void* fn_ptr() {
-  return reinterpret_cast<const void*>(&k_tile<K, C, NT, S, M>);
+  return reinterpret_cast<const void*>(&k_tile<K, C, NT, S, M, CG>);
 }
 
-template <int C, int NT, int S, int M>
+template <int C, int NT, int S, int M, bool CG>
 static cudaError_t dispatch_k(const TileConfig& tc, const CUtensorMap& map, const TileArgs& A,
                               cudaStream_t s, bool cfg_only, const void** fp) {
   switch (tc.K) {
 #define CTRI_K(KK)                                                       \
   case KK:                                                               \
-    if (fp) *fp = fn_ptr<KK, C, NT, S, M>();                              \
-    return fp ? cudaSuccess : launch_one<KK, C, NT, S, M>(tc, map, A, s, cfg_only);
+    if (fp) *fp = fn_ptr<KK, C, NT, S, M, CG>();                          \
+    return fp ? cudaSuccess : launch_one<KK, C, NT, S, M, CG>(tc, map, A, s, cfg_only);
     CTRI_K(4) CTRI_K(8) CTRI_K(16) CTRI_K(32)
 #undef CTRI_K
   }
@@ -310,17 +356,19 @@ static cudaError_t dispatch_k(const TileConfig& tc, const CUtensorMap& map, cons
 static cudaError_t dispatch(const TileConfig& tc, const CUtensorMap& map, const TileArgs& A,
                             cudaStream_t s, bool cfg_only, const void** fp = nullptr) {
   switch (tc.variant) {
-    case 0: return dispatch_k<16, 512, 1, 1>(tc, map, A, s, cfg_only, fp);
-    case 1: return dispatch_k<8, 512, 1, 1>(tc, map, A, s, cfg_only, fp);
-    case 2: return dispatch_k<4, 512, 1, 1>(tc, map, A, s, cfg_only, fp);
-    case 3: return dispatch_k<8, 256, 1, 2>(tc, map, A, s, cfg_only, fp);
-    case 4: return dispatch_k<16, 256, 1, 2>(tc, map, A, s, cfg_only, fp);
+    case 0: return dispatch_k<16, 512, 1, 1, false>(tc, map, A, s, cfg_only, fp);
+    case 1: return dispatch_k<8, 512, 1, 1, false>(tc, map, A, s, cfg_only, fp);
+    case 2: return dispatch_k<4, 512, 1, 1, false>(tc, map, A, s, cfg_only, fp);
+    case 3: return dispatch_k<8, 256, 1, 2, false>(tc, map, A, s, cfg_only, fp);
+    case 4: return dispatch_k<16, 256, 1, 2, false>(tc, map, A, s, cfg_only, fp);
+    case 5: return dispatch_k<16, 512, 1, 1, true>(tc, map, A, s, cfg_only, fp);
+    case 6: return dispatch_k<8, 256, 1, 2, true>(tc, map, A, s, cfg_only, fp);
   }
   return cudaErrorInvalidValue;
 }
 
 // Preference order when CTRI_TILE_VARIANT is not set: the first variant whose geometry fits n.
-static const int kPreference[] = {4, 0, 1, 3, 2};
+static const int kPreference[] = {4, 0, 1, 3, 2, 5, 6};
 
 static int forced_variant() {
   const char* e = std::getenv("CTRI_TILE_VARIANT");  // experiment knob (bench sweeps)
@@ -337,7 +385,12 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
   tc = TileConfig();
   const Layout& L = P.lay;
   const Variant& V = kVariants[vi];
-  if (L.inner < V.C || (L.inner % 2) != 0) { *why = "contiguous or narrow solve axis"; return false; }
+  if (V.contig) {
+    if (L.inner != 1 || (L.n % 2) != 0) { *why = "contiguous variant needs inner == 1, n even"; return false; }
+  } else if (L.inner < V.C || (L.inner % 2) != 0) {
+    *why = "contiguous or narrow solve axis";
+    return false;
+  }
   if (L.outer > ((int64_t)1 << 30) || L.inner > ((int64_t)1 << 31) || L.n > ((int64_t)1 << 31)) {
     *why = "dims too large for TMA coordinates";
     return false;
@@ -357,6 +410,7 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
   }
   if (!K) { *why = "n not expressible as K*G*chunks (K<=32, G<=8)"; return false; }
   tc.variant = (int)(&V - kVariants);
+  tc.contig = V.contig;
   tc.C = V.C;
   tc.NT = V.NT;
   tc.STAGES = V.STAGES;
@@ -392,7 +446,8 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
   tc.G = G;
   tc.Q = Q;
   const int rows_cta = cpc * K;
-  tc.smem_bytes = (int)(sizeof(double) * ((size_t)V.STAGES * rows_cta * V.C + 7 * (size_t)V.NT +
+  const size_t ring = V.contig ? (size_t)V.C * cpc * (K + 2) : (size_t)rows_cta * V.C;
+  tc.smem_bytes = (int)(sizeof(double) * ((size_t)V.STAGES * ring + 7 * (size_t)V.NT +
                                           (2 * (size_t)tc.pcr.stages + 1) * Q) +
                         8 * (V.STAGES + 2));
   const void* fn = nullptr;
@@ -428,8 +483,8 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
     *why = "cluster occupancy query failed";
     return false;
   }
-  const int64_t tiles_per_outer = (L.inner + V.C - 1) / V.C;
-  const int64_t num_tiles = L.outer * tiles_per_outer;
+  const int64_t num_tiles =
+      V.contig ? (L.outer + V.C - 1) / V.C : L.outer * ((L.inner + V.C - 1) / V.C);
   const int64_t ncl = std::min<int64_t>(nclusters, num_tiles);
   tc.grid = (int)(ncl * G);
   tc.ok = true;
@@ -469,6 +524,8 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   const Layout& L = P.lay;
   const int rows_cta = (tc.NT / tc.C) * tc.K;
   CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  if (!tc.contig) {
   cuuint64_t gdim[3] = {(cuuint64_t)L.inner, (cuuint64_t)L.n, (cuuint64_t)L.outer};
   cuuint64_t gstride[2] = {(cuuint64_t)L.inner * 8, (cuuint64_t)(L.n * L.inner * 8)};
   cuuint32_t box[3] = {(cuuint32_t)tc.C, (cuuint32_t)std::min(rows_cta, 256), 1};
@@ -483,12 +540,13 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, prom,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
   TileArgs A;
   A.b = b;
   A.x = x;
   A.lay = L;
-  A.tiles_per_outer = (L.inner + tc.C - 1) / tc.C;
-  A.num_tiles = L.outer * A.tiles_per_outer;
+  A.tiles_per_outer = tc.contig ? 1 : (L.inner + tc.C - 1) / tc.C;
+  A.num_tiles = tc.contig ? (L.outer + tc.C - 1) / tc.C : L.outer * A.tiles_per_outer;
   A.Q = tc.Q;
   A.G = tc.G;
   A.rows_per_cta = rows_cta;

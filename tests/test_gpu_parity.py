@@ -45,7 +45,11 @@ def test_cfg1_tile_and_generic():
     ((96, 4, 20), 0, 0),        # n = 96: not K*G*32 -> column-serial
     ((256, 3, 40), 0, 1),       # ragged batch: inner = 120 (7.5 tiles)
     ((8, 512, 32), 1, 1),       # solve along index 1 (strided 2 KiB rows)
-    ((4, 6, 256), 2, 0),        # contiguous solve axis -> column-serial
+    ((4, 6, 256), 2, 2),        # contiguous solve axis -> cp.async tile variant
+    ((3, 7, 512), 2, 2),        # contiguous axis, ragged batch (21 columns)
+    ((2, 40, 1024), 2, 2),      # contiguous axis, K=32, G=1
+    ((1, 16, 8192), 2, 2),      # contiguous axis, benchmark column length (cluster)
+    ((2, 3, 96), 2, 0),         # contiguous axis, n = 96 -> column-serial
     ((1024, 2, 16), 0, 1),      # K=32, G=1
     ((2048, 1, 32), 0, 1),      # K=32, G=2 (cluster, DSMEM)
     ((8192, 1, 16), 0, 1),      # K=32, G=8: the benchmark column length
