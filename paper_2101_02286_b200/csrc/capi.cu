@@ -326,8 +326,11 @@ void record(Plan& P, int slot, cudaStream_t s) {
   if (!P.ev.empty()) cudaEventRecord(P.ev[slot], s);
 }
 
-ctri_status local_phase(Plan& P, const double* b, double* x, cudaStream_t s) {
-  cudaError_t e = (P.local_kernel >= 1) ? launch_tile(P, b, x, s) : launch_local_generic(P, b, x, s);
+// (a1) local solve; with `deriv` the tile kernel reads f and forms the stencil RHS itself (a0).
+ctri_status local_phase(Plan& P, const double* b, double* x, cudaStream_t s, bool deriv = false,
+                        double ca = 0.0, double cb = 0.0) {
+  cudaError_t e = (P.local_kernel >= 1) ? launch_tile(P, b, x, s, deriv, ca, cb)
+                                        : launch_local_generic(P, b, x, s);
   if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("local solve launch: ") + cudaGetErrorString(e));
   return CTRI_OK;
 }
@@ -346,7 +349,7 @@ ctri_status stage_kernel(Plan& P, int k, cudaStream_t s) {
 
 // The whole solve for a set of co-scheduled plans: one plan (NCCL) or a loopback group.
 ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* const* x,
-                        cudaStream_t s) {
+                        cudaStream_t s, bool deriv = false, double ca = 0.0, double cb = 0.0) {
   const bool nccl = !G[0]->loopback;
   Plan& P0 = *G[0];
   for (size_t r = 0; r < G.size(); ++r) {
@@ -356,7 +359,7 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
   }
   for (Plan* P : G) P->solves++;
   record(P0, EV_START, s);
-  for (size_t r = 0; r < G.size(); ++r) TRY(local_phase(*G[r], b[r], x[r], s));
+  for (size_t r = 0; r < G.size(); ++r) TRY(local_phase(*G[r], b[r], x[r], s, deriv, ca, cb));
   record(P0, EV_LOCAL, s);
   if (P0.p == 1) return CTRI_OK;
   if (P0.p2p) {  // fused device-initiated (a2)-(a4)
@@ -443,14 +446,20 @@ ctri_status deriv_group(std::vector<Plan*>& G, const double* const* f, double* c
     if (!f[r] || !df[r] || f[r] == df[r]) return fail(CTRI_ERR_INVALID_ARG, "f/df NULL or aliased");
     if (h == 0.0 || !std::isfinite(h)) return fail(CTRI_ERR_INVALID_ARG, "bad h");
   }
-  if (G[0]->p > 1) {
+  bool fused = true;
+  for (Plan* P : G) fused = fused && P->local_kernel == 1 && P->tile.deriv_ok;
+  if (G[0]->p > 1 || fused) {  // halo planes (with one partition: the slab's own wrap rows)
     for (size_t r = 0; r < G.size(); ++r) {
       cudaError_t e = launch_pack_halo(*G[r], f[r], s);
       if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, cudaGetErrorString(e));
     }
+  }
+  if (G[0]->p > 1) {
     if (!G[0]->loopback) TRY(exchange_nccl(*G[0], round_halo(*G[0]), s));
     else TRY(exchange_loopback(G, [](Plan& P) { return round_halo(P); }, s));
   }
+  if (fused)  // (a0) fused into (a1): f read once, df written once
+    return solve_group(G, f, df, s, true, a / (2.0 * h), bc / (4.0 * h));
   for (size_t r = 0; r < G.size(); ++r) {
     cudaError_t e = launch_stencil(*G[r], f[r], df[r], a, bc, h, s);
     if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, cudaGetErrorString(e));

@@ -19,8 +19,8 @@ constexpr int kMaxClusterNonPortable = 16;  // opt-in (cudaFuncAttributeNonPorta
 // Layout of a local slab viewed as (outer, n, inner): element (o, r, c) at (o*n + r)*inner + c.
 struct Layout {
   int64_t outer = 1, n = 0, inner = 1;
-  int64_t m() const { return outer * inner; }
-  int64_t elems() const { return outer * n * inner; }
+  __host__ __device__ int64_t m() const { return outer * inner; }
+  __host__ __device__ int64_t elems() const { return outer * n * inner; }
 };
 
 // Parameters of the cluster-tile kernel that live in the kernel's constant bank.
@@ -52,6 +52,10 @@ struct TileArgs {
   double* plane_yf;  // mode 1: y_D at interior row 1
   double* plane_yl;  // mode 1: y_D at row n-1
   double* plane_bt;  // mode 1: b at row 0 (b~_i)
+  // fused compact-derivative stencil (LAYOUT 2): b = ca (f_{+1} - f_{-1}) + cb (f_{+2} - f_{-2})
+  double ca, cb;
+  const double* halo_lo;  // [2][m]: rows n-2, n-1 of the slab above
+  const double* halo_hi;  // [2][m]: rows 0, 1 of the slab below
 };
 
 struct TileConfig {
@@ -62,6 +66,8 @@ struct TileConfig {
   int K = 0, G = 0, Q = 0;
   int smem_bytes = 0;
   int grid = 0;  // CTAs launched (multiple of G)
+  bool deriv_ok = false;               // fused-stencil instantiation configured
+  int smem_deriv = 0, grid_deriv = 0;
   std::vector<double> consts;  // serialized TileConsts<K> (l, u, then 4 tables of K-1)
   PcrTables pcr;
   double* d_pcr = nullptr;     // device: alpha | gamma | inv
@@ -161,6 +167,7 @@ cudaError_t launch_stencil(const Plan& P, const double* f, double* rhs, double a
                            double h, cudaStream_t s);
 bool tile_configure(Plan& P, std::string* why);
 const char* tile_variant_name(int v);
-cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t s);
+cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t s,
+                        bool deriv = false, double ca = 0.0, double cb = 0.0);
 
 }  // namespace ctri

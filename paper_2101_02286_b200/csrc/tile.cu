@@ -36,9 +36,15 @@
 
 namespace ctri {
 
-template <int K, int C, int NT, int STAGES, int MINB, bool CONTIG>
+template <int K, int C, int NT, int STAGES, int MINB, int LAYOUT>
 __global__ void __launch_bounds__(NT, MINB)
-    k_tile(const __grid_constant__ CUtensorMap tmap, const TileArgs A, const TileConsts<K> T) {
+    k_tile(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap hmap,
+           const TileArgs A, const TileConsts<K> T) {
+  // LAYOUT 0: strided solve axis; 1: contiguous solve axis; 2: strided + fused compact-derivative
+  // RHS stencil (a0): the kernel reads f, forms b in registers and never writes it
+  constexpr bool CONTIG = (LAYOUT == 1);
+  constexpr bool DERIV = (LAYOUT == 2);
+  constexpr int HALO = DERIV ? 2 : 0;     // stencil half-width (rows)
   static_assert(K >= 4 && NT % C == 0 && (C == 4 || C == 8 || C == 16), "tile geometry");
   static_assert(!CONTIG || (NT / C == 32 && STAGES == 1), "contiguous axis: 32 chunks per CTA");
   constexpr int CPC = NT / C;             // chunks per CTA
@@ -47,7 +53,7 @@ __global__ void __launch_bounds__(NT, MINB)
   // contiguous axis: chunks are (K+2)*8 bytes apart, half-warps rotate by one row
   constexpr int PRD = CONTIG ? 2 : 16 / C;
   constexpr int CSTRIDE = K + 2;          // contiguous axis: padded chunk stride (doubles)
-  constexpr int RING = CONTIG ? C * CPC * CSTRIDE : ROWS * C;  // doubles per ring stage
+  constexpr int RING = CONTIG ? C * CPC * CSTRIDE : (ROWS + 2 * HALO) * C;  // doubles per stage
   static_assert(K % PRD == 0, "K must be a multiple of the bank period");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int Q = A.Q;
@@ -98,7 +104,7 @@ __global__ void __launch_bounds__(NT, MINB)
 
   const uint32_t ncl = (G > 1) ? dev::ncluster_x() : gridDim.x;
   const int64_t first = (G > 1) ? (int64_t)dev::cluster_id_x() : (int64_t)blockIdx.x;
-  constexpr uint32_t kTileBytes = (uint32_t)ROWS * C * (uint32_t)sizeof(double);
+  constexpr uint32_t kTileBytes = (uint32_t)(ROWS + 2 * HALO) * C * (uint32_t)sizeof(double);
   const int boxr = A.rows_box;
   const int row0 = (int)g * ROWS;
   const uint64_t pol = dev::policy_evict_first();
@@ -111,7 +117,12 @@ __global__ void __launch_bounds__(NT, MINB)
     dev::fence_proxy_async();
     dev::mbar_expect_tx(bar, kTileBytes);
     for (int r = 0; r < ROWS; r += boxr)
-      dev::tma_load_3d(dev::smem_u32(dst + (size_t)r * C), &tmap, col0, row0 + r, o, bar, pol);
+      dev::tma_load_3d(dev::smem_u32(dst + (size_t)(r + HALO) * C), &tmap, col0, row0 + r, o, bar, pol);
+    if (DERIV) {  // stencil halo rows row0-2, row0-1 and row0+ROWS, +1 (zero-filled outside the slab)
+      dev::tma_load_3d(dev::smem_u32(dst), &hmap, col0, row0 - HALO, o, bar, pol);
+      dev::tma_load_3d(dev::smem_u32(dst + (size_t)(ROWS + HALO) * C), &hmap, col0, row0 + ROWS, o,
+                       bar, pol);
+    }
   };
 
   // remote addresses: my (b~, y_first, y_last) -> owner; my x~ -> holders of chunks oc, oc-1
@@ -170,10 +181,25 @@ __global__ void __launch_bounds__(NT, MINB)
     } else {
       dev::mbar_wait(dev::smem_u32(mbar + s), (uint32_t)(it / STAGES) & 1u);
     }
-    const double* tile = ring + (size_t)s * RING;
-    double v[K];
+    double* tile = ring + (size_t)s * RING;
+    if (DERIV) {
+      // slab-edge CTAs: the halo rows outside the slab come from the neighbour slabs (halo planes)
+      const int64_t oo = t / A.tiles_per_outer;
+      const int64_t cc0 = (t - oo * A.tiles_per_outer) * C;
+      if (g == 0 && tid < HALO * C) {
+        const int64_t cc = cc0 + (tid % C);
+        if (cc < A.lay.inner) tile[(tid / C) * C + tid % C] = A.halo_lo[(tid / C) * A.lay.m() + oo * A.lay.inner + cc];
+      }
+      if ((int)g == G - 1 && tid < HALO * C) {
+        const int64_t cc = cc0 + (tid % C);
+        if (cc < A.lay.inner)
+          tile[(ROWS + HALO + tid / C) * C + tid % C] = A.halo_hi[(tid / C) * A.lay.m() + oo * A.lay.inner + cc];
+      }
+      __syncthreads();
+    }
+    double v[K + 2 * HALO];
 #pragma unroll
-    for (int k = 0; k < K; k += PRD) {
+    for (int k = 0; k < K + 2 * HALO; k += PRD) {
       double a[PRD];
 #pragma unroll
       for (int i = 0; i < PRD; ++i) {
@@ -188,6 +214,10 @@ __global__ void __launch_bounds__(NT, MINB)
           if ((i + rot) % PRD == m) r = a[i];
         v[k + m] = r;
       }
+    }
+    if (DERIV) {  // b_k = a (f_{k+1} - f_{k-1}) / 2h + bc (f_{k+2} - f_{k-2}) / 4h, in place
+#pragma unroll
+      for (int k = 0; k < K; ++k) v[k] = A.ca * (v[k + 3] - v[k + 1]) + A.cb * (v[k + 4] - v[k]);
     }
     __syncthreads();  // every thread has its chunk in registers: stage s is free
     if (CONTIG) {
@@ -309,10 +339,10 @@ static void fill_consts(const TileConfig& tc, TileConsts<K>* T) {
   }
 }
 
-template <int K, int C, int NT, int S, int M, bool CG>
-static cudaError_t launch_one(const TileConfig& tc, const CUtensorMap& map, const TileArgs& A,
-                              cudaStream_t s, bool configure_only) {
-  auto fn = k_tile<K, C, NT, S, M, CG>;
+template <int K, int C, int NT, int S, int M, int LY>
+static cudaError_t launch_one(const TileConfig& tc, const CUtensorMap& map, const CUtensorMap& hmap,
+                              const TileArgs& A, cudaStream_t s, bool configure_only) {
+  auto fn = k_tile<K, C, NT, S, M, LY>;
   if (configure_only) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc.smem_bytes);
     return e;
@@ -320,9 +350,9 @@ static cudaError_t launch_one(const TileConfig& tc, const CUtensorMap& map, cons
   TileConsts<K> T;
   fill_consts<K>(tc, &T);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(tc.grid, 1, 1);
+  cfg.gridDim = dim3(LY == 2 ? tc.grid_deriv : tc.grid, 1, 1);
   cfg.blockDim = dim3(NT, 1, 1);
-  cfg.dynamicSmemBytes = tc.smem_bytes;
+  cfg.dynamicSmemBytes = LY == 2 ? tc.smem_deriv : tc.smem_bytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -331,39 +361,49 @@ static cudaError_t launch_one(const TileConfig& tc, const CUtensorMap& map, cons
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, fn, map, A, T);
+  return cudaLaunchKernelEx(&cfg, fn, map, hmap, A, T);
 }
 
-template <int K, int C, int NT, int S, int M, bool CG>
+template <int K, int C, int NT, int S, int M, int LY>
 static const void* fn_ptr() {
-  return reinterpret_cast<const void*>(&k_tile<K, C, NT, S, M, CG>);
+  return reinterpret_cast<const void*>(&k_tile<K, C, NT, S, M, LY>);
 }
 
-template <int C, int NT, int S, int M, bool CG>
-static cudaError_t dispatch_k(const TileConfig& tc, const CUtensorMap& map, const TileArgs& A,
-                              cudaStream_t s, bool cfg_only, const void** fp) {
+template <int C, int NT, int S, int M, int LY>
+static cudaError_t dispatch_k(const TileConfig& tc, const CUtensorMap& map, const CUtensorMap& hmap,
+                              const TileArgs& A, cudaStream_t s, bool cfg_only, const void** fp) {
   switch (tc.K) {
 #define CTRI_K(KK)                                                       \
   case KK:                                                               \
-    if (fp) *fp = fn_ptr<KK, C, NT, S, M, CG>();                          \
-    return fp ? cudaSuccess : launch_one<KK, C, NT, S, M, CG>(tc, map, A, s, cfg_only);
+    if (fp) *fp = fn_ptr<KK, C, NT, S, M, LY>();                          \
+    return fp ? cudaSuccess : launch_one<KK, C, NT, S, M, LY>(tc, map, hmap, A, s, cfg_only);
     CTRI_K(4) CTRI_K(8) CTRI_K(16) CTRI_K(32)
 #undef CTRI_K
   }
   return cudaErrorInvalidValue;
 }
 
-static cudaError_t dispatch(const TileConfig& tc, const CUtensorMap& map, const TileArgs& A,
-                            cudaStream_t s, bool cfg_only, const void** fp = nullptr) {
-  switch (tc.variant) {
-    case 0: return dispatch_k<16, 512, 1, 1, false>(tc, map, A, s, cfg_only, fp);
-    case 1: return dispatch_k<8, 512, 1, 1, false>(tc, map, A, s, cfg_only, fp);
-    case 2: return dispatch_k<4, 512, 1, 1, false>(tc, map, A, s, cfg_only, fp);
-    case 3: return dispatch_k<8, 256, 1, 2, false>(tc, map, A, s, cfg_only, fp);
-    case 4: return dispatch_k<16, 256, 1, 2, false>(tc, map, A, s, cfg_only, fp);
-    case 5: return dispatch_k<16, 512, 1, 1, true>(tc, map, A, s, cfg_only, fp);
-    case 6: return dispatch_k<8, 256, 1, 2, true>(tc, map, A, s, cfg_only, fp);
+static cudaError_t dispatch(const TileConfig& tc, bool deriv, const CUtensorMap& map,
+                            const CUtensorMap& hmap, const TileArgs& A, cudaStream_t s,
+                            bool cfg_only, const void** fp = nullptr) {
+#define CTRI_V(C, NT, S, M, LY) return dispatch_k<C, NT, S, M, LY>(tc, map, hmap, A, s, cfg_only, fp)
+  if (deriv) {  // fused stencil: strided 16-column variants only
+    switch (tc.variant) {
+      case 0: CTRI_V(16, 512, 1, 1, 2);
+      case 4: CTRI_V(16, 256, 1, 2, 2);
+    }
+    return cudaErrorInvalidValue;
   }
+  switch (tc.variant) {
+    case 0: CTRI_V(16, 512, 1, 1, 0);
+    case 1: CTRI_V(8, 512, 1, 1, 0);
+    case 2: CTRI_V(4, 512, 1, 1, 0);
+    case 3: CTRI_V(8, 256, 1, 2, 0);
+    case 4: CTRI_V(16, 256, 1, 2, 0);
+    case 5: CTRI_V(16, 512, 1, 1, 1);
+    case 6: CTRI_V(8, 256, 1, 2, 1);
+  }
+#undef CTRI_V
   return cudaErrorInvalidValue;
 }
 
@@ -450,43 +490,55 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
   tc.smem_bytes = (int)(sizeof(double) * ((size_t)V.STAGES * ring + 7 * (size_t)V.NT +
                                           (2 * (size_t)tc.pcr.stages + 1) * Q) +
                         8 * (V.STAGES + 2));
-  const void* fn = nullptr;
-  CUtensorMap dummy;
-  TileArgs dA;
-  dispatch(tc, dummy, dA, 0, true, &fn);
-  if (!fn || cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc.smem_bytes) !=
-                 cudaSuccess) {
-    cudaGetLastError();
-    *why = "cudaFuncSetAttribute(smem) failed";
-    return false;
+  // configure one instantiation (solve, or the fused-stencil one): smem attribute + grid
+  auto setup = [&](bool deriv, int smem, int* grid_out) -> bool {
+    const void* fn = nullptr;
+    CUtensorMap dummy;
+    TileArgs dA;
+    dispatch(tc, deriv, dummy, dummy, dA, 0, true, &fn);
+    if (!fn || cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+      cudaGetLastError();
+      *why = "cudaFuncSetAttribute(smem) failed";
+      return false;
+    }
+    if (G > kMaxCluster &&
+        cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+      cudaGetLastError();
+      *why = "non-portable cluster size refused";
+      return false;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G, 1, 1);
+    cfg.blockDim = dim3(V.NT, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = G;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) != cudaSuccess || nclusters < 1) {
+      cudaGetLastError();
+      *why = "cluster occupancy query failed";
+      return false;
+    }
+    const int64_t num_tiles =
+        V.contig ? (L.outer + V.C - 1) / V.C : L.outer * ((L.inner + V.C - 1) / V.C);
+    *grid_out = (int)(std::min<int64_t>(nclusters, num_tiles) * G);
+    return true;
+  };
+  if (!setup(false, tc.smem_bytes, &tc.grid)) return false;
+  // fused-stencil instantiation (ctri_deriv): 4 extra ring rows per stage
+  tc.deriv_ok = false;
+  if (!V.contig && V.C == 16 && (P.flags & CTRI_FLAG_DERIV)) {
+    tc.smem_deriv = tc.smem_bytes + (int)(sizeof(double) * 4 * V.C * V.STAGES);
+    std::string w2;
+    std::swap(w2, *why);
+    tc.deriv_ok = setup(true, tc.smem_deriv, &tc.grid_deriv);
+    std::swap(w2, *why);
   }
-  if (G > kMaxCluster &&
-      cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
-    cudaGetLastError();
-    *why = "non-portable cluster size refused";
-    return false;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(G, 1, 1);
-  cfg.blockDim = dim3(V.NT, 1, 1);
-  cfg.dynamicSmemBytes = tc.smem_bytes;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = G;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int nclusters = 0;
-  if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) != cudaSuccess || nclusters < 1) {
-    cudaGetLastError();
-    *why = "cluster occupancy query failed";
-    return false;
-  }
-  const int64_t num_tiles =
-      V.contig ? (L.outer + V.C - 1) / V.C : L.outer * ((L.inner + V.C - 1) / V.C);
-  const int64_t ncl = std::min<int64_t>(nclusters, num_tiles);
-  tc.grid = (int)(ncl * G);
   tc.ok = true;
   return true;
 }
@@ -517,29 +569,39 @@ static EncodeTiledFn get_encode() {
   return fn;
 }
 
-cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t s) {
+cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t s, bool deriv,
+                        double ca, double cb) {
   const TileConfig& tc = P.tile;
+  if (deriv && !tc.deriv_ok) return cudaErrorNotSupported;
   EncodeTiledFn enc = get_encode();
   if (!enc) return cudaErrorNotSupported;
   const Layout& L = P.lay;
   const int rows_cta = (tc.NT / tc.C) * tc.K;
-  CUtensorMap map;
+  CUtensorMap map, hmap;
   std::memset(&map, 0, sizeof(map));
+  std::memset(&hmap, 0, sizeof(hmap));
   if (!tc.contig) {
-  cuuint64_t gdim[3] = {(cuuint64_t)L.inner, (cuuint64_t)L.n, (cuuint64_t)L.outer};
-  cuuint64_t gstride[2] = {(cuuint64_t)L.inner * 8, (cuuint64_t)(L.n * L.inner * 8)};
-  cuuint32_t box[3] = {(cuuint32_t)tc.C, (cuuint32_t)std::min(rows_cta, 256), 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUtensorMapL2promotion prom = CU_TENSOR_MAP_L2_PROMOTION_NONE;
-  if (const char* e = std::getenv("CTRI_TMA_L2_PROMOTION")) {  // measurement knob
-    if (!std::strcmp(e, "64")) prom = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
-    if (!std::strcmp(e, "128")) prom = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-    if (!std::strcmp(e, "256")) prom = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-  }
-  CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(b), gdim, gstride,
-                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, prom,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    cuuint64_t gdim[3] = {(cuuint64_t)L.inner, (cuuint64_t)L.n, (cuuint64_t)L.outer};
+    cuuint64_t gstride[2] = {(cuuint64_t)L.inner * 8, (cuuint64_t)(L.n * L.inner * 8)};
+    cuuint32_t box[3] = {(cuuint32_t)tc.C, (cuuint32_t)std::min(rows_cta, 256), 1};
+    cuuint32_t hbox[3] = {(cuuint32_t)tc.C, 2, 1};  // stencil halo rows (fused derivative)
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUtensorMapL2promotion prom = CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    if (const char* e = std::getenv("CTRI_TMA_L2_PROMOTION")) {  // measurement knob
+      if (!std::strcmp(e, "64")) prom = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+      if (!std::strcmp(e, "128")) prom = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+      if (!std::strcmp(e, "256")) prom = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }
+    CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(b), gdim,
+                      gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, prom, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    if (deriv) {
+      cr = enc(&hmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(b), gdim, gstride,
+               hbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, prom,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
   }
   TileArgs A;
   A.b = b;
@@ -560,7 +622,13 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   A.plane_yf = P.yf;
   A.plane_yl = P.yl;
   A.plane_bt = P.bt;
-  return dispatch(tc, map, A, s, false);
+  A.ca = ca;
+  A.cb = cb;
+  // halo planes: rows n-2, n-1 of the slab above and rows 0, 1 of the slab below; with one
+  // partition they are this slab's own rows (periodic wrap), packed into send_hi / send_lo
+  A.halo_lo = (P.p == 1) ? P.send_hi : P.halo_lo;
+  A.halo_hi = (P.p == 1) ? P.send_lo : P.halo_hi;
+  return dispatch(tc, deriv, map, hmap, A, s, false);
 }
 
 }  // namespace ctri

@@ -183,39 +183,52 @@ def test_direction_permutation():
     assert rel_err(np.transpose(x2, (2, 0, 1)), x0, 0) < 1e-14
 
 
-@pytest.mark.parametrize("p", [1, 2, 4])
-def test_deriv_matches_oracle_and_wavenumber(p):
+@pytest.mark.parametrize("p,shape,sd,generic", [
+    (1, (1024, 2, 16), 0, False), (2, (1024, 2, 16), 0, False), (4, (1024, 2, 16), 0, False),
+    (1, (2048, 3, 16), 0, False),   # fused stencil + solve across a 4-CTA cluster
+    (1, (8192, 1, 16), 0, False),   # 16-CTA cluster, slab-edge halos from the wrap rows
+    (2, (4, 1024, 32), 1, False),   # index 1
+    (8, (1024, 4, 16), 0, False),
+    (1, (1024, 2, 16), 0, True), (4, (1024, 2, 16), 0, True),  # unfused stencil + solve
+    (2, (2, 3, 512), 2, False),     # contiguous axis: unfused stencil + contiguous tile solve
+])
+def test_deriv_matches_oracle_and_wavenumber(p, shape, sd, generic):
     import torch
 
-    from paper_2101_02286_b200 import CTRI_FLAG_DERIV, ctri
-    N = 1024
-    shape = (N, 2, 16)
-    f = workloads.cfg5_field(shape, 0, 5)
-    ref = oracle.deriv(f, 0)
+    from paper_2101_02286_b200 import CTRI_FLAG_DERIV, CTRI_FLAG_GENERIC_LOCAL, ctri
+    N = shape[sd]
+    flags = CTRI_FLAG_DERIV | (CTRI_FLAG_GENERIC_LOCAL if generic else 0)
+    f = workloads.cfg5_field(shape, sd, 5)
+    ref = oracle.deriv(f, sd)
     dev = torch.device("cuda:0")
-    fs = [torch.from_numpy(workloads.slab(f, 0, p, r)).to(dev) for r in range(p)]
+    fs = [torch.from_numpy(workloads.slab(f, sd, p, r)).to(dev) for r in range(p)]
     ds = [torch.empty_like(t) for t in fs]
     if p == 1:
-        plan = ctri.Plan(shape, 0, 1, 0, flags=CTRI_FLAG_DERIV)
+        plan = ctri.Plan(shape, sd, 1, 0, flags=flags)
         plan.deriv(fs[0], ds[0])
         torch.cuda.synchronize()
         plan.close()
     else:
-        g = ctri.LoopbackGroup(shape, 0, p, flags=CTRI_FLAG_DERIV)
+        g = ctri.LoopbackGroup(shape, sd, p, flags=flags)
         g.deriv(fs, ds)
         torch.cuda.synchronize()
         g.close()
-    df = workloads.assemble([t.cpu().numpy() for t in ds], 0)
-    assert rel_err(df, ref, 0) < 1e-12
+    df = workloads.assemble([t.cpu().numpy() for t in ds], sd)
+    assert rel_err(df, ref, sd) < 1e-12
     # closed form: sum_k A_k k'(kappa) cos(kappa x + phi)
-    amps, ph = workloads.cfg5_modes(shape, 0, 5)
+    amps, ph = workloads.cfg5_modes(shape, sd, 5)
     h = 2 * math.pi / N
-    x = (2 * math.pi * np.arange(N) / N)[:, None, None]
+    sh = [1, 1, 1]
+    sh[sd] = N
+    x = (2 * math.pi * np.arange(N) / N).reshape(sh)
     expect = np.zeros(shape)
     for q, kap in enumerate(workloads.CFG5_KAPPAS):
+        if kap >= N // 2:
+            continue
         kp = (14 / 9 * math.sin(kap * h) + 1 / 18 * math.sin(2 * kap * h)) / (1 + 2 / 3 * math.cos(kap * h)) / h
-        expect += amps[q][None] * kp * np.cos(kap * x + ph[q][None])
-    assert np.max(np.abs(df - expect)) < 1e-9 * np.max(np.abs(expect))
+        expect += np.expand_dims(amps[q], sd) * kp * np.cos(kap * x + np.expand_dims(ph[q], sd))
+    if all(k < N // 2 for k in workloads.CFG5_KAPPAS):
+        assert np.max(np.abs(df - expect)) < 1e-9 * np.max(np.abs(expect))
 
 
 def test_solve_host_e2e():
