@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--config", default="cfg2",
                     choices=["cfg1", "cfg2", "cfg3", "cfg4_d1", "cfg4_d2", "cfg5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dims", default=None, help="override: global dims N0,N1,N2 (measurement)")
+    ap.add_argument("--sd", type=int, default=0, help="solve dim with --dims")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -250,6 +252,10 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     p = world
     dims, sd, name = workload(args.config, p)
+    if args.dims:
+        dims = tuple(int(v) for v in args.dims.split(","))
+        sd = args.sd
+        name = f"custom {dims} solve index {sd}"
     deriv = args.config == "cfg5"
     flags = CTRI_FLAG_TIMING | (CTRI_FLAG_DERIV if deriv else 0)
     if world > 1:

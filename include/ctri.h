@@ -95,6 +95,9 @@ typedef struct ctri_stats {
   int32_t reduced_path;         /* nparts > 1: 0 = NCCL rounds, 1 = fused P2P kernel (t_backsub_us
                                    then times the whole fused (a2)-(a4) kernel) */
   int32_t device_error;         /* nonzero: a P2P wait hit its deadline (peer missing) */
+  int32_t vparts;               /* nparts == 1: partitions of the slab solved on this GPU (the
+                                   paper's partition method; (a2)-(a4) then run on-device) */
+  int32_t grid_ctas;            /* CTAs of the local-solve launch */
 } ctri_stats;
 
 /* Human-readable status name; never NULL. */

@@ -118,19 +118,34 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   CUDA_TRY(cudaGetDevice(&P->device));
   CUDA_TRY(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device));
 
+  // virtual partitions (nparts == 1): the slab is solved as vp partitions of n/vp rows so the
+  // local-solve clusters are small enough to occupy every GPC
+  P->vp = 1;
+  if (p == 1 && !(flags & CTRI_FLAG_DERIV) && P->lay.inner >= 16) {  // strided axis only
+    // measured: virtual slabs of 1024 rows (clusters of 4) are fastest for n >= 4096
+    int want = n >= 4096 ? (int)std::min<int64_t>(8, n / 1024) : 1;
+    if (const char* e = std::getenv("CTRI_VPARTS")) want = std::atoi(e);  // measurement knob
+    if (want > 1 && want <= 8 && is_pow2(want) && n % want == 0 && n / want >= 512) P->vp = want;
+  }
+  P->tlay = P->lay;
+  P->tlay.outer = P->lay.outer * P->vp;
+  P->tlay.n = n / P->vp;
+  const int64_t nv = P->tlay.n;
+  const int pr = (p > 1) ? p : P->vp;  // rows of the reduced system
+
   // ---- pre-factorisation ----
   FactorError fe;
-  if (!partition_factor(n - 1, P->bands, &P->part, &fe)) return fail((ctri_status)fe.code, fe.detail);
+  if (!partition_factor(nv - 1, P->bands, &P->part, &fe)) return fail((ctri_status)fe.code, fe.detail);
   const Partition& pt = P->part;
-  const int64_t last = n - 2;
-  std::vector<double> L(p), D(p), U(p);
-  for (int i = 0; i < p; ++i) {
-    const bool lft = cyclic || i > 0, rgt = cyclic || i < p - 1;
+  const int64_t last = nv - 2;
+  std::vector<double> L(pr), D(pr), U(pr);
+  for (int i = 0; i < pr; ++i) {
+    const bool lft = cyclic || i > 0, rgt = cyclic || i < pr - 1;
     L[i] = lft ? -P->bands.l * pt.S[last] : 0.0;                                 // Eq. Li_hat
     D[i] = P->bands.d - (lft ? P->bands.l * pt.R[last] : 0.0) - P->bands.u * pt.S[0];  // Eq. Di_hat
     U[i] = rgt ? -P->bands.u * pt.R[0] : 0.0;                                    // Eq. Ui_hat
   }
-  if (!pcr_factor(p, cyclic != 0, L, D, U, pivot_threshold(P->bands), &P->gpcr, &fe))
+  if (!pcr_factor(pr, cyclic != 0, L, D, U, pivot_threshold(P->bands), &P->gpcr, &fe))
     return fail((ctri_status)fe.code, fe.detail);
   if (P->gpcr.stages > CTRI_MAX_STAGES) return fail(CTRI_ERR_UNSUPPORTED, "too many PCR stages");
   P->inv_closure = P->gpcr.inv[0];
@@ -153,10 +168,10 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
     TRY(upload(&P->d_cp, pt.th.cp, s));
     TRY(upload(&P->d_inv_den, pt.th.inv_den, s));
   }
-  if (p > 1) {
+  if (p > 1 || P->vp > 1) {
     double** planes[] = {&P->yf, &P->yl, &P->bt, &P->yl_prev, &P->bh, &P->recv_m, &P->recv_p,
                          &P->xt, &P->xt_next};
-    for (double** pl : planes) TRY(alloc_plane(pl, m));
+    for (double** pl : planes) TRY(alloc_plane(pl, m * P->vp));
   }
   if (p > 1 && p <= kMaxP2PRanks && !(flags & CTRI_FLAG_NCCL_ROUNDS)) {
     // fused device-initiated reduced phase: double-buffered mailbox + epoch flags
@@ -183,6 +198,7 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   // launches per solve
   int launches = 1;
   if (p > 1) launches += P->p2p ? 1 : 1 /*bhat*/ + P->gpcr.stages + 1 /*backsub*/;
+  if (p == 1 && P->vp > 1) launches += 1;  // local reduced system + window back-substitution
   P->launches_per_solve = launches;
   CUDA_TRY(cudaStreamSynchronize(s));
   return CTRI_OK;
@@ -361,7 +377,17 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
   record(P0, EV_START, s);
   for (size_t r = 0; r < G.size(); ++r) TRY(local_phase(*G[r], b[r], x[r], s, deriv, ca, cb));
   record(P0, EV_LOCAL, s);
-  if (P0.p == 1) return CTRI_OK;
+  if (P0.p == 1) {
+    if (P0.vp > 1) {  // (a2)-(a4) across the virtual partitions of this slab
+      for (size_t r = 0; r < G.size(); ++r) {
+        cudaError_t e = launch_reduced_local(*G[r], x[r], s);
+        if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("local reduced: ") + cudaGetErrorString(e));
+      }
+      record(P0, EV_BACK, s);
+      for (Plan* P : G) P->timed_valid = !P->ev.empty();
+    }
+    return CTRI_OK;
+  }
   if (P0.p2p) {  // fused device-initiated (a2)-(a4)
     P2PArgs A;
     std::memset(&A, 0, sizeof(A));
@@ -636,11 +662,13 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
   out->tile_variant = P->local_kernel ? P->tile.variant : -1;
   out->tile_stages = P->local_kernel ? P->tile.STAGES : 0;
   out->reduced_path = (P->p > 1 && P->p2p) ? 1 : 0;
+  out->vparts = P->vp;
+  out->grid_ctas = P->local_kernel ? P->tile.grid : (int32_t)((P->tlay.m() + 127) / 128);
   out->device_error = 0;
   if (P->d_err) CUDA_TRY(cudaMemcpy(&out->device_error, P->d_err, sizeof(int), cudaMemcpyDeviceToHost));
   out->chunk_heads = P->local_kernel ? P->tile.Q : 1;
-  const bool full = (P->flags & CTRI_FLAG_FULL_BACKSUB) || (2 * P->window >= P->lay.n - 1);
-  out->window_rows = (int32_t)(full ? P->lay.n - 1 : P->window);
+  const bool full = (P->flags & CTRI_FLAG_FULL_BACKSUB) || (2 * P->window >= P->tlay.n - 1);
+  out->window_rows = (int32_t)(full ? P->tlay.n - 1 : P->window);
   out->pcr_stages = P->gpcr.stages;
   if (P->p > 1) {
     out->comm_rounds = 2 + P->gpcr.stages;
@@ -657,7 +685,8 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
   for (float* t : ts) *t = -1.f;
   for (int k = 0; k < CTRI_MAX_STAGES; ++k) out->t_stage_us[k] = -1.f;
   if (P->timed_valid || (!P->ev.empty() && P->solves > 0)) {
-    CUDA_TRY(cudaEventSynchronize(P->ev[P->p > 1 ? EV_BACK : EV_LOCAL]));
+    const bool two = P->p > 1 || P->vp > 1;
+    CUDA_TRY(cudaEventSynchronize(P->ev[two ? EV_BACK : EV_LOCAL]));
     out->t_local_us = elapsed(*P, EV_START, EV_LOCAL);
     if (P->p > 1 && P->p2p) {
       out->t_backsub_us = elapsed(*P, EV_LOCAL, EV_BACK);  // the whole fused (a2)-(a4) kernel
@@ -672,6 +701,9 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
       }
       out->t_xexchange_us = elapsed(*P, prev, EV_XX);
       out->t_backsub_us = elapsed(*P, EV_XX, EV_BACK);
+      out->t_total_us = elapsed(*P, EV_START, EV_BACK);
+    } else if (P->vp > 1) {
+      out->t_backsub_us = elapsed(*P, EV_LOCAL, EV_BACK);  // local reduced + window back-sub
       out->t_total_us = elapsed(*P, EV_START, EV_BACK);
     } else {
       out->t_total_us = out->t_local_us;

@@ -34,6 +34,8 @@ struct TileConsts {
   double R[K > 1 ? K - 1 : 1];        // chunk-level R_K = D_K^{-1} u e_last
 };
 
+constexpr int kMaxUniformStages = 12;  // head-system PCR stages passed as kernel parameters
+
 struct TileArgs {
   const double* b;
   double* x;
@@ -46,6 +48,8 @@ struct TileArgs {
   int mode;         // 0: complete cyclic solve (p = 1); 1: y_D = D_i^{-1} b_i + planes (p >= 2);
                     // 2: complete acyclic solve (p = 1)
   int rows_box;     // TMA box rows (<= 256)
+  int pcr_uniform;  // 1: per-stage multipliers below (cyclic uniform head system); 0: tables
+  double ualpha[kMaxUniformStages], ugamma[kMaxUniformStages], uinv;
   const double* pcr_alpha;  // [stages][Q]
   const double* pcr_gamma;  // [stages][Q]
   const double* pcr_inv;    // [Q]
@@ -56,12 +60,15 @@ struct TileArgs {
   double ca, cb;
   const double* halo_lo;  // [2][m]: rows n-2, n-1 of the slab above
   const double* halo_hi;  // [2][m]: rows 0, 1 of the slab below
+  unsigned long long* trace;  // measurement only (CTRI_TILE_TRACE)
 };
 
 struct TileConfig {
   bool ok = false;
   int variant = 0;  // index into the tile variant table (tile.cu)
-  int C = 0, NT = 0, STAGES = 0, MINB = 0;  // columns per tile, threads, smem ring depth, CTAs/SM
+  int C = 0, NT = 0, STAGES = 0, MINB = 0;  // columns per tile, threads, ring slots, CTAs/SM
+  int SUB = 1;                              // sub-tiles per CTA tile (ring slot granularity)
+  bool pcr_uniform = false;
   bool contig = false;                      // contiguous solve axis variant
   int K = 0, G = 0, Q = 0;
   int smem_bytes = 0;
@@ -105,6 +112,9 @@ struct Plan {
   uint32_t flags = 0;
   Bands bands{};
   Layout lay;           // local slab
+  int vp = 1;           // virtual partitions of the slab solved as separate partitions on this
+                        // GPU (nparts == 1 only; the paper's method with more partitions than GPUs)
+  Layout tlay;          // layout the local-solve kernels see: (outer*vp, n/vp, inner)
   int device = 0;
   int num_sms = 0;
   bool loopback = false;
@@ -162,6 +172,7 @@ cudaError_t launch_local_generic(const Plan& P, const double* b, double* x, cuda
 cudaError_t launch_bhat(const Plan& P, cudaStream_t s);
 cudaError_t launch_pcr_stage(const Plan& P, int k, bool last, cudaStream_t s);
 cudaError_t launch_backsub(const Plan& P, double* x, cudaStream_t s);
+cudaError_t launch_reduced_local(const Plan& P, double* x, cudaStream_t s);
 cudaError_t launch_pack_halo(const Plan& P, const double* f, cudaStream_t s);
 cudaError_t launch_stencil(const Plan& P, const double* f, double* rhs, double a, double bc,
                            double h, cudaStream_t s);

@@ -19,6 +19,8 @@
 
 namespace ctri {
 
+static inline unsigned blocks_for(int64_t m, int bs) { return (unsigned)((m + bs - 1) / bs); }
+
 
 // ------------------------------------------------------------------------------------------
 // (a1) generic column-serial local solve: one thread per batch column, any n >= 3, any layout.
@@ -113,6 +115,105 @@ __global__ void k_backsub(double* x, int64_t outer, int64_t n, int64_t inner,
   }
 }
 
+// (a2)-(a4) for the virtual partitions of one GPU (nparts == 1, vp > 1): per batch column the
+// vp-row reduced system (cyclic or acyclic) is formed from the planes (Eq. bi_hat), solved with
+// the plan's PCR multipliers (fold R3) and back-substituted on the window rows of
+// every virtual slab (Eq. xi_app).  No communication: all partitions live in this slab.
+struct LocalRedArgs {
+  int vp, q, cyclic, full;
+  int64_t outer, nv, inner, W;
+  double l, u;
+  const double *S, *R, *yf, *yl, *bt;
+  double alpha[4 * 8], gamma[4 * 8], inv[8];  // [stage][row], vp <= 8
+};
+
+__global__ void k_reduced_local(const LocalRedArgs A, double* __restrict__ x) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t m = A.outer * A.inner;
+  if (j >= m) return;
+  const int vp = A.vp;
+  const int64_t o = j / A.inner, c = j - o * A.inner;
+  double bh[8];
+  for (int v = 0; v < 8; ++v) {
+    if (v >= vp) break;
+    const int64_t pj = (o * vp + v) * A.inner + c;
+    const int vl = (v + vp - 1) % vp;
+    const double ylp = (A.cyclic || v > 0) ? A.yl[(o * vp + vl) * A.inner + c] : 0.0;
+    bh[v] = A.bt[pj] - A.l * ylp - A.u * A.yf[pj];
+  }
+  for (int k = 0; k < A.q; ++k) {
+    const int s = 1 << k;
+    double nb[8];
+    for (int v = 0; v < 8; ++v) {
+      if (v >= vp) break;
+      int lm = v - s, lp = v + s;
+      double vm = 0.0, vpv = 0.0;
+      if (A.cyclic) {
+        vm = bh[((lm % vp) + vp) % vp];
+        vpv = bh[lp % vp];
+      } else {
+        if (lm >= 0) vm = bh[lm];
+        if (lp < vp) vpv = bh[lp];
+      }
+      nb[v] = bh[v] - A.alpha[k * 8 + v] * vm - A.gamma[k * 8 + v] * vpv;
+    }
+    for (int v = 0; v < 8; ++v)
+      if (v < vp) bh[v] = nb[v];
+  }
+  for (int v = 0; v < 8; ++v)
+    if (v < vp) bh[v] *= A.inv[v];
+  const int64_t rows = A.full ? A.nv - 1 : 2 * A.W;
+  for (int v = 0; v < 8; ++v) {
+    if (v >= vp) break;
+    const double xa = bh[v];
+    const double xn = (A.cyclic || v + 1 < vp) ? bh[(v + 1) % vp] : 0.0;
+    double* xc = x + ((o * vp + v) * A.nv) * A.inner + c;
+    xc[0] = xa;
+    for (int64_t r0 = 0; r0 < rows; r0 += 8) {
+      double val[8];
+      int64_t rr[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t ry = r0 + u;
+        rr[u] = A.full ? ry + 1 : (ry < A.W ? ry + 1 : A.nv - 2 * A.W + ry);
+        if (ry < rows) val[u] = xc[rr[u] * A.inner];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (r0 + u < rows) xc[rr[u] * A.inner] = val[u] - A.S[rr[u] - 1] * xa - A.R[rr[u] - 1] * xn;
+    }
+  }
+}
+
+cudaError_t launch_reduced_local(const Plan& P, double* x, cudaStream_t s) {
+  LocalRedArgs A;
+  A.vp = P.vp;
+  A.q = P.gpcr.stages;
+  A.cyclic = P.cyclic;
+  A.full = ((P.flags & CTRI_FLAG_FULL_BACKSUB) || (2 * P.window >= P.tlay.n - 1)) ? 1 : 0;
+  A.outer = P.lay.outer;
+  A.nv = P.tlay.n;
+  A.inner = P.lay.inner;
+  A.W = P.window;
+  A.l = P.bands.l;
+  A.u = P.bands.u;
+  A.S = P.d_S;
+  A.R = P.d_R;
+  A.yf = P.yf;
+  A.yl = P.yl;
+  A.bt = P.bt;
+  for (int i = 0; i < 32; ++i) A.alpha[i] = A.gamma[i] = 0.0;
+  for (int kk = 0; kk < A.q && kk < 4; ++kk)
+    for (int v = 0; v < P.vp; ++v) {
+      A.alpha[kk * 8 + v] = P.gpcr.alpha[(size_t)kk * P.vp + v];
+      A.gamma[kk * 8 + v] = P.gpcr.gamma[(size_t)kk * P.vp + v];
+    }
+  for (int v = 0; v < 8; ++v) A.inv[v] = v < P.vp ? P.gpcr.inv[v] : 0.0;
+  const int64_t m = P.lay.m();
+  k_reduced_local<<<blocks_for(m, 128), 128, 0, s>>>(A, x);
+  return cudaGetLastError();
+}
+
 // (a0) pack the two first / two last planes of f into contiguous send buffers (halo exchange).
 __global__ void k_pack_halo(const double* __restrict__ f, int64_t outer, int64_t n, int64_t inner,
                             double* __restrict__ send_lo, double* __restrict__ send_hi) {
@@ -152,14 +253,14 @@ __global__ void k_stencil(const double* __restrict__ f, double* __restrict__ rhs
 // ------------------------------------------------------------------------------------------
 // host launchers
 // ------------------------------------------------------------------------------------------
-static inline unsigned blocks_for(int64_t m, int bs) { return (unsigned)((m + bs - 1) / bs); }
 
 cudaError_t launch_local_generic(const Plan& P, const double* b, double* x, cudaStream_t s) {
-  const int64_t m = P.lay.m();
+  const Layout& L = P.tlay;
+  const int64_t m = L.m();
   const int bs = 128;
   k_local_generic<<<blocks_for(m, bs), bs, 0, s>>>(
-      b, x, P.lay.outer, P.lay.n, P.lay.inner, P.d_cp, P.d_inv_den, P.bands.l, P.bands.u,
-      P.p == 1 ? 0 : 1, P.d_S, P.d_R, P.inv_closure, P.cyclic, P.yf, P.yl, P.bt);
+      b, x, L.outer, L.n, L.inner, P.d_cp, P.d_inv_den, P.bands.l, P.bands.u,
+      (P.p == 1 && P.vp == 1) ? 0 : 1, P.d_S, P.d_R, P.inv_closure, P.cyclic, P.yf, P.yl, P.bt);
   return cudaGetLastError();
 }
 

@@ -29,14 +29,16 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
+#include <vector>
 
 #include "internal.h"
 #include "ptx.cuh"
 
 namespace ctri {
 
-template <int K, int C, int NT, int STAGES, int MINB, int LAYOUT>
+template <int K, int C, int NT, int SUB, int SLOTS, int MINB, int LAYOUT>
 __global__ void __launch_bounds__(NT, MINB)
     k_tile(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap hmap,
            const TileArgs A, const TileConsts<K> T) {
@@ -45,21 +47,27 @@ __global__ void __launch_bounds__(NT, MINB)
   constexpr bool CONTIG = (LAYOUT == 1);
   constexpr bool DERIV = (LAYOUT == 2);
   constexpr int HALO = DERIV ? 2 : 0;     // stencil half-width (rows)
-  static_assert(K >= 4 && NT % C == 0 && (C == 4 || C == 8 || C == 16), "tile geometry");
-  static_assert(!CONTIG || (NT / C == 32 && STAGES == 1), "contiguous axis: 32 chunks per CTA");
+  static_assert(K >= 4 && NT % C == 0 && (C == 4 || C == 8 || C == 16 || C == 32), "tile geometry");
+  static_assert(!CONTIG || (NT / C == 32 && SUB == 1 && SLOTS == 1), "contiguous: 32 chunks/CTA");
+  static_assert(!DERIV || SUB == 1, "fused stencil: whole-tile ring slots");
+  static_assert(SLOTS >= SUB, "ring must hold one tile");
   constexpr int CPC = NT / C;             // chunks per CTA
   constexpr int ROWS = CPC * K;           // rows per CTA
   // strided axis: rows of C columns (C*8 bytes) share the 32 banks with PRD-1 other rows;
   // contiguous axis: chunks are (K+2)*8 bytes apart, half-warps rotate by one row
-  constexpr int PRD = CONTIG ? 2 : 16 / C;
+  constexpr int PRD = CONTIG ? 2 : (C >= 16 ? 1 : 16 / C);
   constexpr int CSTRIDE = K + 2;          // contiguous axis: padded chunk stride (doubles)
-  constexpr int RING = CONTIG ? C * CPC * CSTRIDE : (ROWS + 2 * HALO) * C;  // doubles per stage
+  // TMA ring: SLOTS slots of one sub-tile each (SUB sub-tiles of SR rows per CTA tile), so up to
+  // SLOTS sub-tiles are in flight while the current tile is computed from registers
+  constexpr int CPS = CPC / SUB;          // chunks per sub-tile
+  constexpr int SR = CPS * K;             // rows per sub-tile
+  constexpr int RING = CONTIG ? C * CPC * CSTRIDE : (SR + 2 * HALO) * C;  // doubles per slot
   static_assert(K % PRD == 0, "K must be a multiple of the bank period");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int Q = A.Q;
   const int stages = A.stages;
   double* ring = reinterpret_cast<double*>(smem_raw);
-  double* ex_bt = ring + (size_t)STAGES * RING;       // owner: b~ of every head it owns
+  double* ex_bt = ring + (size_t)SLOTS * RING;        // owner: b~ of every head it owns
   double* ex_yf = ex_bt + NT;                        // owner: y_c[first]
   double* ex_yl = ex_yf + NT;                        // owner: y_c[last]
   double* pb0 = ex_yl + NT;                          // owner: PCR ping-pong
@@ -69,8 +77,9 @@ __global__ void __launch_bounds__(NT, MINB)
   double* s_alpha = rx_b + NT;                       // PCR multipliers [stages][Q]
   double* s_gamma = s_alpha + (size_t)stages * Q;
   double* s_inv = s_gamma + (size_t)stages * Q;      // [Q]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(s_inv + Q);  // [STAGES] ring, ex, rx
-  uint64_t* mbar_ex = mbar + STAGES;
+  const bool tab = !A.pcr_uniform;  // per-row PCR multipliers in smem (acyclic head systems)
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(tab ? s_inv + Q : s_alpha);  // [SLOTS] ring, ex, rx
+  uint64_t* mbar_ex = mbar + SLOTS;
   uint64_t* mbar_rx = mbar_ex + 1;
 
   const int tid = threadIdx.x;
@@ -90,40 +99,49 @@ __global__ void __launch_bounds__(NT, MINB)
   // rotation of the smem row reads so that the PRD groups of a warp hit disjoint banks
   const int rot = CONTIG ? ((tid & 31) >> 4) : ((tid & 31) / C) % PRD;
 
-  for (int i = tid; i < stages * Q; i += NT) {
-    s_alpha[i] = A.pcr_alpha[i];
-    s_gamma[i] = A.pcr_gamma[i];
+  if (tab) {
+    for (int i = tid; i < stages * Q; i += NT) {
+      s_alpha[i] = A.pcr_alpha[i];
+      s_gamma[i] = A.pcr_gamma[i];
+    }
+    for (int i = tid; i < Q; i += NT) s_inv[i] = A.pcr_inv[i];
   }
-  for (int i = tid; i < Q; i += NT) s_inv[i] = A.pcr_inv[i];
-  if (tid < STAGES) dev::mbar_init(dev::smem_u32(mbar + tid), 1);
-  if (tid == STAGES) dev::mbar_init(dev::smem_u32(mbar_ex), 1);
-  if (tid == STAGES + 1) dev::mbar_init(dev::smem_u32(mbar_rx), 1);
+  if (tid < SLOTS) dev::mbar_init(dev::smem_u32(mbar + tid), 1);
+  if (tid == SLOTS) dev::mbar_init(dev::smem_u32(mbar_ex), 1);
+  if (tid == SLOTS + 1) dev::mbar_init(dev::smem_u32(mbar_rx), 1);
   if (tid == 0) dev::fence_mbar_init();
   __syncthreads();
   if (G > 1) dev::cluster_sync();  // barriers initialised cluster-wide before any st.async
 
   const uint32_t ncl = (G > 1) ? dev::ncluster_x() : gridDim.x;
   const int64_t first = (G > 1) ? (int64_t)dev::cluster_id_x() : (int64_t)blockIdx.x;
-  constexpr uint32_t kTileBytes = (uint32_t)(ROWS + 2 * HALO) * C * (uint32_t)sizeof(double);
+  constexpr uint32_t kSubBytes = (uint32_t)(SR + 2 * HALO) * C * (uint32_t)sizeof(double);
   const int boxr = A.rows_box;
   const int row0 = (int)g * ROWS;
   const uint64_t pol = dev::policy_evict_first();
 
-  auto issue = [&](int64_t t, int s) {
+  // sub-tile sequence number seq -> (tile first + (seq / SUB) * ncl, part seq % SUB), slot seq % SLOTS
+  auto issue = [&](int64_t seq) {
+    const int64_t t = first + (seq / SUB) * (int64_t)ncl;
+    if (t >= A.num_tiles) return;
+    const int h = (int)(seq % SUB);
+    const int s = (int)(seq % SLOTS);
     const int o = (int)(t / A.tiles_per_outer);
     const int col0 = (int)(t - (int64_t)o * A.tiles_per_outer) * C;
     const uint32_t bar = dev::smem_u32(mbar + s);
     double* dst = ring + (size_t)s * RING;
+    const int r0 = row0 + h * SR;
     dev::fence_proxy_async();
-    dev::mbar_expect_tx(bar, kTileBytes);
-    for (int r = 0; r < ROWS; r += boxr)
-      dev::tma_load_3d(dev::smem_u32(dst + (size_t)(r + HALO) * C), &tmap, col0, row0 + r, o, bar, pol);
+    dev::mbar_expect_tx(bar, kSubBytes);
+    for (int r = 0; r < SR; r += boxr)
+      dev::tma_load_3d(dev::smem_u32(dst + (size_t)(r + HALO) * C), &tmap, col0, r0 + r, o, bar, pol);
     if (DERIV) {  // stencil halo rows row0-2, row0-1 and row0+ROWS, +1 (zero-filled outside the slab)
       dev::tma_load_3d(dev::smem_u32(dst), &hmap, col0, row0 - HALO, o, bar, pol);
       dev::tma_load_3d(dev::smem_u32(dst + (size_t)(ROWS + HALO) * C), &hmap, col0, row0 + ROWS, o,
                        bar, pol);
     }
   };
+  const int hsub = cl / CPS, lc = cl - (cl / CPS) * CPS;  // my sub-tile and chunk within it
 
   // remote addresses: my (b~, y_first, y_last) -> owner; my x~ -> holders of chunks oc, oc-1
   uint32_t r_bt = dev::smem_u32(ex_bt + slot), r_yf = dev::smem_u32(ex_yf + slot),
@@ -161,13 +179,23 @@ __global__ void __launch_bounds__(NT, MINB)
   if (CONTIG) {
     if (first < A.num_tiles) issue_contig(first);
   } else if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s)
-      if (first + (int64_t)s * ncl < A.num_tiles) issue(first + (int64_t)s * ncl, s);
+    for (int s = 0; s < SLOTS; ++s) issue(s);
   }
 
+  // measurement only (CTRI_TILE_TRACE): CTA 0 stamps its first 64 tiles' phases
+  unsigned long long* tr = (A.trace && blockIdx.x == 0) ? A.trace : nullptr;
+  auto stamp = [&](int it_, int k) {
+    if (tr && tid == 0 && it_ < 64) {
+      unsigned long long tt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+      tr[it_ * 8 + k] = tt;
+    }
+  };
   int it = 0;
   for (int64_t t = first; t < A.num_tiles; t += ncl, ++it) {
-    const int s = it % STAGES;
+    stamp(it, 0);
+    const int64_t seq = (int64_t)it * SUB + hsub;
+    const int s = (int)(seq % SLOTS);
     // global column: strided axis (o, col) with col < inner; contiguous axis column = o
     const int64_t o = CONTIG ? t * C + j : t / A.tiles_per_outer;
     const int64_t col = CONTIG ? 0 : (t - o * A.tiles_per_outer) * C + j;
@@ -179,7 +207,7 @@ __global__ void __launch_bounds__(NT, MINB)
       dev::cp_async_wait_all();
       __syncthreads();
     } else {
-      dev::mbar_wait(dev::smem_u32(mbar + s), (uint32_t)(it / STAGES) & 1u);
+      dev::mbar_wait(dev::smem_u32(mbar + s), (uint32_t)(seq / SLOTS) & 1u);
     }
     double* tile = ring + (size_t)s * RING;
     if (DERIV) {
@@ -204,7 +232,7 @@ __global__ void __launch_bounds__(NT, MINB)
 #pragma unroll
       for (int i = 0; i < PRD; ++i) {
         const int kk = k + ((i + rot) % PRD);
-        a[i] = CONTIG ? tile[(j * CPC + cl) * CSTRIDE + kk] : tile[(cl * K + kk) * C + j];
+        a[i] = CONTIG ? tile[(j * CPC + cl) * CSTRIDE + kk] : tile[(lc * K + kk) * C + j];
       }
 #pragma unroll
       for (int m = 0; m < PRD; ++m) {  // a[i] holds row k + (i + rot) % PRD
@@ -219,11 +247,12 @@ __global__ void __launch_bounds__(NT, MINB)
 #pragma unroll
       for (int k = 0; k < K; ++k) v[k] = A.ca * (v[k + 3] - v[k + 1]) + A.cb * (v[k + 4] - v[k]);
     }
+    stamp(it, 1);
     __syncthreads();  // every thread has its chunk in registers: stage s is free
     if (CONTIG) {
       if (t + ncl < A.num_tiles) issue_contig(t + ncl);
-    } else if (tid == 0 && t + (int64_t)STAGES * ncl < A.num_tiles) {
-      issue(t + (int64_t)STAGES * ncl, s);
+    } else if (tid == 0) {
+      for (int hh = 0; hh < SUB; ++hh) issue((int64_t)it * SUB + hh + SLOTS);  // freed slots
     }
     const bool valid = CONTIG ? (o < A.lay.outer) : (col < A.lay.inner);
     auto store_chunk = [&]() {
@@ -255,6 +284,7 @@ __global__ void __launch_bounds__(NT, MINB)
 #pragma unroll
       for (int k = K - 2; k >= 1; --k) v[k] = fma(-T.cp[k - 1], v[k + 1], v[k]);
     }
+    stamp(it, 2);
     // ---- (b~_c, y_c[first], y_c[last]) -> owner CTA, completing on its exchange barrier ----
     dev::st_async_f64(r_bt, btv, r_exbar);
     dev::st_async_f64(r_yf, v[1], r_exbar);
@@ -262,6 +292,7 @@ __global__ void __launch_bounds__(NT, MINB)
     // ---- owner: head system b^_c (Eq. bi_hat at chunk level), then PCR stages ----
     {
       dev::mbar_wait(dev::smem_u32(mbar_ex), (uint32_t)it & 1u);
+      stamp(it, 3);
       const double lt = (A.mode == 2 && oc == 0) ? 0.0 : T.l * ex_yl[prev_row];  // acyclic top
       double bh = ex_bt[tid] - lt - T.u * ex_yf[tid];
       if (A.mode == 1 && oc == 0) bh = 0.0;  // slab row 0 is the GPU interface, not in D_i
@@ -273,17 +304,21 @@ __global__ void __launch_bounds__(NT, MINB)
         const int sh = 1 << k;
         const double vm = cur[oj * Q + ((oc - sh) & (Q - 1))];
         const double vp = cur[oj * Q + ((oc + sh) & (Q - 1))];
-        bh = bh - s_alpha[k * Q + oc] * vm - s_gamma[k * Q + oc] * vp;
+        const double al = tab ? s_alpha[k * Q + oc] : A.ualpha[k];
+        const double ga = tab ? s_gamma[k * Q + oc] : A.ugamma[k];
+        bh = bh - al * vm - ga * vp;
         double* tmp = cur;
         cur = nxt;
         nxt = tmp;
       }
-      const double xt = bh * s_inv[oc];
+      const double xt = bh * (tab ? s_inv[oc] : A.uinv);
+      stamp(it, 4);
       // x~_oc -> x_a of chunk oc's holder and x_b of chunk oc-1's holder
       dev::st_async_f64(r_xa, xt, r_rxa);
       dev::st_async_f64(r_xb, xt, r_rxb);
     }
     dev::mbar_wait(dev::smem_u32(mbar_rx), (uint32_t)it & 1u);
+    stamp(it, 5);
     const double xa = rx_a[tid];
     const double xb = (A.mode != 0 && c == Q - 1) ? 0.0 : rx_b[tid];  // x~_{i+1} outside D_i / acyclic end
     // ---- chunk back-substitution, Eq. xi_app at chunk level ----
@@ -291,6 +326,7 @@ __global__ void __launch_bounds__(NT, MINB)
 #pragma unroll
     for (int k = 1; k < K; ++k) v[k] = v[k] - T.S[k - 1] * xa - T.R[k - 1] * xb;
     store_chunk();
+    stamp(it, 6);
     if (valid) {
       if (A.mode == 1) {
         const int64_t pj = o * A.lay.inner + col;
@@ -310,17 +346,28 @@ __global__ void __launch_bounds__(NT, MINB)
 // ------------------------------------------------------------------------------------------
 struct Variant {
   const char* name;
-  int C, NT, STAGES, MINB;
+  int C, NT, SUB, SLOTS, MINB;
   bool contig;  // contiguous solve axis (inner == 1): cp.async into a padded ring
+  int kmax = 32;  // largest rows-per-thread K
 };
 static const Variant kVariants[] = {
-    {"c16t512s1", 16, 512, 1, 1, false},
-    {"c8t512s1", 8, 512, 1, 1, false},
-    {"c4t512s1", 4, 512, 1, 1, false},
-    {"c8t256s1", 8, 256, 1, 2, false},
-    {"c16t256s1", 16, 256, 1, 2, false},
-    {"c16t512s1_contig", 16, 512, 1, 1, true},
-    {"c8t256s1_contig", 8, 256, 1, 2, true},
+    {"c16t512s1", 16, 512, 1, 1, 1, false},
+    {"c8t512s1", 8, 512, 1, 1, 1, false},
+    {"c4t512s1", 4, 512, 1, 1, 1, false},
+    {"c8t256s1", 8, 256, 1, 1, 2, false},
+    {"c16t256s1", 16, 256, 1, 1, 2, false},
+    {"c16t512s1_contig", 16, 512, 1, 1, 1, true},
+    {"c8t256s1_contig", 8, 256, 1, 1, 2, true},
+    {"c16t256x3", 16, 256, 2, 3, 2, false},   // half-tile ring slots, 1.5 tiles in flight
+    {"c16t512x5", 16, 512, 4, 5, 1, false},   // quarter-tile ring slots, 1.25 tiles in flight
+    {"c16t256x6", 16, 256, 4, 6, 2, false},   // quarter-tile slots, 1.5 tiles in flight
+    {"c32t512s1", 32, 512, 1, 1, 1, false},   // 256-byte row segments
+    {"c32t512x3", 32, 512, 2, 3, 1, false},   // 256-byte rows, half-tile ring slots
+    {"c32t256x3", 32, 256, 2, 3, 2, false},   // 256-byte rows, 2 CTA/SM, half-tile slots
+    {"c32t256s1", 32, 256, 1, 1, 2, false},   // 256-byte rows, 2 CTA/SM
+    {"c32t256k16", 32, 256, 1, 1, 4, false, 16},  // 256-byte rows, K <= 16, 4 CTA/SM
+    {"c16t256k16", 16, 256, 1, 1, 4, false, 16},  // 128-byte rows, K <= 16, 4 CTA/SM
+    {"c32t256k16x3", 32, 256, 2, 3, 3, false, 16},  // K <= 16, half-tile slots, 3 CTA/SM
 };
 static constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -339,10 +386,10 @@ static void fill_consts(const TileConfig& tc, TileConsts<K>* T) {
   }
 }
 
-template <int K, int C, int NT, int S, int M, int LY>
+template <int K, int C, int NT, int SB, int S, int M, int LY>
 static cudaError_t launch_one(const TileConfig& tc, const CUtensorMap& map, const CUtensorMap& hmap,
                               const TileArgs& A, cudaStream_t s, bool configure_only) {
-  auto fn = k_tile<K, C, NT, S, M, LY>;
+  auto fn = k_tile<K, C, NT, SB, S, M, LY>;
   if (configure_only) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc.smem_bytes);
     return e;
@@ -364,19 +411,19 @@ static cudaError_t launch_one(const TileConfig& tc, const CUtensorMap& map, cons
   return cudaLaunchKernelEx(&cfg, fn, map, hmap, A, T);
 }
 
-template <int K, int C, int NT, int S, int M, int LY>
+template <int K, int C, int NT, int SB, int S, int M, int LY>
 static const void* fn_ptr() {
-  return reinterpret_cast<const void*>(&k_tile<K, C, NT, S, M, LY>);
+  return reinterpret_cast<const void*>(&k_tile<K, C, NT, SB, S, M, LY>);
 }
 
-template <int C, int NT, int S, int M, int LY>
+template <int C, int NT, int SB, int S, int M, int LY>
 static cudaError_t dispatch_k(const TileConfig& tc, const CUtensorMap& map, const CUtensorMap& hmap,
                               const TileArgs& A, cudaStream_t s, bool cfg_only, const void** fp) {
   switch (tc.K) {
 #define CTRI_K(KK)                                                       \
   case KK:                                                               \
-    if (fp) *fp = fn_ptr<KK, C, NT, S, M, LY>();                          \
-    return fp ? cudaSuccess : launch_one<KK, C, NT, S, M, LY>(tc, map, hmap, A, s, cfg_only);
+    if (fp) *fp = fn_ptr<KK, C, NT, SB, S, M, LY>();                      \
+    return fp ? cudaSuccess : launch_one<KK, C, NT, SB, S, M, LY>(tc, map, hmap, A, s, cfg_only);
     CTRI_K(4) CTRI_K(8) CTRI_K(16) CTRI_K(32)
 #undef CTRI_K
   }
@@ -386,29 +433,42 @@ static cudaError_t dispatch_k(const TileConfig& tc, const CUtensorMap& map, cons
 static cudaError_t dispatch(const TileConfig& tc, bool deriv, const CUtensorMap& map,
                             const CUtensorMap& hmap, const TileArgs& A, cudaStream_t s,
                             bool cfg_only, const void** fp = nullptr) {
-#define CTRI_V(C, NT, S, M, LY) return dispatch_k<C, NT, S, M, LY>(tc, map, hmap, A, s, cfg_only, fp)
-  if (deriv) {  // fused stencil: strided 16-column variants only
+#define CTRI_V(C, NT, SB, S, M, LY) return dispatch_k<C, NT, SB, S, M, LY>(tc, map, hmap, A, s, cfg_only, fp)
+  if (deriv) {  // fused stencil: strided whole-tile variants with 16 or 32 columns
     switch (tc.variant) {
-      case 0: CTRI_V(16, 512, 1, 1, 2);
-      case 4: CTRI_V(16, 256, 1, 2, 2);
+      case 0: CTRI_V(16, 512, 1, 1, 1, 2);
+      case 4: CTRI_V(16, 256, 1, 1, 2, 2);
+      case 13: CTRI_V(32, 256, 1, 1, 2, 2);
     }
     return cudaErrorInvalidValue;
   }
   switch (tc.variant) {
-    case 0: CTRI_V(16, 512, 1, 1, 0);
-    case 1: CTRI_V(8, 512, 1, 1, 0);
-    case 2: CTRI_V(4, 512, 1, 1, 0);
-    case 3: CTRI_V(8, 256, 1, 2, 0);
-    case 4: CTRI_V(16, 256, 1, 2, 0);
-    case 5: CTRI_V(16, 512, 1, 1, 1);
-    case 6: CTRI_V(8, 256, 1, 2, 1);
+    case 0: CTRI_V(16, 512, 1, 1, 1, 0);
+    case 1: CTRI_V(8, 512, 1, 1, 1, 0);
+    case 2: CTRI_V(4, 512, 1, 1, 1, 0);
+    case 3: CTRI_V(8, 256, 1, 1, 2, 0);
+    case 4: CTRI_V(16, 256, 1, 1, 2, 0);
+    case 5: CTRI_V(16, 512, 1, 1, 1, 1);
+    case 6: CTRI_V(8, 256, 1, 1, 2, 1);
+    case 7: CTRI_V(16, 256, 2, 3, 2, 0);
+    case 8: CTRI_V(16, 512, 4, 5, 1, 0);
+    case 9: CTRI_V(16, 256, 4, 6, 2, 0);
+    case 10: CTRI_V(32, 512, 1, 1, 1, 0);
+    case 11: CTRI_V(32, 512, 2, 3, 1, 0);
+    case 12: CTRI_V(32, 256, 2, 3, 2, 0);
+    case 13: CTRI_V(32, 256, 1, 1, 2, 0);
+    case 14: CTRI_V(32, 256, 1, 1, 4, 0);
+    case 15: CTRI_V(16, 256, 1, 1, 4, 0);
+    case 16: CTRI_V(32, 256, 2, 3, 3, 0);
   }
 #undef CTRI_V
   return cudaErrorInvalidValue;
 }
 
 // Preference order when CTRI_TILE_VARIANT is not set: the first variant whose geometry fits n.
-static const int kPreference[] = {4, 0, 1, 3, 2, 5, 6};
+// Measured on B200 (profiles/round1_tile_variants.md): 256-byte row segments with 2 CTA/SM
+// first, then 128-byte tiles; portable clusters (<= 8) before 16-CTA ones.
+static const int kPreference[] = {13, 4, 0, 12, 3, 1, 2, 5, 6};
 
 static int forced_variant() {
   const char* e = std::getenv("CTRI_TILE_VARIANT");  // experiment knob (bench sweeps)
@@ -423,7 +483,7 @@ const char* tile_variant_name(int v) { return (v >= 0 && v < kNumVariants) ? kVa
 static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
   TileConfig& tc = P.tile;
   tc = TileConfig();
-  const Layout& L = P.lay;
+  const Layout& L = P.tlay;
   const Variant& V = kVariants[vi];
   if (V.contig) {
     if (L.inner != 1 || (L.n % 2) != 0) { *why = "contiguous variant needs inner == 1, n even"; return false; }
@@ -440,7 +500,7 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
   const int64_t kg = L.n / cpc;  // K * G
   int K = 0, G = 0;
   for (int k : {32, 16, 8, 4}) {
-    if (kg % k) continue;
+    if (k > V.kmax || kg % k) continue;
     const int64_t g = kg / k;
     if (g >= 1 && g <= kMaxClusterNonPortable && (g & (g - 1)) == 0 && V.C % g == 0) {
       K = k;
@@ -453,7 +513,8 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
   tc.contig = V.contig;
   tc.C = V.C;
   tc.NT = V.NT;
-  tc.STAGES = V.STAGES;
+  tc.STAGES = V.SLOTS;
+  tc.SUB = V.SUB;
   tc.MINB = V.MINB;
   const int Q = cpc * G;
   // chunk-level tables (Eqs. Si, Ri, Li_hat..Ui_hat on the (K-1)-row chunk interior)
@@ -468,8 +529,8 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
   for (int k = 0; k < K - 1; ++k) tc.consts.push_back(cp.S[k]);
   for (int k = 0; k < K - 1; ++k) tc.consts.push_back(cp.R[k]);
   std::vector<double> Lr(Q, cp.Lh), Dr(Q, cp.Dh), Ur(Q, cp.Uh);
-  const bool cyc = (P.p == 1 && P.cyclic);
-  if (P.p > 1) {  // dummy decoupled row 0 (the GPU interface), acyclic over the other heads
+  const bool cyc = (P.p == 1 && P.vp == 1 && P.cyclic);
+  if (P.p > 1 || P.vp > 1) {  // dummy decoupled row 0 (the GPU interface), acyclic over the other heads
     Lr[0] = 0.0; Dr[0] = 1.0; Ur[0] = 0.0;
     Lr[1] = 0.0;
     Ur[Q - 1] = 0.0;
@@ -486,10 +547,21 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
   tc.G = G;
   tc.Q = Q;
   const int rows_cta = cpc * K;
-  const size_t ring = V.contig ? (size_t)V.C * cpc * (K + 2) : (size_t)rows_cta * V.C;
-  tc.smem_bytes = (int)(sizeof(double) * ((size_t)V.STAGES * ring + 7 * (size_t)V.NT +
-                                          (2 * (size_t)tc.pcr.stages + 1) * Q) +
-                        8 * (V.STAGES + 2));
+  if (cpc % V.SUB) { *why = "sub-tiles must split the chunks evenly"; return false; }
+  // uniform (cyclic p = 1) head systems: the PCR multipliers are per-stage constants and travel
+  // in the kernel parameters; otherwise per-row tables live in shared memory
+  tc.pcr_uniform = tc.pcr.stages <= kMaxUniformStages;
+  for (int k = 0; k < tc.pcr.stages && tc.pcr_uniform; ++k)
+    for (int c = 1; c < Q; ++c)
+      if (tc.pcr.alpha[(size_t)k * Q + c] != tc.pcr.alpha[(size_t)k * Q] ||
+          tc.pcr.gamma[(size_t)k * Q + c] != tc.pcr.gamma[(size_t)k * Q])
+        tc.pcr_uniform = false;
+  for (int c = 1; c < Q && tc.pcr_uniform; ++c)
+    if (tc.pcr.inv[c] != tc.pcr.inv[0]) tc.pcr_uniform = false;
+  const size_t ring = V.contig ? (size_t)V.C * cpc * (K + 2) : (size_t)(rows_cta / V.SUB) * V.C;
+  const size_t tables = tc.pcr_uniform ? 0 : (2 * (size_t)tc.pcr.stages + 1) * Q;
+  tc.smem_bytes = (int)(sizeof(double) * ((size_t)V.SLOTS * ring + 7 * (size_t)V.NT + tables) +
+                        8 * (V.SLOTS + 2));
   // configure one instantiation (solve, or the fused-stencil one): smem attribute + grid
   auto setup = [&](bool deriv, int smem, int* grid_out) -> bool {
     const void* fn = nullptr;
@@ -532,8 +604,9 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
   if (!setup(false, tc.smem_bytes, &tc.grid)) return false;
   // fused-stencil instantiation (ctri_deriv): 4 extra ring rows per stage
   tc.deriv_ok = false;
-  if (!V.contig && V.C == 16 && (P.flags & CTRI_FLAG_DERIV)) {
-    tc.smem_deriv = tc.smem_bytes + (int)(sizeof(double) * 4 * V.C * V.STAGES);
+  if (!V.contig && V.C >= 16 && V.SUB == 1 && (vi == 0 || vi == 4 || vi == 13) &&
+      (P.flags & CTRI_FLAG_DERIV)) {
+    tc.smem_deriv = tc.smem_bytes + (int)(sizeof(double) * 4 * V.C * V.SLOTS);
     std::string w2;
     std::swap(w2, *why);
     tc.deriv_ok = setup(true, tc.smem_deriv, &tc.grid_deriv);
@@ -547,8 +620,9 @@ bool tile_configure(Plan& P, std::string* why) {
   if (P.flags & CTRI_FLAG_GENERIC_LOCAL) { *why = "forced generic"; return false; }
   const int f = forced_variant();
   if (f >= 0) return tile_configure_variant(P, f, why);
-  for (int vi : kPreference)
-    if (tile_configure_variant(P, vi, why)) return true;
+  for (int pass = 0; pass < 2; ++pass)  // pass 0: portable clusters only
+    for (int vi : kPreference)
+      if (tile_configure_variant(P, vi, why) && (pass == 1 || P.tile.G <= kMaxCluster)) return true;
   return false;
 }
 
@@ -575,7 +649,7 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   if (deriv && !tc.deriv_ok) return cudaErrorNotSupported;
   EncodeTiledFn enc = get_encode();
   if (!enc) return cudaErrorNotSupported;
-  const Layout& L = P.lay;
+  const Layout& L = P.tlay;
   const int rows_cta = (tc.NT / tc.C) * tc.K;
   CUtensorMap map, hmap;
   std::memset(&map, 0, sizeof(map));
@@ -583,7 +657,7 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   if (!tc.contig) {
     cuuint64_t gdim[3] = {(cuuint64_t)L.inner, (cuuint64_t)L.n, (cuuint64_t)L.outer};
     cuuint64_t gstride[2] = {(cuuint64_t)L.inner * 8, (cuuint64_t)(L.n * L.inner * 8)};
-    cuuint32_t box[3] = {(cuuint32_t)tc.C, (cuuint32_t)std::min(rows_cta, 256), 1};
+    cuuint32_t box[3] = {(cuuint32_t)tc.C, (cuuint32_t)std::min(rows_cta / tc.SUB, 256), 1};
     cuuint32_t hbox[3] = {(cuuint32_t)tc.C, 2, 1};  // stencil halo rows (fused derivative)
     cuuint32_t estr[3] = {1, 1, 1};
     CUtensorMapL2promotion prom = CU_TENSOR_MAP_L2_PROMOTION_NONE;
@@ -612,10 +686,22 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   A.Q = tc.Q;
   A.G = tc.G;
   A.rows_per_cta = rows_cta;
-  A.rows_box = std::min(rows_cta, 256);
+  A.rows_box = std::min(rows_cta / tc.SUB, 256);
   A.stages = tc.pcr.stages;
-  A.mode = (P.p > 1) ? 1 : (P.cyclic ? 0 : 2);
+  A.mode = (P.p > 1 || P.vp > 1) ? 1 : (P.cyclic ? 0 : 2);
   if (std::getenv("CTRI_TILE_COPY_ONLY")) A.mode = 3;  // measurement knob: memory ceiling
+  A.pcr_uniform = tc.pcr_uniform ? 1 : 0;
+  for (int k = 0; k < kMaxUniformStages; ++k) {
+    A.ualpha[k] = (tc.pcr_uniform && k < tc.pcr.stages) ? tc.pcr.alpha[(size_t)k * tc.Q] : 0.0;
+    A.ugamma[k] = (tc.pcr_uniform && k < tc.pcr.stages) ? tc.pcr.gamma[(size_t)k * tc.Q] : 0.0;
+  }
+  A.uinv = tc.pcr.inv[0];
+  A.trace = nullptr;
+  if (std::getenv("CTRI_TILE_TRACE")) {  // measurement only
+    static unsigned long long* d_tr = nullptr;
+    if (!d_tr) cudaMalloc(&d_tr, 64 * 8 * sizeof(unsigned long long));
+    A.trace = d_tr;
+  }
   A.pcr_alpha = tc.d_pcr;
   A.pcr_gamma = tc.d_pcr + (size_t)tc.pcr.stages * tc.Q;
   A.pcr_inv = tc.d_pcr + (size_t)2 * tc.pcr.stages * tc.Q;
@@ -628,7 +714,28 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   // partition they are this slab's own rows (periodic wrap), packed into send_hi / send_lo
   A.halo_lo = (P.p == 1) ? P.send_hi : P.halo_lo;
   A.halo_hi = (P.p == 1) ? P.send_lo : P.halo_hi;
-  return dispatch(tc, deriv, map, hmap, A, s, false);
+  cudaError_t e = dispatch(tc, deriv, map, hmap, A, s, false);
+  if (A.trace && e == cudaSuccess) {  // measurement only: print CTA 0's per-phase averages
+    std::vector<unsigned long long> h(64 * 8);
+    cudaMemcpyAsync(h.data(), A.trace, h.size() * 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double acc[8] = {0};
+    int cnt = 0;
+    for (int i = 4; i < 60; ++i) {
+      if (!h[i * 8 + 6] || !h[(i + 1) * 8]) break;
+      for (int k = 1; k <= 6; ++k) acc[k] += (double)(h[i * 8 + k] - h[i * 8 + k - 1]);
+      acc[7] += (double)(h[(i + 1) * 8] - h[i * 8 + 6]);
+      ++cnt;
+    }
+    if (cnt)
+      std::fprintf(stderr,
+                   "[tile trace] per tile (ns): ring_wait+lds %.0f thomas %.0f ex_wait %.0f pcr %.0f "
+                   "rx_wait %.0f backsub+store %.0f loop %.0f total %.0f (%d tiles)\n",
+                   acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt,
+                   acc[6] / cnt, acc[7] / cnt,
+                   (acc[1] + acc[2] + acc[3] + acc[4] + acc[5] + acc[6] + acc[7]) / cnt, cnt);
+  }
+  return e;
 }
 
 }  // namespace ctri

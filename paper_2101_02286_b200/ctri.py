@@ -62,7 +62,8 @@ class ctri_stats(ctypes.Structure):
                 ("t_stage_us", ctypes.c_float * CTRI_MAX_STAGES),
                 ("t_xexchange_us", ctypes.c_float), ("t_backsub_us", ctypes.c_float),
                 ("tile_variant", ctypes.c_int32), ("tile_stages", ctypes.c_int32),
-                ("reduced_path", ctypes.c_int32), ("device_error", ctypes.c_int32)]
+                ("reduced_path", ctypes.c_int32), ("device_error", ctypes.c_int32),
+                ("vparts", ctypes.c_int32), ("grid_ctas", ctypes.c_int32)]
 
     def as_dict(self):
         d = {}

@@ -3,7 +3,7 @@
 cfg=${1:-cfg2}
 steps=${2:-300}
 mkdir -p gpurun_out
-for v in c16t512s1 c8t512s1 c4t512s1 c8t256s1 c16t256s1; do
+for v in ${VARIANTS:-c16t512s1 c16t256s1 c16t256x3 c16t512x5 c16t256x6}; do
   echo "== $v" >> gpurun_out/sweep_$cfg.log
   CTRI_TILE_VARIANT=$v timeout 300 python bench.py --config $cfg --steps $steps --warmup 10 \
       --no-cpu-baseline --no-e2e >> gpurun_out/sweep_$cfg.log 2>&1
