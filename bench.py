@@ -225,7 +225,7 @@ def load_traffic(cfg, p):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             d = json.load(fh)
-        return d.get(f"{cfg}_p{p}")
+        return d.get(f"{cfg}_p{p}")  # dram read+write bytes per launch of the dominant kernel
     except Exception:
         return None
 

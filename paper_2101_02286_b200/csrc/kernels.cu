@@ -127,7 +127,15 @@ struct LocalRedArgs {
   double alpha[4 * 8], gamma[4 * 8], inv[8];  // [stage][row], vp <= 8
 };
 
-__global__ void k_reduced_local(const LocalRedArgs A, double* __restrict__ x) {
+__device__ __forceinline__ double bh_get(const double (&bh)[8], int v) {
+  double r = bh[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i)
+    if (v == i) r = bh[i];
+  return r;
+}
+
+__global__ void __launch_bounds__(128) k_reduced_local(const LocalRedArgs A, double* __restrict__ x) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t m = A.outer * A.inner;
   if (j >= m) return;
@@ -163,24 +171,37 @@ __global__ void k_reduced_local(const LocalRedArgs A, double* __restrict__ x) {
   for (int v = 0; v < 8; ++v)
     if (v < vp) bh[v] *= A.inv[v];
   const int64_t rows = A.full ? A.nv - 1 : 2 * A.W;
-  for (int v = 0; v < 8; ++v) {
-    if (v >= vp) break;
-    const double xa = bh[v];
-    const double xn = (A.cyclic || v + 1 < vp) ? bh[(v + 1) % vp] : 0.0;
-    double* xc = x + ((o * vp + v) * A.nv) * A.inner + c;
-    xc[0] = xa;
-    for (int64_t r0 = 0; r0 < rows; r0 += 8) {
-      double val[8];
-      int64_t rr[8];
+  // window back-substitution of every virtual slab: groups of 4 slabs x 4 rows = 16 loads
+  for (int v0 = 0; v0 < vp; v0 += 4) {
+    double* xc[4];
+    double xa[4], xn[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+    for (int i = 0; i < 4; ++i) {
+      const int v = (v0 + i < vp) ? v0 + i : v0;
+      xa[i] = bh_get(bh, v);
+      xn[i] = (A.cyclic || v + 1 < vp) ? bh_get(bh, (v + 1) % vp) : 0.0;
+      xc[i] = x + ((o * vp + v) * A.nv) * A.inner + c;
+      if (v0 + i < vp) xc[i][0] = xa[i];
+    }
+    for (int64_t r0 = 0; r0 < rows; r0 += 4) {
+      double val[4][4];
+      int64_t rr[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
         const int64_t ry = r0 + u;
         rr[u] = A.full ? ry + 1 : (ry < A.W ? ry + 1 : A.nv - 2 * A.W + ry);
-        if (ry < rows) val[u] = xc[rr[u] * A.inner];
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (r0 + u < rows) xc[rr[u] * A.inner] = val[u] - A.S[rr[u] - 1] * xa - A.R[rr[u] - 1] * xn;
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (v0 + i < vp && r0 + u < rows) val[i][u] = xc[i][rr[u] * A.inner];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (v0 + i < vp && r0 + u < rows)
+            xc[i][rr[u] * A.inner] = val[i][u] - A.S[rr[u] - 1] * xa[i] - A.R[rr[u] - 1] * xn[i];
     }
   }
 }

@@ -37,7 +37,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 constexpr int kP2PThreads = 256;
-constexpr int kMaxCpt = 8;  // columns per thread
+constexpr int kMaxCpt = 4;  // columns per thread (compile-time indexed: registers only)
 
 // LL send: value + epoch tag as two 8-byte words in one 16-byte store (peer memory).
 __device__ __forceinline__ void ll_send(unsigned long long* dst, double v, uint32_t ep) {
@@ -96,16 +96,25 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
   double bh[kMaxCpt];
   int64_t col[kMaxCpt];
   int nc = 0;
-  for (int64_t j = c0 + threadIdx.x; j < c1 && nc < kMaxCpt; j += kP2PThreads) col[nc++] = j;
+#pragma unroll
+  for (int i = 0; i < kMaxCpt; ++i) {
+    const int64_t j = c0 + threadIdx.x + (int64_t)i * kP2PThreads;
+    col[i] = j;
+    if (j < c1) nc = i + 1;
+  }
   bool ok = true;
 
   // ---- (a2) y_i[last] -> right neighbour; b^ ----
   if (right >= 0) {
     unsigned long long* dst = R.peer_mbox[right] + copy_off + OFF_Y;
-    for (int i = 0; i < nc; ++i) ll_send(dst + 2 * col[i], R.yl[col[i]], ep);
+#pragma unroll
+    for (int i = 0; i < kMaxCpt; ++i)
+      if (i < nc) ll_send(dst + 2 * col[i], R.yl[col[i]], ep);
   }
   stamp(1);
-  for (int i = 0; i < nc; ++i) {
+#pragma unroll
+  for (int i = 0; i < kMaxCpt; ++i) {
+    if (i >= nc) continue;
     const int64_t j = col[i];
     double ylp = 0.0;
     if (left >= 0) ok = ok && ll_recv(mine + OFF_Y + 2 * j, ep, deadline, &ylp);
@@ -127,14 +136,20 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
     // my b^ is the "from i-s" message (slot 0) of rank lp and the "from i+s" one (slot 1) of lm
     if (lp >= 0) {
       unsigned long long* dst = R.peer_mbox[lp] + copy_off + OFF_S(k, 0);
-      for (int i = 0; i < nc; ++i) ll_send(dst + 2 * col[i], bh[i], ep);
+#pragma unroll
+      for (int i = 0; i < kMaxCpt; ++i)
+        if (i < nc) ll_send(dst + 2 * col[i], bh[i], ep);
     }
     if (lm >= 0 && !single) {
       unsigned long long* dst = R.peer_mbox[lm] + copy_off + OFF_S(k, 1);
-      for (int i = 0; i < nc; ++i) ll_send(dst + 2 * col[i], bh[i], ep);
+#pragma unroll
+      for (int i = 0; i < kMaxCpt; ++i)
+        if (i < nc) ll_send(dst + 2 * col[i], bh[i], ep);
     }
     const double a = R.alpha[k], g = R.gamma[k];
-    for (int i = 0; i < nc && ok; ++i) {
+#pragma unroll
+    for (int i = 0; i < kMaxCpt; ++i) {
+      if (i >= nc || !ok) continue;
       const int64_t j = col[i];
       double vm = 0.0, vp = 0.0;
       if (lm >= 0) ok = ok && ll_recv(mine + OFF_S(k, 0) + 2 * j, ep, deadline, &vm);
@@ -146,16 +161,20 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
     }
   }
   stamp(3);
-  for (int i = 0; i < nc; ++i) bh[i] *= R.inv;  // x~_i
+#pragma unroll
+  for (int i = 0; i < kMaxCpt; ++i) bh[i] *= R.inv;  // x~_i
   // ---- (a4) x~_i -> left neighbour; back-substitution on the window ----
   if (ok && left >= 0) {
     unsigned long long* dst = R.peer_mbox[left] + copy_off + OFF_X;
-    for (int i = 0; i < nc; ++i) ll_send(dst + 2 * col[i], bh[i], ep);
+#pragma unroll
+    for (int i = 0; i < kMaxCpt; ++i)
+      if (i < nc) ll_send(dst + 2 * col[i], bh[i], ep);
   }
   double xb[kMaxCpt];
-  for (int i = 0; i < nc && ok; ++i) {
+#pragma unroll
+  for (int i = 0; i < kMaxCpt; ++i) {
     xb[i] = 0.0;
-    if (right >= 0) ok = ok && ll_recv(mine + OFF_X + 2 * col[i], ep, deadline, &xb[i]);
+    if (i < nc && ok && right >= 0) ok = ll_recv(mine + OFF_X + 2 * col[i], ep, deadline, &xb[i]);
   }
   if (!ok) {
     atomicExch(A.err, 1);
@@ -164,30 +183,49 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
   stamp(4);
   const int64_t n = A.lay.n, inner = A.lay.inner;
   const int64_t rows = A.full ? n - 1 : 2 * A.W;  // interior rows touched
-  for (int i = 0; i < nc; ++i) {
-    const int64_t j = col[i];
-    const double xa = bh[i], xn = xb[i];
-    const int64_t o = j / inner, c = j - o * inner;
-    double* xc = R.x + o * n * inner + c;
-    xc[0] = xa;
-    // 8 independent loads in flight per column, then the updates (memory-level parallelism)
-    for (int64_t r0 = 0; r0 < rows; r0 += 8) {
-      double v[8];
-      int64_t rr[8];
+  // window back-substitution: kMaxCpt (4) columns x 4 rows = 16 independent loads in flight
+  double* xc[kMaxCpt];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+  for (int i = 0; i < kMaxCpt; ++i) {
+    const int64_t j = col[i] < m ? col[i] : 0;
+    const int64_t o = j / inner, c = j - o * inner;
+    xc[i] = R.x + o * n * inner + c;
+    if (i < nc) xc[i][0] = bh[i];
+  }
+  if (nc == 1) {  // one column per thread: 16 rows per batch
+    for (int64_t r0 = 0; r0 < rows; r0 += 16) {
+      double v[16];
+      int64_t rr[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
         const int64_t ry = r0 + u;
         rr[u] = A.full ? ry + 1 : (ry < A.W ? ry + 1 : n - 2 * A.W + ry);
-        if (ry < rows) v[u] = xc[rr[u] * inner];
+        if (ry < rows) v[u] = xc[0][rr[u] * inner];
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (r0 + u < rows) {
-          const int64_t r = rr[u];
-          xc[r * inner] = v[u] - A.S[r - 1] * xa - A.R[r - 1] * xn;
-        }
-      }
+      for (int u = 0; u < 16; ++u)
+        if (r0 + u < rows) xc[0][rr[u] * inner] = v[u] - A.S[rr[u] - 1] * bh[0] - A.R[rr[u] - 1] * xb[0];
     }
+  } else
+  for (int64_t r0 = 0; r0 < rows; r0 += 4) {
+    double v[kMaxCpt][4];
+    int64_t rr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t ry = r0 + u;
+      rr[u] = A.full ? ry + 1 : (ry < A.W ? ry + 1 : n - 2 * A.W + ry);
+    }
+#pragma unroll
+    for (int i = 0; i < kMaxCpt; ++i)
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i < nc && r0 + u < rows) v[i][u] = xc[i][rr[u] * inner];
+#pragma unroll
+    for (int i = 0; i < kMaxCpt; ++i)
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i < nc && r0 + u < rows)
+          xc[i][rr[u] * inner] = v[i][u] - A.S[rr[u] - 1] * bh[i] - A.R[rr[u] - 1] * xb[i];
   }
   if (tr) {
     __syncthreads();

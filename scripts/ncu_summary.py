@@ -33,8 +33,10 @@ def summarise(rep):
         wr = num(d.get("dram__bytes_write.sum"))
         u_dur = units.get("gpu__time_duration.sum")
         u_b = units.get("dram__bytes_read.sum")
-        scale_b = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u_b, 1)
-        scale_t = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1}.get(u_dur, 1)
+        scale_b = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6,
+                   "GB": 1e9}.get(u_b, 1)
+        scale_t = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1, "ns": 1e-9,
+                   "us": 1e-6, "ms": 1e-3, "s": 1}.get(u_dur, 1)
         res.append({
             "kernel": d.get("Kernel Name", "")[:80],
             "grid": d.get("launch__grid_size"), "block": d.get("launch__block_size"),
@@ -45,7 +47,7 @@ def summarise(rep):
             "dram_write_bytes": wr * scale_b if wr else None,
             "dram_GBps": ((rd + wr) * scale_b / (dur * scale_t) / 1e9) if (rd and wr and dur) else None,
             "dram_pct_peak": num(d.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")),
-            "sm_active_pct": None,
+            "units": {"duration": u_dur, "bytes": u_b},
             "achieved_occupancy": num(d.get("sm__warps_active.avg.pct_of_peak_sustained_active")),
             "stalls_pct": {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): round(100 * v / tot, 1) for k, v in top},
         })
