@@ -50,7 +50,7 @@ typedef struct CUstream_st* ctri_stream; /* == cudaStream_t */
 typedef enum ctri_status {
   CTRI_OK = 0,
   CTRI_ERR_INVALID_ARG = 1,     /* bad pointer, dims, solve_dim, rank, alignment */
-  CTRI_ERR_UNSUPPORTED = 2,     /* e.g. cyclic with non-power-of-two nparts (detach/reattach not built) */
+  CTRI_ERR_UNSUPPORTED = 2,     /* e.g. cyclic non-power-of-two nparts with CTRI_FLAG_NCCL_ROUNDS */
   CTRI_ERR_SINGULAR = 3,        /* plan-time pivot guard: |pivot| < 1e-13 * max|band| */
   CTRI_ERR_PARTITION_TOO_SMALL = 4, /* n = N/nparts < 3 or N not divisible by nparts */
   CTRI_ERR_CUDA = 5,            /* a CUDA runtime call or kernel launch failed */
@@ -98,6 +98,8 @@ typedef struct ctri_stats {
   int32_t vparts;               /* nparts == 1: partitions of the slab solved on this GPU (the
                                    paper's partition method; (a2)-(a4) then run on-device) */
   int32_t grid_ctas;            /* CTAs of the local-solve launch */
+  int32_t detach_stages;        /* nparts > 1 cyclic, not a power of two: detach stages */
+  int32_t detached_rows;        /* rows detached and reattached: nparts - 2^floor(log2 nparts) */
 } ctri_stats;
 
 /* Human-readable status name; never NULL. */
@@ -123,8 +125,8 @@ ctri_status ctri_get_unique_id(void* out128);
  *   nccl_unique_id  128-byte ncclUniqueId shared by all ranks; NULL iff nparts == 1.
  *   flags        CTRI_FLAG_*.
  *   stream       stream used for the table uploads during create.
- * Errors: INVALID_ARG, PARTITION_TOO_SMALL, UNSUPPORTED (cyclic with non-power-of-two
- * nparts), SINGULAR (pivot guard), CUDA, NCCL, OOM.  On error *out is NULL.
+ * Errors: INVALID_ARG, PARTITION_TOO_SMALL, UNSUPPORTED (cyclic non-power-of-two nparts on the
+ * NCCL-rounds path or nparts > 8), SINGULAR (pivot guard), CUDA, NCCL, OOM.  On error *out is NULL.
  * The plan owns its device tables, plane buffers, events and NCCL communicator. */
 ctri_status ctri_plan_create(ctri_plan* out, const int64_t global_dims[3], int solve_dim,
                              int nparts, int rank, const double bands[3], int cyclic,
@@ -197,6 +199,18 @@ ctri_status ctri_factor_query(int64_t n, const double bands[3], double* S, doubl
 ctri_status ctri_pcr_coefficients(int P, int cyclic, const double* L, const double* D,
                                   const double* U, double* alpha, double* gamma, double* inv,
                                   int* stages);
+
+/* Reduced-system schedule of nparts = P rows (one per rank): power-of-two cyclic and all acyclic
+ * systems use PCR; cyclic systems of any other dimension use the paper's
+ * detach / PCR / fold / reattach procedure (worked 11x11 example P:294).  Step s, row i:
+ *     v_i <- w[s*P+i] v_i - c[2(s*P+i)] v_{src[2(s*P+i)]} - c[2(s*P+i)+1] v_{src[2(s*P+i)+1]}
+ * with synchronous semantics (src = -1: no term); v starts as b^ and ends as x~.
+ * kinds[s]: 0 detach, 1 PCR, 2 fold, 3 reattach.  counts[3] = {PCR stages, detach stages,
+ * detached rows}.  Arrays hold max_steps*P (w) and 2*max_steps*P (src, c) entries.
+ * Errors: INVALID_ARG (sizes, max_steps too small), SINGULAR (pivot guard). */
+ctri_status ctri_reduced_schedule(int P, int cyclic, const double* L, const double* D,
+                                  const double* U, int max_steps, int* nsteps, int* kinds,
+                                  double* w, int* src, double* c, int* counts);
 
 #ifdef __cplusplus
 }

@@ -8,7 +8,7 @@ from .ctri import (CTRI_FLAG_DERIV, CTRI_FLAG_FULL_BACKSUB, CTRI_FLAG_GENERIC_LO
                    CTRI_FLAG_NCCL_ROUNDS,
                    CTRI_FLAG_TIMING, CtriError, LoopbackGroup, Plan, ctri_deriv,
                    ctri_deriv_loopback, ctri_factor_query, ctri_get_stats, ctri_get_unique_id,
-                   ctri_pcr_coefficients, ctri_plan_create, ctri_plan_create_loopback,
+                   ctri_pcr_coefficients, ctri_plan_create, ctri_reduced_schedule, ctri_plan_create_loopback,
                    ctri_plan_destroy, ctri_solve, ctri_solve_host, ctri_solve_loopback, load,
                    local_shape)
 

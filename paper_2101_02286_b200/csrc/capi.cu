@@ -100,9 +100,10 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
     return fail(CTRI_ERR_PARTITION_TOO_SMALL, "N is not divisible by nparts (equal split, P:5)");
   const int64_t n = gd[sd] / p;
   if (n < 3) return fail(CTRI_ERR_PARTITION_TOO_SMALL, "n = N/nparts < 3 (N_i = n-1 >= 2r)");
-  if (cyclic && !is_pow2(p))
+  if (cyclic && !is_pow2(p) && (p > kMaxP2PRanks || (flags & CTRI_FLAG_NCCL_ROUNDS)))
     return fail(CTRI_ERR_UNSUPPORTED,
-                "cyclic solve with non-power-of-two nparts needs detach/reattach (P:271), not built");
+                "cyclic non-power-of-two nparts: detach/reattach (P:271) runs in the fused P2P path "
+                "only (nparts <= 16, without CTRI_FLAG_NCCL_ROUNDS)");
   std::memcpy(P->gdims, gd, sizeof(P->gdims));
   P->sd = sd;
   P->p = p;
@@ -145,8 +146,20 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
     D[i] = P->bands.d - (lft ? P->bands.l * pt.R[last] : 0.0) - P->bands.u * pt.S[0];  // Eq. Di_hat
     U[i] = rgt ? -P->bands.u * pt.R[0] : 0.0;                                    // Eq. Ui_hat
   }
-  if (!pcr_factor(pr, cyclic != 0, L, D, U, pivot_threshold(P->bands), &P->gpcr, &fe))
+  // reduced-system schedule (PCR, or detach/PCR/fold/reattach for cyclic non-power-of-two p)
+  if (!reduced_schedule(pr, cyclic != 0, L, D, U, pivot_threshold(P->bands), &P->sched, &fe))
     return fail((ctri_status)fe.code, fe.detail);
+  if ((int)P->sched.steps.size() > kMaxP2PSteps)
+    return fail(CTRI_ERR_UNSUPPORTED, "reduced-system schedule too long");
+  if (!cyclic || is_pow2(pr)) {  // stride-PCR multipliers for the NCCL-rounds / local kernels
+    if (!pcr_factor(pr, cyclic != 0, L, D, U, pivot_threshold(P->bands), &P->gpcr, &fe))
+      return fail((ctri_status)fe.code, fe.detail);
+  } else {
+    P->gpcr = PcrTables();
+    P->gpcr.P = pr;
+    P->gpcr.stages = P->sched.pcr_stages;
+    P->gpcr.inv.assign(pr, 0.0);
+  }
   if (P->gpcr.stages > CTRI_MAX_STAGES) return fail(CTRI_ERR_UNSUPPORTED, "too many PCR stages");
   P->inv_closure = P->gpcr.inv[0];
   P->window = backsub_window(pt);
@@ -175,7 +188,7 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   }
   if (p > 1 && p <= kMaxP2PRanks && !(flags & CTRI_FLAG_NCCL_ROUNDS)) {
     // fused device-initiated reduced phase: double-buffered mailbox + epoch flags
-    const int q = P->gpcr.stages;
+    const int q = (int)P->sched.steps.size();
     P->p2p_nslices = p2p_slices(m, P->loopback ? p : 1, P->num_sms);
     P->mbox_bytes = sizeof(unsigned long long) * p2p_mailbox_words(m, q);
     CUDA_TRY(cudaMalloc(&P->mbox_alloc, P->mbox_bytes));
@@ -237,7 +250,6 @@ ctri_status p2p_connect_ipc(Plan* P, cudaStream_t s) {
 }
 
 void p2p_fill_rank(const Plan& P, double* x, P2PRank* R) {
-  const int q = P.gpcr.stages;
   R->rank = P.rank;
   R->x = x;
   R->yf = P.yf;
@@ -246,11 +258,43 @@ void p2p_fill_rank(const Plan& P, double* x, P2PRank* R) {
   R->mbox = reinterpret_cast<unsigned long long*>(P.mbox_alloc);
   for (int r = 0; r < kMaxP2PRanks; ++r) R->peer_mbox[r] = nullptr;
   for (int r = 0; r < P.p; ++r) R->peer_mbox[r] = reinterpret_cast<unsigned long long*>(P.peer_alloc[r]);
-  for (int k = 0; k < CTRI_MAX_STAGES; ++k) {
-    R->alpha[k] = k < q ? P.gpcr.alpha[(size_t)k * P.p + P.rank] : 0.0;
-    R->gamma[k] = k < q ? P.gpcr.gamma[(size_t)k * P.p + P.rank] : 0.0;
+  const Schedule& sc = P.sched;
+  for (int s = 0; s < kMaxP2PSteps; ++s) {
+    P2PStep& t = R->step[s];
+    t = P2PStep{1.0, 0.0, 0.0, -1, -1, -1, -1, 0, 0};
+    if (s >= (int)sc.steps.size()) continue;
+    const SchedEntry& e = sc.steps[s][P.rank];
+    t.w = e.w;
+    t.c0 = e.c[0];
+    t.c1 = e.c[1];
+    t.src0 = (int8_t)e.src[0];
+    t.src1 = (int8_t)e.src[1];
+    int nd = 0;  // ranks that read this rank's value in step s, and their slot
+    for (int i = 0; i < P.p; ++i)
+      for (int k = 0; k < 2; ++k)
+        if (sc.steps[s][i].src[k] == P.rank) {
+          if (nd == 0) { t.dst0 = (int8_t)i; t.dslot0 = (int8_t)k; }
+          else { t.dst1 = (int8_t)i; t.dslot1 = (int8_t)k; }
+          ++nd;
+        }
   }
-  R->inv = P.gpcr.inv[P.rank];
+}
+
+// messages this rank sends per solve, and dependent exchange rounds, from the schedule
+void schedule_counts(const Plan& P, int* sends, int* rounds) {
+  const Schedule& sc = P.sched;
+  int sd = (has_right(P) ? 1 : 0) + (has_left(P) ? 1 : 0), rd = 2;
+  for (size_t s = 0; s < sc.steps.size(); ++s) {
+    bool any = false;
+    for (int i = 0; i < P.p; ++i)
+      for (int k = 0; k < 2; ++k) {
+        if (sc.steps[s][i].src[k] >= 0) any = true;
+        if (sc.steps[s][i].src[k] == P.rank) ++sd;
+      }
+    rd += any ? 1 : 0;
+  }
+  *sends = sd;
+  *rounds = rd;
 }
 
 // ---------------- exchanges ----------------
@@ -392,7 +436,7 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
     P2PArgs A;
     std::memset(&A, 0, sizeof(A));
     A.p = P0.p;
-    A.q = P0.gpcr.stages;
+    A.q = (int)P0.sched.steps.size();
     A.cyclic = P0.cyclic;
     A.nslices = P0.p2p_nslices;
     A.m = P0.lay.m();
@@ -669,12 +713,13 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
   out->chunk_heads = P->local_kernel ? P->tile.Q : 1;
   const bool full = (P->flags & CTRI_FLAG_FULL_BACKSUB) || (2 * P->window >= P->tlay.n - 1);
   out->window_rows = (int32_t)(full ? P->tlay.n - 1 : P->window);
-  out->pcr_stages = P->gpcr.stages;
+  out->pcr_stages = P->sched.pcr_stages;
+  out->detach_stages = P->sched.detach_stages;
+  out->detached_rows = P->sched.detached_rows;
   if (P->p > 1) {
-    out->comm_rounds = 2 + P->gpcr.stages;
-    int sends = (has_right(*P) ? 1 : 0) + (has_left(*P) ? 1 : 0);
-    for (int k = 0; k < P->gpcr.stages; ++k)
-      for (const Xfer& x : round_stage(*P, k)) sends += (x.send_to >= 0);
+    int sends = 0, rounds = 0;
+    schedule_counts(*P, &sends, &rounds);
+    out->comm_rounds = rounds;
     out->sends_per_solve = sends;
     out->bytes_sent_per_solve = (int64_t)sends * 8 * P->lay.m();
   }
@@ -758,6 +803,39 @@ ctri_status ctri_pcr_coefficients(int P, int cyclic, const double* L, const doub
   if (alpha) std::memcpy(alpha, t.alpha.data(), sizeof(double) * t.alpha.size());
   if (gamma) std::memcpy(gamma, t.gamma.data(), sizeof(double) * t.gamma.size());
   std::memcpy(inv, t.inv.data(), sizeof(double) * P);
+  return CTRI_OK;
+}
+
+ctri_status ctri_reduced_schedule(int P, int cyclic, const double* L, const double* D,
+                                  const double* U, int max_steps, int* nsteps, int* kinds,
+                                  double* w, int* src, double* c, int* counts) {
+  if (P < 1 || !L || !D || !U || !nsteps || !kinds || !w || !src || !c || !counts)
+    return fail(CTRI_ERR_INVALID_ARG, "bad arguments");
+  double mx = 0;
+  for (int i = 0; i < P; ++i)
+    mx = std::max(mx, std::max(std::fabs(D[i]), std::max(std::fabs(L[i]), std::fabs(U[i]))));
+  Schedule sc;
+  FactorError fe;
+  if (!reduced_schedule(P, cyclic != 0, std::vector<double>(L, L + P), std::vector<double>(D, D + P),
+                        std::vector<double>(U, U + P), 1e-13 * mx, &sc, &fe))
+    return fail((ctri_status)fe.code, fe.detail);
+  const int ns = (int)sc.steps.size();
+  if (ns > max_steps) return fail(CTRI_ERR_INVALID_ARG, "max_steps too small");
+  *nsteps = ns;
+  for (int s = 0; s < ns; ++s) {
+    kinds[s] = sc.kind[s];
+    for (int i = 0; i < P; ++i) {
+      const SchedEntry& e = sc.steps[s][i];
+      w[(size_t)s * P + i] = e.w;
+      for (int k = 0; k < 2; ++k) {
+        src[2 * ((size_t)s * P + i) + k] = e.src[k];
+        c[2 * ((size_t)s * P + i) + k] = e.c[k];
+      }
+    }
+  }
+  counts[0] = sc.pcr_stages;
+  counts[1] = sc.detach_stages;
+  counts[2] = sc.detached_rows;
   return CTRI_OK;
 }
 

@@ -144,4 +144,156 @@ bool pcr_factor(int P, bool cyclic, const std::vector<double>& L0, const std::ve
   return true;
 }
 
+bool reduced_schedule(int P, bool cyclic, const std::vector<double>& L0,
+                      const std::vector<double>& D0, const std::vector<double>& U0, double guard,
+                      Schedule* out, FactorError* err) {
+  *out = Schedule();
+  out->P = P;
+  out->cyclic = cyclic;
+  if (P < 1 || (int)L0.size() != P || (int)D0.size() != P || (int)U0.size() != P)
+    return fail(err, kInvalid, "reduced_schedule: bad sizes");
+  if (!cyclic || is_pow2(P)) {  // stride PCR (pcr_factor), then the final scaling
+    PcrTables t;
+    if (!pcr_factor(P, cyclic, L0, D0, U0, guard, &t, err)) return false;
+    const int q = t.stages;
+    for (int k = 0; k < q; ++k) {
+      const int s = 1 << k;
+      std::vector<SchedEntry> st(P);
+      for (int c = 0; c < P; ++c) {
+        int lm = c - s, lp = c + s;
+        if (cyclic) {
+          lm = ((lm % P) + P) % P;
+          lp = lp % P;
+        } else {
+          if (lm < 0) lm = -1;
+          if (lp >= P) lp = -1;
+        }
+        const double a = t.alpha[(size_t)k * P + c], g = t.gamma[(size_t)k * P + c];
+        if (lm >= 0 && lm == lp) {  // single partner (s = P/2)
+          st[c].src[0] = lm;
+          st[c].c[0] = a + g;
+        } else {
+          if (lm >= 0) { st[c].src[0] = lm; st[c].c[0] = a; }
+          if (lp >= 0) { st[c].src[1] = lp; st[c].c[1] = g; }
+        }
+      }
+      out->kind.push_back(kStepPcr);
+      out->steps.push_back(st);
+    }
+    std::vector<SchedEntry> fold(P);
+    for (int c = 0; c < P; ++c) fold[c].w = t.inv[c];
+    out->kind.push_back(kStepFold);
+    out->steps.push_back(fold);
+    out->pcr_stages = q;
+    return true;
+  }
+  // ---- cyclic, P not a power of two: detach / PCR / fold / reattach ----
+  // Every row keeps coefficients on its previous (Lc) and next (Uc) row within its current
+  // cyclic sub-system; the two may alias (dimension 2).
+  std::vector<double> Lc = L0, Dc = D0, Uc = U0;
+  std::vector<std::vector<int>> subs(1);
+  for (int i = 0; i < P; ++i) subs[0].push_back(i);
+  struct Det { int z, y, a; double Lz, Dz, Uz; };
+  std::vector<std::vector<Det>> levels;
+  auto check = [&](double v) -> bool {
+    if (!(std::fabs(v) >= guard)) return fail(err, kSingular, "reduced_schedule: pivot guard");
+    return true;
+  };
+  while (subs[0].size() > 1) {
+    const int d = (int)subs[0].size();
+    if (d % 2) {  // detach the last row of every sub-system
+      std::vector<SchedEntry> st(P);
+      std::vector<Det> lv;
+      std::vector<int> rows;
+      for (auto& sub : subs) {
+        const int z = sub[d - 1], y = sub[d - 2], a = sub[0];
+        if (!check(Dc[z])) return false;
+        const double cy = Uc[y] / Dc[z];  // row y: upper off-diagonal on z
+        const double ca = Lc[a] / Dc[z];  // row a: lower off-diagonal on z (cyclic wrap)
+        st[y].src[0] = z;
+        st[y].c[0] = cy;
+        st[a].src[0] = z;
+        st[a].c[0] = ca;
+        lv.push_back(Det{z, y, a, Lc[z], Dc[z], Uc[z]});
+        rows.push_back(z);
+        // row y - cy * row z: z's lower entry sits on y, its upper entry on a
+        Dc[y] -= cy * Lc[z];
+        const double newUy = -cy * Uc[z];
+        // row a - ca * row z: z's upper entry sits on a, its lower entry on y
+        Dc[a] -= ca * Uc[z];
+        const double newLa = -ca * Lc[z];
+        Uc[y] = newUy;  // y's next row is now a ("placed in the last column")
+        Lc[a] = newLa;  // a's previous row is now y
+        sub.pop_back();
+      }
+      levels.push_back(lv);
+      out->detached.push_back(rows);
+      out->kind.push_back(kStepDetach);
+      out->steps.push_back(st);
+      out->detach_stages++;
+      out->detached_rows += (int)lv.size();
+      continue;
+    }
+    // one PCR step on every (even) sub-system, then split into even / odd positions
+    std::vector<SchedEntry> st(P);
+    std::vector<double> nL = Lc, nD = Dc, nU = Uc;
+    std::vector<std::vector<int>> next;
+    for (auto& sub : subs) {
+      for (int k = 0; k < d; ++k) {
+        const int i = sub[k], pm = sub[(k + d - 1) % d], pn = sub[(k + 1) % d];
+        if (!check(Dc[pm]) || !check(Dc[pn])) return false;
+        const double a = Lc[i] / Dc[pm], g = Uc[i] / Dc[pn];
+        if (pm == pn) {
+          st[i].src[0] = pm;
+          st[i].c[0] = a + g;
+        } else {
+          st[i].src[0] = pm;
+          st[i].c[0] = a;
+          st[i].src[1] = pn;
+          st[i].c[1] = g;
+        }
+        // row pm: Lc on sub[k-2], Uc on i; row pn: Lc on i, Uc on sub[k+2]
+        nL[i] = -a * Lc[pm];
+        nU[i] = -g * Uc[pn];
+        nD[i] = Dc[i] - a * Uc[pm] - g * Lc[pn];
+      }
+      std::vector<int> ev, od;
+      for (int k = 0; k < d; ++k) (k % 2 ? od : ev).push_back(sub[k]);
+      next.push_back(ev);
+      next.push_back(od);
+    }
+    Lc.swap(nL);
+    Dc.swap(nD);
+    Uc.swap(nU);
+    subs.swap(next);
+    out->kind.push_back(kStepPcr);
+    out->steps.push_back(st);
+    out->pcr_stages++;
+  }
+  // fold the wrapped couplings of the 1x1 sub-systems into the diagonal (R3)
+  std::vector<SchedEntry> fold(P);
+  for (auto& sub : subs) {
+    const int i = sub[0];
+    const double dd = Lc[i] + Dc[i] + Uc[i];
+    if (!check(dd)) return false;
+    fold[i].w = 1.0 / dd;
+  }
+  out->kind.push_back(kStepFold);
+  out->steps.push_back(fold);
+  // reattach the detached rows, last level first (rows 9, 10 then row 11)
+  for (int lvl = (int)levels.size() - 1; lvl >= 0; --lvl) {
+    std::vector<SchedEntry> st(P);
+    for (const Det& t : levels[lvl]) {
+      st[t.z].w = 1.0 / t.Dz;
+      st[t.z].src[0] = t.y;
+      st[t.z].c[0] = t.Lz / t.Dz;
+      st[t.z].src[1] = t.a;
+      st[t.z].c[1] = t.Uz / t.Dz;
+    }
+    out->kind.push_back(kStepReattach);
+    out->steps.push_back(st);
+  }
+  return true;
+}
+
 }  // namespace ctri

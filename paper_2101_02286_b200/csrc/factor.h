@@ -57,6 +57,29 @@ struct PcrTables {
 bool pcr_factor(int P, bool cyclic, const std::vector<double>& L, const std::vector<double>& D,
                 const std::vector<double>& U, double guard, PcrTables* out, FactorError* err);
 
+// Reduced-system schedule executed per batch column by the ranks (one row each):
+//   step s, rank i:  v_i <- w * v_i - c[0] * v_{src[0]} - c[1] * v_{src[1]}
+// with synchronous semantics (sources read before the step's updates).  Built from PCR steps
+// for power-of-two cyclic and all acyclic systems, and from the paper's
+// detach / PCR / fold / reattach procedure (worked 11x11 example P:294) for cyclic
+// systems of any other dimension.  All coefficients are RHS-independent.
+enum StepKind { kStepDetach = 0, kStepPcr = 1, kStepFold = 2, kStepReattach = 3 };
+struct SchedEntry {
+  double w = 1.0;
+  int src[2] = {-1, -1};
+  double c[2] = {0.0, 0.0};
+};
+struct Schedule {
+  int P = 0;
+  bool cyclic = true;
+  std::vector<int> kind;                       // per step
+  std::vector<std::vector<SchedEntry>> steps;  // [step][row]
+  std::vector<std::vector<int>> detached;      // rows detached at each detach level
+  int pcr_stages = 0, detach_stages = 0, detached_rows = 0;
+};
+bool reduced_schedule(int P, bool cyclic, const std::vector<double>& L, const std::vector<double>& D,
+                      const std::vector<double>& U, double guard, Schedule* out, FactorError* err);
+
 inline bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 inline int ilog2(int64_t v) {
   int q = 0;

@@ -81,17 +81,25 @@ struct TileConfig {
 };
 
 // ---- fused device-initiated reduced phase (p2p.cu) ----
-constexpr int kMaxP2PRanks = 8;
+constexpr int kMaxP2PRanks = 16;  // real multi-GPU: <= 8 per box; loopback tests up to 16
+constexpr int kMaxP2PSteps = 16;
+// One rank's part of a reduced-system schedule step (factor.h Schedule):
+//   v <- w v - c0 u0 - c1 u1, u_k received in mailbox slot k from rank src_k;
+//   this rank's pre-step v is sent to ranks dst_k, slot dslot_k.
+struct P2PStep {
+  double w, c0, c1;
+  int8_t src0, src1, dst0, dst1, dslot0, dslot1;
+};
 struct P2PRank {
   int rank;
   double* x;
   const double *yf, *yl, *bt;
   unsigned long long* mbox;      // own mailbox of LL words (2 epoch copies)
   unsigned long long* peer_mbox[kMaxP2PRanks];  // every rank's mailbox as addressable here
-  double alpha[CTRI_MAX_STAGES], gamma[CTRI_MAX_STAGES], inv;
+  P2PStep step[kMaxP2PSteps];
 };
 struct P2PArgs {
-  int p, q, cyclic, nslices, full;
+  int p, q, cyclic, nslices, full;  // q = number of schedule steps
   int64_t slice_cols, m, W;
   Layout lay;
   double l, u;
@@ -121,7 +129,8 @@ struct Plan {
 
   // host tables
   Partition part;       // GPU-level S_i, R_i, L^, D^, U^ (p >= 2); (n-1)-row interior
-  PcrTables gpcr;       // GPU-level PCR over the p reduced rows
+  PcrTables gpcr;       // GPU-level PCR over the p reduced rows (power-of-two or acyclic)
+  Schedule sched;       // reduced-system step schedule (PCR / detach / fold / reattach)
   int64_t window = 0;   // rows per end for (a4)
   double inv_closure = 0;  // p = 1 generic path: 1/(L^ + D^ + U^)
 

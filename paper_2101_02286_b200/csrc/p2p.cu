@@ -121,48 +121,33 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
     bh[i] = R.bt[j] - A.l * ylp - A.u * R.yf[j];
   }
   stamp(2);
-  // ---- (a3) PCR stages over the p reduced rows ----
-  for (int k = 0; k < q && ok; ++k) {
-    const int s = 1 << k;
-    int lm = rank - s, lp = rank + s;
-    if (cyc) {
-      lm = ((lm % p) + p) % p;
-      lp = lp % p;
-    } else {
-      if (lm < 0) lm = -1;
-      if (lp >= p) lp = -1;
-    }
-    const bool single = (lm >= 0 && lm == lp);
-    // my b^ is the "from i-s" message (slot 0) of rank lp and the "from i+s" one (slot 1) of lm
-    if (lp >= 0) {
-      unsigned long long* dst = R.peer_mbox[lp] + copy_off + OFF_S(k, 0);
+  // ---- (a3) reduced-system schedule: PCR stages, or detach / PCR / fold /
+  //      reattach for cyclic non-power-of-two p; the fold is the last PCR step ----
+  for (int s = 0; s < q && ok; ++s) {
+    const P2PStep& S = R.step[s];
+    if (S.dst0 >= 0) {
+      unsigned long long* dst = R.peer_mbox[S.dst0] + copy_off + OFF_S(s, S.dslot0);
 #pragma unroll
       for (int i = 0; i < kMaxCpt; ++i)
         if (i < nc) ll_send(dst + 2 * col[i], bh[i], ep);
     }
-    if (lm >= 0 && !single) {
-      unsigned long long* dst = R.peer_mbox[lm] + copy_off + OFF_S(k, 1);
+    if (S.dst1 >= 0) {
+      unsigned long long* dst = R.peer_mbox[S.dst1] + copy_off + OFF_S(s, S.dslot1);
 #pragma unroll
       for (int i = 0; i < kMaxCpt; ++i)
         if (i < nc) ll_send(dst + 2 * col[i], bh[i], ep);
     }
-    const double a = R.alpha[k], g = R.gamma[k];
 #pragma unroll
     for (int i = 0; i < kMaxCpt; ++i) {
       if (i >= nc || !ok) continue;
       const int64_t j = col[i];
-      double vm = 0.0, vp = 0.0;
-      if (lm >= 0) ok = ok && ll_recv(mine + OFF_S(k, 0) + 2 * j, ep, deadline, &vm);
-      if (lp >= 0) {
-        if (single) vp = vm;
-        else ok = ok && ll_recv(mine + OFF_S(k, 1) + 2 * j, ep, deadline, &vp);
-      }
-      bh[i] = bh[i] - a * vm - g * vp;
+      double u0 = 0.0, u1 = 0.0;
+      if (S.src0 >= 0) ok = ok && ll_recv(mine + OFF_S(s, 0) + 2 * j, ep, deadline, &u0);
+      if (S.src1 >= 0) ok = ok && ll_recv(mine + OFF_S(s, 1) + 2 * j, ep, deadline, &u1);
+      bh[i] = S.w * bh[i] - S.c0 * u0 - S.c1 * u1;
     }
   }
   stamp(3);
-#pragma unroll
-  for (int i = 0; i < kMaxCpt; ++i) bh[i] *= R.inv;  // x~_i
   // ---- (a4) x~_i -> left neighbour; back-substitution on the window ----
   if (ok && left >= 0) {
     unsigned long long* dst = R.peer_mbox[left] + copy_off + OFF_X;

@@ -34,7 +34,8 @@ STATUS = {0: "CTRI_OK", 1: "CTRI_ERR_INVALID_ARG", 2: "CTRI_ERR_UNSUPPORTED", 3:
 ABI_SYMBOLS = ("ctri_status_string", "ctri_last_error", "ctri_abi_version", "ctri_get_unique_id",
                "ctri_plan_create", "ctri_plan_create_loopback", "ctri_solve", "ctri_solve_loopback",
                "ctri_solve_host", "ctri_deriv", "ctri_deriv_loopback", "ctri_get_stats",
-               "ctri_plan_destroy", "ctri_factor_query", "ctri_pcr_coefficients")
+               "ctri_plan_destroy", "ctri_factor_query", "ctri_pcr_coefficients",
+               "ctri_reduced_schedule")
 
 
 class CtriError(RuntimeError):
@@ -63,7 +64,8 @@ class ctri_stats(ctypes.Structure):
                 ("t_xexchange_us", ctypes.c_float), ("t_backsub_us", ctypes.c_float),
                 ("tile_variant", ctypes.c_int32), ("tile_stages", ctypes.c_int32),
                 ("reduced_path", ctypes.c_int32), ("device_error", ctypes.c_int32),
-                ("vparts", ctypes.c_int32), ("grid_ctas", ctypes.c_int32)]
+                ("vparts", ctypes.c_int32), ("grid_ctas", ctypes.c_int32),
+                ("detach_stages", ctypes.c_int32), ("detached_rows", ctypes.c_int32)]
 
     def as_dict(self):
         d = {}
@@ -116,6 +118,10 @@ def load(build_if_missing: bool = False):
         "ctri_plan_destroy": (st, [P]),
         "ctri_factor_query": (st, [ctypes.c_int64, dp, dp, dp, dp, ctypes.POINTER(ctypes.c_int)]),
         "ctri_pcr_coefficients": (st, [ctypes.c_int, ctypes.c_int, dp, dp, dp, dp, dp, dp,
+                                       ctypes.POINTER(ctypes.c_int)]),
+        "ctri_reduced_schedule": (st, [ctypes.c_int, ctypes.c_int, dp, dp, dp, ctypes.c_int,
+                                       ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), dp,
+                                       ctypes.POINTER(ctypes.c_int), dp,
                                        ctypes.POINTER(ctypes.c_int)]),
     }
     for name, (res, args) in sig.items():
@@ -262,6 +268,33 @@ def ctri_pcr_coefficients(L, D, U, cyclic=True):
            "ctri_pcr_coefficients")
     q = stages.value
     return a[: q * P].reshape(q, P), g[: q * P].reshape(q, P), inv
+
+
+def ctri_reduced_schedule(L, D, U, cyclic=True, max_steps=32):
+    """Host-only: the reduced-system step schedule (see include/ctri.h).  Returns
+    (kinds[nsteps], w[nsteps, P], src[nsteps, P, 2], c[nsteps, P, 2], counts dict)."""
+    L = np.ascontiguousarray(L, dtype=np.float64)
+    D = np.ascontiguousarray(D, dtype=np.float64)
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    P = len(D)
+    ip = ctypes.POINTER(ctypes.c_int)
+    dp = ctypes.POINTER(ctypes.c_double)
+    kinds = np.zeros(max_steps, dtype=np.int32)
+    w = np.zeros(max_steps * P)
+    src = np.zeros(2 * max_steps * P, dtype=np.int32)
+    c = np.zeros(2 * max_steps * P)
+    counts = np.zeros(3, dtype=np.int32)
+    ns = ctypes.c_int()
+    _check(load().ctri_reduced_schedule(P, int(bool(cyclic)), L.ctypes.data_as(dp), D.ctypes.data_as(dp),
+                                        U.ctypes.data_as(dp), max_steps, ctypes.byref(ns),
+                                        kinds.ctypes.data_as(ip), w.ctypes.data_as(dp),
+                                        src.ctypes.data_as(ip), c.ctypes.data_as(dp),
+                                        counts.ctypes.data_as(ip)), "ctri_reduced_schedule")
+    n = ns.value
+    return (kinds[:n].copy(), w[: n * P].reshape(n, P), src[: 2 * n * P].reshape(n, P, 2),
+            c[: 2 * n * P].reshape(n, P, 2),
+            {"pcr_stages": int(counts[0]), "detach_stages": int(counts[1]),
+             "detached_rows": int(counts[2])})
 
 
 # ---------------------------------------------------------------- conveniences

@@ -28,12 +28,14 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     results = {}
     cases = [((64 * world, 8, 16), 0, (1 / 3, 1.0, 1 / 3), True),
-             ((1024, 4, 32), 0, (0.45, 1.0, 0.45), True),
+             ((256 * world, 4, 32), 0, (0.45, 1.0, 0.45), True),
              ((256 * world, 2, 48), 0, (0.2, 1.1, 0.4), True),
              ((8, 128 * world, 32), 1, (1 / 3, 1.0, 1 / 3), True),
              ((4, 6, 64 * world), 2, (1 / 3, 1.0, 1 / 3), True),
              ((96 * world, 3, 16), 0, (0.2, 1.1, 0.4), False)]
-    runs = [(c, fl) for c in cases for fl in (0, CTRI_FLAG_NCCL_ROUNDS)]
+    pow2 = (world & (world - 1)) == 0
+    runs = [(c, fl) for c in cases for fl in (0, CTRI_FLAG_NCCL_ROUNDS)
+            if pow2 or fl == 0 or not c[3]]  # cyclic non-power-of-two: P2P path only
     for idx, ((dims, sd, bands, cyc), fl) in enumerate(runs):
         b = workloads.uniform(dims, 6 + idx)
         plan = pdist.plan_from_process_group(dims, sd, bands, cyc, flags=CTRI_FLAG_TIMING | fl)

@@ -88,6 +88,36 @@ def test_loopback_partitions(p, shape, bands, path):
     assert st["sends_per_solve"] == 2 * int(math.log2(p)) + 1
 
 
+@pytest.mark.parametrize("p", [3, 5, 6, 7, 11])
+@pytest.mark.parametrize("bands", [SYM, NONSYM, (0.45, 1.0, 0.45), (0.499, 1.0, 0.499)])
+def test_loopback_cyclic_detach_reattach(p, bands):
+    """Cyclic non-power-of-two partitions: detach / PCR / reattach (counts P:346)."""
+    shape = (p * 16, 4, 16) if bands[0] > 0.4 else (p * 64, 4, 16)
+    b = workloads.uniform(shape, 6)
+    tol = 1e-12 if bands[0] < 0.49 else 1e-11
+    x, st = check(b, 0, p, bands, tol=tol)
+    q = int(math.floor(math.log2(p)))
+    assert st["reduced_path"] == 1 and st["device_error"] == 0
+    assert st["pcr_stages"] == q
+    assert st["detached_rows"] == p - 2 ** q
+    assert st["detach_stages"] == bin(p).count("1") - 1
+
+
+@pytest.mark.parametrize("p", [3, 6])
+def test_detach_green_function(p):
+    """Delta RHS at the partition edges for non-power-of-two p (closed form, alpha = 0.45)."""
+    alpha = 0.45
+    N = p * 16
+    n = N // p
+    lam = (-1 + math.sqrt(1 - 4 * alpha ** 2)) / (2 * alpha)
+    for r in sorted({0, n - 1, n, n + 1, N - 1}):
+        b = workloads.delta((N, 2, 16), 0, r)
+        x = gpu_solve(b, 0, p, (alpha, 1.0, alpha))
+        dl = (np.arange(N) - r) % N
+        g = (lam ** dl + lam ** (N - dl)) / (math.sqrt(1 - 4 * alpha ** 2) * (1 - lam ** N))
+        assert np.max(np.abs(x - g[:, None, None])) < 1e-14, (p, r)
+
+
 @pytest.mark.parametrize("p", [2, 3, 4, 5, 8])
 @pytest.mark.parametrize("flags", [0, 16])
 def test_loopback_acyclic(p, flags):
@@ -261,8 +291,8 @@ def test_errors():
     import torch
 
     from paper_2101_02286_b200 import CtriError, ctri
-    with pytest.raises(CtriError) as e:
-        ctri.LoopbackGroup((96, 2, 16), 0, 3)  # cyclic, non-power-of-two p
+    with pytest.raises(CtriError) as e:  # detach/reattach is P2P-path only
+        ctri.LoopbackGroup((96, 2, 16), 0, 3, flags=16)
     assert e.value.name == "CTRI_ERR_UNSUPPORTED"
     with pytest.raises(CtriError) as e:
         ctri.Plan((100, 2, 16), 0, 1, 0, bands=(1.0, 0.0, 1.0))

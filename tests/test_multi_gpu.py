@@ -15,7 +15,7 @@ def _ngpu():
     return torch.cuda.device_count()
 
 
-@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_nccl_partitions(world):
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")

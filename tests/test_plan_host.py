@@ -170,3 +170,85 @@ def test_golden_pcr_step_p4():
     assert 1 / inv[0] == pytest.approx(float(gold["fold_diag"]), abs=1e-15)
     x = apply_pcr(a, g, inv, np.ones(4))
     assert np.allclose(x, float(gold["x"]), rtol=0, atol=1e-15)
+
+
+# ---------------------------------------------------------------- reduced-system schedule (N2)
+def run_schedule(kinds, w, src, c, b):
+    """Execute the step schedule on a RHS (synchronous semantics, include/ctri.h)."""
+    v = np.array(b, dtype=np.float64)
+    for s in range(len(kinds)):
+        nv = w[s] * v
+        for k in range(2):
+            idx = src[s, :, k]
+            term = np.where(idx >= 0, v[np.maximum(idx, 0)], 0.0)
+            nv = nv - c[s, :, k] * term
+        v = nv
+    return v
+
+
+def dense_band(L, D, U, cyclic):
+    P = len(D)
+    A = np.zeros((P, P))
+    for i in range(P):
+        A[i, i] += D[i]
+        if cyclic or i > 0:
+            A[i, (i - 1) % P] += L[i]
+        if cyclic or i < P - 1:
+            A[i, (i + 1) % P] += U[i]
+    return A
+
+
+@pytest.mark.parametrize("P", list(range(1, 17)) + [23, 31, 33])
+@pytest.mark.parametrize("cyclic", [True, False])
+def test_reduced_schedule_vs_dense(P, cyclic):
+    rng = np.random.default_rng(1000 + P)
+    L = rng.uniform(-0.4, 0.4, P)
+    U = rng.uniform(-0.4, 0.4, P)
+    D = rng.uniform(1.0, 1.3, P)
+    kinds, w, src, c, cnt = pk.ctri_reduced_schedule(L, D, U, cyclic=cyclic, max_steps=64)
+    A = dense_band(L, D, U, cyclic)
+    for _ in range(3):
+        b = rng.uniform(-1, 1, P)
+        assert np.max(np.abs(run_schedule(kinds, w, src, c, b) - np.linalg.solve(A, b))) < 1e-14
+    if cyclic:  # stage counts, P:346
+        q = int(math.floor(math.log2(P)))
+        assert cnt["pcr_stages"] == q
+        assert cnt["detached_rows"] == P - 2 ** q
+        assert cnt["detach_stages"] == sum((P >> n) & 1 for n in range(q + 1)) - 1
+    else:
+        assert cnt["pcr_stages"] == (math.ceil(math.log2(P)) if P > 1 else 0)
+        assert cnt["detach_stages"] == 0
+
+
+def test_reduced_schedule_worked_example_11():
+    """The paper's 11x11 walkthrough (tests/golden/detach_11x11.txt)."""
+    P = 11
+    kinds, w, src, c, cnt = pk.ctri_reduced_schedule([1 / 3] * P, [1.0] * P, [1 / 3] * P)
+    names = {0: "detach", 1: "pcr", 2: "fold", 3: "reattach"}
+    gold = {}
+    for line in open(os.path.join(GOLDEN, "detach_11x11.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        f = line.split()
+        gold.setdefault(int(f[0]), []).append((f[1], [int(x) for x in f[2:]]))
+    assert len(kinds) == len(gold)
+    for s, entries in gold.items():
+        assert names[int(kinds[s])] == entries[0][0]
+        if entries[0][0] == "detach":
+            got = set()
+            for r in range(P):  # rows that eliminate a detached row this step
+                if src[s, r, 0] >= 0:
+                    got.add((int(src[s, r, 0]) + 1, r + 1))
+            want = set()
+            for _, (z, y, a) in entries:
+                want |= {(z, y), (z, a)}
+            assert got == want, (s, got, want)
+        if entries[0][0] == "reattach":
+            got = {(r + 1, int(src[s, r, 0]) + 1, int(src[s, r, 1]) + 1) for r in range(P)
+                   if src[s, r, 0] >= 0}
+            assert got == {tuple(e[1]) for e in entries}, (s, got)
+    assert cnt == {"pcr_stages": 3, "detach_stages": 2, "detached_rows": 3}
+    # and it solves the benchmark reduced system (b = 1 -> x~ = 1 / (L+D+U) row sums)
+    b = np.ones(P)
+    A = dense_band([1 / 3] * P, [1.0] * P, [1 / 3] * P, True)
+    assert np.allclose(run_schedule(kinds, w, src, c, b), np.linalg.solve(A, b), rtol=0, atol=1e-15)
