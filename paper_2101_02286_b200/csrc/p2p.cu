@@ -103,6 +103,20 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
     if (j < c1) nc = i + 1;
   }
   bool ok = true;
+  const int64_t n = A.lay.n, inner = A.lay.inner;
+  const int64_t rows = A.full ? n - 1 : 2 * A.W;  // interior rows touched by (a4)
+  // The window rows of y do not depend on any message: pull them into L2 now, while this rank
+  // waits for its peers (they finish their local solves at slightly different times).
+#pragma unroll
+  for (int i = 0; i < kMaxCpt; ++i) {
+    if (i >= nc) continue;
+    const int64_t o = col[i] / inner, c = col[i] - (col[i] / inner) * inner;
+    const double* xcol = R.x + o * n * inner + c;
+    for (int64_t ry = 0; ry < rows; ++ry) {
+      const int64_t r = A.full ? ry + 1 : (ry < A.W ? ry + 1 : n - 2 * A.W + ry);
+      asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(xcol + r * inner));
+    }
+  }
 
   // ---- (a2) y_i[last] -> right neighbour; b^ ----
   if (right >= 0) {
@@ -166,8 +180,6 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
     return;
   }
   stamp(4);
-  const int64_t n = A.lay.n, inner = A.lay.inner;
-  const int64_t rows = A.full ? n - 1 : 2 * A.W;  // interior rows touched
   // window back-substitution: kMaxCpt (4) columns x 4 rows = 16 independent loads in flight
   double* xc[kMaxCpt];
 #pragma unroll
