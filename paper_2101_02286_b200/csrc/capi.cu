@@ -77,6 +77,7 @@ void free_plan(Plan* P) {
     if (r < P->peer_ipc.size() && P->peer_ipc[r] && P->peer_alloc[r]) cudaIpcCloseMemHandle(P->peer_alloc[r]);
   if (P->mbox_alloc) cudaFree(P->mbox_alloc);
   if (P->d_err) cudaFree(P->d_err);
+  if (P->d_epoch) cudaFree(P->d_epoch);
   if (P->d_trace) cudaFree(P->d_trace);
   if (P->comm) ncclCommDestroy(P->comm);
   delete P;
@@ -195,6 +196,8 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
     CUDA_TRY(cudaMemsetAsync(P->mbox_alloc, 0, P->mbox_bytes, s));
     CUDA_TRY(cudaMalloc(&P->d_err, sizeof(int)));
     CUDA_TRY(cudaMemsetAsync(P->d_err, 0, sizeof(int), s));
+    CUDA_TRY(cudaMalloc(&P->d_epoch, sizeof(unsigned int) * P->p2p_nslices));
+    CUDA_TRY(cudaMemsetAsync(P->d_epoch, 0, sizeof(unsigned int) * P->p2p_nslices, s));
     P->p2p = true;
   }
   if (flags & CTRI_FLAG_DERIV) {
@@ -256,6 +259,7 @@ void p2p_fill_rank(const Plan& P, double* x, P2PRank* R) {
   R->yl = P.yl;
   R->bt = P.bt;
   R->mbox = reinterpret_cast<unsigned long long*>(P.mbox_alloc);
+  R->epoch = P.d_epoch;
   for (int r = 0; r < kMaxP2PRanks; ++r) R->peer_mbox[r] = nullptr;
   for (int r = 0; r < P.p; ++r) R->peer_mbox[r] = reinterpret_cast<unsigned long long*>(P.peer_alloc[r]);
   const Schedule& sc = P.sched;
@@ -448,9 +452,6 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
     A.u = P0.bands.u;
     A.S = P0.d_S;
     A.R = P0.d_R;
-    const unsigned long long ep = ++P0.epoch;
-    for (Plan* P : G) P->epoch = ep;
-    A.epoch = ep;
     A.err = P0.d_err;
     const int grid = A.nslices * (int)G.size();
     if (std::getenv("CTRI_P2P_TRACE") && !P0.d_trace)
@@ -465,7 +466,7 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
       CUDA_TRY(cudaStreamSynchronize(s));
       unsigned long long t0 = ~0ull;
       for (int b = 0; b < grid; ++b) t0 = std::min(t0, t[8 * b]);
-      std::fprintf(stderr, "[p2p trace rank %d epoch %llu]", P0.rank, (unsigned long long)ep);
+      std::fprintf(stderr, "[p2p trace rank %d solve %llu]", P0.rank, (unsigned long long)P0.solves);
       const char* nm[6] = {"start", "y_sent", "y_recv", "stages", "x_recv", "end"};
       for (int k = 0; k < 6; ++k) {
         std::vector<double> v;

@@ -95,6 +95,8 @@ struct P2PRank {
   double* x;
   const double *yf, *yl, *bt;
   unsigned long long* mbox;      // own mailbox of LL words (2 epoch copies)
+  unsigned int* epoch;           // per slice: epoch of the last solve (device-resident, so a
+                                 // solve captured in a CUDA graph advances it on every replay)
   unsigned long long* peer_mbox[kMaxP2PRanks];  // every rank's mailbox as addressable here
   P2PStep step[kMaxP2PSteps];
 };
@@ -104,7 +106,6 @@ struct P2PArgs {
   Layout lay;
   double l, u;
   const double *S, *R;
-  unsigned long long epoch;
   int* err;
   unsigned long long* trace;  // measurement only (CTRI_P2P_TRACE): [grid][8] globaltimer stamps
   P2PRank rk[kMaxP2PRanks];
@@ -158,6 +159,7 @@ struct Plan {
   bool p2p = false;
   int p2p_nslices = 0;
   void* mbox_alloc = nullptr;          // own LL mailbox (cudaMalloc, IPC-exported)
+  unsigned int* d_epoch = nullptr;     // per-slice solve epochs of the fused P2P kernel
   size_t mbox_bytes = 0;
   std::vector<void*> peer_alloc;       // peer allocations as mapped here (IPC) or direct
   std::vector<bool> peer_ipc;          // opened with cudaIpcOpenMemHandle

@@ -76,7 +76,9 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
   const int64_t m = A.m;
   const int64_t c0 = (int64_t)slice * A.slice_cols;
   const int64_t c1 = std::min<int64_t>(m, c0 + A.slice_cols);
-  const uint32_t ep = (uint32_t)A.epoch;
+  // epoch of this solve: every rank runs the same sequence of solves, so slice `slice` of every
+  // rank reads the same value; only this CTA touches its slot (written back at the end)
+  const uint32_t ep = R.epoch[slice] + 1u;
   const unsigned long long deadline = globaltimer() + 20ull * 1000000000ull;  // 20 s
   // mailbox copy (epoch parity): [y: 2m][stage k, slot 0/1: 2m each][x: 2m] 64-bit words
   const int64_t per_copy = (int64_t)(2 + 2 * q) * 2 * m;
@@ -177,6 +179,8 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
   }
   if (!ok) {
     atomicExch(A.err, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) R.epoch[slice] = ep;
     return;
   }
   stamp(4);
@@ -224,10 +228,9 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
         if (i < nc && r0 + u < rows)
           xc[i][rr[u] * inner] = v[i][u] - A.S[rr[u] - 1] * bh[i] - A.R[rr[u] - 1] * xb[i];
   }
-  if (tr) {
-    __syncthreads();
-    stamp(5);
-  }
+  __syncthreads();  // every thread has read this solve's epoch
+  if (threadIdx.x == 0) R.epoch[slice] = ep;
+  if (tr) stamp(5);
 }
 
 cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s) {

@@ -201,6 +201,42 @@ def test_p2p_many_consecutive_solves():
     assert rel_err(x, ref, 0) < TOL_REL
 
 
+@pytest.mark.parametrize("p", [1, 4, 3])
+def test_cuda_graph_replay(p):
+    """A solve captured in a CUDA graph and replayed (streams + graphs, no tracing compiler);
+    the fused P2P kernel keeps its epochs on the device, so every replay is a fresh solve."""
+    import torch
+
+    from paper_2101_02286_b200 import ctri
+    shape = (p * 256, 4, 32)
+    rng_seeds = (6, 7, 8)
+    dev = torch.device("cuda:0")
+    bufs = [torch.zeros(ctri.local_shape(shape, 0, p), dtype=torch.float64, device=dev) for _ in range(p)]
+    outs = [torch.zeros_like(t) for t in bufs]
+    if p == 1:
+        plan = ctri.Plan(shape, 0)
+        run = lambda: plan.solve(bufs[0], outs[0])
+    else:
+        grp = ctri.LoopbackGroup(shape, 0, p)
+        run = lambda: grp.solve(bufs, outs)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        run()  # warm-up outside the capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        run()
+    for seed in rng_seeds:
+        b = workloads.uniform(shape, seed)
+        for r in range(p):
+            bufs[r].copy_(torch.from_numpy(workloads.slab(b, 0, p, r)))
+        g.replay()
+        torch.cuda.synchronize()
+        x = workloads.assemble([t.cpu().numpy() for t in outs], 0)
+        assert rel_err(x, oracle.cyclic_solve(b, 0), 0) < TOL_REL, seed
+
+
 def test_inplace_and_determinism():
     b = workloads.uniform((2048, 2, 48), 6)
     x1 = gpu_solve(b, 0)
