@@ -191,7 +191,7 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
     // fused device-initiated reduced phase: double-buffered mailbox + epoch flags
     const int q = (int)P->sched.steps.size();
     P->p2p_nslices = p2p_slices(m, P->loopback ? p : 1, P->num_sms);
-    P->mbox_bytes = sizeof(unsigned long long) * p2p_mailbox_words(m, q);
+    P->mbox_bytes = sizeof(unsigned long long) * p2p_mailbox_words(m, q, (flags & CTRI_FLAG_DERIV) != 0);
     CUDA_TRY(cudaMalloc(&P->mbox_alloc, P->mbox_bytes));
     CUDA_TRY(cudaMemsetAsync(P->mbox_alloc, 0, P->mbox_bytes, s));
     CUDA_TRY(cudaMalloc(&P->d_err, sizeof(int)));
@@ -252,6 +252,24 @@ ctri_status p2p_connect_ipc(Plan* P, cudaStream_t s) {
   return CTRI_OK;
 }
 
+void p2p_args(const Plan& P0, P2PArgs* A) {
+  std::memset(A, 0, sizeof(*A));
+  A->p = P0.p;
+  A->q = (int)P0.sched.steps.size();
+  A->cyclic = P0.cyclic;
+  A->nslices = P0.p2p_nslices;
+  A->m = P0.lay.m();
+  A->slice_cols = (A->m + A->nslices - 1) / A->nslices;
+  A->full = ((P0.flags & CTRI_FLAG_FULL_BACKSUB) || (2 * P0.window >= P0.lay.n - 1)) ? 1 : 0;
+  A->W = P0.window;
+  A->lay = P0.lay;
+  A->l = P0.bands.l;
+  A->u = P0.bands.u;
+  A->S = P0.d_S;
+  A->R = P0.d_R;
+  A->err = P0.d_err;
+}
+
 void p2p_fill_rank(const Plan& P, double* x, P2PRank* R) {
   R->rank = P.rank;
   R->x = x;
@@ -260,6 +278,9 @@ void p2p_fill_rank(const Plan& P, double* x, P2PRank* R) {
   R->bt = P.bt;
   R->mbox = reinterpret_cast<unsigned long long*>(P.mbox_alloc);
   R->epoch = P.d_epoch;
+  R->f = nullptr;
+  R->halo_lo = P.halo_lo;
+  R->halo_hi = P.halo_hi;
   for (int r = 0; r < kMaxP2PRanks; ++r) R->peer_mbox[r] = nullptr;
   for (int r = 0; r < P.p; ++r) R->peer_mbox[r] = reinterpret_cast<unsigned long long*>(P.peer_alloc[r]);
   const Schedule& sc = P.sched;
@@ -438,21 +459,7 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
   }
   if (P0.p2p) {  // fused device-initiated (a2)-(a4)
     P2PArgs A;
-    std::memset(&A, 0, sizeof(A));
-    A.p = P0.p;
-    A.q = (int)P0.sched.steps.size();
-    A.cyclic = P0.cyclic;
-    A.nslices = P0.p2p_nslices;
-    A.m = P0.lay.m();
-    A.slice_cols = (A.m + A.nslices - 1) / A.nslices;
-    A.full = ((P0.flags & CTRI_FLAG_FULL_BACKSUB) || (2 * P0.window >= P0.lay.n - 1)) ? 1 : 0;
-    A.W = P0.window;
-    A.lay = P0.lay;
-    A.l = P0.bands.l;
-    A.u = P0.bands.u;
-    A.S = P0.d_S;
-    A.R = P0.d_R;
-    A.err = P0.d_err;
+    p2p_args(P0, &A);
     const int grid = A.nslices * (int)G.size();
     if (std::getenv("CTRI_P2P_TRACE") && !P0.d_trace)
       CUDA_TRY(cudaMalloc(&P0.d_trace, sizeof(unsigned long long) * 8 * grid));
@@ -519,13 +526,23 @@ ctri_status deriv_group(std::vector<Plan*>& G, const double* const* f, double* c
   }
   bool fused = true;
   for (Plan* P : G) fused = fused && P->local_kernel == 1 && P->tile.deriv_ok;
-  if (G[0]->p > 1 || fused) {  // halo planes (with one partition: the slab's own wrap rows)
+  const bool need_pack = (G[0]->p == 1 && fused) || (G[0]->p > 1 && !G[0]->p2p);
+  if (need_pack) {  // halo planes (with one partition: the slab's own wrap rows)
     for (size_t r = 0; r < G.size(); ++r) {
       cudaError_t e = launch_pack_halo(*G[r], f[r], s);
       if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, cudaGetErrorString(e));
     }
   }
-  if (G[0]->p > 1) {
+  if (G[0]->p > 1 && G[0]->p2p) {  // halo rows as LL words over the P2P mailboxes
+    P2PArgs A;
+    p2p_args(*G[0], &A);
+    for (size_t r = 0; r < G.size(); ++r) {
+      p2p_fill_rank(*G[r], nullptr, &A.rk[r]);
+      A.rk[r].f = f[r];
+    }
+    cudaError_t e = launch_halo_p2p(A, (int)G.size(), s);
+    if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("p2p halo: ") + cudaGetErrorString(e));
+  } else if (G[0]->p > 1) {
     if (!G[0]->loopback) TRY(exchange_nccl(*G[0], round_halo(*G[0]), s));
     else TRY(exchange_loopback(G, [](Plan& P) { return round_halo(P); }, s));
   }

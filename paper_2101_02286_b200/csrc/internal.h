@@ -94,6 +94,8 @@ struct P2PRank {
   int rank;
   double* x;
   const double *yf, *yl, *bt;
+  const double* f;               // derivative halo kernel: this rank's f slab
+  double *halo_lo, *halo_hi;     // derivative halo planes [2][m]
   unsigned long long* mbox;      // own mailbox of LL words (2 epoch copies)
   unsigned int* epoch;           // per slice: epoch of the last solve (device-resident, so a
                                  // solve captured in a CUDA graph advances it on every replay)
@@ -112,7 +114,8 @@ struct P2PArgs {
 };
 cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s);
 int p2p_slices(int64_t m, int nranks_launch, int num_sms);
-size_t p2p_mailbox_words(int64_t m, int q);
+size_t p2p_mailbox_words(int64_t m, int q, bool halo);
+cudaError_t launch_halo_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s);
 
 struct Plan {
   // configuration

@@ -260,6 +260,64 @@ int p2p_slices(int64_t m, int nranks_launch, int num_sms) {
   return (int)std::max<int64_t>(1, ns);
 }
 
-size_t p2p_mailbox_words(int64_t m, int q) { return (size_t)2 * (2 + 2 * q) * 2 * (size_t)m; }
+// [2 epoch copies][2 + 2q slots][2m LL words]  +  (derivative) [2 copies][4 halo rows][2m]
+size_t p2p_mailbox_words(int64_t m, int q, bool halo) {
+  return (size_t)2 * (2 + 2 * q) * 2 * (size_t)m + (halo ? (size_t)2 * 4 * 2 * (size_t)m : 0);
+}
+
+// (a0) halo of the compact-derivative stencil for nparts > 1: rows 0, 1 of this slab
+// go to the left neighbour (its rows n, n+1) and rows n-2, n-1 to the right neighbour (its rows
+// -2, -1), as LL words into their mailboxes; the incoming words become halo_lo / halo_hi.
+__global__ void __launch_bounds__(kP2PThreads) k_halo_p2p(const P2PArgs A) {
+  const int r_local = blockIdx.x / A.nslices;
+  const int slice = blockIdx.x - r_local * A.nslices;
+  const P2PRank& R = A.rk[r_local];
+  const int p = A.p, rank = R.rank;
+  const int64_t m = A.m, n = A.lay.n, inner = A.lay.inner;
+  const uint32_t ep = R.epoch[slice] + 1u;
+  const unsigned long long deadline = globaltimer() + 20ull * 1000000000ull;
+  const int64_t hoff = (int64_t)2 * (2 + 2 * A.q) * 2 * m + (int64_t)(ep & 1u) * 8 * m;
+  const int left = (rank + p - 1) % p, right = (rank + 1) % p;
+  const int64_t c0 = (int64_t)slice * A.slice_cols;
+  const int64_t c1 = std::min<int64_t>(m, c0 + A.slice_cols);
+  bool ok = true;
+  for (int64_t j = c0 + threadIdx.x; j < c1; j += kP2PThreads) {
+    const int64_t o = j / inner, c = j - o * inner;
+    const double* fc = R.f + o * n * inner + c;
+    unsigned long long* lo = R.peer_mbox[right] + hoff;  // right neighbour's rows -2, -1
+    unsigned long long* hi = R.peer_mbox[left] + hoff;   // left neighbour's rows n, n+1
+    ll_send(lo + 2 * j, fc[(n - 2) * inner], ep);
+    ll_send(lo + 2 * m + 2 * j, fc[(n - 1) * inner], ep);
+    ll_send(hi + 4 * m + 2 * j, fc[0], ep);
+    ll_send(hi + 6 * m + 2 * j, fc[inner], ep);
+  }
+  const unsigned long long* mine = R.mbox + hoff;
+  for (int64_t j = c0 + threadIdx.x; j < c1 && ok; j += kP2PThreads) {
+    double v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) ok = ok && ll_recv(mine + (int64_t)k * 2 * m + 2 * j, ep, deadline, &v[k]);
+    if (!ok) break;
+    R.halo_lo[j] = v[0];
+    R.halo_lo[m + j] = v[1];
+    R.halo_hi[j] = v[2];
+    R.halo_hi[m + j] = v[3];
+  }
+  if (!ok) atomicExch(A.err, 2);
+  __syncthreads();
+  if (threadIdx.x == 0) R.epoch[slice] = ep;
+}
+
+cudaError_t launch_halo_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(A.nslices * nranks_launch), 1, 1);
+  cfg.blockDim = dim3(kP2PThreads, 1, 1);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = nranks_launch > 1 ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k_halo_p2p, A);
+}
 
 }  // namespace ctri
