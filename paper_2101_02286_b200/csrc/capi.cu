@@ -213,8 +213,8 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   }
   // launches per solve
   int launches = 1;
-  if (p > 1) launches += P->p2p ? 1 : 1 /*bhat*/ + P->gpcr.stages + 1 /*backsub*/;
-  if (p == 1 && P->vp > 1) launches += 1;  // local reduced system + window back-substitution
+  if (p > 1) launches += P->p2p ? 2 /*reduced + window*/ : 1 /*bhat*/ + P->gpcr.stages + 1 /*backsub*/;
+  if (p == 1 && P->vp > 1) launches += 2;  // local reduced system; window back-substitution
   P->launches_per_solve = launches;
   CUDA_TRY(cudaStreamSynchronize(s));
   return CTRI_OK;
@@ -276,6 +276,7 @@ void p2p_fill_rank(const Plan& P, double* x, P2PRank* R) {
   R->yf = P.yf;
   R->yl = P.yl;
   R->bt = P.bt;
+  R->xnext = P.xt_next;
   R->mbox = reinterpret_cast<unsigned long long*>(P.mbox_alloc);
   R->epoch = P.d_epoch;
   R->f = nullptr;
@@ -450,6 +451,7 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
     if (P0.vp > 1) {  // (a2)-(a4) across the virtual partitions of this slab
       for (size_t r = 0; r < G.size(); ++r) {
         cudaError_t e = launch_reduced_local(*G[r], x[r], s);
+        if (e == cudaSuccess) e = launch_window(*G[r], x[r], nullptr, s);
         if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("local reduced: ") + cudaGetErrorString(e));
       }
       record(P0, EV_BACK, s);
@@ -467,6 +469,10 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
     for (size_t r = 0; r < G.size(); ++r) p2p_fill_rank(*G[r], x[r], &A.rk[r]);
     cudaError_t e = launch_reduced_p2p(A, (int)G.size(), s);
     if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("p2p reduced kernel: ") + cudaGetErrorString(e));
+    for (size_t r = 0; r < G.size(); ++r) {  // (a4) window pass of every rank
+      e = launch_window(*G[r], x[r], G[r]->xt_next, s);
+      if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("window: ") + cudaGetErrorString(e));
+    }
     if (P0.d_trace) {  // measurement only: per-phase durations across CTAs
       std::vector<unsigned long long> t(8 * (size_t)grid);
       CUDA_TRY(cudaMemcpyAsync(t.data(), P0.d_trace, t.size() * 8, cudaMemcpyDeviceToHost, s));

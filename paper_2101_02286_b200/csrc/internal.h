@@ -94,6 +94,7 @@ struct P2PRank {
   int rank;
   double* x;
   const double *yf, *yl, *bt;
+  double* xnext;                 // x~_{i+1} per batch column, read by the window pass
   const double* f;               // derivative halo kernel: this rank's f slab
   double *halo_lo, *halo_hi;     // derivative halo planes [2][m]
   unsigned long long* mbox;      // own mailbox of LL words (2 epoch copies)
@@ -187,6 +188,7 @@ cudaError_t launch_bhat(const Plan& P, cudaStream_t s);
 cudaError_t launch_pcr_stage(const Plan& P, int k, bool last, cudaStream_t s);
 cudaError_t launch_backsub(const Plan& P, double* x, cudaStream_t s);
 cudaError_t launch_reduced_local(const Plan& P, double* x, cudaStream_t s);
+cudaError_t launch_window(const Plan& P, double* x, const double* next, cudaStream_t s);
 cudaError_t launch_pack_halo(const Plan& P, const double* f, cudaStream_t s);
 cudaError_t launch_stencil(const Plan& P, const double* f, double* rhs, double a, double bc,
                            double h, cudaStream_t s);

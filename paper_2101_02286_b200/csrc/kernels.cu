@@ -115,6 +115,107 @@ __global__ void k_backsub(double* x, int64_t outer, int64_t n, int64_t inner,
   }
 }
 
+// (a4) windowed back-substitution x = y - S x~_s - R x~_{s+1} (Eq. xi_app; window R15)
+// of every (virtual) slab s, after the reduced kernel stored x~_s in row 0 of slab s.
+// x~_{s+1} is row 0 of slab s+1, or for the last slab: next[j] (the right neighbour's x~, p > 1),
+// else row 0 of slab 0 (p == 1 cyclic), else 0 (acyclic end).  A separate high-occupancy
+// pass: HBM-bound read-modify-write of 2W rows per slab, 8 independent rows in flight per thread.
+struct WindowArgs {
+  double* x;
+  const double *S, *R, *next;
+  int64_t outer, nv, inner, W, rows;
+  int vp, full, wrap;
+};
+constexpr int kWinRows = 8;
+
+__device__ __forceinline__ int64_t window_row(const WindowArgs& A, int64_t ry) {
+  return A.full ? ry + 1 : (ry < A.W ? ry + 1 : A.nv - 2 * A.W + ry);
+}
+
+// strided axis (inner > 1): block = 256 consecutive columns x kWinRows rows of one slab
+__global__ void __launch_bounds__(256) k_window(const WindowArgs A) {
+  const int64_t j = blockIdx.x * 256ll + threadIdx.x;
+  const int64_t m = A.outer * A.inner;
+  if (j >= m) return;
+  const int s = blockIdx.z;
+  const int64_t o = j / A.inner, c = j - o * A.inner;
+  const int64_t sl = A.nv * A.inner;  // one slab
+  double* xs = A.x + (o * A.vp + s) * sl + c;
+  const double xa = xs[0];
+  double xn = 0.0;
+  if (s + 1 < A.vp) xn = xs[sl];
+  else if (A.next) xn = A.next[j];
+  else if (A.wrap) xn = A.x[o * A.vp * sl + c];
+  const int64_t r0 = (int64_t)blockIdx.y * kWinRows;
+  double v[kWinRows];
+#pragma unroll
+  for (int u = 0; u < kWinRows; ++u)
+    if (r0 + u < A.rows) v[u] = xs[window_row(A, r0 + u) * A.inner];
+#pragma unroll
+  for (int u = 0; u < kWinRows; ++u)
+    if (r0 + u < A.rows) {
+      const int64_t r = window_row(A, r0 + u);
+      dev::st_global_cs(xs + r * A.inner, v[u] - __ldg(A.S + r - 1) * xa - __ldg(A.R + r - 1) * xn);
+    }
+}
+
+// contiguous axis (inner == 1): one warp per column, lanes along the (contiguous) rows
+__global__ void __launch_bounds__(256) k_window_contig(const WindowArgs A) {
+  const int64_t w = blockIdx.x * 8ll + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= A.outer * A.vp) return;
+  const int64_t o = w / A.vp;
+  const int s = (int)(w - o * A.vp);
+  double* xs = A.x + w * A.nv;
+  const double xa = xs[0];
+  double xn = 0.0;
+  if (s + 1 < A.vp) xn = xs[A.nv];
+  else if (A.next) xn = A.next[o];
+  else if (A.wrap) xn = A.x[o * A.vp * A.nv];
+  for (int64_t r0 = 0; r0 < A.rows; r0 += 32 * 4) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t ry = r0 + u * 32 + lane;
+      if (ry < A.rows) v[u] = xs[window_row(A, ry)];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t ry = r0 + u * 32 + lane;
+      if (ry < A.rows) {
+        const int64_t r = window_row(A, ry);
+        xs[r] = v[u] - __ldg(A.S + r - 1) * xa - __ldg(A.R + r - 1) * xn;
+      }
+    }
+  }
+}
+
+cudaError_t launch_window(const Plan& P, double* x, const double* next, cudaStream_t s) {
+  WindowArgs A;
+  A.x = x;
+  A.S = P.d_S;
+  A.R = P.d_R;
+  A.next = next;
+  A.outer = P.lay.outer;
+  A.nv = P.tlay.n;
+  A.inner = P.lay.inner;
+  A.W = P.window;
+  A.full = ((P.flags & CTRI_FLAG_FULL_BACKSUB) || (2 * P.window >= P.tlay.n - 1)) ? 1 : 0;
+  A.rows = A.full ? A.nv - 1 : 2 * A.W;
+  A.vp = P.vp;
+  A.wrap = (P.p == 1 && P.cyclic) ? 1 : 0;
+  if (A.rows <= 0) return cudaSuccess;
+  if (A.inner == 1) {
+    const int64_t warps = A.outer * A.vp;
+    k_window_contig<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(A);
+  } else {
+    const int64_t m = P.lay.m();
+    dim3 grid((unsigned)((m + 255) / 256), (unsigned)((A.rows + kWinRows - 1) / kWinRows), (unsigned)A.vp);
+    k_window<<<grid, 256, 0, s>>>(A);
+  }
+  return cudaGetLastError();
+}
+
 // (a2)-(a4) for the virtual partitions of one GPU (nparts == 1, vp > 1): per batch column the
 // vp-row reduced system (cyclic or acyclic) is formed from the planes (Eq. bi_hat), solved with
 // the plan's PCR multipliers (fold R3) and back-substituted on the window rows of
@@ -170,40 +271,9 @@ __global__ void __launch_bounds__(128) k_reduced_local(const LocalRedArgs A, dou
   }
   for (int v = 0; v < 8; ++v)
     if (v < vp) bh[v] *= A.inv[v];
-  const int64_t rows = A.full ? A.nv - 1 : 2 * A.W;
-  // window back-substitution of every virtual slab: groups of 4 slabs x 4 rows = 16 loads
-  for (int v0 = 0; v0 < vp; v0 += 4) {
-    double* xc[4];
-    double xa[4], xn[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int v = (v0 + i < vp) ? v0 + i : v0;
-      xa[i] = bh_get(bh, v);
-      xn[i] = (A.cyclic || v + 1 < vp) ? bh_get(bh, (v + 1) % vp) : 0.0;
-      xc[i] = x + ((o * vp + v) * A.nv) * A.inner + c;
-      if (v0 + i < vp) xc[i][0] = xa[i];
-    }
-    for (int64_t r0 = 0; r0 < rows; r0 += 4) {
-      double val[4][4];
-      int64_t rr[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t ry = r0 + u;
-        rr[u] = A.full ? ry + 1 : (ry < A.W ? ry + 1 : A.nv - 2 * A.W + ry);
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (v0 + i < vp && r0 + u < rows) val[i][u] = xc[i][rr[u] * A.inner];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (v0 + i < vp && r0 + u < rows)
-            xc[i][rr[u] * A.inner] = val[i][u] - A.S[rr[u] - 1] * xa[i] - A.R[rr[u] - 1] * xn[i];
-    }
-  }
+  // x~ of every virtual slab into its row 0; the window pass (k_window) follows
+  for (int v = 0; v < 8; ++v)
+    if (v < vp) x[((o * vp + v) * A.nv) * A.inner + c] = bh[v];
 }
 
 cudaError_t launch_reduced_local(const Plan& P, double* x, cudaStream_t s) {

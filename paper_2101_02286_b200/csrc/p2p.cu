@@ -106,20 +106,6 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
   }
   bool ok = true;
   const int64_t n = A.lay.n, inner = A.lay.inner;
-  const int64_t rows = A.full ? n - 1 : 2 * A.W;  // interior rows touched by (a4)
-  // The window rows of y do not depend on any message: pull them into L2 now, while this rank
-  // waits for its peers (they finish their local solves at slightly different times).
-#pragma unroll
-  for (int i = 0; i < kMaxCpt; ++i) {
-    if (i >= nc) continue;
-    const int64_t o = col[i] / inner, c = col[i] - (col[i] / inner) * inner;
-    const double* xcol = R.x + o * n * inner + c;
-    for (int64_t ry = 0; ry < rows; ++ry) {
-      const int64_t r = A.full ? ry + 1 : (ry < A.W ? ry + 1 : n - 2 * A.W + ry);
-      asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(xcol + r * inner));
-    }
-  }
-
   // ---- (a2) y_i[last] -> right neighbour; b^ ----
   if (right >= 0) {
     unsigned long long* dst = R.peer_mbox[right] + copy_off + OFF_Y;
@@ -184,49 +170,15 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
     return;
   }
   stamp(4);
-  // window back-substitution: kMaxCpt (4) columns x 4 rows = 16 independent loads in flight
-  double* xc[kMaxCpt];
+  // x~_i into row 0 of this slab and x~_{i+1} into the next-plane; the window pass (k_window)
+  // follows as its own high-occupancy launch
 #pragma unroll
   for (int i = 0; i < kMaxCpt; ++i) {
-    const int64_t j = col[i] < m ? col[i] : 0;
+    if (i >= nc) continue;
+    const int64_t j = col[i];
     const int64_t o = j / inner, c = j - o * inner;
-    xc[i] = R.x + o * n * inner + c;
-    if (i < nc) xc[i][0] = bh[i];
-  }
-  if (nc == 1) {  // one column per thread: 16 rows per batch
-    for (int64_t r0 = 0; r0 < rows; r0 += 16) {
-      double v[16];
-      int64_t rr[16];
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int64_t ry = r0 + u;
-        rr[u] = A.full ? ry + 1 : (ry < A.W ? ry + 1 : n - 2 * A.W + ry);
-        if (ry < rows) v[u] = xc[0][rr[u] * inner];
-      }
-#pragma unroll
-      for (int u = 0; u < 16; ++u)
-        if (r0 + u < rows) xc[0][rr[u] * inner] = v[u] - A.S[rr[u] - 1] * bh[0] - A.R[rr[u] - 1] * xb[0];
-    }
-  } else
-  for (int64_t r0 = 0; r0 < rows; r0 += 4) {
-    double v[kMaxCpt][4];
-    int64_t rr[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t ry = r0 + u;
-      rr[u] = A.full ? ry + 1 : (ry < A.W ? ry + 1 : n - 2 * A.W + ry);
-    }
-#pragma unroll
-    for (int i = 0; i < kMaxCpt; ++i)
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (i < nc && r0 + u < rows) v[i][u] = xc[i][rr[u] * inner];
-#pragma unroll
-    for (int i = 0; i < kMaxCpt; ++i)
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (i < nc && r0 + u < rows)
-          xc[i][rr[u] * inner] = v[i][u] - A.S[rr[u] - 1] * bh[i] - A.R[rr[u] - 1] * xb[i];
+    R.x[o * n * inner + c] = bh[i];
+    R.xnext[j] = xb[i];
   }
   __syncthreads();  // every thread has read this solve's epoch
   if (threadIdx.x == 0) R.epoch[slice] = ep;

@@ -2,7 +2,7 @@
 # Strong (cfg2) and weak (cfg3) scaling at N = 1, 2, 4, 8 (as many GPUs as the box has).
 mkdir -p gpurun_out
 ng=$(nvidia-smi -L | wc -l)
-for cfg in cfg2 cfg3; do
+for cfg in ${CFGS:-cfg2 cfg3}; do
   for n in 1 2 4 8; do
     [ $n -gt $ng ] && continue
     echo "== $cfg N=$n" >> gpurun_out/scale.log
