@@ -45,9 +45,11 @@ def _load():
         lib.oracle_acyclic_solve.argtypes = [i64p, ctypes.c_int, dp, dp, dp]
         lib.oracle_rhs_stencil.argtypes = [i64p, ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                            ctypes.c_double, dp, dp]
+        lib.oracle_rhs_stencil5.argtypes = [i64p, ctypes.c_int, dp, dp, dp]
         lib.oracle_deriv.argtypes = [i64p, ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                      ctypes.c_double, ctypes.c_double, dp, dp]
         for fn in (lib.oracle_cyclic_solve, lib.oracle_acyclic_solve, lib.oracle_rhs_stencil,
+                   lib.oracle_rhs_stencil5,
                    lib.oracle_deriv):
             fn.restype = ctypes.c_int
         lib.oracle_num_threads.restype = ctypes.c_int
@@ -108,6 +110,47 @@ def rhs_stencil(f: np.ndarray, solve_dim: int, a: float, bc: float, h: float) ->
     if rc:
         raise ValueError("oracle_rhs_stencil: invalid argument")
     return out.reshape(shape)
+
+
+def rhs_stencil5(f: np.ndarray, solve_dim: int, coef) -> np.ndarray:
+    """b_j = sum_{k=-2..2} coef[k+2] f_{(j+k) mod N} along solve_dim (P:202-206 schemes)."""
+    shape = f.shape
+    f3 = _as3d(f)
+    sd = solve_dim if f.ndim == 3 else 0
+    c = np.ascontiguousarray(coef, dtype=np.float64)
+    if c.shape != (5,):
+        raise ValueError("coef must hold 5 values (offsets -2..2)")
+    out = np.empty_like(f3)
+    rc = _load().oracle_rhs_stencil5(_dims(f3.shape), sd, c.ctypes.data, f3.ctypes.data,
+                                     out.ctypes.data)
+    if rc:
+        raise ValueError("oracle_rhs_stencil5: invalid argument")
+    return out.reshape(shape)
+
+
+def compact_apply(f: np.ndarray, solve_dim: int, coef, bands) -> np.ndarray:
+    """A compact scheme: the five-point RHS, then x = A^{-1} rhs with cyclic `bands`."""
+    return cyclic_solve(rhs_stencil5(f, solve_dim, coef), solve_dim, bands)
+
+
+# The staggered sixth-order schemes of PAPER.md P:202-206, with half-node values
+# g_i = f_{i+1/2} stored at index i (so f_{i-1/2} = g_{i-1}, f_{i+3/2} = g_{i+1}, ...).
+#   9/62 f'_{i-1} + f'_i + 9/62 f'_{i+1} = 63/62 (f_{i+1/2}-f_{i-1/2})/D + 17/62 (f_{i+3/2}-f_{i-3/2})/(3D)
+#   3/10 fI_{i-1} + fI_i + 3/10 fI_{i+1} = 3/2 (f_{i+1/2}+f_{i-1/2})/2 + 1/10 (f_{i+3/2}+f_{i-3/2})/2
+STAGGERED_DERIV_ALPHA = 9.0 / 62.0
+STAGGERED_INTERP_ALPHA = 3.0 / 10.0
+
+
+def staggered_deriv_coef(delta: float):
+    """Offsets -2..2 of the staggered-derivative RHS in the g-indexing."""
+    a, b = 63.0 / 62.0, 17.0 / 62.0
+    return [-b / (3 * delta), -a / delta, a / delta, b / (3 * delta), 0.0]
+
+
+def staggered_interp_coef():
+    """Offsets -2..2 of the staggered-interpolation RHS in the g-indexing."""
+    a, b = 3.0 / 2.0, 1.0 / 10.0
+    return [b / 2, a / 2, a / 2, b / 2, 0.0]
 
 
 def deriv(f: np.ndarray, solve_dim: int = 0, alpha: float = 1 / 3, a: float = 14 / 9,

@@ -31,6 +31,13 @@
  *                         compact first derivative; a = 14/9, bc = 1/9 are the
  *                         caller's inputs, reading R8).
  *
+ *   oracle_rhs_stencil5   b_j = sum_{k=-2..2} c_k f_{(j+k) mod N}: the general
+ *                         five-point right-hand side of a compact scheme with
+ *                         periodic wrap.  Covers the staggered sixth-order
+ *                         derivative and interpolation of PAPER.md P:202-206
+ *                         (half-node values g_i = f_{i+1/2} stored at index i)
+ *                         as well as the collocated derivative above.
+ *
  *   oracle_deriv          stencil followed by the cyclic solve with bands
  *                         (alpha, 1, alpha): the compact first derivative f'.
  *
@@ -223,6 +230,28 @@ int oracle_rhs_stencil(const int64_t dims[3], int sd, double a, double bc,
       for (int64_t c = 0; c < inner; ++c) {
         ro[c] = a * (fo[jp1 * inner + c] - fo[jm1 * inner + c]) / (2.0 * h) +
                 bc * (fo[jp2 * inner + c] - fo[jm2 * inner + c]) / (4.0 * h);
+      }
+    }
+  }
+  return 0;
+}
+
+/* General five-point periodic stencil (PAPER.md P:202-206 schemes): plain definition. */
+int oracle_rhs_stencil5(const int64_t dims[3], int sd, const double coef[5], const double* f,
+                        double* rhs) {
+  if (!dims || !coef || !f || !rhs || sd < 0 || sd > 2 || f == rhs) return 1;
+  int64_t outer, N, inner;
+  layout(dims, sd, &outer, &N, &inner);
+  if (N < 5) return 1;
+#pragma omp parallel for schedule(static) collapse(2)
+  for (int64_t o = 0; o < outer; ++o) {
+    for (int64_t j = 0; j < N; ++j) {
+      const double* fo = f + o * N * inner;
+      double* ro = rhs + o * N * inner + j * inner;
+      for (int64_t c = 0; c < inner; ++c) {
+        double acc = 0.0;
+        for (int k = -2; k <= 2; ++k) acc += coef[k + 2] * fo[((j + k + N) % N) * inner + c];
+        ro[c] = acc;
       }
     }
   }

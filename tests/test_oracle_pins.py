@@ -212,3 +212,90 @@ def test_oracle_layout_permutation():
 def test_oracle_rejects_bad_args():
     with pytest.raises(ValueError):
         oracle.cyclic_solve(np.ones((2, 3, 3)), 0)
+
+
+# ---- staggered sixth-order schemes ----
+def _half_node_mode(N, k, fn):
+    """fn(kappa x_{i+1/2}) with x = 2 pi (i + 1/2)/N, the argument reduced in integers."""
+    i = np.arange(N, dtype=np.int64)
+    return fn(math.pi * ((k * (2 * i + 1)) % (2 * N)) / N)
+
+
+def _node_mode(N, k, fn):
+    i = np.arange(N, dtype=np.int64)
+    return fn(2 * math.pi * ((k * i) % N) / N)
+
+
+def test_stencil5_matches_dense_circulant():
+    """rhs_stencil5 equals the dense circulant product C f with C[j, j+k mod N] = c_k (N = 7)."""
+    N = 7
+    coef = [0.3, -1.7, 0.25, 2.1, -0.6]
+    C = np.zeros((N, N))
+    for j in range(N):
+        for k in range(-2, 3):
+            C[j, (j + k) % N] += coef[k + 2]
+    f = workloads.uniform((N, 3, 2), 11)
+    got = oracle.rhs_stencil5(f, 0, coef)
+    expect = np.einsum("jk,kab->jab", C, f)
+    assert np.max(np.abs(got - expect)) < 1e-15
+    got2 = oracle.rhs_stencil5(np.ascontiguousarray(np.transpose(f, (1, 2, 0))), 2, coef)
+    assert np.max(np.abs(np.transpose(got2, (2, 0, 1)) - expect)) < 1e-15
+
+
+def test_stencil5_reduces_to_collocated():
+    """The collocated derivative stencil is the 5-point stencil (-b/4h, -a/2h, 0, a/2h, b/4h)."""
+    N = 32
+    h = 2 * math.pi / N
+    f = workloads.uniform((N, 4, 3), 12)
+    a, b = 14 / 9, 1 / 9
+    got = oracle.rhs_stencil5(f, 0, [-b / (4 * h), -a / (2 * h), 0.0, a / (2 * h), b / (4 * h)])
+    assert np.max(np.abs(got - oracle.rhs_stencil(f, 0, a, b, h))) < 1e-13
+
+
+@pytest.mark.parametrize("N,k", [(64, 1), (64, 5), (64, 17), (64, 31), (128, 40), (30, 7)])
+def test_staggered_deriv_modified_wavenumber(N, k):
+    """Fourier analysis of P:203-204 with g_i = sin(k x_{i+1/2}):
+    f'_i = k'(k) cos(k x_i),  k' h = [2a sin(kh/2) + (2b/3) sin(3kh/2)] / (1 + 2 alpha cos kh)."""
+    h = 2 * math.pi / N
+    g = _half_node_mode(N, k, np.sin).reshape(N, 1, 1)
+    df = oracle.compact_apply(g, 0, oracle.staggered_deriv_coef(h),
+                              (oracle.STAGGERED_DERIV_ALPHA, 1.0, oracle.STAGGERED_DERIV_ALPHA))
+    kp = (2 * 63 / 62 * math.sin(k * h / 2) + 2 * 17 / 62 / 3 * math.sin(3 * k * h / 2)) / (
+        1 + 2 * 9 / 62 * math.cos(k * h)) / h
+    assert np.max(np.abs(df.ravel() - kp * _node_mode(N, k, np.cos))) < 1e-13 * max(1.0, kp)
+
+
+@pytest.mark.parametrize("N,k", [(64, 0), (64, 3), (64, 20), (64, 32), (30, 11)])
+def test_staggered_interp_transfer_function(N, k):
+    """Fourier analysis of P:205-206 with g_i = cos(k x_{i+1/2}):
+    fI_i = T(k) cos(k x_i),  T = [a cos(kh/2) + b cos(3kh/2)] / (1 + 2 alpha cos kh)."""
+    h = 2 * math.pi / N
+    g = _half_node_mode(N, k, np.cos).reshape(N, 1, 1)
+    fi = oracle.compact_apply(g, 0, oracle.staggered_interp_coef(),
+                              (oracle.STAGGERED_INTERP_ALPHA, 1.0, oracle.STAGGERED_INTERP_ALPHA))
+    T = (1.5 * math.cos(k * h / 2) + 0.1 * math.cos(3 * k * h / 2)) / (1 + 0.6 * math.cos(k * h))
+    assert np.max(np.abs(fi.ravel() - T * _node_mode(N, k, np.cos))) < 1e-14
+    if k == N // 2:  # Nyquist: cos(k x_{i+1/2}) = 0 exactly, the interpolant is 0
+        assert abs(T) < 1e-15
+
+
+@pytest.mark.parametrize("which", ["deriv", "interp"])
+def test_staggered_sixth_order(which):
+    """Both staggered schemes converge at sixth order on exp(sin x) (P:201 'sixth order')."""
+    errs = []
+    for N in (16, 32, 64):
+        h = 2 * math.pi / N
+        xh = h * (np.arange(N) + 0.5)
+        xn = h * np.arange(N)
+        g = np.exp(np.sin(xh)).reshape(N, 1, 1)
+        if which == "deriv":
+            out = oracle.compact_apply(g, 0, oracle.staggered_deriv_coef(h),
+                                       (9 / 62, 1.0, 9 / 62)).ravel()
+            exact = np.cos(xn) * np.exp(np.sin(xn))
+        else:
+            out = oracle.compact_apply(g, 0, oracle.staggered_interp_coef(),
+                                       (3 / 10, 1.0, 3 / 10)).ravel()
+            exact = np.exp(np.sin(xn))
+        errs.append(np.max(np.abs(out - exact)))
+    orders = [math.log2(errs[i] / errs[i + 1]) for i in range(2)]
+    assert all(5.5 <= o <= 7.0 for o in orders), (which, orders, errs)
