@@ -42,6 +42,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dims", default=None, help="override: global dims N0,N1,N2 (measurement)")
     ap.add_argument("--sd", type=int, default=0, help="solve dim with --dims")
+    ap.add_argument("--scheme", default="collocated",
+                    choices=["collocated", "staggered_deriv", "staggered_interp"],
+                    help="cfg5 compact scheme: collocated derivative (P:65-67) or the staggered "
+                         "sixth-order derivative / interpolation (P:202-206)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -258,10 +262,18 @@ def main():
         name = f"custom {dims} solve index {sd}"
     deriv = args.config == "cfg5"
     flags = CTRI_FLAG_TIMING | (CTRI_FLAG_DERIV if deriv else 0)
+    bands, coef = (1 / 3, 1.0, 1 / 3), None
+    if deriv and args.scheme != "collocated":
+        delta = 2 * math.pi / dims[sd]
+        if args.scheme == "staggered_deriv":
+            bands, coef = ctri.STAGGERED_DERIV_BANDS, ctri.staggered_deriv_coef(delta)
+        else:
+            bands, coef = ctri.STAGGERED_INTERP_BANDS, ctri.staggered_interp_coef()
+        name = f"{name.replace('compact 6th-order first derivative', args.scheme.replace('_', ' '))} (P:202-206)"
     if world > 1:
-        plan = pdist.plan_from_process_group(dims, sd, flags=flags)
+        plan = pdist.plan_from_process_group(dims, sd, bands, flags=flags)
     else:
-        plan = ctri.Plan(dims, sd, 1, 0, flags=flags)
+        plan = ctri.Plan(dims, sd, 1, 0, bands=bands, flags=flags)
     lshape = plan.local_shape
     b = workloads.device_uniform(lshape, 1000 * 2 + rank, dev)
     x = torch.empty_like(b)
@@ -269,7 +281,9 @@ def main():
     pts_local = b.numel()
 
     def step():
-        if deriv:
+        if coef is not None:
+            plan.compact_apply(coef, b, x)
+        elif deriv:
             plan.deriv(b, x)
         else:
             plan.solve(b, x)

@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define CTRI_ABI_VERSION 1
+#define CTRI_ABI_VERSION 2
 
 typedef struct ctri_plan_s* ctri_plan;
 typedef struct CUstream_st* ctri_stream; /* == cudaStream_t */
@@ -169,6 +169,25 @@ ctri_status ctri_deriv(ctri_plan plan, const double* f, double* df, double a, do
 ctri_status ctri_deriv_loopback(const ctri_plan* plans, int nparts, const double* const* f,
                                 double* const* df, double a, double bc, double h,
                                 ctri_stream stream);
+
+/* A compact scheme with a five-point periodic right-hand side:
+ *   rhs_j = sum_{k=-2..2} coef[k+2] f_{j+k}   (indices along solve_dim; periodic, halo
+ *   planes from ranks i-1 / i+1),   out = A^{-1} rhs with this plan's bands.
+ * Covers the collocated derivative above (coef = {-bc/4h, -a/2h, 0, a/2h, bc/4h}) and the
+ * staggered sixth-order derivative and interpolation of PAPER.md P:202-206, whose half-node
+ * inputs f_{i+1/2} are stored at index i:
+ *   derivative    bands (9/62, 1, 9/62), coef = {-17/(186D), -63/(62D), 63/(62D), 17/(186D), 0}
+ *   interpolation bands (3/10, 1, 3/10), coef = {1/20, 3/4, 3/4, 1/20, 0}.
+ * coef is a host array of 5 finite doubles (copied; the caller keeps ownership).  Same
+ * plan requirements, aliasing rules and ordering as ctri_deriv; CTRI_ERR_INVALID_ARG for a
+ * NULL or non-finite coef. */
+ctri_status ctri_compact_apply(ctri_plan plan, const double coef[5], const double* f, double* out,
+                               ctri_stream stream);
+
+/* TEST-ONLY: ctri_compact_apply for a loopback group. */
+ctri_status ctri_compact_apply_loopback(const ctri_plan* plans, int nparts, const double coef[5],
+                                        const double* const* f, double* const* out,
+                                        ctri_stream stream);
 
 /* Copy the plan's configuration, counters and (with CTRI_FLAG_TIMING) last-solve
  * phase times into *out.  Synchronises the plan's timing events. */

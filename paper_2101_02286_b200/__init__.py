@@ -10,7 +10,10 @@ from .ctri import (CTRI_FLAG_DERIV, CTRI_FLAG_FULL_BACKSUB, CTRI_FLAG_GENERIC_LO
                    ctri_deriv_loopback, ctri_factor_query, ctri_get_stats, ctri_get_unique_id,
                    ctri_pcr_coefficients, ctri_plan_create, ctri_reduced_schedule, ctri_plan_create_loopback,
                    ctri_plan_destroy, ctri_solve, ctri_solve_host, ctri_solve_loopback, load,
-                   local_shape)
+                   local_shape, ctri_compact_apply, ctri_compact_apply_loopback,
+                   STAGGERED_DERIV_BANDS, STAGGERED_INTERP_BANDS, staggered_deriv_coef,
+                   staggered_interp_coef)
 
 __all__ = [n for n in dir() if n.startswith(("ctri_", "CTRI_")) or n in
-           ("Plan", "LoopbackGroup", "CtriError", "load", "local_shape")]
+           ("Plan", "LoopbackGroup", "CtriError", "load", "local_shape", "STAGGERED_DERIV_BANDS",
+            "STAGGERED_INTERP_BANDS", "staggered_deriv_coef", "staggered_interp_coef")]

@@ -413,9 +413,9 @@ void record(Plan& P, int slot, cudaStream_t s) {
 }
 
 // (a1) local solve; with `deriv` the tile kernel reads f and forms the stencil RHS itself (a0).
-ctri_status local_phase(Plan& P, const double* b, double* x, cudaStream_t s, bool deriv = false,
-                        double ca = 0.0, double cb = 0.0) {
-  cudaError_t e = (P.local_kernel >= 1) ? launch_tile(P, b, x, s, deriv, ca, cb)
+ctri_status local_phase(Plan& P, const double* b, double* x, cudaStream_t s,
+                        const Stencil5* st = nullptr) {
+  cudaError_t e = (P.local_kernel >= 1) ? launch_tile(P, b, x, s, st)
                                         : launch_local_generic(P, b, x, s);
   if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("local solve launch: ") + cudaGetErrorString(e));
   return CTRI_OK;
@@ -435,7 +435,7 @@ ctri_status stage_kernel(Plan& P, int k, cudaStream_t s) {
 
 // The whole solve for a set of co-scheduled plans: one plan (NCCL) or a loopback group.
 ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* const* x,
-                        cudaStream_t s, bool deriv = false, double ca = 0.0, double cb = 0.0) {
+                        cudaStream_t s, const Stencil5* st = nullptr) {
   const bool nccl = !G[0]->loopback;
   Plan& P0 = *G[0];
   for (size_t r = 0; r < G.size(); ++r) {
@@ -445,7 +445,7 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
   }
   for (Plan* P : G) P->solves++;
   record(P0, EV_START, s);
-  for (size_t r = 0; r < G.size(); ++r) TRY(local_phase(*G[r], b[r], x[r], s, deriv, ca, cb));
+  for (size_t r = 0; r < G.size(); ++r) TRY(local_phase(*G[r], b[r], x[r], s, st));
   record(P0, EV_LOCAL, s);
   if (P0.p == 1) {
     if (P0.vp > 1) {  // (a2)-(a4) across the virtual partitions of this slab
@@ -522,14 +522,18 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
   return CTRI_OK;
 }
 
+// A compact scheme: df = A^{-1} (five-point periodic stencil of f); halos from the neighbours.
 ctri_status deriv_group(std::vector<Plan*>& G, const double* const* f, double* const* df,
-                        double a, double bc, double h, cudaStream_t s) {
+                        const double coef[5], cudaStream_t s) {
   for (size_t r = 0; r < G.size(); ++r) {
     Plan& P = *G[r];
     if (!(P.flags & CTRI_FLAG_DERIV)) return fail(CTRI_ERR_INVALID_ARG, "plan lacks CTRI_FLAG_DERIV");
     if (!f[r] || !df[r] || f[r] == df[r]) return fail(CTRI_ERR_INVALID_ARG, "f/df NULL or aliased");
-    if (h == 0.0 || !std::isfinite(h)) return fail(CTRI_ERR_INVALID_ARG, "bad h");
   }
+  if (!coef) return fail(CTRI_ERR_INVALID_ARG, "NULL coef");
+  for (int k = 0; k < 5; ++k)
+    if (!std::isfinite(coef[k])) return fail(CTRI_ERR_INVALID_ARG, "non-finite stencil coefficient");
+  const Stencil5 st = make_stencil5(coef);
   bool fused = true;
   for (Plan* P : G) fused = fused && P->local_kernel == 1 && P->tile.deriv_ok;
   const bool need_pack = (G[0]->p == 1 && fused) || (G[0]->p > 1 && !G[0]->p2p);
@@ -553,9 +557,9 @@ ctri_status deriv_group(std::vector<Plan*>& G, const double* const* f, double* c
     else TRY(exchange_loopback(G, [](Plan& P) { return round_halo(P); }, s));
   }
   if (fused)  // (a0) fused into (a1): f read once, df written once
-    return solve_group(G, f, df, s, true, a / (2.0 * h), bc / (4.0 * h));
+    return solve_group(G, f, df, s, &st);
   for (size_t r = 0; r < G.size(); ++r) {
-    cudaError_t e = launch_stencil(*G[r], f[r], df[r], a, bc, h, s);
+    cudaError_t e = launch_stencil(*G[r], f[r], df[r], st, s);
     if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, cudaGetErrorString(e));
   }
   return solve_group(G, df, df, s);
@@ -690,26 +694,59 @@ ctri_status ctri_solve_host(ctri_plan plan, const double* b_host, double* x_host
   return CTRI_OK;
 }
 
-ctri_status ctri_deriv(ctri_plan plan, const double* f, double* df, double a, double bc, double h,
-                       ctri_stream stream) {
+// collocated compact first derivative as a five-point stencil
+static bool deriv_coef(double a, double bc, double h, double c[5]) {
+  if (h == 0.0 || !std::isfinite(h)) return false;
+  c[0] = -bc / (4.0 * h);
+  c[1] = -a / (2.0 * h);
+  c[2] = 0.0;
+  c[3] = a / (2.0 * h);
+  c[4] = bc / (4.0 * h);
+  return true;
+}
+
+static ctri_status compact_loopback_group(const ctri_plan* plans, int nparts, std::vector<Plan*>* G) {
+  if (!plans || nparts < 1) return fail(CTRI_ERR_INVALID_ARG, "NULL arguments");
+  G->resize(nparts);
+  for (int r = 0; r < nparts; ++r) {
+    (*G)[r] = reinterpret_cast<Plan*>(plans[r]);
+    if (!(*G)[r] || (*G)[r]->rank != r || (*G)[r]->p != nparts || !(*G)[r]->loopback)
+      return fail(CTRI_ERR_INVALID_ARG, "plans must be one loopback group in rank order");
+  }
+  return CTRI_OK;
+}
+
+ctri_status ctri_compact_apply(ctri_plan plan, const double coef[5], const double* f, double* out,
+                               ctri_stream stream) {
   if (!plan) return fail(CTRI_ERR_INVALID_ARG, "NULL plan");
   Plan* P = reinterpret_cast<Plan*>(plan);
   std::vector<Plan*> G{P};
-  if (P->loopback && P->p > 1) return fail(CTRI_ERR_INVALID_ARG, "loopback plan: use ctri_deriv_loopback");
-  return deriv_group(G, &f, &df, a, bc, h, (cudaStream_t)stream);
+  if (P->loopback && P->p > 1) return fail(CTRI_ERR_INVALID_ARG, "loopback plan: use ctri_compact_apply_loopback");
+  return deriv_group(G, &f, &out, coef, (cudaStream_t)stream);
+}
+
+ctri_status ctri_compact_apply_loopback(const ctri_plan* plans, int nparts, const double coef[5],
+                                        const double* const* f, double* const* out,
+                                        ctri_stream stream) {
+  std::vector<Plan*> G;
+  TRY(compact_loopback_group(plans, nparts, &G));
+  if (!f || !out) return fail(CTRI_ERR_INVALID_ARG, "NULL arguments");
+  return deriv_group(G, f, out, coef, (cudaStream_t)stream);
+}
+
+ctri_status ctri_deriv(ctri_plan plan, const double* f, double* df, double a, double bc, double h,
+                       ctri_stream stream) {
+  double c[5];
+  if (!deriv_coef(a, bc, h, c)) return fail(CTRI_ERR_INVALID_ARG, "bad h");
+  return ctri_compact_apply(plan, c, f, df, stream);
 }
 
 ctri_status ctri_deriv_loopback(const ctri_plan* plans, int nparts, const double* const* f,
                                 double* const* df, double a, double bc, double h,
                                 ctri_stream stream) {
-  if (!plans || !f || !df || nparts < 1) return fail(CTRI_ERR_INVALID_ARG, "NULL arguments");
-  std::vector<Plan*> G(nparts);
-  for (int r = 0; r < nparts; ++r) {
-    G[r] = reinterpret_cast<Plan*>(plans[r]);
-    if (!G[r] || G[r]->rank != r || G[r]->p != nparts || !G[r]->loopback)
-      return fail(CTRI_ERR_INVALID_ARG, "plans must be one loopback group in rank order");
-  }
-  return deriv_group(G, f, df, a, bc, h, (cudaStream_t)stream);
+  double c[5];
+  if (!deriv_coef(a, bc, h, c)) return fail(CTRI_ERR_INVALID_ARG, "bad h");
+  return ctri_compact_apply_loopback(plans, nparts, c, f, df, stream);
 }
 
 ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {

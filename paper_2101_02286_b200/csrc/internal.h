@@ -36,6 +36,41 @@ struct TileConsts {
 
 constexpr int kMaxUniformStages = 12;  // head-system PCR stages passed as kernel parameters
 
+// Five-point periodic RHS of a compact scheme, b_j = sum_{k=-2..2} c_k f_{j+k} (P:65-67 collocated
+// derivative; P:202-206 staggered derivative / interpolation).  The three schemes of the paper are
+// pair forms that keep the exact differences / sums of their definitions and cost 2 FMAs:
+//   kind 1  c = (-q, -p, 0, p, q):    p (f_1 - f_-1) + q (f_2 - f_-2)    collocated derivative
+//   kind 2  c = (-q, -p, p, q, 0):    p (f_0 - f_-1) + q (f_1 - f_-2)    staggered derivative
+//   kind 3  c = (q, p, p, q, 0):      p (f_0 + f_-1) + q (f_1 + f_-2)    staggered interpolation
+//   kind 0  anything else:            sum_k c_k f_k (5 FMAs)
+struct Stencil5 {
+  double c[5] = {0, 0, 0, 0, 0};
+  double p = 0, q = 0;
+  int kind = 0;
+};
+inline Stencil5 make_stencil5(const double c[5]) {
+  Stencil5 s;
+  for (int k = 0; k < 5; ++k) s.c[k] = c[k];
+  if (c[2] == 0.0 && c[1] == -c[3] && c[0] == -c[4]) {
+    s.kind = 1, s.p = c[3], s.q = c[4];
+  } else if (c[4] == 0.0 && c[1] == -c[2] && c[0] == -c[3]) {
+    s.kind = 2, s.p = c[2], s.q = c[3];
+  } else if (c[4] == 0.0 && c[1] == c[2] && c[0] == c[3]) {
+    s.kind = 3, s.p = c[2], s.q = c[3];
+  }
+  return s;
+}
+// v0..v4 = f_{j-2} .. f_{j+2}
+__host__ __device__ __forceinline__ double apply_stencil5(const Stencil5& s, double v0, double v1,
+                                                          double v2, double v3, double v4) {
+  switch (s.kind) {
+    case 1: return s.p * (v3 - v1) + s.q * (v4 - v0);
+    case 2: return s.p * (v2 - v1) + s.q * (v3 - v0);
+    case 3: return s.p * (v2 + v1) + s.q * (v3 + v0);
+    default: return s.c[0] * v0 + s.c[1] * v1 + s.c[2] * v2 + s.c[3] * v3 + s.c[4] * v4;
+  }
+}
+
 struct TileArgs {
   const double* b;
   double* x;
@@ -56,8 +91,8 @@ struct TileArgs {
   double* plane_yf;  // mode 1: y_D at interior row 1
   double* plane_yl;  // mode 1: y_D at row n-1
   double* plane_bt;  // mode 1: b at row 0 (b~_i)
-  // fused compact-derivative stencil (LAYOUT 2): b = ca (f_{+1} - f_{-1}) + cb (f_{+2} - f_{-2})
-  double ca, cb;
+  // fused compact-scheme RHS stencil (LAYOUT 2), see Stencil5
+  Stencil5 st;
   const double* halo_lo;  // [2][m]: rows n-2, n-1 of the slab above
   const double* halo_hi;  // [2][m]: rows 0, 1 of the slab below
   unsigned long long* trace;  // measurement only (CTRI_TILE_TRACE)
@@ -190,11 +225,11 @@ cudaError_t launch_backsub(const Plan& P, double* x, cudaStream_t s);
 cudaError_t launch_reduced_local(const Plan& P, double* x, cudaStream_t s);
 cudaError_t launch_window(const Plan& P, double* x, const double* next, cudaStream_t s);
 cudaError_t launch_pack_halo(const Plan& P, const double* f, cudaStream_t s);
-cudaError_t launch_stencil(const Plan& P, const double* f, double* rhs, double a, double bc,
-                           double h, cudaStream_t s);
+cudaError_t launch_stencil(const Plan& P, const double* f, double* rhs, const Stencil5& st,
+                           cudaStream_t s);
 bool tile_configure(Plan& P, std::string* why);
 const char* tile_variant_name(int v);
 cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t s,
-                        bool deriv = false, double ca = 0.0, double cb = 0.0);
+                        const Stencil5* st = nullptr);
 
 }  // namespace ctri

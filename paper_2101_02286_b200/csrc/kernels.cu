@@ -324,7 +324,7 @@ __global__ void k_pack_halo(const double* __restrict__ f, int64_t outer, int64_t
 // rank i+1); with nparts = 1 the wrap stays inside the slab.
 __global__ void k_stencil(const double* __restrict__ f, double* __restrict__ rhs, int64_t outer,
                           int64_t n, int64_t inner, const double* __restrict__ halo_lo,
-                          const double* __restrict__ halo_hi, int wrap, double ca, double cb) {
+                          const double* __restrict__ halo_hi, int wrap, const Stencil5 st) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t m = outer * inner;
   if (j >= m) return;
@@ -337,7 +337,7 @@ __global__ void k_stencil(const double* __restrict__ f, double* __restrict__ rhs
     if (rr < 0) return halo_lo[(rr + 2) * m + j];
     return halo_hi[(rr - n) * m + j];
   };
-  const double v = ca * (at(r + 1) - at(r - 1)) + cb * (at(r + 2) - at(r - 2));
+  const double v = apply_stencil5(st, at(r - 2), at(r - 1), at(r), at(r + 1), at(r + 2));
   rhs[(o * n + r) * inner + c] = v;
 }
 
@@ -387,12 +387,12 @@ cudaError_t launch_pack_halo(const Plan& P, const double* f, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_stencil(const Plan& P, const double* f, double* rhs, double a, double bc,
-                           double h, cudaStream_t s) {
+cudaError_t launch_stencil(const Plan& P, const double* f, double* rhs, const Stencil5& st,
+                           cudaStream_t s) {
   const int64_t m = P.lay.m();
   dim3 grid(blocks_for(m, 256), (unsigned)P.lay.n);
   k_stencil<<<grid, 256, 0, s>>>(f, rhs, P.lay.outer, P.lay.n, P.lay.inner, P.halo_lo, P.halo_hi,
-                                 P.p == 1 ? 1 : 0, a / (2.0 * h), bc / (4.0 * h));
+                                 P.p == 1 ? 1 : 0, st);
   return cudaGetLastError();
 }
 

@@ -243,9 +243,28 @@ __global__ void __launch_bounds__(NT, MINB)
         v[k + m] = r;
       }
     }
-    if (DERIV) {  // b_k = a (f_{k+1} - f_{k-1}) / 2h + bc (f_{k+2} - f_{k-2}) / 4h, in place
+    if (DERIV) {  // b_k = sum_j c_j f_{k+j} (compact-scheme RHS, Stencil5), in place;
+                  // one uniform branch per tile selects the scheme's pair form
+      const double p = A.st.p, q = A.st.q;
+      switch (A.st.kind) {
+        case 1:
 #pragma unroll
-      for (int k = 0; k < K; ++k) v[k] = A.ca * (v[k + 3] - v[k + 1]) + A.cb * (v[k + 4] - v[k]);
+          for (int k = 0; k < K; ++k) v[k] = p * (v[k + 3] - v[k + 1]) + q * (v[k + 4] - v[k]);
+          break;
+        case 2:
+#pragma unroll
+          for (int k = 0; k < K; ++k) v[k] = p * (v[k + 2] - v[k + 1]) + q * (v[k + 3] - v[k]);
+          break;
+        case 3:
+#pragma unroll
+          for (int k = 0; k < K; ++k) v[k] = p * (v[k + 2] + v[k + 1]) + q * (v[k + 3] + v[k]);
+          break;
+        default:
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+            v[k] = A.st.c[0] * v[k] + A.st.c[1] * v[k + 1] + A.st.c[2] * v[k + 2] +
+                   A.st.c[3] * v[k + 3] + A.st.c[4] * v[k + 4];
+      }
     }
     stamp(it, 1);
     __syncthreads();  // every thread has its chunk in registers: stage s is free
@@ -643,8 +662,9 @@ static EncodeTiledFn get_encode() {
   return fn;
 }
 
-cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t s, bool deriv,
-                        double ca, double cb) {
+cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t s,
+                        const Stencil5* st) {
+  const bool deriv = st != nullptr;
   const TileConfig& tc = P.tile;
   if (deriv && !tc.deriv_ok) return cudaErrorNotSupported;
   EncodeTiledFn enc = get_encode();
@@ -708,8 +728,7 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   A.plane_yf = P.yf;
   A.plane_yl = P.yl;
   A.plane_bt = P.bt;
-  A.ca = ca;
-  A.cb = cb;
+  if (st) A.st = *st;
   // halo planes: rows n-2, n-1 of the slab above and rows 0, 1 of the slab below; with one
   // partition they are this slab's own rows (periodic wrap), packed into send_hi / send_lo
   A.halo_lo = (P.p == 1) ? P.send_hi : P.halo_lo;

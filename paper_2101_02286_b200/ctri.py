@@ -24,7 +24,7 @@ CTRI_FLAG_TIMING = 1 << 2
 CTRI_FLAG_DERIV = 1 << 3
 CTRI_FLAG_NCCL_ROUNDS = 1 << 4
 CTRI_MAX_STAGES = 16
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 STATUS = {0: "CTRI_OK", 1: "CTRI_ERR_INVALID_ARG", 2: "CTRI_ERR_UNSUPPORTED", 3: "CTRI_ERR_SINGULAR",
           4: "CTRI_ERR_PARTITION_TOO_SMALL", 5: "CTRI_ERR_CUDA", 6: "CTRI_ERR_NCCL",
@@ -35,7 +35,7 @@ ABI_SYMBOLS = ("ctri_status_string", "ctri_last_error", "ctri_abi_version", "ctr
                "ctri_plan_create", "ctri_plan_create_loopback", "ctri_solve", "ctri_solve_loopback",
                "ctri_solve_host", "ctri_deriv", "ctri_deriv_loopback", "ctri_get_stats",
                "ctri_plan_destroy", "ctri_factor_query", "ctri_pcr_coefficients",
-               "ctri_reduced_schedule")
+               "ctri_reduced_schedule", "ctri_compact_apply", "ctri_compact_apply_loopback")
 
 
 class CtriError(RuntimeError):
@@ -114,6 +114,9 @@ def load(build_if_missing: bool = False):
         "ctri_deriv_loopback": (st, [ctypes.POINTER(P), ctypes.c_int, ctypes.POINTER(P),
                                      ctypes.POINTER(P), ctypes.c_double, ctypes.c_double,
                                      ctypes.c_double, P]),
+        "ctri_compact_apply": (st, [P, dp, P, P, P]),
+        "ctri_compact_apply_loopback": (st, [ctypes.POINTER(P), ctypes.c_int, dp, ctypes.POINTER(P),
+                                             ctypes.POINTER(P), P]),
         "ctri_get_stats": (st, [P, ctypes.POINTER(ctri_stats)]),
         "ctri_plan_destroy": (st, [P]),
         "ctri_factor_query": (st, [ctypes.c_int64, dp, dp, dp, dp, ctypes.POINTER(ctypes.c_int)]),
@@ -228,6 +231,45 @@ def ctri_deriv_loopback(plans, fs, dfs, a, bc, h, stream=None):
                                       _stream_ptr(stream)), "ctri_deriv_loopback")
 
 
+def _coef5(coef):
+    c = (ctypes.c_double * 5)(*[float(v) for v in coef])
+    if len(coef) != 5:
+        raise ValueError("coef must hold 5 values (offsets -2..2)")
+    return ctypes.cast(c, ctypes.POINTER(ctypes.c_double)), c
+
+
+def ctri_compact_apply(plan: int, coef, f, out, stream=None):
+    cp, _keep = _coef5(coef)
+    _check(load().ctri_compact_apply(plan, cp, _ptr(f), _ptr(out), _stream_ptr(stream)),
+           "ctri_compact_apply")
+
+
+def ctri_compact_apply_loopback(plans, coef, fs, outs, stream=None):
+    n = len(plans)
+    hp = (ctypes.c_void_p * n)(*plans)
+    fp = (ctypes.c_void_p * n)(*[_ptr(f) for f in fs])
+    op = (ctypes.c_void_p * n)(*[_ptr(o) for o in outs])
+    cp, _keep = _coef5(coef)
+    _check(load().ctri_compact_apply_loopback(hp, n, cp, fp, op, _stream_ptr(stream)),
+           "ctri_compact_apply_loopback")
+
+
+# Right-hand sides of the staggered sixth-order schemes as five-point
+# stencils over half-node values g_i = f_{i+1/2} stored at index i (offsets -2..2).
+STAGGERED_DERIV_BANDS = (9 / 62, 1.0, 9 / 62)
+STAGGERED_INTERP_BANDS = (3 / 10, 1.0, 3 / 10)
+
+
+def staggered_deriv_coef(delta: float):
+    a, b = 63 / 62, 17 / 62
+    return (-b / (3 * delta), -a / delta, a / delta, b / (3 * delta), 0.0)
+
+
+def staggered_interp_coef():
+    a, b = 3 / 2, 1 / 10
+    return (b / 2, a / 2, a / 2, b / 2, 0.0)
+
+
 def ctri_get_stats(plan: int) -> dict:
     s = ctri_stats()
     _check(load().ctri_get_stats(plan, ctypes.byref(s)), "ctri_get_stats")
@@ -338,6 +380,10 @@ class Plan:
         ctri_deriv(self.handle, f, df, a, bc, h, stream)
         return df
 
+    def compact_apply(self, coef, f, out, stream=None):
+        ctri_compact_apply(self.handle, coef, f, out, stream)
+        return out
+
     def stats(self) -> dict:
         return ctri_get_stats(self.handle)
 
@@ -382,6 +428,9 @@ class LoopbackGroup:
             import math
             h = 2 * math.pi / self.global_dims[self.solve_dim]
         ctri_deriv_loopback(self.handles, fs, dfs, a, bc, h, stream)
+
+    def compact_apply(self, coef, fs, outs, stream=None):
+        ctri_compact_apply_loopback(self.handles, coef, fs, outs, stream)
 
     def stats(self, rank=0):
         return ctri_get_stats(self.handles[rank])

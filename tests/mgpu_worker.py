@@ -66,9 +66,23 @@ def main():
     plan.close()
     if rank == 0:
         results["deriv"] = {"err": rel_err(d.cpu().numpy(), oracle.deriv(f, 0), 0)}
+    # staggered sixth-order interpolation through ctri_compact_apply
+    from paper_2101_02286_b200 import ctri
+    plan = pdist.plan_from_process_group(dims, 0, ctri.STAGGERED_INTERP_BANDS, True, flags=CTRI_FLAG_DERIV)
+    plan.compact_apply(ctri.staggered_interp_coef(), fl, dl)
+    torch.cuda.synchronize()
+    d = pdist.gather_to_rank0(dl, 0)
+    plan.close()
+    if rank == 0:
+        ref = oracle.compact_apply(f, 0, oracle.staggered_interp_coef(), oracle_bands_interp())
+        results["sinterp"] = {"err": rel_err(d.cpu().numpy(), ref, 0)}
         print("RESULTS " + json.dumps(results), flush=True)
     dist.barrier()
     dist.destroy_process_group()
+
+
+def oracle_bands_interp():
+    return (oracle.STAGGERED_INTERP_ALPHA, 1.0, oracle.STAGGERED_INTERP_ALPHA)
 
 
 if __name__ == "__main__":
