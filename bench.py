@@ -46,6 +46,9 @@ def parse():
                     choices=["collocated", "staggered_deriv", "staggered_interp"],
                     help="cfg5 compact scheme: collocated derivative (P:65-67) or the staggered "
                          "sixth-order derivative / interpolation (P:202-206)")
+    ap.add_argument("--reduced", default="pcr", choices=["pcr", "allgather", "nccl"],
+                    help="nparts > 1 reduced system: fused P2P pairwise schedule (default), the "
+                         "P2P all-gather with A^-1 rows (N4), or host-issued NCCL rounds")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -262,6 +265,10 @@ def main():
         name = f"custom {dims} solve index {sd}"
     deriv = args.config == "cfg5"
     flags = CTRI_FLAG_TIMING | (CTRI_FLAG_DERIV if deriv else 0)
+    if world > 1 and args.reduced == "allgather":
+        flags |= ctri.CTRI_FLAG_ALLGATHER
+    elif world > 1 and args.reduced == "nccl":
+        flags |= ctri.CTRI_FLAG_NCCL_ROUNDS
     bands, coef = (1 / 3, 1.0, 1 / 3), None
     if deriv and args.scheme != "collocated":
         delta = 2 * math.pi / dims[sd]
@@ -379,7 +386,8 @@ def main():
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": name, "global_dims": list(dims), "solve_dim": sd,
                            "nparts": p, "local_dims": list(lshape),
-                           "bands": [1 / 3, 1.0, 1 / 3], "cyclic": True,
+                           "bands": list(bands), "cyclic": True,
+                           "reduced": args.reduced if p > 1 else None,
                            "l2": "inputs larger than L2 (%.2f GB per array per GPU)" % (pts_local * 8 / 1e9),
                            "local_kernel": roof["kernel"]},
                 "pct_hbm_roofline": 100.0 * step_gbs / peak,
@@ -389,10 +397,11 @@ def main():
                 "e2e": e2e,
                 "gpu_launches": launches,
                 "comm_us": ({"fused_reduced_kernel_us": back,
-                             "note": "device-initiated (a2)-(a4): LL P2P stores over NVLink + "
-                                     "windowed back-substitution, one kernel; includes waiting "
-                                     "for the slowest peer's local solve"}
-                            if st["reduced_path"] == 1 else
+                             "note": "device-initiated (a2)-(a4): LL P2P stores over NVLink "
+                                     "(pairwise schedule, or one all-gather round) + the window "
+                                     "back-substitution kernel; includes waiting for the slowest "
+                                     "peer's local solve"}
+                            if st["reduced_path"] in (1, 2) else
                             {"y_exchange": yx, "stages": stage_us, "x_exchange": xx,
                              "backsub_kernel": back}) if p > 1 else None,
                 "clocks": sampler.summary() if sampler else None}

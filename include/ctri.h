@@ -65,6 +65,10 @@ typedef enum ctri_status {
 #define CTRI_FLAG_DERIV          (1u << 3) /* allocate halo planes so ctri_deriv may be called */
 #define CTRI_FLAG_NCCL_ROUNDS    (1u << 4) /* nparts > 1: host-issued NCCL rounds instead of the fused
                                               device-initiated P2P reduced phase */
+#define CTRI_FLAG_ALLGATHER      (1u << 5) /* 2 <= nparts <= 8, P2P path: solve the reduced system with
+                                              ONE all-gather round of 2 planes per rank and plan-time
+                                              rows of A^{-1} (latency comparison for
+                                              the log2 p pairwise stages).  UNSUPPORTED otherwise. */
 
 #define CTRI_MAX_STAGES 16
 
@@ -93,7 +97,7 @@ typedef struct ctri_stats {
   int32_t tile_variant;         /* cluster-tile variant index (columns/threads/ring depth), -1 if none */
   int32_t tile_stages;          /* TMA shared-memory ring depth of the tile kernel */
   int32_t reduced_path;         /* nparts > 1: 0 = NCCL rounds, 1 = fused P2P kernel (t_backsub_us
-                                   then times the whole fused (a2)-(a4) kernel) */
+                                   then times the whole fused (a2)-(a4) kernel), 2 = P2P all-gather */
   int32_t device_error;         /* nonzero: a P2P wait hit its deadline (peer missing) */
   int32_t vparts;               /* nparts == 1: partitions of the slab solved on this GPU (the
                                    paper's partition method; (a2)-(a4) then run on-device) */
@@ -230,6 +234,13 @@ ctri_status ctri_pcr_coefficients(int P, int cyclic, const double* L, const doub
 ctri_status ctri_reduced_schedule(int P, int cyclic, const double* L, const double* D,
                                   const double* U, int max_steps, int* nsteps, int* kinds,
                                   double* w, int* src, double* c, int* counts);
+
+/* Dense inverse of the P x P reduced matrix A^ (bands L, D, U per row; cyclic corners;
+ * couplings that coincide for P <= 2 add up) into inv[P*P], row-major: the plan-time table of
+ * the all-gather reduced solve (CTRI_FLAG_ALLGATHER).  Gauss-Jordan with
+ * partial pivoting; SINGULAR if a pivot falls below 1e-13 * max|coefficient|. */
+ctri_status ctri_reduced_inverse(int P, int cyclic, const double* L, const double* D,
+                                 const double* U, double* inv);
 
 #ifdef __cplusplus
 }

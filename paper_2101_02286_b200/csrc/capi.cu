@@ -187,11 +187,19 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
                          &P->xt, &P->xt_next};
     for (double** pl : planes) TRY(alloc_plane(pl, m * P->vp));
   }
+  if (flags & CTRI_FLAG_ALLGATHER) {
+    if (p < 2 || p > kMaxAG || (flags & CTRI_FLAG_NCCL_ROUNDS))
+      return fail(CTRI_ERR_UNSUPPORTED, "CTRI_FLAG_ALLGATHER needs 2 <= nparts <= 8 and the P2P path");
+    if (!reduced_inverse(p, cyclic != 0, L, D, U, pivot_threshold(P->bands), &P->ainv, &fe))
+      return fail((ctri_status)fe.code, fe.detail);
+    P->allgather = true;
+  }
   if (p > 1 && p <= kMaxP2PRanks && !(flags & CTRI_FLAG_NCCL_ROUNDS)) {
     // fused device-initiated reduced phase: double-buffered mailbox + epoch flags
     const int q = (int)P->sched.steps.size();
-    P->p2p_nslices = p2p_slices(m, P->loopback ? p : 1, P->num_sms);
-    P->mbox_bytes = sizeof(unsigned long long) * p2p_mailbox_words(m, q, (flags & CTRI_FLAG_DERIV) != 0);
+    P->p2p_nslices = p2p_slices(m, P->loopback ? p : 1, P->num_sms, P->allgather);
+    P->mbox_bytes = sizeof(unsigned long long) *
+                    p2p_mailbox_words(p2p_copy_words(m, q, p, P->allgather), m, (flags & CTRI_FLAG_DERIV) != 0);
     CUDA_TRY(cudaMalloc(&P->mbox_alloc, P->mbox_bytes));
     CUDA_TRY(cudaMemsetAsync(P->mbox_alloc, 0, P->mbox_bytes, s));
     CUDA_TRY(cudaMalloc(&P->d_err, sizeof(int)));
@@ -256,6 +264,8 @@ void p2p_args(const Plan& P0, P2PArgs* A) {
   std::memset(A, 0, sizeof(*A));
   A->p = P0.p;
   A->q = (int)P0.sched.steps.size();
+  A->allgather = P0.allgather ? 1 : 0;
+  A->copy_words = p2p_copy_words(P0.lay.m(), A->q, P0.p, P0.allgather);
   A->cyclic = P0.cyclic;
   A->nslices = P0.p2p_nslices;
   A->m = P0.lay.m();
@@ -284,6 +294,13 @@ void p2p_fill_rank(const Plan& P, double* x, P2PRank* R) {
   R->halo_hi = P.halo_hi;
   for (int r = 0; r < kMaxP2PRanks; ++r) R->peer_mbox[r] = nullptr;
   for (int r = 0; r < P.p; ++r) R->peer_mbox[r] = reinterpret_cast<unsigned long long*>(P.peer_alloc[r]);
+  for (int r = 0; r < kMaxAG; ++r) {
+    R->ag0[r] = R->ag1[r] = 0.0;
+    if (!P.allgather || r >= P.p) continue;
+    const int nx = P.rank + 1;  // x~_{i+1}: rank i+1, wrapping to 0 (cyclic) or absent (acyclic)
+    R->ag0[r] = P.ainv[(size_t)P.rank * P.p + r];
+    if (nx < P.p || P.cyclic) R->ag1[r] = P.ainv[(size_t)(nx % P.p) * P.p + r];
+  }
   const Schedule& sc = P.sched;
   for (int s = 0; s < kMaxP2PSteps; ++s) {
     P2PStep& t = R->step[s];
@@ -308,6 +325,11 @@ void p2p_fill_rank(const Plan& P, double* x, P2PRank* R) {
 
 // messages this rank sends per solve, and dependent exchange rounds, from the schedule
 void schedule_counts(const Plan& P, int* sends, int* rounds) {
+  if (P.allgather) {  // one round: 2 planes to each of the p - 1 peers
+    *sends = 2 * (P.p - 1);
+    *rounds = 1;
+    return;
+  }
   const Schedule& sc = P.sched;
   int sd = (has_right(P) ? 1 : 0) + (has_left(P) ? 1 : 0), rd = 2;
   for (size_t s = 0; s < sc.steps.size(); ++s) {
@@ -766,7 +788,7 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
   out->tile_columns = P->local_kernel ? P->tile.C : 1;
   out->tile_variant = P->local_kernel ? P->tile.variant : -1;
   out->tile_stages = P->local_kernel ? P->tile.STAGES : 0;
-  out->reduced_path = (P->p > 1 && P->p2p) ? 1 : 0;
+  out->reduced_path = (P->p > 1 && P->p2p) ? (P->allgather ? 2 : 1) : 0;
   out->vparts = P->vp;
   out->grid_ctas = P->local_kernel ? P->tile.grid : (int32_t)((P->tlay.m() + 127) / 128);
   out->device_error = 0;
@@ -897,6 +919,21 @@ ctri_status ctri_reduced_schedule(int P, int cyclic, const double* L, const doub
   counts[0] = sc.pcr_stages;
   counts[1] = sc.detach_stages;
   counts[2] = sc.detached_rows;
+  return CTRI_OK;
+}
+
+ctri_status ctri_reduced_inverse(int P, int cyclic, const double* L, const double* D,
+                                 const double* U, double* inv) {
+  if (P < 1 || !L || !D || !U || !inv) return fail(CTRI_ERR_INVALID_ARG, "bad arguments");
+  double mx = 0;
+  for (int i = 0; i < P; ++i)
+    mx = std::max(mx, std::max(std::fabs(D[i]), std::max(std::fabs(L[i]), std::fabs(U[i]))));
+  std::vector<double> out;
+  FactorError fe;
+  if (!reduced_inverse(P, cyclic != 0, std::vector<double>(L, L + P), std::vector<double>(D, D + P),
+                       std::vector<double>(U, U + P), 1e-13 * mx, &out, &fe))
+    return fail((ctri_status)fe.code, fe.detail);
+  std::memcpy(inv, out.data(), sizeof(double) * out.size());
   return CTRI_OK;
 }
 

@@ -144,6 +144,47 @@ bool pcr_factor(int P, bool cyclic, const std::vector<double>& L0, const std::ve
   return true;
 }
 
+bool reduced_inverse(int P, bool cyclic, const std::vector<double>& L, const std::vector<double>& D,
+                     const std::vector<double>& U, double guard, std::vector<double>* inv,
+                     FactorError* err) {
+  if (P < 1 || (int)L.size() != P || (int)D.size() != P || (int)U.size() != P)
+    return fail(err, kInvalid, "reduced_inverse: bad sizes");
+  std::vector<double> a((size_t)P * P, 0.0), e((size_t)P * P, 0.0);
+  for (int i = 0; i < P; ++i) {
+    a[(size_t)i * P + i] += D[i];
+    if (cyclic || i > 0) a[(size_t)i * P + (i + P - 1) % P] += L[i];
+    if (cyclic || i < P - 1) a[(size_t)i * P + (i + 1) % P] += U[i];
+    e[(size_t)i * P + i] = 1.0;
+  }
+  for (int k = 0; k < P; ++k) {
+    int piv = k;
+    for (int i = k + 1; i < P; ++i)
+      if (std::fabs(a[(size_t)i * P + k]) > std::fabs(a[(size_t)piv * P + k])) piv = i;
+    if (!(std::fabs(a[(size_t)piv * P + k]) >= guard)) return fail(err, kSingular, "reduced_inverse: pivot guard");
+    if (piv != k)
+      for (int j = 0; j < P; ++j) {
+        std::swap(a[(size_t)k * P + j], a[(size_t)piv * P + j]);
+        std::swap(e[(size_t)k * P + j], e[(size_t)piv * P + j]);
+      }
+    const double r = 1.0 / a[(size_t)k * P + k];
+    for (int j = 0; j < P; ++j) {
+      a[(size_t)k * P + j] *= r;
+      e[(size_t)k * P + j] *= r;
+    }
+    for (int i = 0; i < P; ++i) {
+      if (i == k) continue;
+      const double f = a[(size_t)i * P + k];
+      if (f == 0.0) continue;
+      for (int j = 0; j < P; ++j) {
+        a[(size_t)i * P + j] -= f * a[(size_t)k * P + j];
+        e[(size_t)i * P + j] -= f * e[(size_t)k * P + j];
+      }
+    }
+  }
+  *inv = e;
+  return true;
+}
+
 bool reduced_schedule(int P, bool cyclic, const std::vector<double>& L0,
                       const std::vector<double>& D0, const std::vector<double>& U0, double guard,
                       Schedule* out, FactorError* err) {

@@ -80,6 +80,13 @@ struct Schedule {
 bool reduced_schedule(int P, bool cyclic, const std::vector<double>& L, const std::vector<double>& D,
                       const std::vector<double>& U, double guard, Schedule* out, FactorError* err);
 
+// Dense inverse of the P x P reduced matrix A^ (rows L/D/U, cyclic corners; couplings that
+// coincide for P <= 2 add up), Gauss-Jordan with partial pivoting, row-major [P][P].  Used by the
+// all-gather reduced solve: x~_i = sum_r (A^{-1})_{ir} b^_r.
+bool reduced_inverse(int P, bool cyclic, const std::vector<double>& L, const std::vector<double>& D,
+                     const std::vector<double>& U, double guard, std::vector<double>* inv,
+                     FactorError* err);
+
 inline bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 inline int ilog2(int64_t v) {
   int q = 0;

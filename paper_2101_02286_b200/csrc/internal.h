@@ -118,6 +118,7 @@ struct TileConfig {
 // ---- fused device-initiated reduced phase (p2p.cu) ----
 constexpr int kMaxP2PRanks = 16;  // real multi-GPU: <= 8 per box; loopback tests up to 16
 constexpr int kMaxP2PSteps = 16;
+constexpr int kMaxAG = 8;  // all-gather reduced solve (CTRI_FLAG_ALLGATHER): nparts <= 8
 // One rank's part of a reduced-system schedule step (factor.h Schedule):
 //   v <- w v - c0 u0 - c1 u1, u_k received in mailbox slot k from rank src_k;
 //   this rank's pre-step v is sent to ranks dst_k, slot dslot_k.
@@ -137,10 +138,13 @@ struct P2PRank {
                                  // solve captured in a CUDA graph advances it on every replay)
   unsigned long long* peer_mbox[kMaxP2PRanks];  // every rank's mailbox as addressable here
   P2PStep step[kMaxP2PSteps];
+  double ag0[kMaxAG], ag1[kMaxAG];  // all-gather mode: rows i and i+1 of A^{-1} (zeros past p)
 };
 struct P2PArgs {
   int p, q, cyclic, nslices, full;  // q = number of schedule steps
+  int allgather;                    // 1: one all-gather round + A^{-1} rows instead of the schedule
   int64_t slice_cols, m, W;
+  int64_t copy_words;               // mailbox words of one epoch copy of the reduced-phase region
   Layout lay;
   double l, u;
   const double *S, *R;
@@ -149,8 +153,9 @@ struct P2PArgs {
   P2PRank rk[kMaxP2PRanks];
 };
 cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s);
-int p2p_slices(int64_t m, int nranks_launch, int num_sms);
-size_t p2p_mailbox_words(int64_t m, int q, bool halo);
+int p2p_slices(int64_t m, int nranks_launch, int num_sms, bool allgather);
+int64_t p2p_copy_words(int64_t m, int q, int p, bool allgather);
+size_t p2p_mailbox_words(int64_t copy_words, int64_t m, bool halo);
 cudaError_t launch_halo_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s);
 
 struct Plan {
@@ -196,6 +201,8 @@ struct Plan {
 
   // fused P2P reduced phase
   bool p2p = false;
+  bool allgather = false;         // CTRI_FLAG_ALLGATHER: reduced system by A^{-1} rows
+  std::vector<double> ainv;       // [p][p] A^{-1} (all-gather mode)
   int p2p_nslices = 0;
   void* mbox_alloc = nullptr;          // own LL mailbox (cudaMalloc, IPC-exported)
   unsigned int* d_epoch = nullptr;     // per-slice solve epochs of the fused P2P kernel

@@ -65,6 +65,32 @@ __device__ __forceinline__ bool ll_recv(const unsigned long long* src, uint32_t 
   *out = __longlong_as_double((long long)((w1 << 32) | (w0 & 0xffffffffull)));
   return true;
 }
+// Batched LL receive of the words at src + r * stride for the ranks r in `mask` (r < kMaxAG):
+// every sweep issues all pending loads before testing any, so the waits overlap.
+__device__ __forceinline__ bool ll_recv_batch(const unsigned long long* src, int64_t stride,
+                                              uint32_t mask, uint32_t ep, unsigned long long deadline,
+                                              double (&v)[kMaxAG]) {
+  int spins = 0;
+  while (mask) {
+    unsigned long long w0[kMaxAG], w1[kMaxAG];
+#pragma unroll
+    for (int k = 0; k < kMaxAG; ++k)
+      if (mask & (1u << k))
+        asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];"
+                     : "=l"(w0[k]), "=l"(w1[k]) : "l"(src + k * stride) : "memory");
+#pragma unroll
+    for (int k = 0; k < kMaxAG; ++k)
+      if ((mask & (1u << k)) && (uint32_t)(w0[k] >> 32) == ep && (uint32_t)(w1[k] >> 32) == ep) {
+        v[k] = __longlong_as_double((long long)((w1[k] << 32) | (w0[k] & 0xffffffffull)));
+        mask &= ~(1u << k);
+      }
+    if (mask && ++spins == 64) {
+      spins = 0;
+      if (globaltimer() > deadline) return false;
+    }
+  }
+  return true;
+}
 }  // namespace
 
 __global__ void __launch_bounds__(kP2PThreads, 2)
@@ -81,8 +107,7 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
   const uint32_t ep = R.epoch[slice] + 1u;
   const unsigned long long deadline = globaltimer() + 20ull * 1000000000ull;  // 20 s
   // mailbox copy (epoch parity): [y: 2m][stage k, slot 0/1: 2m each][x: 2m] 64-bit words
-  const int64_t per_copy = (int64_t)(2 + 2 * q) * 2 * m;
-  const int64_t copy_off = (int64_t)(ep & 1u) * per_copy;
+  const int64_t copy_off = (int64_t)(ep & 1u) * A.copy_words;
   const int64_t OFF_Y = 0, OFF_X = (int64_t)(1 + 2 * q) * 2 * m;
   auto OFF_S = [&](int k, int slot) -> int64_t { return (int64_t)(1 + 2 * k + slot) * 2 * m; };
   const bool cyc = A.cyclic != 0;
@@ -185,6 +210,80 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
   if (tr) stamp(5);
 }
 
+// All-gather variant of (a2)-(a3) (CTRI_FLAG_ALLGATHER): one exchange round
+// instead of 2 + log2 p dependent ones; its own kernel so each variant keeps its registers.
+__global__ void __launch_bounds__(kP2PThreads, 1)
+    k_reduced_allgather(const P2PArgs A) {
+  const int r_local = blockIdx.x / A.nslices;
+  const int slice = blockIdx.x - r_local * A.nslices;
+  const P2PRank& R = A.rk[r_local];
+  const int p = A.p, rank = R.rank;
+  const int64_t m = A.m;
+  const int64_t c0 = (int64_t)slice * A.slice_cols;
+  const int64_t c1 = std::min<int64_t>(m, c0 + A.slice_cols);
+  const uint32_t ep = R.epoch[slice] + 1u;
+  const unsigned long long deadline = globaltimer() + 20ull * 1000000000ull;  // 20 s
+  const int64_t copy_off = (int64_t)(ep & 1u) * A.copy_words;
+  const bool cyc = A.cyclic != 0;
+  unsigned long long* const mine = R.mbox + copy_off;
+  unsigned long long* tr = A.trace ? A.trace + (size_t)blockIdx.x * 8 : nullptr;
+  auto stamp = [&](int k) {
+    if (tr && threadIdx.x == 0) tr[k] = globaltimer();
+  };
+  stamp(0);
+  bool ok = true;
+  const int64_t n = A.lay.n, inner = A.lay.inner;
+  // ---- (a2)+(a3) as ONE round: c_i = b~_i - u y_i[first] and y_i[last] go to
+  //      every peer; every rank forms all b^_r = c_r - l y_{r-1}[last] (Eq. bi_hat) and
+  //      evaluates x~_i, x~_{i+1} with two plan-time rows of A^{-1} (no x~ round) ----
+#pragma unroll 1
+  for (int64_t j = c0 + threadIdx.x; j < c1; j += kP2PThreads) {
+    const double cv = R.bt[j] - A.u * R.yf[j], yl = R.yl[j];
+    for (int r = 0; r < p; ++r) {
+      if (r == rank) continue;
+      unsigned long long* dst = R.peer_mbox[r] + copy_off;
+      ll_send(dst + (int64_t)rank * 2 * m + 2 * j, cv, ep);
+      ll_send(dst + (int64_t)(p + rank) * 2 * m + 2 * j, yl, ep);
+    }
+  }
+  stamp(1);
+#pragma unroll 1
+  for (int64_t j = c0 + threadIdx.x; j < c1 && ok; j += kP2PThreads) {  // 2 x 8 loads in flight
+    double c[kMaxAG], y[kMaxAG];
+    uint32_t mask = 0;
+#pragma unroll
+    for (int r = 0; r < kMaxAG; ++r) {
+      c[r] = y[r] = 0.0;
+      if (r < p && r != rank) mask |= 1u << r;
+    }
+    ok = ll_recv_batch(mine + 2 * j, 2 * m, mask, ep, deadline, c) &&
+         ll_recv_batch(mine + (int64_t)p * 2 * m + 2 * j, 2 * m, mask, ep, deadline, y);
+    if (!ok) continue;
+#pragma unroll
+    for (int r = 0; r < kMaxAG; ++r)
+      if (r == rank) { c[r] = R.bt[j] - A.u * R.yf[j]; y[r] = R.yl[j]; }
+    double ywrap = 0.0;  // y_{p-1}[last], the left neighbour of rank 0 (cyclic)
+#pragma unroll
+    for (int r = 0; r < kMaxAG; ++r)
+      if (r == p - 1 && cyc) ywrap = y[r];
+    double xt = 0.0, xn = 0.0;
+#pragma unroll
+    for (int r = 0; r < kMaxAG; ++r) {
+      if (r >= p) continue;
+      const double bh_r = c[r] - A.l * (r > 0 ? y[r > 0 ? r - 1 : 0] : ywrap);  // Eq. bi_hat
+      xt += R.ag0[r] * bh_r;
+      xn += R.ag1[r] * bh_r;
+    }
+    const int64_t o = j / inner, cc = j - o * inner;
+    R.x[o * n * inner + cc] = xt;
+    R.xnext[j] = xn;
+  }
+  if (!ok) atomicExch(A.err, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) R.epoch[slice] = ep;
+  for (int k = 2; k < 6; ++k) stamp(k);
+}
+
 cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(A.nslices * nranks_launch), 1, 1);
@@ -195,26 +294,34 @@ cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = nranks_launch > 1 ? 1 : 0;  // one rank per launch: the grid fits anyway
-  return cudaLaunchKernelEx(&cfg, k_reduced_p2p, A);
+  return A.allgather ? cudaLaunchKernelEx(&cfg, k_reduced_allgather, A)
+                     : cudaLaunchKernelEx(&cfg, k_reduced_p2p, A);
 }
 
-int p2p_slices(int64_t m, int nranks_launch, int num_sms) {
+int p2p_slices(int64_t m, int nranks_launch, int num_sms, bool allgather) {
   // one wave: <= resident CTAs in total, <= kMaxCpt columns per thread
   int per_sm = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_reduced_p2p, kP2PThreads, 0) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm, allgather ? (const void*)k_reduced_allgather : (const void*)k_reduced_p2p,
+          kP2PThreads, 0) !=
           cudaSuccess || per_sm < 1) {
     cudaGetLastError();
     per_sm = 1;
   }
   const int64_t cap = std::max<int64_t>(1, (int64_t)per_sm * num_sms / nranks_launch);
   int64_t ns = std::min<int64_t>(cap, (m + kP2PThreads - 1) / kP2PThreads);
-  while ((m + ns - 1) / ns > (int64_t)kP2PThreads * kMaxCpt) ++ns;
+  if (!allgather)  // the schedule kernel keeps <= kMaxCpt columns per thread in registers
+    while ((m + ns - 1) / ns > (int64_t)kP2PThreads * kMaxCpt) ++ns;
   return (int)std::max<int64_t>(1, ns);
 }
 
-// [2 epoch copies][2 + 2q slots][2m LL words]  +  (derivative) [2 copies][4 halo rows][2m]
-size_t p2p_mailbox_words(int64_t m, int q, bool halo) {
-  return (size_t)2 * (2 + 2 * q) * 2 * (size_t)m + (halo ? (size_t)2 * 4 * 2 * (size_t)m : 0);
+// one epoch copy: [2 + 2q slots][2m LL words] (schedule) or [2 planes][p sources][2m] (all-gather)
+int64_t p2p_copy_words(int64_t m, int q, int p, bool allgather) {
+  return (int64_t)std::max(2 + 2 * q, allgather ? 2 * p : 0) * 2 * m;
+}
+// [2 epoch copies][copy]  +  (derivative) [2 copies][4 halo rows][2m]
+size_t p2p_mailbox_words(int64_t copy_words, int64_t m, bool halo) {
+  return (size_t)2 * (size_t)copy_words + (halo ? (size_t)2 * 4 * 2 * (size_t)m : 0);
 }
 
 // (a0) halo of the compact-derivative stencil for nparts > 1: rows 0, 1 of this slab
@@ -228,7 +335,7 @@ __global__ void __launch_bounds__(kP2PThreads) k_halo_p2p(const P2PArgs A) {
   const int64_t m = A.m, n = A.lay.n, inner = A.lay.inner;
   const uint32_t ep = R.epoch[slice] + 1u;
   const unsigned long long deadline = globaltimer() + 20ull * 1000000000ull;
-  const int64_t hoff = (int64_t)2 * (2 + 2 * A.q) * 2 * m + (int64_t)(ep & 1u) * 8 * m;
+  const int64_t hoff = 2 * A.copy_words + (int64_t)(ep & 1u) * 8 * m;
   const int left = (rank + p - 1) % p, right = (rank + 1) % p;
   const int64_t c0 = (int64_t)slice * A.slice_cols;
   const int64_t c1 = std::min<int64_t>(m, c0 + A.slice_cols);

@@ -23,6 +23,7 @@ CTRI_FLAG_GENERIC_LOCAL = 1 << 1
 CTRI_FLAG_TIMING = 1 << 2
 CTRI_FLAG_DERIV = 1 << 3
 CTRI_FLAG_NCCL_ROUNDS = 1 << 4
+CTRI_FLAG_ALLGATHER = 1 << 5
 CTRI_MAX_STAGES = 16
 ABI_VERSION = 2
 
@@ -35,7 +36,8 @@ ABI_SYMBOLS = ("ctri_status_string", "ctri_last_error", "ctri_abi_version", "ctr
                "ctri_plan_create", "ctri_plan_create_loopback", "ctri_solve", "ctri_solve_loopback",
                "ctri_solve_host", "ctri_deriv", "ctri_deriv_loopback", "ctri_get_stats",
                "ctri_plan_destroy", "ctri_factor_query", "ctri_pcr_coefficients",
-               "ctri_reduced_schedule", "ctri_compact_apply", "ctri_compact_apply_loopback")
+               "ctri_reduced_schedule", "ctri_compact_apply", "ctri_compact_apply_loopback",
+               "ctri_reduced_inverse")
 
 
 class CtriError(RuntimeError):
@@ -115,6 +117,7 @@ def load(build_if_missing: bool = False):
                                      ctypes.POINTER(P), ctypes.c_double, ctypes.c_double,
                                      ctypes.c_double, P]),
         "ctri_compact_apply": (st, [P, dp, P, P, P]),
+        "ctri_reduced_inverse": (st, [ctypes.c_int, ctypes.c_int, dp, dp, dp, dp]),
         "ctri_compact_apply_loopback": (st, [ctypes.POINTER(P), ctypes.c_int, dp, ctypes.POINTER(P),
                                              ctypes.POINTER(P), P]),
         "ctri_get_stats": (st, [P, ctypes.POINTER(ctri_stats)]),
@@ -340,6 +343,18 @@ def ctri_reduced_schedule(L, D, U, cyclic=True, max_steps=32):
 
 
 # ---------------------------------------------------------------- conveniences
+def ctri_reduced_inverse(L, D, U, cyclic=True):
+    """Host-only: dense A^{-1} of the reduced system (all-gather table), P x P."""
+    L, D, U = (np.ascontiguousarray(v, dtype=np.float64) for v in (L, D, U))
+    P_ = len(D)
+    out = np.zeros((P_, P_))
+    dp = ctypes.POINTER(ctypes.c_double)
+    _check(load().ctri_reduced_inverse(P_, int(bool(cyclic)), L.ctypes.data_as(dp), D.ctypes.data_as(dp),
+                                       U.ctypes.data_as(dp), out.ctypes.data_as(dp)),
+           "ctri_reduced_inverse")
+    return out
+
+
 def local_shape(global_dims, solve_dim, nparts):
     s = list(global_dims)
     s[solve_dim] //= nparts

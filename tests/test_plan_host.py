@@ -252,3 +252,22 @@ def test_reduced_schedule_worked_example_11():
     b = np.ones(P)
     A = dense_band([1 / 3] * P, [1.0] * P, [1 / 3] * P, True)
     assert np.allclose(run_schedule(kinds, w, src, c, b), np.linalg.solve(A, b), rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 5, 7, 8])
+@pytest.mark.parametrize("cyclic", [True, False])
+def test_reduced_inverse_vs_dense(P, cyclic):
+    """All-gather table: ctri_reduced_inverse is the dense inverse of A^."""
+    rng = np.random.default_rng(2000 + P)
+    L = rng.uniform(-0.4, 0.4, P)
+    U = rng.uniform(-0.4, 0.4, P)
+    D = rng.uniform(1.0, 1.3, P)
+    inv = pk.ctri_reduced_inverse(L, D, U, cyclic=cyclic)
+    A = dense_band(L, D, U, cyclic)
+    assert np.max(np.abs(inv @ A - np.eye(P))) < 1e-14
+    assert np.max(np.abs(inv - np.linalg.inv(A))) < 1e-14
+
+
+def test_reduced_inverse_singular():
+    with pytest.raises(pk.CtriError, match="SINGULAR"):
+        pk.ctri_reduced_inverse([0.5, 0.5], [1.0, 1.0], [0.5, 0.5], cyclic=True)  # [[1, 1], [1, 1]]
