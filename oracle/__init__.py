@@ -29,7 +29,7 @@ def build(force: bool = False) -> str:
     """Compile the oracle shared library with gcc (-O2, OpenMP, no fast-math)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         cmd = ["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11",
-               "-fno-fast-math", "-ffp-contract=off", _SRC, "-o", _LIB]
+               "-fno-fast-math", "-ffp-contract=off", _SRC, "-o", _LIB, "-lm"]
         subprocess.run(cmd, check=True)
     return _LIB
 
@@ -46,10 +46,11 @@ def _load():
         lib.oracle_rhs_stencil.argtypes = [i64p, ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                            ctypes.c_double, dp, dp]
         lib.oracle_rhs_stencil5.argtypes = [i64p, ctypes.c_int, dp, dp, dp]
+        lib.oracle_penta_solve.argtypes = [i64p, ctypes.c_int, dp, ctypes.c_int, dp, dp]
         lib.oracle_deriv.argtypes = [i64p, ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                      ctypes.c_double, ctypes.c_double, dp, dp]
         for fn in (lib.oracle_cyclic_solve, lib.oracle_acyclic_solve, lib.oracle_rhs_stencil,
-                   lib.oracle_rhs_stencil5,
+                   lib.oracle_rhs_stencil5, lib.oracle_penta_solve,
                    lib.oracle_deriv):
             fn.restype = ctypes.c_int
         lib.oracle_num_threads.restype = ctypes.c_int
@@ -110,6 +111,23 @@ def rhs_stencil(f: np.ndarray, solve_dim: int, a: float, bc: float, h: float) ->
     if rc:
         raise ValueError("oracle_rhs_stencil: invalid argument")
     return out.reshape(shape)
+
+
+def penta_solve(b: np.ndarray, solve_dim: int = 0, bands=(0.05, 0.3, 1.0, 0.3, 0.05),
+                cyclic: bool = True) -> np.ndarray:
+    """x = A^{-1} b, A pentadiagonal with bands (e, l, d, u, f) = A[i, i-2..i+2] (r = 2)."""
+    shape = b.shape
+    b3 = _as3d(b)
+    sd = solve_dim if b.ndim == 3 else 0
+    x = np.empty_like(b3)
+    bnd = np.ascontiguousarray(bands, dtype=np.float64)
+    if bnd.shape != (5,):
+        raise ValueError("bands must be (e, l, d, u, f)")
+    rc = _load().oracle_penta_solve(_dims(b3.shape), sd, bnd.ctypes.data, int(bool(cyclic)),
+                                    b3.ctypes.data, x.ctypes.data)
+    if rc:
+        raise ValueError("oracle_penta_solve: invalid argument")
+    return x.reshape(shape)
 
 
 def rhs_stencil5(f: np.ndarray, solve_dim: int, coef) -> np.ndarray:

@@ -38,6 +38,17 @@
  *                         (half-node values g_i = f_{i+1/2} stored at index i)
  *                         as well as the collocated derivative above.
  *
+ *   oracle_penta_solve    x = A^{-1} b with A the PENTADIAGONAL matrix of constant
+ *                         bands (e, l, d, u, f) = (A[i,i-2], A[i,i-1], A[i,i],
+ *                         A[i,i+1], A[i,i+2]), cyclic (wrapped corners) or not.
+ *                         PAPER.md P:212 (bandwidth w = 2r+1, r = 2: "penta-diagonal
+ *                         system, D~_i is 2x2"), SURVEY 8(f) N3.  Computed by plain
+ *                         banded Gaussian elimination without pivoting (the
+ *                         matrices are diagonally dominant) and, for the cyclic
+ *                         corners, the Sherman-Morrison-Woodbury identity with a
+ *                         rank-4 correction (the textbook generalisation of the
+ *                         cyclic Thomas algorithm above).  No partitioning, no PCR.
+ *
  *   oracle_deriv          stencil followed by the cyclic solve with bands
  *                         (alpha, 1, alpha): the compact first derivative f'.
  *
@@ -58,6 +69,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <math.h>
 #ifdef _OPENMP
 #include <omp.h>
 #endif
@@ -234,6 +246,132 @@ int oracle_rhs_stencil(const int64_t dims[3], int sd, double a, double bc,
     }
   }
   return 0;
+}
+
+/* Banded Gaussian elimination without pivoting, one column of length N >= 1 (element
+ * stride st): rows i hold A[i,i-2..i+2] = (e, l, d, u, f) truncated at the ends.  The
+ * work arrays hold the current band entries of every row while columns are eliminated. */
+static void penta_column(int64_t N, const double bd[5], const double* rhs, double* out,
+                         int64_t st, double* w /* scratch: 6N */) {
+  double *s2 = w, *s1 = w + N, *dg = w + 2 * N, *p1 = w + 3 * N, *p2 = w + 4 * N, *r = w + 5 * N;
+  for (int64_t i = 0; i < N; ++i) {
+    s2[i] = bd[0];
+    s1[i] = bd[1];
+    dg[i] = bd[2];
+    p1[i] = bd[3];
+    p2[i] = bd[4];
+    r[i] = rhs[i * st];
+  }
+  for (int64_t k = 0; k + 1 < N; ++k) {  /* eliminate column k from rows k+1, k+2 */
+    const double m1 = s1[k + 1] / dg[k];
+    dg[k + 1] -= m1 * p1[k];
+    if (k + 2 < N) p1[k + 1] -= m1 * p2[k];
+    r[k + 1] -= m1 * r[k];
+    if (k + 2 < N) {
+      const double m2 = s2[k + 2] / dg[k];
+      s1[k + 2] -= m2 * p1[k];
+      dg[k + 2] -= m2 * p2[k];
+      r[k + 2] -= m2 * r[k];
+    }
+  }
+  for (int64_t i = N - 1; i >= 0; --i) {
+    double v = r[i];
+    if (i + 1 < N) v -= p1[i] * out[(i + 1) * st];
+    if (i + 2 < N) v -= p2[i] * out[(i + 2) * st];
+    out[i * st] = v / dg[i];
+  }
+}
+
+/* Gauss-Jordan inverse of a 4x4 matrix with partial pivoting (in place). */
+static int inverse4(double a[16]) {
+  double e[16] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1};
+  for (int k = 0; k < 4; ++k) {
+    int pv = k;
+    for (int i = k + 1; i < 4; ++i)
+      if (fabs(a[i * 4 + k]) > fabs(a[pv * 4 + k])) pv = i;
+    if (a[pv * 4 + k] == 0.0) return 1;
+    for (int j = 0; j < 4; ++j) {
+      double t = a[k * 4 + j]; a[k * 4 + j] = a[pv * 4 + j]; a[pv * 4 + j] = t;
+      t = e[k * 4 + j]; e[k * 4 + j] = e[pv * 4 + j]; e[pv * 4 + j] = t;
+    }
+    const double rp = 1.0 / a[k * 4 + k];
+    for (int j = 0; j < 4; ++j) { a[k * 4 + j] *= rp; e[k * 4 + j] *= rp; }
+    for (int i = 0; i < 4; ++i) {
+      if (i == k) continue;
+      const double m = a[i * 4 + k];
+      for (int j = 0; j < 4; ++j) { a[i * 4 + j] -= m * a[k * 4 + j]; e[i * 4 + j] -= m * e[k * 4 + j]; }
+    }
+  }
+  memcpy(a, e, sizeof(e));
+  return 0;
+}
+
+/* Pentadiagonal solve of every column.  Acyclic: penta_column.  Cyclic (N >= 5): the six
+ * corner entries A[0,N-2] = e, A[0,N-1] = l, A[1,N-1] = e, A[N-2,0] = f, A[N-1,0] = u,
+ * A[N-1,1] = f live in rows J = {0, 1, N-2, N-1}, so A = B + E_J V^T with B the banded
+ * part, E_J the columns e_j (j in J) and V^T the corner rows.  Woodbury:
+ *   y = B^{-1} b,  Z = B^{-1} E_J (once),  M = I + V^T Z (4x4, once),
+ *   x = y - Z M^{-1} V^T y. */
+int oracle_penta_solve(const int64_t dims[3], int sd, const double bands[5], int cyclic,
+                       const double* b, double* x) {
+  if (!dims || !bands || !b || !x || sd < 0 || sd > 2) return 1;
+  int64_t outer, N, inner;
+  layout(dims, sd, &outer, &N, &inner);
+  if (N < (cyclic ? 5 : 1) || outer < 1 || inner < 1) return 1;
+  const double e = bands[0], l = bands[1], u = bands[3], f = bands[4];
+  double* Z = NULL;
+  double M[16];
+  if (cyclic) {
+    Z = (double*)malloc(sizeof(double) * 4 * N);
+    double* w = (double*)malloc(sizeof(double) * 7 * N);
+    if (!Z || !w) { free(Z); free(w); return 1; }
+    const int64_t J[4] = {0, 1, N - 2, N - 1};
+    for (int c = 0; c < 4; ++c) {
+      double* unit = w + 6 * N;
+      for (int64_t i = 0; i < N; ++i) unit[i] = 0.0;
+      unit[J[c]] = 1.0;
+      penta_column(N, bands, unit, Z + c * N, 1, w);
+    }
+    free(w);
+    /* V^T z for a column z: the corner rows applied to z */
+    for (int c = 0; c < 4; ++c) {
+      const double* z = Z + c * N;
+      const double vz[4] = {e * z[N - 2] + l * z[N - 1], e * z[N - 1], f * z[0], u * z[0] + f * z[1]};
+      for (int rr = 0; rr < 4; ++rr) M[rr * 4 + c] = (rr == c ? 1.0 : 0.0) + vz[rr];
+    }
+    if (inverse4(M)) { free(Z); return 1; }
+  }
+  const int64_t ncols = outer * inner;
+  int bad = 0;
+#pragma omp parallel
+  {
+    double* w = (double*)malloc(sizeof(double) * 6 * N);
+    if (!w) {
+#pragma omp atomic write
+      bad = 1;
+    } else {
+#pragma omp for schedule(static)
+      for (int64_t t = 0; t < ncols; ++t) {
+        const int64_t o = t / inner, c = t % inner;
+        const double* bc = b + o * N * inner + c;
+        double* xc = x + o * N * inner + c;
+        penta_column(N, bands, bc, xc, inner, w);
+        if (cyclic) {
+          const double vy[4] = {e * xc[(N - 2) * inner] + l * xc[(N - 1) * inner],
+                                e * xc[(N - 1) * inner], f * xc[0], u * xc[0] + f * xc[inner]};
+          double g[4];
+          for (int rr = 0; rr < 4; ++rr)
+            g[rr] = M[rr * 4 + 0] * vy[0] + M[rr * 4 + 1] * vy[1] + M[rr * 4 + 2] * vy[2] +
+                    M[rr * 4 + 3] * vy[3];
+          for (int64_t i = 0; i < N; ++i)
+            xc[i * inner] -= Z[i] * g[0] + Z[N + i] * g[1] + Z[2 * N + i] * g[2] + Z[3 * N + i] * g[3];
+        }
+      }
+      free(w);
+    }
+  }
+  free(Z);
+  return bad;
 }
 
 /* General five-point periodic stencil (PAPER.md P:202-206 schemes): plain definition. */

@@ -299,3 +299,67 @@ def test_staggered_sixth_order(which):
         errs.append(np.max(np.abs(out - exact)))
     orders = [math.log2(errs[i] / errs[i + 1]) for i in range(2)]
     assert all(5.5 <= o <= 7.0 for o in orders), (which, orders, errs)
+
+
+# ---- pentadiagonal (r = 2) oracle: PAPER.md P:212 (w = 5), SURVEY 8(f) N3 ----
+PENTA_BANDS = [(0.05, 0.3, 1.0, 0.3, 0.05),          # symmetric, diagonally dominant
+               (-0.07, 0.21, 1.3, -0.33, 0.11),      # non-symmetric
+               (1 / 20, 1 / 2, 1.0, 1 / 2, 1 / 20)]  # Lele's tenth-order LHS (beta, alpha)
+
+
+def _dense_penta(N, bands, cyclic):
+    e, l, d, u, f = bands
+    A = np.zeros((N, N))
+    for i in range(N):
+        for off, v in ((-2, e), (-1, l), (0, d), (1, u), (2, f)):
+            j = i + off
+            if 0 <= j < N:
+                A[i, j] += v
+            elif cyclic:
+                A[i, j % N] += v
+    return A
+
+
+@pytest.mark.parametrize("bands", PENTA_BANDS)
+@pytest.mark.parametrize("cyclic", [True, False])
+@pytest.mark.parametrize("N", [5, 6, 7, 8, 11, 32, 64])
+def test_penta_oracle_vs_dense(bands, cyclic, N):
+    """Dense LAPACK solve of the explicitly assembled (cyclic) pentadiagonal matrix."""
+    b = workloads.uniform((N, 3, 2), 50 + N)
+    x = oracle.penta_solve(b, 0, bands, cyclic)
+    A = _dense_penta(N, bands, cyclic)
+    expect = np.einsum("ij,jab->iab", np.linalg.inv(A), b)
+    assert np.max(np.abs(x - expect)) < 1e-14 * max(1.0, np.max(np.abs(expect)))
+
+
+@pytest.mark.parametrize("bands", PENTA_BANDS)
+@pytest.mark.parametrize("N,k", [(64, 0), (64, 5), (64, 32), (1024, 77), (1000, 333)])
+def test_penta_oracle_fourier_eigenvector(bands, N, k):
+    """b_j = cos(theta j) => x_j = Re(e^{i theta j} / lambda(theta)),
+    lambda = d + l e^{-i theta} + u e^{i theta} + e e^{-2 i theta} + f e^{2 i theta}."""
+    e, l, d, u, f = bands
+    th = 2 * math.pi * k / N
+    lam = d + l * np.exp(-1j * th) + u * np.exp(1j * th) + e * np.exp(-2j * th) + f * np.exp(2j * th)
+    j = np.arange(N, dtype=np.int64)
+    ph = 2 * math.pi * ((k * j) % N) / N
+    b = np.cos(ph).reshape(N, 1, 1)
+    x = oracle.penta_solve(np.broadcast_to(b, (N, 2, 3)).copy(), 0, bands, True)
+    expect = np.real(np.exp(1j * ph) / lam).reshape(N, 1, 1)
+    assert np.max(np.abs(x - expect)) < 1e-14
+
+
+def test_penta_oracle_reduces_to_tridiagonal():
+    """e = f = 0: the pentadiagonal oracle equals the (pinned) tridiagonal one, both layouts."""
+    b = workloads.uniform((40, 5, 6), 61)
+    for sd in (0, 1, 2):
+        for cyc in (True, False):
+            x5 = oracle.penta_solve(b, sd, (0.0, 0.2, 1.1, 0.4, 0.0), cyc)
+            x3 = (oracle.cyclic_solve if cyc else oracle.acyclic_solve)(b, sd, (0.2, 1.1, 0.4))
+            assert np.max(np.abs(x5 - x3)) < 1e-15
+
+
+def test_penta_oracle_layout_permutation():
+    b0 = workloads.uniform((48, 6, 4), 62)
+    x0 = oracle.penta_solve(b0, 0, PENTA_BANDS[1], True)
+    x2 = oracle.penta_solve(np.ascontiguousarray(np.transpose(b0, (1, 2, 0))), 2, PENTA_BANDS[1], True)
+    assert np.max(np.abs(np.transpose(x2, (2, 0, 1)) - x0)) < 1e-15
