@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--reduced", default="pcr", choices=["pcr", "allgather", "nccl"],
                     help="nparts > 1 reduced system: fused P2P pairwise schedule (default), the "
                          "P2P all-gather with A^-1 rows (N4), or host-issued NCCL rounds")
+    ap.add_argument("--penta", action="store_true",
+                    help="pentadiagonal system (r = 2, SURVEY N3) on the config's grid: Lele's "
+                         "tenth-order compact LHS (1/20, 1/2, 1, 1/2, 1/20)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -277,6 +280,11 @@ def main():
         else:
             bands, coef = ctri.STAGGERED_INTERP_BANDS, ctri.staggered_interp_coef()
         name = f"{name.replace('compact 6th-order first derivative', args.scheme.replace('_', ' '))} (P:202-206)"
+    if args.penta:
+        if deriv:
+            raise SystemExit("--penta applies to the solve configs (cfg1-cfg4)")
+        bands = (1 / 20, 1 / 2, 1.0, 1 / 2, 1 / 20)
+        name = f"pentadiagonal (Lele 10th-order LHS, r = 2): {name}"
     if world > 1:
         plan = pdist.plan_from_process_group(dims, sd, bands, flags=flags)
     else:
@@ -375,7 +383,9 @@ def main():
                 "kernel": ("k_tile<%d>%s (cluster %d)" % (st["rows_per_thread"],
                                                           " contiguous-axis" if st["local_kernel"] == 2 else "",
                                                           st["cluster_size"])
-                           if st["local_kernel"] in (1, 2) else "k_local_generic"),
+                           if st["local_kernel"] in (1, 2) else
+                           "k_penta_local (column-serial, 32 B/pt moved)" if st["local_kernel"] == 3
+                           else "k_local_generic"),
                 "algorithmic_bytes_per_launch": bytes_local, "launch_us": t_local,
                 "peak_source": peak_src}
         cpu = None if args.no_cpu_baseline else cpu_oracle_sample(args.config)

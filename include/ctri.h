@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define CTRI_ABI_VERSION 2
+#define CTRI_ABI_VERSION 3
 
 typedef struct ctri_plan_s* ctri_plan;
 typedef struct CUstream_st* ctri_stream; /* == cudaStream_t */
@@ -104,6 +104,7 @@ typedef struct ctri_stats {
   int32_t grid_ctas;            /* CTAs of the local-solve launch */
   int32_t detach_stages;        /* nparts > 1 cyclic, not a power of two: detach stages */
   int32_t detached_rows;        /* rows detached and reattached: nparts - 2^floor(log2 nparts) */
+  int32_t band_halfwidth;       /* r: 1 tridiagonal plan, 2 pentadiagonal plan */
 } ctri_stats;
 
 /* Human-readable status name; never NULL. */
@@ -143,6 +144,27 @@ ctri_status ctri_plan_create(ctri_plan* out, const int64_t global_dims[3], int s
 ctri_status ctri_plan_create_loopback(ctri_plan* plans, int nparts, const int64_t global_dims[3],
                                       int solve_dim, const double bands[3], int cyclic,
                                       uint32_t flags, ctri_stream stream);
+
+/* PENTADIAGONAL plan (r = 2; "for a penta-diagonal system (w = 5), D~_i is
+ * 2x2").  bands = {e, l, d, u, f} = A[i,i-2], A[i,i-1], A[i,i], A[i,i+1],
+ * A[i,i+2] (host array, copied); cyclic wraps the four corner couplings.  Each of the nparts
+ * slabs keeps two interface rows (local rows 0, 1) and n - 2 >= 4 interior rows; the 2x2-block
+ * reduced system is solved with ONE P2P all-gather round and plan-time rows of its inverse
+ * (nparts <= 8).  The plan is used with ctri_solve / ctri_solve_loopback / ctri_solve_host /
+ * ctri_get_stats / ctri_plan_destroy like a tridiagonal one.  Errors: INVALID_ARG (as
+ * ctri_plan_create), PARTITION_TOO_SMALL (n < 6 or N % nparts), UNSUPPORTED (nparts > 8,
+ * CTRI_FLAG_NCCL_ROUNDS, CTRI_FLAG_DERIV or CTRI_FLAG_GENERIC_LOCAL), SINGULAR (pivot guard
+ * 1e-13 * max|band| in the interior LU or the reduced inverse). */
+ctri_status ctri_plan_create_penta(ctri_plan* out, const int64_t global_dims[3], int solve_dim,
+                                   int nparts, int rank, const double bands[5], int cyclic,
+                                   const void* nccl_unique_id, uint32_t flags, ctri_stream stream);
+
+/* TEST-ONLY: a pentadiagonal loopback group on the current device (see
+ * ctri_plan_create_loopback). */
+ctri_status ctri_plan_create_penta_loopback(ctri_plan* plans, int nparts,
+                                            const int64_t global_dims[3], int solve_dim,
+                                            const double bands[5], int cyclic, uint32_t flags,
+                                            ctri_stream stream);
 
 /* Solve on device buffers: x = A^{-1} b for the local slab.  x == b (in place) is
  * allowed; partial overlap is not.  Asynchronous, stream ordered, collective.
@@ -234,6 +256,13 @@ ctri_status ctri_pcr_coefficients(int P, int cyclic, const double* L, const doub
 ctri_status ctri_reduced_schedule(int P, int cyclic, const double* L, const double* D,
                                   const double* U, int max_steps, int* nsteps, int* kinds,
                                   double* w, int* src, double* c, int* counts);
+
+/* Host-only pentadiagonal partition tables for a slab of n rows (n >= 6, interior N = n - 2):
+ * SR[4*N] = columns S0 | S1 | R0 | R1 (S = D^{-1} L, R = D^{-1} U, Eqs. Si/Ri with r = 2),
+ * hat[16] = 2x2 row-major blocks L^ | D^ | U^ | D^ of an acyclic first partition, window = rows
+ * per end of the back-substitution window (2^-64 reading).  SINGULAR on the pivot guard. */
+ctri_status ctri_penta_factor_query(int64_t n, const double bands[5], double* SR, double* hat,
+                                   int* window);
 
 /* Dense inverse of the P x P reduced matrix A^ (bands L, D, U per row; cyclic corners;
  * couplings that coincide for P <= 2 add up) into inv[P*P], row-major: the plan-time table of

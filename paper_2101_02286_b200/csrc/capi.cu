@@ -69,7 +69,8 @@ void free_plan(Plan* P) {
   double* bufs[] = {P->d_cp,    P->d_inv_den, P->d_S,      P->d_R,       P->yf,      P->yl,
                     P->bt,      P->yl_prev,   P->bh,       P->recv_m,    P->recv_p,  P->xt,
                     P->xt_next, P->halo_lo,   P->halo_hi,  P->send_lo,   P->send_hi, P->tile.d_pcr,
-                    P->d_stage_b, P->d_stage_x};
+                    P->d_stage_b, P->d_stage_x, P->d_plu,    P->d_pSR,     P->d_ainv,  P->d_planes4,
+                    P->d_xnext2};
   for (double* b : bufs)
     if (b) cudaFree(b);
   for (cudaEvent_t e : P->ev) cudaEventDestroy(e);
@@ -197,7 +198,7 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   if (p > 1 && p <= kMaxP2PRanks && !(flags & CTRI_FLAG_NCCL_ROUNDS)) {
     // fused device-initiated reduced phase: double-buffered mailbox + epoch flags
     const int q = (int)P->sched.steps.size();
-    P->p2p_nslices = p2p_slices(m, P->loopback ? p : 1, P->num_sms, P->allgather);
+    P->p2p_nslices = p2p_slices(m, P->loopback ? p : 1, P->num_sms, P->allgather ? 1 : 0);
     P->mbox_bytes = sizeof(unsigned long long) *
                     p2p_mailbox_words(p2p_copy_words(m, q, p, P->allgather), m, (flags & CTRI_FLAG_DERIV) != 0);
     CUDA_TRY(cudaMalloc(&P->mbox_alloc, P->mbox_bytes));
@@ -224,6 +225,66 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   if (p > 1) launches += P->p2p ? 2 /*reduced + window*/ : 1 /*bhat*/ + P->gpcr.stages + 1 /*backsub*/;
   if (p == 1 && P->vp > 1) launches += 2;  // local reduced system; window back-substitution
   P->launches_per_solve = launches;
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return CTRI_OK;
+}
+
+// Pentadiagonal plan (r = 2, penta.cu): validation, tables, P2P mailbox.
+ctri_status penta_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, const double bands[5],
+                       int cyclic, uint32_t flags, cudaStream_t s) {
+  if (!gd || !bands) return fail(CTRI_ERR_INVALID_ARG, "NULL dims or bands");
+  if (sd < 0 || sd > 2) return fail(CTRI_ERR_INVALID_ARG, "solve_dim must be 0, 1 or 2");
+  for (int k = 0; k < 3; ++k)
+    if (gd[k] < 1) return fail(CTRI_ERR_INVALID_ARG, "global dims must be >= 1");
+  if (p < 1 || rank < 0 || rank >= p) return fail(CTRI_ERR_INVALID_ARG, "bad nparts/rank");
+  for (int k = 0; k < 5; ++k)
+    if (!std::isfinite(bands[k])) return fail(CTRI_ERR_INVALID_ARG, "bands must be finite");
+  if (gd[sd] % p != 0)
+    return fail(CTRI_ERR_PARTITION_TOO_SMALL, "N is not divisible by nparts (equal split, P:5)");
+  const int64_t n = gd[sd] / p;
+  if (n < 6) return fail(CTRI_ERR_PARTITION_TOO_SMALL, "pentadiagonal: n = N/nparts < 6 (N_i = n-2 >= 4)");
+  if (p > kMaxAG) return fail(CTRI_ERR_UNSUPPORTED, "pentadiagonal: nparts <= 8 (all-gather reduced solve)");
+  if (flags & (CTRI_FLAG_NCCL_ROUNDS | CTRI_FLAG_DERIV | CTRI_FLAG_GENERIC_LOCAL))
+    return fail(CTRI_ERR_UNSUPPORTED, "pentadiagonal plans: P2P all-gather path only, no derivative");
+  std::memcpy(P->gdims, gd, sizeof(P->gdims));
+  P->sd = sd;
+  P->p = p;
+  P->rank = rank;
+  P->cyclic = cyclic ? 1 : 0;
+  P->flags = flags;
+  P->r = 2;
+  std::memcpy(P->bands5, bands, sizeof(P->bands5));
+  P->bands = Bands{bands[1], bands[2], bands[3]};
+  P->lay.n = n;
+  P->lay.outer = 1;
+  P->lay.inner = 1;
+  for (int k = 0; k < sd; ++k) P->lay.outer *= gd[k];
+  for (int k = sd + 1; k < 3; ++k) P->lay.inner *= gd[k];
+  P->tlay = P->lay;
+  P->local_kernel = 3;
+  CUDA_TRY(cudaGetDevice(&P->device));
+  CUDA_TRY(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device));
+  std::string why;
+  ctri_status st = penta_plan_tables(P, s, &why);
+  if (st != CTRI_OK) return fail(st, "pentadiagonal tables: " + why);
+  const int64_t m = P->lay.m();
+  if (p > 1) {
+    P->p2p_nslices = p2p_slices(m, P->loopback ? p : 1, P->num_sms, 2);
+    P->mbox_bytes = sizeof(unsigned long long) *
+                    p2p_mailbox_words(p2p_copy_words(m, 0, p, true, 4), m, false);
+    CUDA_TRY(cudaMalloc(&P->mbox_alloc, P->mbox_bytes));
+    CUDA_TRY(cudaMemsetAsync(P->mbox_alloc, 0, P->mbox_bytes, s));
+    CUDA_TRY(cudaMalloc(&P->d_err, sizeof(int)));
+    CUDA_TRY(cudaMemsetAsync(P->d_err, 0, sizeof(int), s));
+    CUDA_TRY(cudaMalloc(&P->d_epoch, sizeof(unsigned int) * P->p2p_nslices));
+    CUDA_TRY(cudaMemsetAsync(P->d_epoch, 0, sizeof(unsigned int) * P->p2p_nslices, s));
+    P->p2p = true;
+  }
+  if (flags & CTRI_FLAG_TIMING) {
+    P->ev.resize(EV_COUNT);
+    for (auto& e : P->ev) CUDA_TRY(cudaEventCreate(&e));
+  }
+  P->launches_per_solve = 2 + (p > 1 ? 1 : 0);
   CUDA_TRY(cudaStreamSynchronize(s));
   return CTRI_OK;
 }
@@ -265,7 +326,7 @@ void p2p_args(const Plan& P0, P2PArgs* A) {
   A->p = P0.p;
   A->q = (int)P0.sched.steps.size();
   A->allgather = P0.allgather ? 1 : 0;
-  A->copy_words = p2p_copy_words(P0.lay.m(), A->q, P0.p, P0.allgather);
+  A->copy_words = p2p_copy_words(P0.lay.m(), A->q, P0.p, P0.allgather || P0.r == 2, P0.r == 2 ? 4 : 2);
   A->cyclic = P0.cyclic;
   A->nslices = P0.p2p_nslices;
   A->m = P0.lay.m();
@@ -286,7 +347,9 @@ void p2p_fill_rank(const Plan& P, double* x, P2PRank* R) {
   R->yf = P.yf;
   R->yl = P.yl;
   R->bt = P.bt;
-  R->xnext = P.xt_next;
+  R->xnext = P.r == 2 ? P.d_xnext2 : P.xt_next;
+  R->planes4 = P.d_planes4;
+  R->ainv = P.d_ainv;
   R->mbox = reinterpret_cast<unsigned long long*>(P.mbox_alloc);
   R->epoch = P.d_epoch;
   R->f = nullptr;
@@ -325,8 +388,8 @@ void p2p_fill_rank(const Plan& P, double* x, P2PRank* R) {
 
 // messages this rank sends per solve, and dependent exchange rounds, from the schedule
 void schedule_counts(const Plan& P, int* sends, int* rounds) {
-  if (P.allgather) {  // one round: 2 planes to each of the p - 1 peers
-    *sends = 2 * (P.p - 1);
+  if (P.allgather || P.r == 2) {  // one round: 2 (4 for r = 2) planes to each of the p - 1 peers
+    *sends = 2 * P.r * (P.p - 1);
     *rounds = 1;
     return;
   }
@@ -455,9 +518,16 @@ ctri_status stage_kernel(Plan& P, int k, cudaStream_t s) {
   return CTRI_OK;
 }
 
+ctri_status penta_solve_group(std::vector<Plan*>& G, const double* const* b, double* const* x,
+                              cudaStream_t s);
+
 // The whole solve for a set of co-scheduled plans: one plan (NCCL) or a loopback group.
 ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* const* x,
                         cudaStream_t s, const Stencil5* st = nullptr) {
+  if (G[0]->r == 2) {
+    if (st) return fail(CTRI_ERR_UNSUPPORTED, "pentadiagonal plans have no derivative path");
+    return penta_solve_group(G, b, x, s);
+  }
   const bool nccl = !G[0]->loopback;
   Plan& P0 = *G[0];
   for (size_t r = 0; r < G.size(); ++r) {
@@ -545,8 +615,38 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
 }
 
 // A compact scheme: df = A^{-1} (five-point periodic stencil of f); halos from the neighbours.
+// Pentadiagonal solve of a plan group (one plan, or a loopback group).
+ctri_status penta_solve_group(std::vector<Plan*>& G, const double* const* b, double* const* x,
+                              cudaStream_t s) {
+  Plan& P0 = *G[0];
+  for (size_t r = 0; r < G.size(); ++r)
+    if (!b[r] || !x[r]) return fail(CTRI_ERR_INVALID_ARG, "NULL b or x");
+  for (Plan* P : G) P->solves++;
+  record(P0, EV_START, s);
+  for (size_t r = 0; r < G.size(); ++r) {
+    cudaError_t e = launch_penta_local(*G[r], b[r], x[r], s);
+    if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("penta local: ") + cudaGetErrorString(e));
+  }
+  record(P0, EV_LOCAL, s);
+  if (P0.p > 1) {
+    P2PArgs A;
+    p2p_args(P0, &A);
+    for (size_t r = 0; r < G.size(); ++r) p2p_fill_rank(*G[r], x[r], &A.rk[r]);
+    cudaError_t e = launch_reduced_allgather_r2(A, (int)G.size(), s);
+    if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("penta reduced: ") + cudaGetErrorString(e));
+  }
+  for (size_t r = 0; r < G.size(); ++r) {
+    cudaError_t e = launch_penta_window(*G[r], x[r], s);
+    if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("penta window: ") + cudaGetErrorString(e));
+  }
+  record(P0, EV_BACK, s);
+  for (Plan* P : G) P->timed_valid = !P->ev.empty();
+  return CTRI_OK;
+}
+
 ctri_status deriv_group(std::vector<Plan*>& G, const double* const* f, double* const* df,
                         const double coef[5], cudaStream_t s) {
+  if (G[0]->r == 2) return fail(CTRI_ERR_UNSUPPORTED, "pentadiagonal plans have no derivative path");
   for (size_t r = 0; r < G.size(); ++r) {
     Plan& P = *G[r];
     if (!(P.flags & CTRI_FLAG_DERIV)) return fail(CTRI_ERR_INVALID_ARG, "plan lacks CTRI_FLAG_DERIV");
@@ -680,6 +780,58 @@ ctri_status ctri_plan_create_loopback(ctri_plan* plans, int nparts, const int64_
   return CTRI_OK;
 }
 
+ctri_status ctri_plan_create_penta(ctri_plan* out, const int64_t global_dims[3], int solve_dim,
+                                   int nparts, int rank, const double bands[5], int cyclic,
+                                   const void* nccl_unique_id, uint32_t flags, ctri_stream stream) {
+  if (!out) return fail(CTRI_ERR_INVALID_ARG, "NULL out");
+  *out = nullptr;
+  if (nparts > 1 && !nccl_unique_id)
+    return fail(CTRI_ERR_INVALID_ARG, "nparts > 1 needs an NCCL unique id");
+  std::unique_ptr<Plan, void (*)(Plan*)> P(new Plan(), free_plan);
+  ctri_status st = penta_init(P.get(), global_dims, solve_dim, nparts, rank, bands, cyclic, flags,
+                              (cudaStream_t)stream);
+  if (st != CTRI_OK) return st;
+  if (nparts > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    NCCL_TRY(ncclCommInitRank(&P->comm, nparts, id, rank));
+    ctri_status cs = p2p_connect_ipc(P.get(), (cudaStream_t)stream);
+    if (cs != CTRI_OK) return cs;
+  }
+  *out = reinterpret_cast<ctri_plan>(P.release());
+  return CTRI_OK;
+}
+
+ctri_status ctri_plan_create_penta_loopback(ctri_plan* plans, int nparts,
+                                            const int64_t global_dims[3], int solve_dim,
+                                            const double bands[5], int cyclic, uint32_t flags,
+                                            ctri_stream stream) {
+  if (!plans || nparts < 1) return fail(CTRI_ERR_INVALID_ARG, "bad plans/nparts");
+  std::vector<Plan*> made;
+  for (int r = 0; r < nparts; ++r) {
+    Plan* P = new Plan();
+    P->loopback = true;
+    ctri_status st = penta_init(P, global_dims, solve_dim, nparts, r, bands, cyclic, flags,
+                                (cudaStream_t)stream);
+    if (st != CTRI_OK) {
+      free_plan(P);
+      for (Plan* q : made) free_plan(q);
+      return st;
+    }
+    made.push_back(P);
+  }
+  for (int r = 0; r < nparts; ++r) {
+    made[r]->group = made;
+    if (made[r]->p2p) {
+      made[r]->peer_alloc.assign(nparts, nullptr);
+      made[r]->peer_ipc.assign(nparts, false);
+      for (int q = 0; q < nparts; ++q) made[r]->peer_alloc[q] = made[q]->mbox_alloc;
+    }
+    plans[r] = reinterpret_cast<ctri_plan>(made[r]);
+  }
+  return CTRI_OK;
+}
+
 ctri_status ctri_solve(ctri_plan plan, const double* b, double* x, ctri_stream stream) {
   if (!plan) return fail(CTRI_ERR_INVALID_ARG, "NULL plan");
   Plan* P = reinterpret_cast<Plan*>(plan);
@@ -788,14 +940,16 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
   out->tile_columns = P->local_kernel ? P->tile.C : 1;
   out->tile_variant = P->local_kernel ? P->tile.variant : -1;
   out->tile_stages = P->local_kernel ? P->tile.STAGES : 0;
-  out->reduced_path = (P->p > 1 && P->p2p) ? (P->allgather ? 2 : 1) : 0;
+  out->reduced_path = (P->p > 1 && P->p2p) ? ((P->allgather || P->r == 2) ? 2 : 1) : 0;
+  out->band_halfwidth = P->r;
   out->vparts = P->vp;
   out->grid_ctas = P->local_kernel ? P->tile.grid : (int32_t)((P->tlay.m() + 127) / 128);
   out->device_error = 0;
   if (P->d_err) CUDA_TRY(cudaMemcpy(&out->device_error, P->d_err, sizeof(int), cudaMemcpyDeviceToHost));
   out->chunk_heads = P->local_kernel ? P->tile.Q : 1;
-  const bool full = (P->flags & CTRI_FLAG_FULL_BACKSUB) || (2 * P->window >= P->tlay.n - 1);
-  out->window_rows = (int32_t)(full ? P->tlay.n - 1 : P->window);
+  const int64_t interior = P->tlay.n - P->r;
+  const bool full = (P->flags & CTRI_FLAG_FULL_BACKSUB) || (2 * P->window >= interior);
+  out->window_rows = (int32_t)(full ? interior : P->window);
   out->pcr_stages = P->sched.pcr_stages;
   out->detach_stages = P->sched.detach_stages;
   out->detached_rows = P->sched.detached_rows;
@@ -813,7 +967,7 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
   for (float* t : ts) *t = -1.f;
   for (int k = 0; k < CTRI_MAX_STAGES; ++k) out->t_stage_us[k] = -1.f;
   if (P->timed_valid || (!P->ev.empty() && P->solves > 0)) {
-    const bool two = P->p > 1 || P->vp > 1;
+    const bool two = P->p > 1 || P->vp > 1 || P->r == 2;
     CUDA_TRY(cudaEventSynchronize(P->ev[two ? EV_BACK : EV_LOCAL]));
     out->t_local_us = elapsed(*P, EV_START, EV_LOCAL);
     if (P->p > 1 && P->p2p) {
@@ -830,7 +984,7 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
       out->t_xexchange_us = elapsed(*P, prev, EV_XX);
       out->t_backsub_us = elapsed(*P, EV_XX, EV_BACK);
       out->t_total_us = elapsed(*P, EV_START, EV_BACK);
-    } else if (P->vp > 1) {
+    } else if (P->vp > 1 || P->r == 2) {
       out->t_backsub_us = elapsed(*P, EV_LOCAL, EV_BACK);  // local reduced + window back-sub
       out->t_total_us = elapsed(*P, EV_START, EV_BACK);
     } else {
@@ -919,6 +1073,23 @@ ctri_status ctri_reduced_schedule(int P, int cyclic, const double* L, const doub
   counts[0] = sc.pcr_stages;
   counts[1] = sc.detach_stages;
   counts[2] = sc.detached_rows;
+  return CTRI_OK;
+}
+
+ctri_status ctri_penta_factor_query(int64_t n, const double bands[5], double* SR, double* hat,
+                                   int* window) {
+  if (!bands || !SR || !hat || !window) return fail(CTRI_ERR_INVALID_ARG, "NULL argument");
+  Penta pt;
+  FactorError fe;
+  if (!penta_factor(n - 2, bands, &pt, &fe)) return fail((ctri_status)fe.code, fe.detail);
+  const int64_t N = n - 2;
+  const std::vector<double>* v[4] = {&pt.S0, &pt.S1, &pt.R0, &pt.R1};
+  for (int k = 0; k < 4; ++k) std::memcpy(SR + k * N, v[k]->data(), sizeof(double) * N);
+  std::memcpy(hat, pt.Lh, sizeof(pt.Lh));
+  std::memcpy(hat + 4, pt.Dh, sizeof(pt.Dh));
+  std::memcpy(hat + 8, pt.Uh, sizeof(pt.Uh));
+  std::memcpy(hat + 12, pt.DhFirst, sizeof(pt.DhFirst));
+  *window = (int)penta_window(pt);
   return CTRI_OK;
 }
 

@@ -144,6 +144,138 @@ bool pcr_factor(int P, bool cyclic, const std::vector<double>& L0, const std::ve
   return true;
 }
 
+// Gauss-Jordan inverse with partial pivoting of a dense n x n row-major matrix.
+static bool dense_inverse(int n, std::vector<double> a, double guard, std::vector<double>* inv,
+                          FactorError* err, const char* who) {
+  std::vector<double> e((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) e[(size_t)i * n + i] = 1.0;
+  for (int k = 0; k < n; ++k) {
+    int piv = k;
+    for (int i = k + 1; i < n; ++i)
+      if (std::fabs(a[(size_t)i * n + k]) > std::fabs(a[(size_t)piv * n + k])) piv = i;
+    if (!(std::fabs(a[(size_t)piv * n + k]) >= guard))
+      return fail(err, kSingular, std::string(who) + ": pivot guard");
+    if (piv != k)
+      for (int j = 0; j < n; ++j) {
+        std::swap(a[(size_t)k * n + j], a[(size_t)piv * n + j]);
+        std::swap(e[(size_t)k * n + j], e[(size_t)piv * n + j]);
+      }
+    const double r = 1.0 / a[(size_t)k * n + k];
+    for (int j = 0; j < n; ++j) {
+      a[(size_t)k * n + j] *= r;
+      e[(size_t)k * n + j] *= r;
+    }
+    for (int i = 0; i < n; ++i) {
+      if (i == k) continue;
+      const double f = a[(size_t)i * n + k];
+      if (f == 0.0) continue;
+      for (int j = 0; j < n; ++j) {
+        a[(size_t)i * n + j] -= f * a[(size_t)k * n + j];
+        e[(size_t)i * n + j] -= f * e[(size_t)k * n + j];
+      }
+    }
+  }
+  *inv = e;
+  return true;
+}
+
+bool penta_factor(int64_t N, const double bd[5], Penta* out, FactorError* err) {
+  if (N < 4) return fail(err, kInvalid, "penta_factor: interior needs >= 4 rows (n >= 6)");
+  const double e = bd[0], l = bd[1], d = bd[2], u = bd[3], f = bd[4];
+  double mx = 0;
+  for (int k = 0; k < 5; ++k) mx = std::max(mx, std::fabs(bd[k]));
+  const double guard = 1e-13 * mx;
+  Penta p;
+  p.N = N;
+  p.lam1.assign(N, 0.0);
+  p.lam2.assign(N, 0.0);
+  p.nu1.assign(N, 0.0);
+  p.inv_mu.assign(N, 0.0);
+  std::vector<double> mu(N);
+  for (int64_t k = 0; k < N; ++k) {
+    const double l2 = k >= 2 ? e / mu[k - 2] : 0.0;
+    const double l1 = k >= 1 ? (l - (k >= 2 ? l2 * p.nu1[k - 2] : 0.0)) / mu[k - 1] : 0.0;
+    mu[k] = d - (k >= 1 ? l1 * p.nu1[k - 1] : 0.0) - (k >= 2 ? l2 * f : 0.0);
+    if (!(std::fabs(mu[k]) >= guard)) return fail(err, kSingular, "penta_factor: pivot guard");
+    p.lam1[k] = l1;
+    p.lam2[k] = l2;
+    p.nu1[k] = u - l1 * f;
+    p.inv_mu[k] = 1.0 / mu[k];
+  }
+  auto solve = [&](std::vector<double> r) {  // D^{-1} r with the factors above
+    for (int64_t k = 0; k < N; ++k)
+      r[k] -= (k >= 1 ? p.lam1[k] * r[k - 1] : 0.0) + (k >= 2 ? p.lam2[k] * r[k - 2] : 0.0);
+    for (int64_t k = N - 1; k >= 0; --k)
+      r[k] = (r[k] - (k + 1 < N ? p.nu1[k] * r[k + 1] : 0.0) - (k + 2 < N ? f * r[k + 2] : 0.0)) *
+             p.inv_mu[k];
+    return r;
+  };
+  std::vector<double> v(N, 0.0);
+  v[0] = e;
+  p.S0 = solve(v);  // coefficient of x~_i[0]: interior row 0 (slab row 2) has e
+  v.assign(N, 0.0);
+  v[0] = l;
+  v[1] = e;
+  p.S1 = solve(v);  // x~_i[1]: slab rows 2 (l) and 3 (e)
+  v.assign(N, 0.0);
+  v[N - 2] = f;
+  v[N - 1] = u;
+  p.R0 = solve(v);  // x~_{i+1}[0]: slab rows n-2 (f) and n-1 (u)
+  v.assign(N, 0.0);
+  v[N - 1] = f;
+  p.R1 = solve(v);  // x~_{i+1}[1]: slab row n-1 (f)
+  const std::vector<double>* S[2] = {&p.S0, &p.S1};
+  const std::vector<double>* R[2] = {&p.R0, &p.R1};
+  for (int c = 0; c < 2; ++c) {
+    const std::vector<double>& s = *S[c];
+    const std::vector<double>& r = *R[c];
+    p.Lh[0 * 2 + c] = -(e * s[N - 2] + l * s[N - 1]);
+    p.Lh[1 * 2 + c] = -(e * s[N - 1]);
+    const double LR0 = e * r[N - 2] + l * r[N - 1], LR1 = e * r[N - 1];
+    const double US0 = f * s[0], US1 = u * s[0] + f * s[1];
+    const double Dt0 = c == 0 ? d : u, Dt1 = c == 0 ? l : d;  // D~ = [d u; l d]
+    p.Dh[0 * 2 + c] = Dt0 - LR0 - US0;
+    p.Dh[1 * 2 + c] = Dt1 - LR1 - US1;
+    p.DhFirst[0 * 2 + c] = Dt0 - US0;  // acyclic partition 0: no previous interior
+    p.DhFirst[1 * 2 + c] = Dt1 - US1;
+    p.Uh[0 * 2 + c] = -(f * r[0]);
+    p.Uh[1 * 2 + c] = -(u * r[0] + f * r[1]);
+  }
+  *out = std::move(p);
+  return true;
+}
+
+int64_t penta_window(const Penta& p) {
+  const double eps = std::ldexp(1.0, -64);
+  int64_t lo = 0, hi = 0;  // rows from the start / end with a non-negligible entry
+  for (int64_t k = 0; k < p.N; ++k)
+    if (std::fabs(p.S0[k]) > eps || std::fabs(p.S1[k]) > eps) lo = k + 1;
+  for (int64_t k = 0; k < p.N; ++k)
+    if (std::fabs(p.R0[k]) > eps || std::fabs(p.R1[k]) > eps) {
+      hi = p.N - k;
+      break;
+    }
+  const int64_t W = std::max(lo <= p.N / 2 ? lo : p.N, hi <= p.N / 2 ? hi : p.N);
+  return 2 * W >= p.N ? p.N : W;
+}
+
+bool penta_reduced_inverse(int P, bool cyclic, const Penta& pt, double guard, std::vector<double>* inv,
+                           FactorError* err) {
+  if (P < 1) return fail(err, kInvalid, "penta_reduced_inverse: P < 1");
+  const int n = 2 * P;
+  std::vector<double> a((size_t)n * n, 0.0);
+  auto add = [&](int bi, int bj, const double* blk) {
+    for (int r = 0; r < 2; ++r)
+      for (int c = 0; c < 2; ++c) a[(size_t)(2 * bi + r) * n + 2 * bj + c] += blk[r * 2 + c];
+  };
+  for (int i = 0; i < P; ++i) {
+    add(i, i, (cyclic || i > 0) ? pt.Dh : pt.DhFirst);
+    if (cyclic || i > 0) add(i, (i + P - 1) % P, pt.Lh);
+    if (cyclic || i < P - 1) add(i, (i + 1) % P, pt.Uh);
+  }
+  return dense_inverse(n, a, guard, inv, err, "penta_reduced_inverse");
+}
+
 bool reduced_inverse(int P, bool cyclic, const std::vector<double>& L, const std::vector<double>& D,
                      const std::vector<double>& U, double guard, std::vector<double>* inv,
                      FactorError* err) {

@@ -87,6 +87,34 @@ bool reduced_inverse(int P, bool cyclic, const std::vector<double>& L, const std
                      const std::vector<double>& U, double guard, std::vector<double>* inv,
                      FactorError* err);
 
+// ---- pentadiagonal (r = 2; "for a penta-diagonal system D~_i is 2x2") ----
+// Bands (e, l, d, u, f) = (A[i,i-2], A[i,i-1], A[i,i], A[i,i+1], A[i,i+2]).  A partition of n
+// rows: rows 0, 1 are the interface x~_i (r = 2 unknowns), rows 2..n-1 the interior (N = n-2).
+// Interior block D (acyclic pentadiagonal) = L U without pivoting:
+//   lam2[k] = e / mu[k-2],  lam1[k] = (l - lam2[k] nu1[k-2]) / mu[k-1],
+//   mu[k] = d - lam1[k] nu1[k-1] - lam2[k] f,  nu1[k] = u - lam1[k] f;
+//   forward  z_k = b_k - lam1[k] z_{k-1} - lam2[k] z_{k-2},
+//   backward y_k = (z_k - nu1[k] y_{k+1} - f y_{k+2}) / mu[k]          (Eq. yi)
+// Couplings (Eqs. Si, Ri with r = 2): S = D^{-1} L, L = [e l; 0 e; 0 ...] (rows 0, 1),
+// R = D^{-1} U, U = [... ; f 0; u f] (rows N-2, N-1), stored as columns S0, S1, R0, R1.
+// 2x2 reduced blocks (Eqs. Li_hat..Ui_hat), row-major:
+//   L^ = -L~ S,  D^ = D~ - L~ R - U~ S,  U^ = -U~ R,  D~ = [d u; l d],
+//   L~ = rows (e y[N-2] + l y[N-1], e y[N-1]) of the previous interior, U~ = rows
+//   (f y[0], u y[0] + f y[1]) of the own interior.
+struct Penta {
+  int64_t N = 0;
+  std::vector<double> lam1, lam2, nu1, inv_mu;
+  std::vector<double> S0, S1, R0, R1;
+  double Lh[4] = {0, 0, 0, 0}, Dh[4] = {0, 0, 0, 0}, DhFirst[4] = {0, 0, 0, 0}, Uh[4] = {0, 0, 0, 0};
+};
+bool penta_factor(int64_t N, const double bd[5], Penta* out, FactorError* err);
+// rows per end where some |S| or |R| entry exceeds 2^-64 (reading R15 with r = 2); N if they overlap
+int64_t penta_window(const Penta& p);
+// dense inverse of the 2P x 2P block-tridiagonal reduced matrix (2x2 blocks; cyclic corners,
+// coinciding couplings add up; acyclic: first block row uses DhFirst, no L^ / U^ at the ends)
+bool penta_reduced_inverse(int P, bool cyclic, const Penta& pt, double guard, std::vector<double>* inv,
+                           FactorError* err);
+
 inline bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 inline int ilog2(int64_t v) {
   int q = 0;

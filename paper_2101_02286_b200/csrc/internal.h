@@ -139,6 +139,8 @@ struct P2PRank {
   unsigned long long* peer_mbox[kMaxP2PRanks];  // every rank's mailbox as addressable here
   P2PStep step[kMaxP2PSteps];
   double ag0[kMaxAG], ag1[kMaxAG];  // all-gather mode: rows i and i+1 of A^{-1} (zeros past p)
+  const double* planes4;         // pentadiagonal all-gather: [4][m] c0 | c1 | w0 | w1
+  const double* ainv;            // pentadiagonal all-gather: [2p][2p] reduced inverse
 };
 struct P2PArgs {
   int p, q, cyclic, nslices, full;  // q = number of schedule steps
@@ -153,8 +155,9 @@ struct P2PArgs {
   P2PRank rk[kMaxP2PRanks];
 };
 cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s);
-int p2p_slices(int64_t m, int nranks_launch, int num_sms, bool allgather);
-int64_t p2p_copy_words(int64_t m, int q, int p, bool allgather);
+int p2p_slices(int64_t m, int nranks_launch, int num_sms, int kind);  // 0 schedule, 1 all-gather, 2 penta
+cudaError_t launch_reduced_allgather_r2(const P2PArgs& A, int nranks_launch, cudaStream_t s);
+int64_t p2p_copy_words(int64_t m, int q, int p, bool allgather, int planes = 2);
 size_t p2p_mailbox_words(int64_t copy_words, int64_t m, bool halo);
 cudaError_t launch_halo_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s);
 
@@ -217,6 +220,17 @@ struct Plan {
   ncclComm_t comm = nullptr;
   std::vector<Plan*> group;  // loopback peers (index = rank)
 
+  // pentadiagonal plan (r = 2, penta.cu)
+  int r = 1;                      // interface rows per partition: 1 tridiagonal, 2 pentadiagonal
+  double bands5[5] = {0, 0, 0, 0, 0};
+  Penta pt;
+  double pcinv[4] = {0, 0, 0, 0};  // p == 1: inverse of the 2x2 closure
+  double *d_plu = nullptr;         // [4][N]: lam1 | lam2 | nu1 | inv_mu
+  double *d_pSR = nullptr;         // [4][N]: S0 | S1 | R0 | R1
+  double *d_ainv = nullptr;        // [2p][2p] reduced inverse (p > 1)
+  double *d_planes4 = nullptr;     // [4][m]: c0 | c1 | w0 | w1  (c = b~ - U~ y_i, w = L~ y_i)
+  double *d_xnext2 = nullptr;      // [2][m]: x~_{i+1}
+
   // stats
   uint64_t solves = 0;
   std::vector<cudaEvent_t> ev;  // timing events
@@ -231,6 +245,10 @@ cudaError_t launch_pcr_stage(const Plan& P, int k, bool last, cudaStream_t s);
 cudaError_t launch_backsub(const Plan& P, double* x, cudaStream_t s);
 cudaError_t launch_reduced_local(const Plan& P, double* x, cudaStream_t s);
 cudaError_t launch_window(const Plan& P, double* x, const double* next, cudaStream_t s);
+// penta.cu (r = 2)
+ctri_status penta_plan_tables(Plan* P, cudaStream_t s, std::string* why);
+cudaError_t launch_penta_local(const Plan& P, const double* b, double* x, cudaStream_t s);
+cudaError_t launch_penta_window(const Plan& P, double* x, cudaStream_t s);
 cudaError_t launch_pack_halo(const Plan& P, const double* f, cudaStream_t s);
 cudaError_t launch_stencil(const Plan& P, const double* f, double* rhs, const Stencil5& st,
                            cudaStream_t s);

@@ -284,6 +284,100 @@ __global__ void __launch_bounds__(kP2PThreads, 1)
   for (int k = 2; k < 6; ++k) stamp(k);
 }
 
+// Pentadiagonal (r = 2) reduced phase, all-gather form (SURVEY 8(f) N3 + N4): per column every
+// rank sends its 4 plane values c = b~_i - U~ y_i (2) and w = L~ y_i[last two] (2) to every peer,
+// forms the 2x2-block right-hand sides b^_r = c_r - w_{r-1} (Eq. bi_hat with r = 2) and
+// evaluates x~_i, x~_{i+1} (2 values each) with plan-time rows of the 2p x 2p inverse of A^.
+__global__ void __launch_bounds__(kP2PThreads, 1)
+    k_reduced_allgather_r2(const P2PArgs A) {
+  const int r_local = blockIdx.x / A.nslices;
+  const int slice = blockIdx.x - r_local * A.nslices;
+  const P2PRank& R = A.rk[r_local];
+  const int p = A.p, rank = R.rank;
+  const int64_t m = A.m;
+  const int64_t c0 = (int64_t)slice * A.slice_cols;
+  const int64_t c1 = std::min<int64_t>(m, c0 + A.slice_cols);
+  const uint32_t ep = R.epoch[slice] + 1u;
+  const unsigned long long deadline = globaltimer() + 20ull * 1000000000ull;  // 20 s
+  const int64_t copy_off = (int64_t)(ep & 1u) * A.copy_words;
+  const bool cyc = A.cyclic != 0;
+  unsigned long long* const mine = R.mbox + copy_off;
+  const int64_t n = A.lay.n, inner = A.lay.inner;
+  const int nx = rank + 1 < p ? rank + 1 : (cyc ? 0 : -1);  // owner of x~_{i+1}
+  bool ok = true;
+#pragma unroll 1
+  for (int64_t j = c0 + threadIdx.x; j < c1; j += kP2PThreads) {
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = R.planes4[q * m + j];
+    for (int r = 0; r < p; ++r) {
+      if (r == rank) continue;
+      unsigned long long* dst = R.peer_mbox[r] + copy_off;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ll_send(dst + (int64_t)(q * p + rank) * 2 * m + 2 * j, v[q], ep);
+    }
+  }
+#pragma unroll 1
+  for (int64_t j = c0 + threadIdx.x; j < c1 && ok; j += kP2PThreads) {
+    double pl[4][kMaxAG];
+    uint32_t mask = 0;
+#pragma unroll
+    for (int r = 0; r < kMaxAG; ++r) {
+      if (r < p && r != rank) mask |= 1u << r;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) pl[q][r] = 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      ok = ok && ll_recv_batch(mine + (int64_t)q * p * 2 * m + 2 * j, 2 * m, mask, ep, deadline, pl[q]);
+    if (!ok) break;
+#pragma unroll
+    for (int r = 0; r < kMaxAG; ++r)
+      if (r == rank)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pl[q][r] = R.planes4[q * m + j];
+    double wrap0 = 0.0, wrap1 = 0.0;  // w_{p-1}: the left neighbour of rank 0 (cyclic)
+#pragma unroll
+    for (int r = 0; r < kMaxAG; ++r)
+      if (r == p - 1 && cyc) { wrap0 = pl[2][r]; wrap1 = pl[3][r]; }
+    double xa0 = 0.0, xa1 = 0.0, xn0 = 0.0, xn1 = 0.0;
+    const double* gi = R.ainv + (size_t)(2 * rank) * 2 * p;
+    const double* gn = R.ainv + (size_t)(2 * (nx < 0 ? 0 : nx)) * 2 * p;
+#pragma unroll
+    for (int r = 0; r < kMaxAG; ++r) {
+      if (r >= p) continue;
+      const double b0 = pl[0][r] - (r > 0 ? pl[2][r > 0 ? r - 1 : 0] : wrap0);
+      const double b1 = pl[1][r] - (r > 0 ? pl[3][r > 0 ? r - 1 : 0] : wrap1);
+      xa0 += __ldg(gi + 2 * r) * b0 + __ldg(gi + 2 * r + 1) * b1;
+      xa1 += __ldg(gi + 2 * p + 2 * r) * b0 + __ldg(gi + 2 * p + 2 * r + 1) * b1;
+      xn0 += __ldg(gn + 2 * r) * b0 + __ldg(gn + 2 * r + 1) * b1;
+      xn1 += __ldg(gn + 2 * p + 2 * r) * b0 + __ldg(gn + 2 * p + 2 * r + 1) * b1;
+    }
+    if (nx < 0) xn0 = xn1 = 0.0;
+    const int64_t o = j / inner, cc = j - o * inner;
+    R.x[o * n * inner + cc] = xa0;
+    R.x[(o * n + 1) * inner + cc] = xa1;
+    R.xnext[j] = xn0;
+    R.xnext[m + j] = xn1;
+  }
+  if (!ok) atomicExch(A.err, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) R.epoch[slice] = ep;
+}
+
+cudaError_t launch_reduced_allgather_r2(const P2PArgs& A, int nranks_launch, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(A.nslices * nranks_launch), 1, 1);
+  cfg.blockDim = dim3(kP2PThreads, 1, 1);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = nranks_launch > 1 ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k_reduced_allgather_r2, A);
+}
+
 cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(A.nslices * nranks_launch), 1, 1);
@@ -298,12 +392,13 @@ cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t
                      : cudaLaunchKernelEx(&cfg, k_reduced_p2p, A);
 }
 
-int p2p_slices(int64_t m, int nranks_launch, int num_sms, bool allgather) {
+int p2p_slices(int64_t m, int nranks_launch, int num_sms, int kind) {
   // one wave: <= resident CTAs in total, <= kMaxCpt columns per thread
+  const bool allgather = kind != 0;
+  const void* fn = kind == 0 ? (const void*)k_reduced_p2p
+                 : kind == 1 ? (const void*)k_reduced_allgather : (const void*)k_reduced_allgather_r2;
   int per_sm = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &per_sm, allgather ? (const void*)k_reduced_allgather : (const void*)k_reduced_p2p,
-          kP2PThreads, 0) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kP2PThreads, 0) !=
           cudaSuccess || per_sm < 1) {
     cudaGetLastError();
     per_sm = 1;
@@ -316,8 +411,8 @@ int p2p_slices(int64_t m, int nranks_launch, int num_sms, bool allgather) {
 }
 
 // one epoch copy: [2 + 2q slots][2m LL words] (schedule) or [2 planes][p sources][2m] (all-gather)
-int64_t p2p_copy_words(int64_t m, int q, int p, bool allgather) {
-  return (int64_t)std::max(2 + 2 * q, allgather ? 2 * p : 0) * 2 * m;
+int64_t p2p_copy_words(int64_t m, int q, int p, bool allgather, int planes) {
+  return (int64_t)std::max(2 + 2 * q, allgather ? planes * p : 0) * 2 * m;
 }
 // [2 epoch copies][copy]  +  (derivative) [2 copies][4 halo rows][2m]
 size_t p2p_mailbox_words(int64_t copy_words, int64_t m, bool halo) {

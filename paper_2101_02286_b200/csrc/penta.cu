@@ -1,0 +1,271 @@
+// penta.cu -- the partition method for PENTADIAGONAL systems (r = 2).
+//
+// for a system of bandwidth w = 2r + 1 the interface block D~_i is r x r ("for a
+// penta-diagonal system (w = 5), D~_i is 2x2"), L~_i / U~_i are short fat blocks and L_i / U_i
+// tall skinny ones; Eqs. Si, Ri, Li_hat..Ui_hat, bi_hat and xi_app hold unchanged
+// with 2x2 blocks, and "only the last r columns ... are needed for neighbor communication"
+// (P:345).  Per partition of n rows (rows 0, 1 = x~_i, rows 2..n-1 = interior, N = n - 2):
+//   (a1) k_penta_local: y_i = D_i^{-1} b_i by the plan-time LU factors of the pentadiagonal
+//        interior (forward into x, backward in place), plus the planes c = b~_i - U~ y_i and
+//        w = L~ y_i (2 values each); with one partition the 2x2 closure
+//        (L^ + D^ + U^) x~ = c - w (cyclic) or D^ x~ = c (acyclic) is solved in place;
+//   (a2)+(a3) p > 1: k_reduced_allgather_r2 (p2p.cu): one all-gather round of the 4 planes,
+//        b^_r = c_r - w_{r-1}, x~_i and x~_{i+1} from plan-time rows of the 2p x 2p inverse;
+//   (a4) k_penta_window: x = y - S x~_i - R x~_{i+1} on the window rows (reading R15, r = 2).
+// HBM traffic of the column-serial local solve: b read once, the forward result written and
+// read back once, y written once (32 B per point) -- DESIGN.md section 4.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "internal.h"
+
+namespace ctri {
+
+struct PentaArgs {
+  const double* b;
+  double* x;
+  int64_t outer, n, inner;
+  const double* lu;   // [4][N]: lam1 | lam2 | nu1 | inv_mu
+  double e, l, u, f;
+  double* planes4;    // [4][m]
+  int closure, cyclic;
+  double cinv[4];     // p == 1: 2x2 closure inverse (row-major)
+};
+
+constexpr int kPentaRows = 8;  // rows per batch: 8 independent loads in flight per thread
+
+__global__ void __launch_bounds__(128) k_penta_local(const PentaArgs A) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t m = A.outer * A.inner;
+  if (j >= m) return;
+  const int64_t o = j / A.inner, c = j - o * A.inner, st = A.inner;
+  const int64_t N = A.n - 2;
+  const double* bc = A.b + o * A.n * st + c;
+  double* xc = A.x + o * A.n * st + c;
+  const double* lam1 = A.lu;
+  const double* lam2 = A.lu + N;
+  const double* nu1 = A.lu + 2 * N;
+  const double* imu = A.lu + 3 * N;
+  const double bt0 = bc[0], bt1 = bc[st];
+  // forward: z_k = b_k - lam1[k] z_{k-1} - lam2[k] z_{k-2}   (interior row k = slab row k + 2)
+  double z1 = 0.0, z2 = 0.0;
+  for (int64_t k0 = 0; k0 < N; k0 += kPentaRows) {
+    double v[kPentaRows];
+#pragma unroll
+    for (int t = 0; t < kPentaRows; ++t)
+      if (k0 + t < N) v[t] = bc[(k0 + t + 2) * st];
+#pragma unroll
+    for (int t = 0; t < kPentaRows; ++t) {
+      const int64_t k = k0 + t;
+      if (k < N) {
+        const double z = v[t] - __ldg(lam1 + k) * z1 - __ldg(lam2 + k) * z2;
+        xc[(k + 2) * st] = z;
+        z2 = z1;
+        z1 = z;
+      }
+    }
+  }
+  // backward: y_k = (z_k - nu1[k] y_{k+1} - f y_{k+2}) / mu[k]
+  double y1 = 0.0, y2 = 0.0, ylast = 0.0, ylast2 = 0.0;
+  const int64_t nb = (N + kPentaRows - 1) / kPentaRows;
+  for (int64_t bi = nb - 1; bi >= 0; --bi) {
+    const int64_t k0 = bi * kPentaRows;
+    double v[kPentaRows];
+#pragma unroll
+    for (int t = 0; t < kPentaRows; ++t)
+      if (k0 + t < N) v[t] = xc[(k0 + t + 2) * st];
+#pragma unroll
+    for (int t = kPentaRows - 1; t >= 0; --t) {
+      const int64_t k = k0 + t;
+      if (k < N) {
+        const double y = (v[t] - __ldg(nu1 + k) * y1 - A.f * y2) * __ldg(imu + k);
+        xc[(k + 2) * st] = y;
+        if (k == N - 1) ylast = y;
+        if (k == N - 2) ylast2 = y;
+        y2 = y1;
+        y1 = y;
+      }
+    }
+  }
+  // y1 = y[0], y2 = y[1];  planes: c = b~ - U~ y_i[0..1], w = L~ y_i[N-2..N-1]
+  const double c0 = bt0 - A.f * y1;
+  const double c1 = bt1 - (A.u * y1 + A.f * y2);
+  const double w0 = A.e * ylast2 + A.l * ylast;
+  const double w1 = A.e * ylast;
+  if (A.closure) {  // one partition: x~ = (closure)^{-1} b^, b^ = c - w (cyclic) or c (acyclic)
+    const double h0 = c0 - (A.cyclic ? w0 : 0.0), h1 = c1 - (A.cyclic ? w1 : 0.0);
+    xc[0] = A.cinv[0] * h0 + A.cinv[1] * h1;
+    xc[st] = A.cinv[2] * h0 + A.cinv[3] * h1;
+  } else {
+    A.planes4[j] = c0;
+    A.planes4[m + j] = c1;
+    A.planes4[2 * m + j] = w0;
+    A.planes4[3 * m + j] = w1;
+  }
+}
+
+struct PentaWinArgs {
+  double* x;
+  const double* SR;    // [4][N]: S0 | S1 | R0 | R1
+  const double* next;  // [2][m] x~_{i+1} (p > 1), else nullptr
+  int64_t outer, n, inner, N, W, rows;
+  int full, wrap;
+};
+
+__device__ __forceinline__ int64_t penta_row(const PentaWinArgs& A, int64_t ry) {
+  return A.full ? ry : (ry < A.W ? ry : A.N - 2 * A.W + ry);  // interior row index k
+}
+
+// x_k = y_k - S0[k] x~_i[0] - S1[k] x~_i[1] - R0[k] x~_{i+1}[0] - R1[k] x~_{i+1}[1]  (Eq. xi_app)
+__device__ __forceinline__ double penta_fix(const PentaWinArgs& A, int64_t k, double y, double a0,
+                                            double a1, double n0, double n1) {
+  const double* S0 = A.SR;
+  const double* S1 = A.SR + A.N;
+  const double* R0 = A.SR + 2 * A.N;
+  const double* R1 = A.SR + 3 * A.N;
+  return y - (__ldg(S0 + k) * a0 + __ldg(S1 + k) * a1) - (__ldg(R0 + k) * n0 + __ldg(R1 + k) * n1);
+}
+
+__global__ void __launch_bounds__(256) k_penta_window(const PentaWinArgs A) {
+  const int64_t j = blockIdx.x * 256ll + threadIdx.x;
+  const int64_t m = A.outer * A.inner;
+  if (j >= m) return;
+  const int64_t o = j / A.inner, c = j - o * A.inner, st = A.inner;
+  double* xc = A.x + o * A.n * st + c;
+  const double a0 = xc[0], a1 = xc[st];
+  double n0 = 0.0, n1 = 0.0;
+  if (A.next) {
+    n0 = A.next[j];
+    n1 = A.next[m + j];
+  } else if (A.wrap) {
+    n0 = a0;
+    n1 = a1;
+  }
+  const int64_t r0 = (int64_t)blockIdx.y * kPentaRows;
+  double v[kPentaRows];
+#pragma unroll
+  for (int t = 0; t < kPentaRows; ++t)
+    if (r0 + t < A.rows) v[t] = xc[(penta_row(A, r0 + t) + 2) * st];
+#pragma unroll
+  for (int t = 0; t < kPentaRows; ++t)
+    if (r0 + t < A.rows) {
+      const int64_t k = penta_row(A, r0 + t);
+      xc[(k + 2) * st] = penta_fix(A, k, v[t], a0, a1, n0, n1);
+    }
+}
+
+// contiguous solve axis: one warp per column, lanes along the rows
+__global__ void __launch_bounds__(256) k_penta_window_contig(const PentaWinArgs A) {
+  const int64_t w = blockIdx.x * 8ll + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= A.outer) return;
+  double* xc = A.x + w * A.n;
+  const double a0 = xc[0], a1 = xc[1];
+  double n0 = 0.0, n1 = 0.0;
+  if (A.next) {
+    n0 = A.next[w];
+    n1 = A.next[A.outer + w];
+  } else if (A.wrap) {
+    n0 = a0;
+    n1 = a1;
+  }
+  for (int64_t ry = lane; ry < A.rows; ry += 32) {
+    const int64_t k = penta_row(A, ry);
+    xc[k + 2] = penta_fix(A, k, xc[k + 2], a0, a1, n0, n1);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// plan set-up and solve
+// ------------------------------------------------------------------------------------------
+static ctri_status upload_vec(double** d, const std::vector<double>& h, cudaStream_t s) {
+  if (cudaMalloc(d, sizeof(double) * std::max<size_t>(1, h.size())) != cudaSuccess)
+    return CTRI_ERR_OOM;
+  if (cudaMemcpyAsync(*d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return CTRI_ERR_CUDA;
+  return CTRI_OK;
+}
+
+ctri_status penta_plan_tables(Plan* P, cudaStream_t s, std::string* why) {
+  const int64_t n = P->lay.n, N = n - 2, m = P->lay.m();
+  FactorError fe;
+  if (!penta_factor(N, P->bands5, &P->pt, &fe)) {
+    *why = fe.detail;
+    return (ctri_status)fe.code;
+  }
+  const Penta& pt = P->pt;
+  P->window = penta_window(pt);
+  double mx = 0;
+  for (int k = 0; k < 5; ++k) mx = std::max(mx, std::fabs(P->bands5[k]));
+  const double guard = 1e-13 * mx;
+  std::vector<double> inv;
+  if (!penta_reduced_inverse(P->p, P->cyclic != 0, pt, guard, &inv, &fe)) {
+    *why = fe.detail;
+    return (ctri_status)fe.code;
+  }
+  P->ainv = inv;
+  if (P->p == 1) std::memcpy(P->pcinv, inv.data(), sizeof(P->pcinv));
+  std::vector<double> lu, sr;
+  for (const std::vector<double>* v : {&pt.lam1, &pt.lam2, &pt.nu1, &pt.inv_mu}) lu.insert(lu.end(), v->begin(), v->end());
+  for (const std::vector<double>* v : {&pt.S0, &pt.S1, &pt.R0, &pt.R1}) sr.insert(sr.end(), v->begin(), v->end());
+  ctri_status st;
+  if ((st = upload_vec(&P->d_plu, lu, s)) != CTRI_OK) return st;
+  if ((st = upload_vec(&P->d_pSR, sr, s)) != CTRI_OK) return st;
+  if ((st = upload_vec(&P->d_ainv, inv, s)) != CTRI_OK) return st;
+  if (P->p > 1) {
+    if (cudaMalloc(&P->d_planes4, sizeof(double) * 4 * m) != cudaSuccess) return CTRI_ERR_OOM;
+    if (cudaMalloc(&P->d_xnext2, sizeof(double) * 2 * m) != cudaSuccess) return CTRI_ERR_OOM;
+    if (cudaMemsetAsync(P->d_xnext2, 0, sizeof(double) * 2 * m, s) != cudaSuccess) return CTRI_ERR_CUDA;
+  }
+  return CTRI_OK;
+}
+
+cudaError_t launch_penta_local(const Plan& P, const double* b, double* x, cudaStream_t s) {
+  PentaArgs A;
+  A.b = b;
+  A.x = x;
+  A.outer = P.lay.outer;
+  A.n = P.lay.n;
+  A.inner = P.lay.inner;
+  A.lu = P.d_plu;
+  A.e = P.bands5[0];
+  A.l = P.bands5[1];
+  A.u = P.bands5[3];
+  A.f = P.bands5[4];
+  A.planes4 = P.d_planes4;
+  A.closure = P.p == 1 ? 1 : 0;
+  A.cyclic = P.cyclic;
+  std::memcpy(A.cinv, P.pcinv, sizeof(A.cinv));
+  const int64_t m = P.lay.m();
+  k_penta_local<<<(unsigned)((m + 127) / 128), 128, 0, s>>>(A);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_penta_window(const Plan& P, double* x, cudaStream_t s) {
+  PentaWinArgs A;
+  A.x = x;
+  A.SR = P.d_pSR;
+  A.next = P.p > 1 ? P.d_xnext2 : nullptr;
+  A.outer = P.lay.outer;
+  A.n = P.lay.n;
+  A.inner = P.lay.inner;
+  A.N = P.lay.n - 2;
+  A.W = P.window;
+  A.full = ((P.flags & CTRI_FLAG_FULL_BACKSUB) || 2 * P.window >= A.N) ? 1 : 0;
+  A.rows = A.full ? A.N : 2 * A.W;
+  A.wrap = (P.p == 1 && P.cyclic) ? 1 : 0;
+  if (A.rows <= 0) return cudaSuccess;
+  if (A.inner == 1) {
+    k_penta_window_contig<<<(unsigned)((A.outer + 7) / 8), 256, 0, s>>>(A);
+  } else {
+    const int64_t m = P.lay.m();
+    dim3 grid((unsigned)((m + 255) / 256), (unsigned)((A.rows + kPentaRows - 1) / kPentaRows));
+    k_penta_window<<<grid, 256, 0, s>>>(A);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ctri

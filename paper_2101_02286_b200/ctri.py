@@ -25,7 +25,7 @@ CTRI_FLAG_DERIV = 1 << 3
 CTRI_FLAG_NCCL_ROUNDS = 1 << 4
 CTRI_FLAG_ALLGATHER = 1 << 5
 CTRI_MAX_STAGES = 16
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 STATUS = {0: "CTRI_OK", 1: "CTRI_ERR_INVALID_ARG", 2: "CTRI_ERR_UNSUPPORTED", 3: "CTRI_ERR_SINGULAR",
           4: "CTRI_ERR_PARTITION_TOO_SMALL", 5: "CTRI_ERR_CUDA", 6: "CTRI_ERR_NCCL",
@@ -37,7 +37,8 @@ ABI_SYMBOLS = ("ctri_status_string", "ctri_last_error", "ctri_abi_version", "ctr
                "ctri_solve_host", "ctri_deriv", "ctri_deriv_loopback", "ctri_get_stats",
                "ctri_plan_destroy", "ctri_factor_query", "ctri_pcr_coefficients",
                "ctri_reduced_schedule", "ctri_compact_apply", "ctri_compact_apply_loopback",
-               "ctri_reduced_inverse")
+               "ctri_reduced_inverse", "ctri_plan_create_penta", "ctri_plan_create_penta_loopback",
+               "ctri_penta_factor_query")
 
 
 class CtriError(RuntimeError):
@@ -67,7 +68,8 @@ class ctri_stats(ctypes.Structure):
                 ("tile_variant", ctypes.c_int32), ("tile_stages", ctypes.c_int32),
                 ("reduced_path", ctypes.c_int32), ("device_error", ctypes.c_int32),
                 ("vparts", ctypes.c_int32), ("grid_ctas", ctypes.c_int32),
-                ("detach_stages", ctypes.c_int32), ("detached_rows", ctypes.c_int32)]
+                ("detach_stages", ctypes.c_int32), ("detached_rows", ctypes.c_int32),
+                ("band_halfwidth", ctypes.c_int32)]
 
     def as_dict(self):
         d = {}
@@ -118,6 +120,11 @@ def load(build_if_missing: bool = False):
                                      ctypes.c_double, P]),
         "ctri_compact_apply": (st, [P, dp, P, P, P]),
         "ctri_reduced_inverse": (st, [ctypes.c_int, ctypes.c_int, dp, dp, dp, dp]),
+        "ctri_plan_create_penta": (st, [ctypes.POINTER(P), i64p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                        dp, ctypes.c_int, P, ctypes.c_uint32, P]),
+        "ctri_plan_create_penta_loopback": (st, [ctypes.POINTER(P), ctypes.c_int, i64p, ctypes.c_int, dp,
+                                                 ctypes.c_int, ctypes.c_uint32, P]),
+        "ctri_penta_factor_query": (st, [ctypes.c_int64, dp, dp, dp, ctypes.POINTER(ctypes.c_int)]),
         "ctri_compact_apply_loopback": (st, [ctypes.POINTER(P), ctypes.c_int, dp, ctypes.POINTER(P),
                                              ctypes.POINTER(P), P]),
         "ctri_get_stats": (st, [P, ctypes.POINTER(ctri_stats)]),
@@ -201,6 +208,50 @@ def ctri_plan_create_loopback(global_dims, solve_dim, nparts, bands=(1 / 3, 1.0,
                                             int(bool(cyclic)), int(flags), _stream_ptr(stream)),
            "ctri_plan_create_loopback")
     return [hs[i] for i in range(nparts)]
+
+
+def _dbl5(v):
+    if len(v) != 5:
+        raise ValueError("pentadiagonal bands must be (e, l, d, u, f)")
+    return (ctypes.c_double * 5)(*[float(x) for x in v])
+
+
+def ctri_plan_create_penta(global_dims, solve_dim, nparts=1, rank=0, bands=(0.05, 0.3, 1.0, 0.3, 0.05),
+                           cyclic=True, unique_id: bytes | None = None, flags: int = 0, stream=None) -> int:
+    h = ctypes.c_void_p()
+    dims = (ctypes.c_int64 * 3)(*[int(d) for d in global_dims])
+    uid = ctypes.create_string_buffer(unique_id, 128) if unique_id is not None else None
+    _check(load().ctri_plan_create_penta(ctypes.byref(h), dims, int(solve_dim), int(nparts), int(rank),
+                                         _dbl5(bands), int(bool(cyclic)), uid, int(flags),
+                                         _stream_ptr(stream)), "ctri_plan_create_penta")
+    return h.value
+
+
+def ctri_plan_create_penta_loopback(global_dims, solve_dim, nparts, bands=(0.05, 0.3, 1.0, 0.3, 0.05),
+                                    cyclic=True, flags: int = 0, stream=None) -> list[int]:
+    hs = (ctypes.c_void_p * nparts)()
+    dims = (ctypes.c_int64 * 3)(*[int(d) for d in global_dims])
+    _check(load().ctri_plan_create_penta_loopback(hs, int(nparts), dims, int(solve_dim), _dbl5(bands),
+                                                  int(bool(cyclic)), int(flags), _stream_ptr(stream)),
+           "ctri_plan_create_penta_loopback")
+    return [hs[i] for i in range(nparts)]
+
+
+def ctri_penta_factor_query(n: int, bands):
+    """Host-only: S0, S1, R0, R1 (n-2 each), the 2x2 blocks L^, D^, U^, D^(first) and the window."""
+    N = n - 2
+    SR = np.zeros(4 * max(1, N))
+    hat = np.zeros(16)
+    w = ctypes.c_int()
+    dp = ctypes.POINTER(ctypes.c_double)
+    _check(load().ctri_penta_factor_query(int(n), _dbl5(bands), SR.ctypes.data_as(dp),
+                                          hat.ctypes.data_as(dp), ctypes.byref(w)),
+           "ctri_penta_factor_query")
+    S = SR[:2 * N].reshape(2, N).T.copy()
+    R = SR[2 * N:].reshape(2, N).T.copy()
+    blocks = hat.reshape(4, 2, 2)
+    return {"S": S, "R": R, "Lh": blocks[0], "Dh": blocks[1], "Uh": blocks[2], "Dh_first": blocks[3],
+            "window": w.value}
 
 
 def ctri_solve(plan: int, b, x, stream=None):
@@ -371,8 +422,8 @@ class Plan:
         self.solve_dim = int(solve_dim)
         self.nparts = int(nparts)
         self.rank = int(rank)
-        self.handle = ctri_plan_create(global_dims, solve_dim, nparts, rank, bands, cyclic,
-                                       unique_id, flags, stream)
+        create = ctri_plan_create_penta if len(bands) == 5 else ctri_plan_create
+        self.handle = create(global_dims, solve_dim, nparts, rank, bands, cyclic, unique_id, flags, stream)
 
     @property
     def local_shape(self):
@@ -428,8 +479,8 @@ class LoopbackGroup:
         self.global_dims = tuple(int(d) for d in global_dims)
         self.solve_dim = int(solve_dim)
         self.nparts = int(nparts)
-        self.handles = ctri_plan_create_loopback(global_dims, solve_dim, nparts, bands, cyclic, flags,
-                                                 stream)
+        create = ctri_plan_create_penta_loopback if len(bands) == 5 else ctri_plan_create_loopback
+        self.handles = create(global_dims, solve_dim, nparts, bands, cyclic, flags, stream)
 
     @property
     def local_shape(self):

@@ -66,6 +66,19 @@ def main():
     plan.close()
     if rank == 0:
         results["deriv"] = {"err": rel_err(d.cpu().numpy(), oracle.deriv(f, 0), 0)}
+    # pentadiagonal (r = 2) partition method over real GPUs (IPC all-gather)
+    pb = (-0.07, 0.21, 1.3, -0.33, 0.11)
+    pdims = (16 * world, 3, 40)
+    b = workloads.uniform(pdims, 95)
+    plan = pdist.plan_from_process_group(pdims, 0, pb, True)
+    bl = torch.from_numpy(workloads.slab(b, 0, world, rank)).to(dev)
+    xl = torch.empty_like(bl)
+    plan.solve(bl, xl)
+    torch.cuda.synchronize()
+    x = pdist.gather_to_rank0(xl, 0)
+    plan.close()
+    if rank == 0:
+        results["penta"] = {"err": rel_err(x.cpu().numpy(), oracle.penta_solve(b, 0, pb, True), 0)}
     # staggered sixth-order interpolation through ctri_compact_apply
     from paper_2101_02286_b200 import ctri
     plan = pdist.plan_from_process_group(dims, 0, ctri.STAGGERED_INTERP_BANDS, True, flags=CTRI_FLAG_DERIV)

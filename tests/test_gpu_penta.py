@@ -1,0 +1,115 @@
+"""GPU parity of the pentadiagonal partition method (r = 2)
+against the pentadiagonal oracle, through the C ABI: 1..8 partitions (loopback), cyclic and
+acyclic, three band sets (incl. Lele's tenth-order LHS), all three solve directions, window and
+full back-substitution, and the Fourier closed form."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from helpers import TOL_REL, rel_err
+
+pytestmark = pytest.mark.gpu
+
+BANDS = [(0.05, 0.3, 1.0, 0.3, 0.05), (-0.07, 0.21, 1.3, -0.33, 0.11), (1 / 20, 1 / 2, 1.0, 1 / 2, 1 / 20)]
+
+
+def penta_gpu(b, sd, p, bands, cyclic=True, flags=0, inplace=False, return_stats=False):
+    import torch
+
+    from paper_2101_02286_b200 import ctri
+    dev = torch.device("cuda:0")
+    slabs = [torch.from_numpy(workloads.slab(b, sd, p, r)).to(dev) for r in range(p)]
+    xs = slabs if inplace else [torch.empty_like(s) for s in slabs]
+    if p == 1:
+        plan = ctri.Plan(b.shape, sd, 1, 0, bands, cyclic, None, flags)
+        plan.solve(slabs[0], xs[0])
+        torch.cuda.synchronize()
+        st = plan.stats()
+        plan.close()
+    else:
+        g = ctri.LoopbackGroup(b.shape, sd, p, bands, cyclic, flags)
+        g.solve(slabs, xs)
+        torch.cuda.synchronize()
+        st = g.stats(0)
+        g.close()
+    x = workloads.assemble([t.cpu().numpy() for t in xs], sd)
+    return (x, st) if return_stats else x
+
+
+def penta_residual(x, b, sd, bands, cyclic):
+    xc = np.moveaxis(x, sd, 0)
+    bc = np.moveaxis(b, sd, 0)
+    r = -bc.copy()
+    for off, v in zip((-2, -1, 0, 1, 2), bands):
+        sh = np.roll(xc, -off, axis=0)
+        if not cyclic:
+            if off > 0:
+                sh[-off:] = 0
+            elif off < 0:
+                sh[:-off] = 0
+        r += v * sh
+    return float(np.max(np.abs(r)) / np.max(np.abs(bc)))
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("cyclic", [True, False])
+@pytest.mark.parametrize("bands", BANDS)
+def test_penta_matches_oracle(p, cyclic, bands):
+    shape = (12 * p, 3, 40)  # n = 12: reduced couplings far from negligible
+    b = workloads.uniform(shape, 70 + p)
+    x, st = penta_gpu(b, 0, p, bands, cyclic, return_stats=True)
+    ref = oracle.penta_solve(b, 0, bands, cyclic)
+    assert st["band_halfwidth"] == 2
+    assert rel_err(x, ref, 0) < TOL_REL
+    assert penta_residual(x, b, 0, bands, cyclic) < 1e-13
+
+
+@pytest.mark.parametrize("p,shape,sd", [(1, (4096, 2, 64), 0), (2, (2048, 3, 40), 0), (4, (8, 1024, 32), 1),
+                                        (2, (4, 8, 2048), 2), (8, (2048, 2, 33), 0), (1, (3, 5, 700), 2)])
+@pytest.mark.parametrize("full", [False, True])
+def test_penta_layouts_and_window(p, shape, sd, full):
+    from paper_2101_02286_b200 import CTRI_FLAG_FULL_BACKSUB
+    bands = BANDS[1]
+    b = workloads.uniform(shape, 80 + p)
+    x, st = penta_gpu(b, sd, p, bands, True, CTRI_FLAG_FULL_BACKSUB if full else 0, return_stats=True)
+    assert rel_err(x, oracle.penta_solve(b, sd, bands, True), sd) < TOL_REL
+    if not full and shape[sd] // p > 200:
+        assert st["window_rows"] < shape[sd] // p // 2
+
+
+def test_penta_inplace():
+    b = workloads.uniform((1024, 2, 16), 90)
+    x = penta_gpu(b, 0, 4, BANDS[0], inplace=True)
+    assert rel_err(x, oracle.penta_solve(b, 0, BANDS[0], True), 0) < TOL_REL
+
+
+@pytest.mark.parametrize("p", [1, 4])
+def test_penta_fourier_closed_form(p):
+    """b_j = cos(theta j) => x_j = Re(e^{i theta j} / lambda(theta)) (non-symmetric bands)."""
+    e, l, d, u, f = BANDS[1]
+    N, k = 2048, 301
+    th = 2 * math.pi * k / N
+    lam = d + l * np.exp(-1j * th) + u * np.exp(1j * th) + e * np.exp(-2j * th) + f * np.exp(2j * th)
+    j = np.arange(N, dtype=np.int64)
+    ph = 2 * math.pi * ((k * j) % N) / N
+    b = np.broadcast_to(np.cos(ph).reshape(N, 1, 1), (N, 2, 16)).copy()
+    x = penta_gpu(b, 0, p, BANDS[1])
+    expect = np.real(np.exp(1j * ph) / lam).reshape(N, 1, 1)
+    assert np.max(np.abs(x - expect)) < 1e-14
+
+
+def test_penta_unsupported():
+    from paper_2101_02286_b200 import CTRI_FLAG_DERIV, CTRI_FLAG_NCCL_ROUNDS, ctri
+    with pytest.raises(ctri.CtriError, match="UNSUPPORTED"):
+        ctri.LoopbackGroup((16 * 9, 2, 8), 0, 9, BANDS[0])
+    with pytest.raises(ctri.CtriError, match="UNSUPPORTED"):
+        ctri.Plan((64, 2, 8), 0, 1, 0, BANDS[0], True, None, CTRI_FLAG_DERIV)
+    with pytest.raises(ctri.CtriError, match="UNSUPPORTED"):
+        ctri.LoopbackGroup((64, 2, 8), 0, 2, BANDS[0], True, CTRI_FLAG_NCCL_ROUNDS)
+    with pytest.raises(ctri.CtriError, match="PARTITION_TOO_SMALL"):
+        ctri.LoopbackGroup((20, 2, 8), 0, 4, BANDS[0])

@@ -271,3 +271,81 @@ def test_reduced_inverse_vs_dense(P, cyclic):
 def test_reduced_inverse_singular():
     with pytest.raises(pk.CtriError, match="SINGULAR"):
         pk.ctri_reduced_inverse([0.5, 0.5], [1.0, 1.0], [0.5, 0.5], cyclic=True)  # [[1, 1], [1, 1]]
+
+
+# ---- pentadiagonal (r = 2) partition tables ----
+PENTA_BANDS = [(0.05, 0.3, 1.0, 0.3, 0.05), (-0.07, 0.21, 1.3, -0.33, 0.11), (1 / 20, 1 / 2, 1.0, 1 / 2, 1 / 20)]
+
+
+def _dense_penta(N, bands, cyclic):
+    A = np.zeros((N, N))
+    for i in range(N):
+        for off, v in zip((-2, -1, 0, 1, 2), bands):
+            j = i + off
+            if 0 <= j < N:
+                A[i, j] += v
+            elif cyclic:
+                A[i, j % N] += v
+    return A
+
+
+@pytest.mark.parametrize("bands", PENTA_BANDS)
+@pytest.mark.parametrize("n", [6, 7, 12, 40])
+def test_penta_S_R_vs_dense(bands, n):
+    """S = D^{-1} L, R = D^{-1} U with the interior block and couplings of P:212 (r = 2)."""
+    e, l, d, u, f = bands
+    N = n - 2
+    t = pk.ctri_penta_factor_query(n, bands)
+    D = _dense_penta(N, bands, False)
+    L = np.zeros((N, 2))
+    L[0, 0], L[0, 1], L[1, 1] = e, l, e
+    U = np.zeros((N, 2))
+    U[N - 2, 0], U[N - 1, 0], U[N - 1, 1] = f, u, f
+    assert np.max(np.abs(t["S"] - np.linalg.solve(D, L))) < 1e-14
+    assert np.max(np.abs(t["R"] - np.linalg.solve(D, U))) < 1e-14
+
+
+@pytest.mark.parametrize("bands", PENTA_BANDS)
+@pytest.mark.parametrize("p,n,cyclic", [(3, 10, True), (4, 8, True), (3, 12, False), (2, 9, True), (1, 11, True)])
+def test_penta_reduced_blocks_are_the_schur_complement(bands, p, n, cyclic):
+    """Eliminating every interior row of the assembled matrix leaves exactly the 2x2-block
+    tridiagonal reduced matrix [L^, D^, U^] (D^ of the first partition without L~R when
+    acyclic) -- the block-LU statement of P:254 with r = 2."""
+    Ntot = p * n
+    A = _dense_penta(Ntot, bands, cyclic)
+    iface = [i * n + k for i in range(p) for k in (0, 1)]
+    inter = [i for i in range(Ntot) if i not in iface]
+    Aii = A[np.ix_(iface, iface)]
+    Aij = A[np.ix_(iface, inter)]
+    Aji = A[np.ix_(inter, iface)]
+    Ajj = A[np.ix_(inter, inter)]
+    schur = Aii - Aij @ np.linalg.solve(Ajj, Aji)
+    t = pk.ctri_penta_factor_query(n, bands)
+    expect = np.zeros((2 * p, 2 * p))
+    for i in range(p):
+        expect[2 * i:2 * i + 2, 2 * i:2 * i + 2] += t["Dh"] if (cyclic or i > 0) else t["Dh_first"]
+        if cyclic or i > 0:
+            j = (i - 1) % p
+            expect[2 * i:2 * i + 2, 2 * j:2 * j + 2] += t["Lh"]
+        if cyclic or i < p - 1:
+            j = (i + 1) % p
+            expect[2 * i:2 * i + 2, 2 * j:2 * j + 2] += t["Uh"]
+    assert np.max(np.abs(schur - expect)) < 1e-13
+
+
+@pytest.mark.parametrize("bands", PENTA_BANDS)
+def test_penta_window(bands):
+    """Outside the window every |S|, |R| entry is <= 2^-64 (reading R15 with r = 2)."""
+    n = 2048
+    t = pk.ctri_penta_factor_query(n, bands)
+    W, N = t["window"], n - 2
+    assert 0 < W < N // 2
+    mid = slice(W, N - W)
+    assert np.max(np.abs(t["S"][mid])) <= 2.0 ** -64
+    assert np.max(np.abs(t["R"][mid])) <= 2.0 ** -64
+    assert max(np.max(np.abs(t["S"][W - 1])), np.max(np.abs(t["R"][N - W]))) > 2.0 ** -64
+
+
+def test_penta_singular_guard():
+    with pytest.raises(pk.CtriError, match="SINGULAR"):
+        pk.ctri_penta_factor_query(20, (0.0, 1.0, 1.0, 1.0, 0.0))  # mu_1 = d - l u / d = 0
