@@ -33,62 +33,102 @@ struct PentaArgs {
   double* planes4;    // [4][m]
   int closure, cyclic;
   double cinv[4];     // p == 1: 2x2 closure inverse (row-major)
+  int64_t k0c;        // LU factors are bitwise constant from interior row k0c on (plan-time)
+  double c_lam1, c_lam2, c_nu1, c_imu;
 };
 
-constexpr int kPentaRows = 8;  // rows per batch: 8 independent loads in flight per thread
+constexpr int kPentaRows = 8;  // rows per batch (window kernel)
+constexpr int kPB = 8;         // local solve: rows per register batch, next batch in flight
 
-__global__ void __launch_bounds__(128) k_penta_local(const PentaArgs A) {
+__global__ void __launch_bounds__(128, 4) k_penta_local(const PentaArgs A) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t m = A.outer * A.inner;
   if (j >= m) return;
   const int64_t o = j / A.inner, c = j - o * A.inner, st = A.inner;
   const int64_t N = A.n - 2;
-  const double* bc = A.b + o * A.n * st + c;
+  const double* bc = A.b + o * A.n * st + c + 2 * st;  // interior row 0
   double* xc = A.x + o * A.n * st + c;
+  double* xi = xc + 2 * st;
   const double* lam1 = A.lu;
   const double* lam2 = A.lu + N;
   const double* nu1 = A.lu + 2 * N;
   const double* imu = A.lu + 3 * N;
-  const double bt0 = bc[0], bt1 = bc[st];
-  // forward: z_k = b_k - lam1[k] z_{k-1} - lam2[k] z_{k-2}   (interior row k = slab row k + 2)
+  const double bt0 = A.b[o * A.n * st + c];
+  const double bt1 = A.b[(o * A.n + 1) * st + c];
+  const int64_t nb = (N + kPB - 1) / kPB;
+  // forward: z_k = b_k - lam1[k] z_{k-1} - lam2[k] z_{k-2}   (interior row k = slab row k + 2);
+  // software pipelined: batch i+1 is loaded before batch i is eliminated
+  double cur[kPB], nxt[kPB];
+#pragma unroll
+  for (int t = 0; t < kPB; ++t) cur[t] = t < N ? bc[t * st] : 0.0;
   double z1 = 0.0, z2 = 0.0;
-  for (int64_t k0 = 0; k0 < N; k0 += kPentaRows) {
-    double v[kPentaRows];
+  for (int64_t bi = 0; bi < nb; ++bi) {
+    const int64_t k0 = bi * kPB;
+    if (bi + 1 < nb) {
 #pragma unroll
-    for (int t = 0; t < kPentaRows; ++t)
-      if (k0 + t < N) v[t] = bc[(k0 + t + 2) * st];
+      for (int t = 0; t < kPB; ++t)
+        if (k0 + kPB + t < N) nxt[t] = bc[(k0 + kPB + t) * st];
+    }
+    if (k0 >= A.k0c && k0 + kPB <= N) {  // converged factors: scalars, no table loads
 #pragma unroll
-    for (int t = 0; t < kPentaRows; ++t) {
-      const int64_t k = k0 + t;
-      if (k < N) {
-        const double z = v[t] - __ldg(lam1 + k) * z1 - __ldg(lam2 + k) * z2;
-        xc[(k + 2) * st] = z;
+      for (int t = 0; t < kPB; ++t) {
+        const double z = cur[t] - A.c_lam1 * z1 - A.c_lam2 * z2;
+        xi[(k0 + t) * st] = z;
         z2 = z1;
         z1 = z;
       }
+    } else {
+#pragma unroll
+      for (int t = 0; t < kPB; ++t) {
+        const int64_t k = k0 + t;
+        if (k < N) {
+          const double z = cur[t] - __ldg(lam1 + k) * z1 - __ldg(lam2 + k) * z2;
+          xi[k * st] = z;
+          z2 = z1;
+          z1 = z;
+        }
+      }
     }
+#pragma unroll
+    for (int t = 0; t < kPB; ++t) cur[t] = nxt[t];
   }
-  // backward: y_k = (z_k - nu1[k] y_{k+1} - f y_{k+2}) / mu[k]
+  // backward: y_k = (z_k - nu1[k] y_{k+1} - f y_{k+2}) / mu[k], same pipelining
   double y1 = 0.0, y2 = 0.0, ylast = 0.0, ylast2 = 0.0;
-  const int64_t nb = (N + kPentaRows - 1) / kPentaRows;
+  {
+    const int64_t k0 = (nb - 1) * kPB;
+#pragma unroll
+    for (int t = 0; t < kPB; ++t) cur[t] = k0 + t < N ? xi[(k0 + t) * st] : 0.0;
+  }
   for (int64_t bi = nb - 1; bi >= 0; --bi) {
-    const int64_t k0 = bi * kPentaRows;
-    double v[kPentaRows];
+    const int64_t k0 = bi * kPB;
+    if (bi > 0) {
 #pragma unroll
-    for (int t = 0; t < kPentaRows; ++t)
-      if (k0 + t < N) v[t] = xc[(k0 + t + 2) * st];
+      for (int t = 0; t < kPB; ++t) nxt[t] = xi[(k0 - kPB + t) * st];
+    }
+    if (k0 >= A.k0c && k0 + kPB < N - 1) {  // converged factors, not the last two rows
 #pragma unroll
-    for (int t = kPentaRows - 1; t >= 0; --t) {
-      const int64_t k = k0 + t;
-      if (k < N) {
-        const double y = (v[t] - __ldg(nu1 + k) * y1 - A.f * y2) * __ldg(imu + k);
-        xc[(k + 2) * st] = y;
-        if (k == N - 1) ylast = y;
-        if (k == N - 2) ylast2 = y;
+      for (int t = kPB - 1; t >= 0; --t) {
+        const double y = (cur[t] - A.c_nu1 * y1 - A.f * y2) * A.c_imu;
+        xi[(k0 + t) * st] = y;
         y2 = y1;
         y1 = y;
       }
+    } else {
+#pragma unroll
+      for (int t = kPB - 1; t >= 0; --t) {
+        const int64_t k = k0 + t;
+        if (k < N) {
+          const double y = (cur[t] - __ldg(nu1 + k) * y1 - A.f * y2) * __ldg(imu + k);
+          xi[k * st] = y;
+          if (k == N - 1) ylast = y;
+          if (k == N - 2) ylast2 = y;
+          y2 = y1;
+          y1 = y;
+        }
+      }
     }
+#pragma unroll
+    for (int t = 0; t < kPB; ++t) cur[t] = nxt[t];
   }
   // y1 = y[0], y2 = y[1];  planes: c = b~ - U~ y_i[0..1], w = L~ y_i[N-2..N-1]
   const double c0 = bt0 - A.f * y1;
@@ -104,6 +144,135 @@ __global__ void __launch_bounds__(128) k_penta_local(const PentaArgs A) {
     A.planes4[m + j] = c1;
     A.planes4[2 * m + j] = w0;
     A.planes4[3 * m + j] = w1;
+  }
+}
+
+// Contiguous solve axis (inner == 1): a column's rows are contiguous, so the column-serial
+// thread-per-column walk would touch 32 columns n*8 bytes apart per warp access.  Blocks of
+// 32 rows x 128 columns are moved through shared memory instead: lane l of a warp loads row l
+// of 32 columns in turn (256-byte coalesced accesses), each thread then runs the recurrence on
+// its own column out of shared memory, and the block is written back the same way.
+constexpr int kPcRows = 32, kPcCols = 128, kPcPad = kPcRows + 1;
+
+__global__ void __launch_bounds__(kPcCols) k_penta_local_contig(const PentaArgs A) {
+  __shared__ double tile[kPcCols * kPcPad];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t col0 = (int64_t)blockIdx.x * kPcCols;
+  const int64_t mcols = A.outer;  // contiguous axis: one column per outer index
+  const int64_t n = A.n, N = n - 2;
+  const int64_t j = col0 + tid;
+  const bool valid = j < mcols;
+  const double* lam1 = A.lu;
+  const double* lam2 = A.lu + N;
+  const double* nu1 = A.lu + 2 * N;
+  const double* imu = A.lu + 3 * N;
+  double* mycol = tile + tid * kPcPad;
+  // move interior rows [k0, k0 + 32) of the CTA's columns between HBM and shared memory
+  // the next block is fetched into registers (32 loads in flight per thread) while the current
+  // one is eliminated out of shared memory
+  double reg[32];
+  auto fetch_block = [&](const double* src, int64_t k0) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int64_t cj = col0 + warp * 32 + i;
+      const int64_t k = k0 + lane;
+      reg[i] = (cj < mcols && k < N) ? src[cj * n + 2 + k] : 0.0;
+    }
+  };
+  auto put_block = [&]() {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) tile[(warp * 32 + i) * kPcPad + lane] = reg[i];
+  };
+  auto store_block = [&](int64_t k0) {
+    for (int i = 0; i < 32; ++i) {
+      const int cl = warp * 32 + i;
+      const int64_t cj = col0 + cl;
+      const int64_t k = k0 + lane;
+      if (cj < mcols && k < N) A.x[cj * n + 2 + k] = tile[cl * kPcPad + lane];
+    }
+  };
+  double bt0 = 0.0, bt1 = 0.0;
+  if (valid) {
+    bt0 = A.b[j * n];
+    bt1 = A.b[j * n + 1];
+  }
+  double z1 = 0.0, z2 = 0.0;
+  fetch_block(A.b, 0);
+  for (int64_t k0 = 0; k0 < N; k0 += kPcRows) {
+    put_block();
+    __syncthreads();
+    if (k0 + kPcRows < N) fetch_block(A.b, k0 + kPcRows);
+    if (valid) {
+      if (k0 >= A.k0c && k0 + kPcRows <= N) {  // converged factors
+#pragma unroll
+        for (int t = 0; t < kPcRows; ++t) {
+          const double z = mycol[t] - A.c_lam1 * z1 - A.c_lam2 * z2;
+          mycol[t] = z;
+          z2 = z1;
+          z1 = z;
+        }
+      } else {
+        for (int t = 0; t < kPcRows && k0 + t < N; ++t) {
+          const int64_t k = k0 + t;
+          const double z = mycol[t] - __ldg(lam1 + k) * z1 - __ldg(lam2 + k) * z2;
+          mycol[t] = z;
+          z2 = z1;
+          z1 = z;
+        }
+      }
+    }
+    __syncthreads();
+    store_block(k0);
+    __syncthreads();
+  }
+  double y1 = 0.0, y2 = 0.0, ylast = 0.0, ylast2 = 0.0;
+  const int64_t nb = (N + kPcRows - 1) / kPcRows;
+  fetch_block(A.x, (nb - 1) * kPcRows);
+  for (int64_t bi = nb - 1; bi >= 0; --bi) {
+    const int64_t k0 = bi * kPcRows;
+    put_block();
+    __syncthreads();
+    if (bi > 0) fetch_block(A.x, k0 - kPcRows);
+    if (valid) {
+      if (k0 >= A.k0c && k0 + kPcRows < N - 1) {  // converged factors, not the last two rows
+#pragma unroll
+        for (int t = kPcRows - 1; t >= 0; --t) {
+          const double y = (mycol[t] - A.c_nu1 * y1 - A.f * y2) * A.c_imu;
+          mycol[t] = y;
+          y2 = y1;
+          y1 = y;
+        }
+      } else {
+        for (int t = kPcRows - 1; t >= 0; --t) {
+          const int64_t k = k0 + t;
+          if (k >= N) continue;
+          const double y = (mycol[t] - __ldg(nu1 + k) * y1 - A.f * y2) * __ldg(imu + k);
+          mycol[t] = y;
+          if (k == N - 1) ylast = y;
+          if (k == N - 2) ylast2 = y;
+          y2 = y1;
+          y1 = y;
+        }
+      }
+    }
+    __syncthreads();
+    store_block(k0);
+    __syncthreads();
+  }
+  if (!valid) return;
+  const double c0 = bt0 - A.f * y1;
+  const double c1 = bt1 - (A.u * y1 + A.f * y2);
+  const double w0 = A.e * ylast2 + A.l * ylast;
+  const double w1 = A.e * ylast;
+  if (A.closure) {
+    const double h0 = c0 - (A.cyclic ? w0 : 0.0), h1 = c1 - (A.cyclic ? w1 : 0.0);
+    A.x[j * n] = A.cinv[0] * h0 + A.cinv[1] * h1;
+    A.x[j * n + 1] = A.cinv[2] * h0 + A.cinv[3] * h1;
+  } else {
+    A.planes4[j] = c0;
+    A.planes4[mcols + j] = c1;
+    A.planes4[2 * mcols + j] = w0;
+    A.planes4[3 * mcols + j] = w1;
   }
 }
 
@@ -239,8 +408,22 @@ cudaError_t launch_penta_local(const Plan& P, const double* b, double* x, cudaSt
   A.closure = P.p == 1 ? 1 : 0;
   A.cyclic = P.cyclic;
   std::memcpy(A.cinv, P.pcinv, sizeof(A.cinv));
+  const Penta& pt = P.pt;
+  const int64_t N = pt.N;
+  A.k0c = N;  // first row from which all four factors equal their last value bitwise
+  while (A.k0c > 0 && pt.lam1[A.k0c - 1] == pt.lam1[N - 1] && pt.lam2[A.k0c - 1] == pt.lam2[N - 1] &&
+         pt.nu1[A.k0c - 1] == pt.nu1[N - 1] && pt.inv_mu[A.k0c - 1] == pt.inv_mu[N - 1])
+    --A.k0c;
+  A.k0c = std::max<int64_t>(A.k0c, 2);  // rows 0, 1 have lam2 = 0 / lam1 = 0 by construction
+  A.c_lam1 = pt.lam1[N - 1];
+  A.c_lam2 = pt.lam2[N - 1];
+  A.c_nu1 = pt.nu1[N - 1];
+  A.c_imu = pt.inv_mu[N - 1];
   const int64_t m = P.lay.m();
-  k_penta_local<<<(unsigned)((m + 127) / 128), 128, 0, s>>>(A);
+  if (P.lay.inner == 1)
+    k_penta_local_contig<<<(unsigned)((m + kPcCols - 1) / kPcCols), kPcCols, 0, s>>>(A);
+  else
+    k_penta_local<<<(unsigned)((m + 127) / 128), 128, 0, s>>>(A);
   return cudaGetLastError();
 }
 
