@@ -46,9 +46,10 @@ def parse():
                     choices=["collocated", "staggered_deriv", "staggered_interp"],
                     help="cfg5 compact scheme: collocated derivative (P:65-67) or the staggered "
                          "sixth-order derivative / interpolation (P:202-206)")
-    ap.add_argument("--reduced", default="pcr", choices=["pcr", "allgather", "nccl"],
-                    help="nparts > 1 reduced system: fused P2P pairwise schedule (default), the "
-                         "P2P all-gather with A^-1 rows (N4), or host-issued NCCL rounds")
+    ap.add_argument("--reduced", default="pcr", choices=["pcr", "fused", "allgather", "nccl"],
+                    help="nparts > 1 reduced system: the P2P pairwise schedule kernel + window pass "
+                         "(default), fused into the tile kernel (opt-in), the P2P all-gather with "
+                         "A^-1 rows (N4), or host-issued NCCL rounds")
     ap.add_argument("--penta", action="store_true",
                     help="pentadiagonal system (r = 2, SURVEY N3) on the config's grid: Lele's "
                          "tenth-order compact LHS (1/20, 1/2, 1, 1/2, 1/20)")
@@ -268,7 +269,9 @@ def main():
         name = f"custom {dims} solve index {sd}"
     deriv = args.config == "cfg5"
     flags = CTRI_FLAG_TIMING | (CTRI_FLAG_DERIV if deriv else 0)
-    if world > 1 and args.reduced == "allgather":
+    if world > 1 and args.reduced == "fused":
+        flags |= ctri.CTRI_FLAG_FUSED_REDUCED
+    elif world > 1 and args.reduced == "allgather":
         flags |= ctri.CTRI_FLAG_ALLGATHER
     elif world > 1 and args.reduced == "nccl":
         flags |= ctri.CTRI_FLAG_NCCL_ROUNDS
@@ -412,6 +415,10 @@ def main():
                                      "back-substitution kernel; includes waiting for the slowest "
                                      "peer's local solve"}
                             if st["reduced_path"] in (1, 2) else
+                            {"fused_into_tile_kernel": True,
+                             "note": "(a2)-(a4) inside the local-solve kernel: LL all-gather of the "
+                                     "planes per tile, window rows finalised on chip one tile later"}
+                            if st["reduced_path"] == 3 else
                             {"y_exchange": yx, "stages": stage_us, "x_exchange": xx,
                              "backsub_kernel": back}) if p > 1 else None,
                 "clocks": sampler.summary() if sampler else None}

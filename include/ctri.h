@@ -65,6 +65,13 @@ typedef enum ctri_status {
 #define CTRI_FLAG_DERIV          (1u << 3) /* allocate halo planes so ctri_deriv may be called */
 #define CTRI_FLAG_NCCL_ROUNDS    (1u << 4) /* nparts > 1: host-issued NCCL rounds instead of the fused
                                               device-initiated P2P reduced phase */
+#define CTRI_FLAG_FUSED_REDUCED  (1u << 6) /* 2 <= nparts <= 8, real GPUs (not loopback), strided
+                                              tile path: run (a2)-(a4) INSIDE the local-solve tile
+                                              kernel (window rows kept on chip, planes all-gathered
+                                              as LL words, finalised one tile later).  Opt-in: on
+                                              B200 it measures slower than the separate P2P kernel
+                                              + window pass.  Ignored where
+                                              it does not apply. */
 #define CTRI_FLAG_ALLGATHER      (1u << 5) /* 2 <= nparts <= 8, P2P path: solve the reduced system with
                                               ONE all-gather round of 2 planes per rank and plan-time
                                               rows of A^{-1} (latency comparison for
@@ -97,7 +104,8 @@ typedef struct ctri_stats {
   int32_t tile_variant;         /* cluster-tile variant index (columns/threads/ring depth), -1 if none */
   int32_t tile_stages;          /* TMA shared-memory ring depth of the tile kernel */
   int32_t reduced_path;         /* nparts > 1: 0 = NCCL rounds, 1 = fused P2P kernel (t_backsub_us
-                                   then times the whole fused (a2)-(a4) kernel), 2 = P2P all-gather */
+                                   then times the whole fused (a2)-(a4) kernel), 2 = P2P all-gather,
+                                   3 = fused into the local-solve tile kernel (t_local_us = all) */
   int32_t device_error;         /* nonzero: a P2P wait hit its deadline (peer missing) */
   int32_t vparts;               /* nparts == 1: partitions of the slab solved on this GPU (the
                                    paper's partition method; (a2)-(a4) then run on-device) */

@@ -80,6 +80,7 @@ void free_plan(Plan* P) {
   if (P->d_err) cudaFree(P->d_err);
   if (P->d_epoch) cudaFree(P->d_epoch);
   if (P->d_trace) cudaFree(P->d_trace);
+  if (P->d_fctr) cudaFree(P->d_fctr);
   if (P->comm) ncclCommDestroy(P->comm);
   delete P;
 }
@@ -195,12 +196,31 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
       return fail((ctri_status)fe.code, fe.detail);
     P->allgather = true;
   }
+  // (a2)-(a4) fused into the tile kernel (real GPUs; the loopback group cannot co-schedule one
+  // kernel per rank): window rows stashed on chip, planes all-gathered as LL words
+  P->fused = (flags & CTRI_FLAG_FUSED_REDUCED) && p > 1 && p <= 8 && !P->loopback &&
+             P->local_kernel == 1 && P->tile.fused_ok &&
+             !(flags & (CTRI_FLAG_NCCL_ROUNDS | CTRI_FLAG_FULL_BACKSUB | CTRI_FLAG_ALLGATHER));
+  if (P->fused) {
+    std::vector<double> inv;
+    if (!reduced_inverse(p, cyclic != 0, L, D, U, pivot_threshold(P->bands), &inv, &fe))
+      return fail((ctri_status)fe.code, fe.detail);
+    const int nx = rank + 1;
+    for (int r = 0; r < p; ++r) {
+      P->fg0[r] = inv[(size_t)rank * p + r];
+      P->fg1[r] = (nx < p || cyclic) ? inv[(size_t)(nx % p) * p + r] : 0.0;
+    }
+    CUDA_TRY(cudaMalloc(&P->d_fctr, 2 * sizeof(unsigned int)));
+    CUDA_TRY(cudaMemsetAsync(P->d_fctr, 0, 2 * sizeof(unsigned int), s));
+    P->p2p_off = (int64_t)8 * p * m;  // [2 copies][2 planes][p rows][m] LL words
+  }
   if (p > 1 && p <= kMaxP2PRanks && !(flags & CTRI_FLAG_NCCL_ROUNDS)) {
-    // fused device-initiated reduced phase: double-buffered mailbox + epoch flags
+    // device-initiated reduced phase: double-buffered mailbox + epoch flags
     const int q = (int)P->sched.steps.size();
     P->p2p_nslices = p2p_slices(m, P->loopback ? p : 1, P->num_sms, P->allgather ? 1 : 0);
     P->mbox_bytes = sizeof(unsigned long long) *
-                    p2p_mailbox_words(p2p_copy_words(m, q, p, P->allgather), m, (flags & CTRI_FLAG_DERIV) != 0);
+                    ((size_t)P->p2p_off +
+                     p2p_mailbox_words(p2p_copy_words(m, q, p, P->allgather), m, (flags & CTRI_FLAG_DERIV) != 0));
     CUDA_TRY(cudaMalloc(&P->mbox_alloc, P->mbox_bytes));
     CUDA_TRY(cudaMemsetAsync(P->mbox_alloc, 0, P->mbox_bytes, s));
     CUDA_TRY(cudaMalloc(&P->d_err, sizeof(int)));
@@ -222,7 +242,7 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   }
   // launches per solve
   int launches = 1;
-  if (p > 1) launches += P->p2p ? 2 /*reduced + window*/ : 1 /*bhat*/ + P->gpcr.stages + 1 /*backsub*/;
+  if (p > 1 && !P->fused) launches += P->p2p ? 2 /*reduced + window*/ : 1 /*bhat*/ + P->gpcr.stages + 1 /*backsub*/;
   if (p == 1 && P->vp > 1) launches += 2;  // local reduced system; window back-substitution
   P->launches_per_solve = launches;
   CUDA_TRY(cudaStreamSynchronize(s));
@@ -350,13 +370,14 @@ void p2p_fill_rank(const Plan& P, double* x, P2PRank* R) {
   R->xnext = P.r == 2 ? P.d_xnext2 : P.xt_next;
   R->planes4 = P.d_planes4;
   R->ainv = P.d_ainv;
-  R->mbox = reinterpret_cast<unsigned long long*>(P.mbox_alloc);
+  R->mbox = reinterpret_cast<unsigned long long*>(P.mbox_alloc) + P.p2p_off;
   R->epoch = P.d_epoch;
   R->f = nullptr;
   R->halo_lo = P.halo_lo;
   R->halo_hi = P.halo_hi;
   for (int r = 0; r < kMaxP2PRanks; ++r) R->peer_mbox[r] = nullptr;
-  for (int r = 0; r < P.p; ++r) R->peer_mbox[r] = reinterpret_cast<unsigned long long*>(P.peer_alloc[r]);
+  for (int r = 0; r < P.p; ++r)
+    R->peer_mbox[r] = reinterpret_cast<unsigned long long*>(P.peer_alloc[r]) + P.p2p_off;
   for (int r = 0; r < kMaxAG; ++r) {
     R->ag0[r] = R->ag1[r] = 0.0;
     if (!P.allgather || r >= P.p) continue;
@@ -539,6 +560,11 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
   record(P0, EV_START, s);
   for (size_t r = 0; r < G.size(); ++r) TRY(local_phase(*G[r], b[r], x[r], s, st));
   record(P0, EV_LOCAL, s);
+  if (P0.fused && !st) {  // (a2)-(a4) ran inside the tile kernel
+    record(P0, EV_BACK, s);
+    for (Plan* P : G) P->timed_valid = !P->ev.empty();
+    return CTRI_OK;
+  }
   if (P0.p == 1) {
     if (P0.vp > 1) {  // (a2)-(a4) across the virtual partitions of this slab
       for (size_t r = 0; r < G.size(); ++r) {
@@ -940,7 +966,7 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
   out->tile_columns = P->local_kernel ? P->tile.C : 1;
   out->tile_variant = P->local_kernel ? P->tile.variant : -1;
   out->tile_stages = P->local_kernel ? P->tile.STAGES : 0;
-  out->reduced_path = (P->p > 1 && P->p2p) ? ((P->allgather || P->r == 2) ? 2 : 1) : 0;
+  out->reduced_path = P->fused ? 3 : (P->p > 1 && P->p2p) ? ((P->allgather || P->r == 2) ? 2 : 1) : 0;
   out->band_halfwidth = P->r;
   out->vparts = P->vp;
   out->grid_ctas = P->local_kernel ? P->tile.grid : (int32_t)((P->tlay.m() + 127) / 128);

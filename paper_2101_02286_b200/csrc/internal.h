@@ -96,6 +96,17 @@ struct TileArgs {
   const double* halo_lo;  // [2][m]: rows n-2, n-1 of the slab above
   const double* halo_hi;  // [2][m]: rows 0, 1 of the slab below
   unsigned long long* trace;  // measurement only (CTRI_TILE_TRACE)
+  // fused reduced phase (LAYOUT 3, nparts > 1): the window rows of every tile stay
+  // in shared memory while the tile's (c = b~ - u y_D[1], y_D[n-1]) go to every rank's mailbox
+  // as LL words; one tile later x~_i, x~_{i+1} = rows i, i+1 of A^{-1} applied to the gathered
+  // b^ (reading R21), and the window rows are corrected (Eq. xi_app) and stored once.
+  int f_P, f_row, f_W, f_srw, f_cyclic;  // reduced rows, this rank's row, window, stash rows/slot
+  unsigned long long* f_peer[8];         // every rank's fused mailbox (own included)
+  int64_t f_m;                           // plane length (batch columns)
+  double f_g0[8], f_g1[8];               // rows f_row and f_row + 1 of A^{-1}
+  const double *f_S, *f_R;               // slab-level S_i, R_i (n - 1)
+  unsigned int *f_epoch, *f_done;        // device epoch of the solve, CTA completion count
+  int* f_err;                            // deadline error word
 };
 
 struct TileConfig {
@@ -110,6 +121,8 @@ struct TileConfig {
   int grid = 0;  // CTAs launched (multiple of G)
   bool deriv_ok = false;               // fused-stencil instantiation configured
   int smem_deriv = 0, grid_deriv = 0;
+  bool fused_ok = false;               // fused reduced-phase instantiation configured (LAYOUT 3)
+  int smem_fused = 0, grid_fused = 0, fused_srw = 0;
   std::vector<double> consts;  // serialized TileConsts<K> (l, u, then 4 tables of K-1)
   PcrTables pcr;
   double* d_pcr = nullptr;     // device: alpha | gamma | inv
@@ -207,6 +220,10 @@ struct Plan {
   bool allgather = false;         // CTRI_FLAG_ALLGATHER: reduced system by A^{-1} rows
   std::vector<double> ainv;       // [p][p] A^{-1} (all-gather mode)
   int p2p_nslices = 0;
+  bool fused = false;                  // (a2)-(a4) fused into the tile kernel (LAYOUT 3)
+  double fg0[8] = {0}, fg1[8] = {0};   // fused: rows rank, rank + 1 of A^{-1}
+  unsigned int* d_fctr = nullptr;      // fused: [epoch, CTA completion count]
+  int64_t p2p_off = 0;                 // words before the P2P-kernel region of the mailbox
   void* mbox_alloc = nullptr;          // own LL mailbox (cudaMalloc, IPC-exported)
   unsigned int* d_epoch = nullptr;     // per-slice solve epochs of the fused P2P kernel
   size_t mbox_bytes = 0;

@@ -74,6 +74,19 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(policy)
       : "memory");
 }
+// TMA tensor store shared -> global (bulk-group completion), and its waits
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1,
+                                             int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -102,6 +115,49 @@ __device__ __forceinline__ void st_global_cs_v4(double* p, double a, double b, d
 }
 __device__ __forceinline__ void st_global_cs(double* p, double v) {
   asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// ---- LL words (csrc/p2p.cu header): an fp64 value travels as two 8-byte words
+//      {32-bit half, 32-bit epoch} written by ONE 16-byte store; an 8-byte word is single-copy
+//      atomic, so a reader that sees the epoch in both words has the value (no fence, no flag).
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void ll_store(unsigned long long* dst, double v, uint32_t ep) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+  const unsigned long long w0 = ((unsigned long long)ep << 32) | (bits & 0xffffffffull);
+  const unsigned long long w1 = ((unsigned long long)ep << 32) | (bits >> 32);
+  asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(dst), "l"(w0), "l"(w1)
+               : "memory");
+}
+__device__ __forceinline__ void ll_load(const unsigned long long* src, unsigned long long* w0,
+                                        unsigned long long* w1) {
+  asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(*w0), "=l"(*w1) : "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ bool ll_ready(unsigned long long w0, unsigned long long w1, uint32_t ep) {
+  return (uint32_t)(w0 >> 32) == ep && (uint32_t)(w1 >> 32) == ep;
+}
+__device__ __forceinline__ double ll_value(unsigned long long w0, unsigned long long w1) {
+  return __longlong_as_double((long long)((w1 << 32) | (w0 & 0xffffffffull)));
+}
+// spin until the word pair carries `ep`; false after `deadline` (%globaltimer ns)
+__device__ __forceinline__ bool ll_wait(const unsigned long long* src, uint32_t ep,
+                                        unsigned long long deadline, double* out) {
+  unsigned long long w0, w1;
+  int spins = 0;
+  while (true) {
+    ll_load(src, &w0, &w1);
+    if (ll_ready(w0, w1, ep)) break;
+    if (++spins == 64) {
+      spins = 0;
+      if (globaltimer_ns() > deadline) return false;
+    }
+  }
+  *out = ll_value(w0, w1);
+  return true;
 }
 }  // namespace dev
 

@@ -41,11 +41,14 @@ namespace ctri {
 template <int K, int C, int NT, int SUB, int SLOTS, int MINB, int LAYOUT>
 __global__ void __launch_bounds__(NT, MINB)
     k_tile(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap hmap,
-           const TileArgs A, const TileConsts<K> T) {
+           const __grid_constant__ CUtensorMap xmap, const TileArgs A, const TileConsts<K> T) {
   // LAYOUT 0: strided solve axis; 1: contiguous solve axis; 2: strided + fused compact-derivative
   // RHS stencil (a0): the kernel reads f, forms b in registers and never writes it
+  // LAYOUT 3: strided + fused reduced phase (nparts > 1): window rows stashed in shared memory,
+  // planes to every rank's mailbox as LL words, finalised one tile later (TileArgs f_*)
   constexpr bool CONTIG = (LAYOUT == 1);
   constexpr bool DERIV = (LAYOUT == 2);
+  constexpr bool FUSED = (LAYOUT == 3);
   constexpr int HALO = DERIV ? 2 : 0;     // stencil half-width (rows)
   static_assert(K >= 4 && NT % C == 0 && (C == 4 || C == 8 || C == 16 || C == 32), "tile geometry");
   static_assert(!CONTIG || (NT / C == 32 && SUB == 1 && SLOTS == 1), "contiguous: 32 chunks/CTA");
@@ -81,6 +84,11 @@ __global__ void __launch_bounds__(NT, MINB)
   uint64_t* mbar = reinterpret_cast<uint64_t*>(tab ? s_inv + Q : s_alpha);  // [SLOTS] ring, ex, rx
   uint64_t* mbar_ex = mbar + SLOTS;
   uint64_t* mbar_rx = mbar_ex + 1;
+  // FUSED: [2][f_srw][C] window rows (128-byte aligned: TMA-store source)
+  double* f_stash = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(mbar_rx + 1) + 127) & ~static_cast<uintptr_t>(127));
+  double* f_red = FUSED ? f_stash + (size_t)2 * A.f_srw * C : nullptr;  // [2][NT] partial x~
+  double* f_sr = FUSED ? f_red + 2 * NT : nullptr;  // [2][f_srw]: S, R of the stashed rows
 
   const int tid = threadIdx.x;
   // strided axis: lanes run over the C columns of a tile row (coalesced rows);
@@ -188,12 +196,114 @@ __global__ void __launch_bounds__(NT, MINB)
     if (tr && tid == 0 && it_ < 64) {
       unsigned long long tt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
-      tr[it_ * 8 + k] = tt;
+      tr[it_ * 16 + k] = tt;
     }
   };
   int it = 0;
+  // ---- fused reduced phase (FUSED): roles, epoch, finalisation of a previous tile ----
+  const bool f_top = FUSED && g == 0;
+  const bool f_bot = FUSED && (int)g == G - 1;
+  const int64_t f_n = A.lay.n;
+  const int f_W = FUSED ? A.f_W : 0;
+  const int f_bbase = (G == 1) ? f_W + 1 : 0;  // stash row of slab row n - W - 1
+  const int64_t f_b0 = f_n - f_W - 1;           // first stashed row of the bottom block
+  uint32_t f_ep = 0;
+  unsigned long long f_deadline = 0;
+  if (FUSED) {
+    f_ep = *reinterpret_cast<volatile unsigned int*>(A.f_epoch) + 1u;
+    f_deadline = dev::globaltimer_ns() + 20ull * 1000000000ull;
+    // slab-level S, R of the rows this CTA stashes (stash row index -> slab row)
+    for (int i = tid; i < A.f_srw; i += NT) {
+      int64_t r = -1;
+      if (f_top && i <= f_W) r = i;
+      else if (f_bot && i >= f_bbase && i <= f_bbase + f_W) r = f_b0 + (i - f_bbase);
+      f_sr[i] = (r >= 1) ? A.f_S[r - 1] : 0.0;
+      f_sr[A.f_srw + i] = (r >= 1) ? A.f_R[r - 1] : 0.0;
+    }
+    __syncthreads();
+  }
+  // plane q, reduced row r, column jo of the current epoch copy (LL words: 2 per value)
+  auto f_word = [&](int q, int r, int64_t jo) -> int64_t {
+    return 2 * (((int64_t)(f_ep & 1u) * 2 * A.f_P + (int64_t)q * A.f_P + r) * A.f_m + jo);
+  };
+  unsigned long long f_w[4] = {0, 0, 0, 0};  // prefetched LL words of the tile to finalise
+  auto f_prefetch = [&](int64_t tp) {
+    const int64_t op = tp / A.tiles_per_outer;
+    const int64_t cj = (tp - op * A.tiles_per_outer) * C + (tid % C);
+    const int kg = tid / C;
+    if (cj < A.lay.inner && kg < A.f_P) {
+      const int64_t jo = op * A.lay.inner + cj;
+      const unsigned long long* mb = A.f_peer[A.f_row];
+      dev::ll_load(mb + f_word(0, kg, jo), &f_w[0], &f_w[1]);
+      if (A.f_cyclic || kg > 0) dev::ll_load(mb + f_word(1, (kg + A.f_P - 1) % A.f_P, jo), &f_w[2], &f_w[3]);
+    }
+  };
+  // x~_i, x~_{i+1} of tile tp for every column, then Eq. xi_app on its stashed window rows
+  auto f_finalize = [&](int64_t tp, int slotp) {
+    stamp(it, 8);
+    if (tid == 0) dev::bulk_wait_read_all();  // the previous TMA store has read its stash slot
+    const int64_t op = tp / A.tiles_per_outer;
+    const int64_t colp = (tp - op * A.tiles_per_outer) * C;
+    const int kg = tid / C;
+    const int64_t cj = colp + (tid % C);
+    double a0 = 0.0, a1 = 0.0;
+    if (cj < A.lay.inner && kg < A.f_P) {
+      const int64_t jo = op * A.lay.inner + cj;
+      const unsigned long long* mb = A.f_peer[A.f_row];
+      double ck = 0.0, ylp = 0.0;
+      bool ok = true;
+      if (dev::ll_ready(f_w[0], f_w[1], f_ep)) ck = dev::ll_value(f_w[0], f_w[1]);
+      else ok = dev::ll_wait(mb + f_word(0, kg, jo), f_ep, f_deadline, &ck);
+      const bool lft = A.f_cyclic || kg > 0;
+      if (lft && ok) {
+        if (dev::ll_ready(f_w[2], f_w[3], f_ep)) ylp = dev::ll_value(f_w[2], f_w[3]);
+        else ok = dev::ll_wait(mb + f_word(1, (kg + A.f_P - 1) % A.f_P, jo), f_ep, f_deadline, &ylp);
+      }
+      if (!ok) atomicExch(A.f_err, 1);
+      const double bh = ck - (lft ? T.l * ylp : 0.0);  // Eq. bi_hat
+      a0 = A.f_g0[kg] * bh;
+      a1 = A.f_g1[kg] * bh;
+    }
+    stamp(it, 9);
+    f_red[tid] = a0;
+    f_red[NT + tid] = a1;
+    __syncthreads();
+    stamp(it, 10);
+    const int64_t colj = colp + j;
+    if (colj < A.lay.inner) {
+      double xa = 0.0, xb = 0.0;
+#pragma unroll
+      for (int q = 0; q < NT / C; ++q) {  // fixed order: deterministic
+        xa += f_red[q * C + j];
+        xb += f_red[NT + q * C + j];
+      }
+      double* stp = f_stash + (size_t)slotp * A.f_srw * C;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int64_t r = (int64_t)c * K + k;
+        int si = -1;
+        if (f_top && r <= f_W) si = (int)r;
+        else if (f_bot && r >= f_b0) si = f_bbase + (int)(r - f_b0);
+        if (si >= 0) {  // Eq. xi_app on the window (R15), in place; row 0 is x~_i
+          const double y = stp[si * C + j];
+          stp[si * C + j] = (r == 0) ? xa : y - f_sr[si] * xa - f_sr[A.f_srw + si] * xb;
+        }
+      }
+    }
+    dev::fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA store
+    __syncthreads();
+    if (tid == 0) {  // the corrected window blocks go out through TMA (off the LSU store path)
+      const uint32_t sb = dev::smem_u32(f_stash + (size_t)slotp * A.f_srw * C);
+      if (f_top) dev::tma_store_3d(&xmap, sb, (int)colp, 0, (int)op);
+      if (f_bot) dev::tma_store_3d(&xmap, sb + (uint32_t)(f_bbase * C * 8), (int)colp, (int)f_b0, (int)op);
+      dev::bulk_commit();
+    }
+    stamp(it, 11);
+  };
+
   for (int64_t t = first; t < A.num_tiles; t += ncl, ++it) {
     stamp(it, 0);
+    if (FUSED && (f_top || f_bot) && it > 0) f_prefetch(t - ncl);
     const int64_t seq = (int64_t)it * SUB + hsub;
     const int s = (int)(seq % SLOTS);
     // global column: strided axis (o, col) with col < inner; contiguous axis column = o
@@ -277,6 +387,17 @@ __global__ void __launch_bounds__(NT, MINB)
     auto store_chunk = [&]() {
       if (!valid) return;
       double* xp = A.x + (o * A.lay.n + (int64_t)c * K) * A.lay.inner + col;
+      if (FUSED) {  // window rows wait in shared memory for x~ (finalised one tile later)
+        double* stp = f_stash + (size_t)(it & 1) * A.f_srw * C;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int64_t r = (int64_t)c * K + k;
+          if (f_top && r <= f_W) stp[r * C + j] = v[k];
+          else if (f_bot && r >= f_b0) stp[(f_bbase + (int)(r - f_b0)) * C + j] = v[k];
+          else dev::st_global_cs(xp + (int64_t)k * A.lay.inner, v[k]);
+        }
+        return;
+      }
       if (CONTIG) {
 #pragma unroll
         for (int k = 0; k < K; k += 4) dev::st_global_cs_v4(xp + k, v[k], v[k + 1], v[k + 2], v[k + 3]);
@@ -308,6 +429,8 @@ __global__ void __launch_bounds__(NT, MINB)
     dev::st_async_f64(r_bt, btv, r_exbar);
     dev::st_async_f64(r_yf, v[1], r_exbar);
     dev::st_async_f64(r_yl, v[K - 1], r_exbar);
+    // FUSED: finalise the previous tile while the cluster exchange is in flight
+    if (FUSED && (f_top || f_bot) && it > 0) f_finalize(t - ncl, (it - 1) & 1);
     // ---- owner: head system b^_c (Eq. bi_hat at chunk level), then PCR stages ----
     {
       dev::mbar_wait(dev::smem_u32(mbar_ex), (uint32_t)it & 1u);
@@ -346,7 +469,15 @@ __global__ void __launch_bounds__(NT, MINB)
     for (int k = 1; k < K; ++k) v[k] = v[k] - T.S[k - 1] * xa - T.R[k - 1] * xb;
     store_chunk();
     stamp(it, 6);
-    if (valid) {
+    if (valid && FUSED) {  // (a2) planes of this tile -> every rank's mailbox (all-gather, R21)
+      const int64_t jo = o * A.lay.inner + col;
+      if (c == 0) {
+        const double cv = btv - T.u * v[1];  // c_i = b~_i - u y_i[first]
+        for (int r = 0; r < A.f_P; ++r) dev::ll_store(A.f_peer[r] + f_word(0, A.f_row, jo), cv, f_ep);
+      }
+      if (c == Q - 1)
+        for (int r = 0; r < A.f_P; ++r) dev::ll_store(A.f_peer[r] + f_word(1, A.f_row, jo), v[K - 1], f_ep);
+    } else if (valid) {
       if (A.mode == 1) {
         const int64_t pj = o * A.lay.inner + col;
         if (c == 0) {
@@ -354,6 +485,22 @@ __global__ void __launch_bounds__(NT, MINB)
           A.plane_bt[pj] = btv;
         }
         if (c == Q - 1) A.plane_yl[pj] = v[K - 1];
+      }
+    }
+  }
+  if (FUSED) {
+    if ((f_top || f_bot) && it > 0) {  // the last tile of this cluster
+      const int64_t tl = first + (int64_t)(it - 1) * ncl;
+      f_prefetch(tl);
+      f_finalize(tl, (it - 1) & 1);
+    }
+    if (tid == 0) dev::bulk_wait_all();  // TMA stores complete before the CTA's smem goes away
+    __syncthreads();
+    if (tid == 0) {  // the last CTA to finish publishes the epoch for the next solve
+      const unsigned int prev = atomicAdd(A.f_done, 1u);
+      if (prev == gridDim.x - 1) {
+        *A.f_done = 0u;
+        *A.f_epoch = f_ep;
       }
     }
   }
@@ -407,7 +554,8 @@ static void fill_consts(const TileConfig& tc, TileConsts<K>* T) {
 
 template <int K, int C, int NT, int SB, int S, int M, int LY>
 static cudaError_t launch_one(const TileConfig& tc, const CUtensorMap& map, const CUtensorMap& hmap,
-                              const TileArgs& A, cudaStream_t s, bool configure_only) {
+                              const CUtensorMap& xmap, const TileArgs& A, cudaStream_t s,
+                              bool configure_only) {
   auto fn = k_tile<K, C, NT, SB, S, M, LY>;
   if (configure_only) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc.smem_bytes);
@@ -416,9 +564,9 @@ static cudaError_t launch_one(const TileConfig& tc, const CUtensorMap& map, cons
   TileConsts<K> T;
   fill_consts<K>(tc, &T);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(LY == 2 ? tc.grid_deriv : tc.grid, 1, 1);
+  cfg.gridDim = dim3(LY == 2 ? tc.grid_deriv : LY == 3 ? tc.grid_fused : tc.grid, 1, 1);
   cfg.blockDim = dim3(NT, 1, 1);
-  cfg.dynamicSmemBytes = LY == 2 ? tc.smem_deriv : tc.smem_bytes;
+  cfg.dynamicSmemBytes = LY == 2 ? tc.smem_deriv : LY == 3 ? tc.smem_fused : tc.smem_bytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -427,7 +575,7 @@ static cudaError_t launch_one(const TileConfig& tc, const CUtensorMap& map, cons
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, fn, map, hmap, A, T);
+  return cudaLaunchKernelEx(&cfg, fn, map, hmap, xmap, A, T);
 }
 
 template <int K, int C, int NT, int SB, int S, int M, int LY>
@@ -437,23 +585,33 @@ static const void* fn_ptr() {
 
 template <int C, int NT, int SB, int S, int M, int LY>
 static cudaError_t dispatch_k(const TileConfig& tc, const CUtensorMap& map, const CUtensorMap& hmap,
-                              const TileArgs& A, cudaStream_t s, bool cfg_only, const void** fp) {
+                              const CUtensorMap& xmap, const TileArgs& A, cudaStream_t s, bool cfg_only,
+                              const void** fp) {
   switch (tc.K) {
 #define CTRI_K(KK)                                                       \
   case KK:                                                               \
     if (fp) *fp = fn_ptr<KK, C, NT, SB, S, M, LY>();                      \
-    return fp ? cudaSuccess : launch_one<KK, C, NT, SB, S, M, LY>(tc, map, hmap, A, s, cfg_only);
+    return fp ? cudaSuccess : launch_one<KK, C, NT, SB, S, M, LY>(tc, map, hmap, xmap, A, s, cfg_only);
     CTRI_K(4) CTRI_K(8) CTRI_K(16) CTRI_K(32)
 #undef CTRI_K
   }
   return cudaErrorInvalidValue;
 }
 
-static cudaError_t dispatch(const TileConfig& tc, bool deriv, const CUtensorMap& map,
-                            const CUtensorMap& hmap, const TileArgs& A, cudaStream_t s,
-                            bool cfg_only, const void** fp = nullptr) {
-#define CTRI_V(C, NT, SB, S, M, LY) return dispatch_k<C, NT, SB, S, M, LY>(tc, map, hmap, A, s, cfg_only, fp)
-  if (deriv) {  // fused stencil: strided whole-tile variants with 16 or 32 columns
+// kind 0: solve; 2: fused stencil + solve; 3: solve with the fused reduced phase (nparts > 1)
+static cudaError_t dispatch(const TileConfig& tc, int kind, const CUtensorMap& map,
+                            const CUtensorMap& hmap, const CUtensorMap& xmap, const TileArgs& A,
+                            cudaStream_t s, bool cfg_only, const void** fp = nullptr) {
+#define CTRI_V(C, NT, SB, S, M, LY) return dispatch_k<C, NT, SB, S, M, LY>(tc, map, hmap, xmap, A, s, cfg_only, fp)
+  if (kind == 3) {  // fused reduced phase: strided whole-tile variants
+    switch (tc.variant) {
+      case 0: CTRI_V(16, 512, 1, 1, 1, 3);
+      case 4: CTRI_V(16, 256, 1, 1, 2, 3);
+      case 13: CTRI_V(32, 256, 1, 1, 2, 3);
+    }
+    return cudaErrorInvalidValue;
+  }
+  if (kind == 2) {  // fused stencil: strided whole-tile variants with 16 or 32 columns
     switch (tc.variant) {
       case 0: CTRI_V(16, 512, 1, 1, 1, 2);
       case 4: CTRI_V(16, 256, 1, 1, 2, 2);
@@ -582,11 +740,11 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
   tc.smem_bytes = (int)(sizeof(double) * ((size_t)V.SLOTS * ring + 7 * (size_t)V.NT + tables) +
                         8 * (V.SLOTS + 2));
   // configure one instantiation (solve, or the fused-stencil one): smem attribute + grid
-  auto setup = [&](bool deriv, int smem, int* grid_out) -> bool {
+  auto setup = [&](int kind, int smem, int* grid_out) -> bool {
     const void* fn = nullptr;
     CUtensorMap dummy;
     TileArgs dA;
-    dispatch(tc, deriv, dummy, dummy, dA, 0, true, &fn);
+    dispatch(tc, kind, dummy, dummy, dummy, dA, 0, true, &fn);
     if (!fn || cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
       cudaGetLastError();
       *why = "cudaFuncSetAttribute(smem) failed";
@@ -620,7 +778,7 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
     *grid_out = (int)(std::min<int64_t>(nclusters, num_tiles) * G);
     return true;
   };
-  if (!setup(false, tc.smem_bytes, &tc.grid)) return false;
+  if (!setup(0, tc.smem_bytes, &tc.grid)) return false;
   // fused-stencil instantiation (ctri_deriv): 4 extra ring rows per stage
   tc.deriv_ok = false;
   if (!V.contig && V.C >= 16 && V.SUB == 1 && (vi == 0 || vi == 4 || vi == 13) &&
@@ -628,8 +786,24 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
     tc.smem_deriv = tc.smem_bytes + (int)(sizeof(double) * 4 * V.C * V.SLOTS);
     std::string w2;
     std::swap(w2, *why);
-    tc.deriv_ok = setup(true, tc.smem_deriv, &tc.grid_deriv);
+    tc.deriv_ok = setup(2, tc.smem_deriv, &tc.grid_deriv);
     std::swap(w2, *why);
+  }
+  // fused reduced-phase instantiation (nparts > 1): a 2-slot stash of the window rows
+  tc.fused_ok = false;
+  if (!V.contig && V.SUB == 1 && (vi == 0 || vi == 4 || vi == 13) && P.p > 1 && P.vp == 1 &&
+      P.window > 0) {
+    const int64_t W = P.window;
+    const int srw = (int)(G == 1 ? 2 * (W + 1) : W + 1);
+    if (W + 1 <= 256 && ((G == 1 && 2 * (W + 1) <= L.n) || (G > 1 && W + 1 <= rows_cta))) {
+      tc.fused_srw = srw;
+      tc.smem_fused = tc.smem_bytes + 128 +
+                      (int)(sizeof(double) * (2 * (size_t)srw * V.C + 2 * (size_t)V.NT + 2 * (size_t)srw));
+      std::string w2;
+      std::swap(w2, *why);
+      tc.fused_ok = setup(3, tc.smem_fused, &tc.grid_fused);
+      std::swap(w2, *why);
+    }
   }
   tc.ok = true;
   return true;
@@ -719,7 +893,7 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   A.trace = nullptr;
   if (std::getenv("CTRI_TILE_TRACE")) {  // measurement only
     static unsigned long long* d_tr = nullptr;
-    if (!d_tr) cudaMalloc(&d_tr, 64 * 8 * sizeof(unsigned long long));
+    if (!d_tr) cudaMalloc(&d_tr, 64 * 16 * sizeof(unsigned long long));
     A.trace = d_tr;
   }
   A.pcr_alpha = tc.d_pcr;
@@ -733,19 +907,61 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   // partition they are this slab's own rows (periodic wrap), packed into send_hi / send_lo
   A.halo_lo = (P.p == 1) ? P.send_hi : P.halo_lo;
   A.halo_hi = (P.p == 1) ? P.send_lo : P.halo_hi;
-  cudaError_t e = dispatch(tc, deriv, map, hmap, A, s, false);
+  const bool fused = !deriv && P.fused;
+  if (fused) {
+    A.f_P = P.p;
+    A.f_row = P.rank;
+    A.f_W = (int)P.window;
+    A.f_srw = tc.fused_srw;
+    A.f_cyclic = P.cyclic;
+    for (int r = 0; r < 8; ++r) {
+      A.f_peer[r] = (r < P.p) ? reinterpret_cast<unsigned long long*>(P.peer_alloc[r]) : nullptr;
+      A.f_g0[r] = (r < P.p) ? P.fg0[r] : 0.0;
+      A.f_g1[r] = (r < P.p) ? P.fg1[r] : 0.0;
+    }
+    A.f_m = P.lay.m();
+    A.f_S = P.d_S;
+    A.f_R = P.d_R;
+    A.f_epoch = P.d_fctr;
+    A.f_done = P.d_fctr + 1;
+    A.f_err = P.d_err;
+  }
+  CUtensorMap xmap;
+  std::memset(&xmap, 0, sizeof(xmap));
+  if (fused) {  // output map for the TMA store of the finalised window blocks (W+1 rows)
+    const Layout& L2 = P.tlay;
+    cuuint64_t gdim[3] = {(cuuint64_t)L2.inner, (cuuint64_t)L2.n, (cuuint64_t)L2.outer};
+    cuuint64_t gstride[2] = {(cuuint64_t)L2.inner * 8, (cuuint64_t)(L2.n * L2.inner * 8)};
+    cuuint32_t box[3] = {(cuuint32_t)tc.C, (cuuint32_t)(P.window + 1), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult cr = enc(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, x, gdim, gstride, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  cudaError_t e = dispatch(tc, deriv ? 2 : (fused ? 3 : 0), map, hmap, xmap, A, s, false);
   if (A.trace && e == cudaSuccess) {  // measurement only: print CTA 0's per-phase averages
-    std::vector<unsigned long long> h(64 * 8);
+    std::vector<unsigned long long> h(64 * 16);
     cudaMemcpyAsync(h.data(), A.trace, h.size() * 8, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     double acc[8] = {0};
     int cnt = 0;
     for (int i = 4; i < 60; ++i) {
-      if (!h[i * 8 + 6] || !h[(i + 1) * 8]) break;
-      for (int k = 1; k <= 6; ++k) acc[k] += (double)(h[i * 8 + k] - h[i * 8 + k - 1]);
-      acc[7] += (double)(h[(i + 1) * 8] - h[i * 8 + 6]);
+      if (!h[i * 16 + 6] || !h[(i + 1) * 16]) break;
+      for (int k = 1; k <= 6; ++k) acc[k] += (double)(h[i * 16 + k] - h[i * 16 + k - 1]);
+      acc[7] += (double)(h[(i + 1) * 16] - h[i * 16 + 6]);
       ++cnt;
     }
+    double fw[4] = {0, 0, 0, 0};
+    int fcnt = 0;
+    for (int i = 4; i < 60; ++i)  // fused finalisation: start, LL ready, reduced, stored
+      if (h[i * 16 + 8] && h[i * 16 + 11]) {
+        for (int k = 0; k < 3; ++k) fw[k] += (double)(h[i * 16 + 9 + k] - h[i * 16 + 8 + k]);
+        ++fcnt;
+      }
+    if (fcnt)
+      std::fprintf(stderr, "[tile trace] fused finalise (ns): LL %.0f reduce %.0f correct+store %.0f\n",
+                   fw[0] / fcnt, fw[1] / fcnt, fw[2] / fcnt);
     if (cnt)
       std::fprintf(stderr,
                    "[tile trace] per tile (ns): ring_wait+lds %.0f thomas %.0f ex_wait %.0f pcr %.0f "

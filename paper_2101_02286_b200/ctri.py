@@ -24,6 +24,7 @@ CTRI_FLAG_TIMING = 1 << 2
 CTRI_FLAG_DERIV = 1 << 3
 CTRI_FLAG_NCCL_ROUNDS = 1 << 4
 CTRI_FLAG_ALLGATHER = 1 << 5
+CTRI_FLAG_FUSED_REDUCED = 1 << 6
 CTRI_MAX_STAGES = 16
 ABI_VERSION = 3
 

@@ -5,7 +5,7 @@ ng=$(nvidia-smi -L | wc -l)
 for cfg in ${CFGS:-cfg2 cfg3}; do
   for n in 2 4; do
     [ $n -gt $ng ] && continue
-    for red in pcr allgather nccl; do
+    for red in ${REDS:-fused pcr allgather nccl}; do
       echo "== $cfg N=$n $red" >> gpurun_out/reduced.log
       timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
         --master-port $((29710 + n)) bench.py --config $cfg --gpus $n --steps 300 --warmup 10 \

@@ -15,7 +15,8 @@ import torch.distributed as dist
 import oracle
 import workloads
 from helpers import rel_err, residual
-from paper_2101_02286_b200 import CTRI_FLAG_DERIV, CTRI_FLAG_NCCL_ROUNDS, CTRI_FLAG_TIMING
+from paper_2101_02286_b200 import (CTRI_FLAG_DERIV, CTRI_FLAG_NCCL_ROUNDS, CTRI_FLAG_TIMING,
+                                   CTRI_FLAG_FUSED_REDUCED)
 from paper_2101_02286_b200 import dist as pdist
 
 
@@ -32,10 +33,15 @@ def main():
              ((256 * world, 2, 48), 0, (0.2, 1.1, 0.4), True),
              ((8, 128 * world, 32), 1, (1 / 3, 1.0, 1 / 3), True),
              ((4, 6, 64 * world), 2, (1 / 3, 1.0, 1 / 3), True),
-             ((96 * world, 3, 16), 0, (0.2, 1.1, 0.4), False)]
+             ((96 * world, 3, 16), 0, (0.2, 1.1, 0.4), False),
+             # slabs the fused tile kernel takes (window rows stashed across a 4/8-CTA cluster)
+             ((1024 * world, 2, 64), 0, (1 / 3, 1.0, 1 / 3), True),
+             ((2048 * world, 1, 40), 0, (0.45, 1.0, 0.45), True),   # ragged batch, wide window
+             ((1024 * world, 2, 64), 0, (0.2, 1.1, 0.4), False),
+             ((4, 1024 * world, 64), 1, (1 / 3, 1.0, 1 / 3), True)]
     pow2 = (world & (world - 1)) == 0
-    runs = [(c, fl) for c in cases for fl in (0, CTRI_FLAG_NCCL_ROUNDS)
-            if pow2 or fl == 0 or not c[3]]  # cyclic non-power-of-two: P2P path only
+    runs = [(c, fl) for c in cases for fl in (0, CTRI_FLAG_FUSED_REDUCED, CTRI_FLAG_NCCL_ROUNDS)
+            if pow2 or fl != CTRI_FLAG_NCCL_ROUNDS or not c[3]]  # cyclic non-power-of-two: P2P only
     for idx, ((dims, sd, bands, cyc), fl) in enumerate(runs):
         b = workloads.uniform(dims, 6 + idx)
         plan = pdist.plan_from_process_group(dims, sd, bands, cyc, flags=CTRI_FLAG_TIMING | fl)
