@@ -125,10 +125,14 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   // virtual partitions (nparts == 1): the slab is solved as vp partitions of n/vp rows so the
   // local-solve clusters are small enough to occupy every GPC
   P->vp = 1;
-  if (p == 1 && !(flags & CTRI_FLAG_DERIV) && P->lay.inner >= 16) {  // strided axis only
-    // measured: virtual slabs of 1024 rows (clusters of 4) are fastest for n >= 4096
-    int want = n >= 4096 ? (int)std::min<int64_t>(8, n / 1024) : 1;
-    if (const char* e = std::getenv("CTRI_VPARTS")) want = std::atoi(e);  // measurement knob
+  const char* vp_env = std::getenv("CTRI_VPARTS");  // measurement knob (any axis)
+  if (p == 1 && !(flags & CTRI_FLAG_DERIV) && (P->lay.inner >= 16 || P->lay.inner == 1 || vp_env)) {
+    // measured: virtual slabs of 1024 rows (clusters of 4) are fastest for n >= 4096 on a
+    // strided axis; 2048 rows (clusters of 2, 4 partitions at n = 8192) on the contiguous axis
+    int want = n >= 4096 ? (int)std::min<int64_t>(P->lay.inner == 1 ? 4 : 8,
+                                                  n / (P->lay.inner == 1 ? 2048 : 1024))
+                         : 1;
+    if (vp_env) want = std::atoi(vp_env);
     if (want > 1 && want <= 8 && is_pow2(want) && n % want == 0 && n / want >= 512) P->vp = want;
   }
   P->tlay = P->lay;

@@ -161,6 +161,16 @@ def test_virtual_partitions(vp, bands, cyclic, monkeypatch):
     assert st["vparts"] == vp
 
 
+@pytest.mark.parametrize("shape,sd", [((3, 13, 8192), 2), ((40, 8192), None)])
+def test_virtual_partitions_contiguous_axis(shape, sd):
+    """Contiguous solve axis, n = 8192: 4 virtual partitions of 2048 rows by default."""
+    if sd is None:
+        shape, sd = (shape[0], 1, shape[1]), 2
+    b = workloads.uniform(shape, 7)
+    x, st = check(b, sd, 1, SYM, True)
+    assert st["vparts"] == 4 and st["local_kernel"] == 2
+
+
 def test_p_independence():
     b = workloads.uniform((1024, 2, 16), 6)
     xs = [gpu_solve(b, 0, p) for p in (1, 2, 4, 8)]
