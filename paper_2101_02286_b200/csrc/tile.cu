@@ -172,17 +172,16 @@ __global__ void __launch_bounds__(NT, MINB)
     r_rxb = dev::mapa(r_rxb, (uint32_t)hb);
   }
 
-  // contiguous axis: every thread copies 16-byte row pairs of the tile into the padded ring
+  // contiguous axis: ONE TMA load per tile through a 3-D view (row in chunk, chunk, column) of
+  // the slab with a box of K+2 rows per chunk: the 2 rows past each chunk are out of bounds of
+  // the view and arrive zero-filled, so the ring gets the padded (K+2)-double chunk stride that
+  // keeps the lane-per-chunk reads conflict-free -- no per-thread copies
   auto issue_contig = [&](int64_t t) {
-    const int64_t gc0 = t * C;
-    for (int i = tid; i < C * (ROWS / 2); i += NT) {
-      const int jj = i / (ROWS / 2), pc = i - jj * (ROWS / 2);  // column, row pair
-      const int64_t gc = gc0 + jj;
-      const int r = 2 * pc;
-      double* d = ring + (size_t)jj * CPC * CSTRIDE + (r / K) * CSTRIDE + (r % K);
-      if (gc < A.lay.outer) dev::cp_async_16(dev::smem_u32(d), A.b + gc * A.lay.n + row0 + r);
-    }
-    dev::cp_async_commit();
+    if (tid != 0) return;
+    const uint32_t bar = dev::smem_u32(mbar);
+    dev::fence_proxy_async();
+    dev::mbar_expect_tx(bar, (uint32_t)(C * CPC * CSTRIDE) * 8u);
+    dev::tma_load_3d(dev::smem_u32(ring), &tmap, 0, (int)(g * CPC), (int)(t * C), bar, pol);
   };
   if (CONTIG) {
     if (first < A.num_tiles) issue_contig(first);
@@ -313,12 +312,7 @@ __global__ void __launch_bounds__(NT, MINB)
       dev::mbar_expect_tx(dev::smem_u32(mbar_ex), (uint32_t)NT * 3u * 8u);
       dev::mbar_expect_tx(dev::smem_u32(mbar_rx), (uint32_t)NT * 2u * 8u);
     }
-    if (CONTIG) {
-      dev::cp_async_wait_all();
-      __syncthreads();
-    } else {
-      dev::mbar_wait(dev::smem_u32(mbar + s), (uint32_t)(seq / SLOTS) & 1u);
-    }
+    dev::mbar_wait(dev::smem_u32(mbar + s), (uint32_t)(seq / SLOTS) & 1u);
     double* tile = ring + (size_t)s * RING;
     if (DERIV) {
       // slab-edge CTAs: the halo rows outside the slab come from the neighbour slabs (halo planes)
@@ -645,7 +639,7 @@ static cudaError_t dispatch(const TileConfig& tc, int kind, const CUtensorMap& m
 // Preference order when CTRI_TILE_VARIANT is not set: the first variant whose geometry fits n.
 // Measured on B200 (profiles/round1_tile_variants.md): 256-byte row segments with 2 CTA/SM
 // first, then 128-byte tiles; portable clusters (<= 8) before 16-CTA ones.
-static const int kPreference[] = {13, 4, 0, 12, 3, 1, 2, 5, 6};
+static const int kPreference[] = {13, 4, 0, 12, 3, 1, 2, 6, 5};  // contiguous: c8t256 (2 CTA/SM) first
 
 static int forced_variant() {
   const char* e = std::getenv("CTRI_TILE_VARIANT");  // experiment knob (bench sweeps)
@@ -848,7 +842,16 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   CUtensorMap map, hmap;
   std::memset(&map, 0, sizeof(map));
   std::memset(&hmap, 0, sizeof(hmap));
-  if (!tc.contig) {
+  if (tc.contig) {  // 3-D view (row in chunk, chunk, column), box K+2 rows: zero-padded chunks
+    cuuint64_t gdim[3] = {(cuuint64_t)tc.K, (cuuint64_t)(L.n / tc.K), (cuuint64_t)L.outer};
+    cuuint64_t gstride[2] = {(cuuint64_t)tc.K * 8, (cuuint64_t)L.n * 8};
+    cuuint32_t box[3] = {(cuuint32_t)(tc.K + 2), (cuuint32_t)(tc.NT / tc.C), (cuuint32_t)tc.C};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(b), gdim, gstride,
+                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  } else {
     cuuint64_t gdim[3] = {(cuuint64_t)L.inner, (cuuint64_t)L.n, (cuuint64_t)L.outer};
     cuuint64_t gstride[2] = {(cuuint64_t)L.inner * 8, (cuuint64_t)(L.n * L.inner * 8)};
     cuuint32_t box[3] = {(cuuint32_t)tc.C, (cuuint32_t)std::min(rows_cta / tc.SUB, 256), 1};
