@@ -81,6 +81,10 @@ void free_plan(Plan* P) {
   if (P->d_epoch) cudaFree(P->d_epoch);
   if (P->d_trace) cudaFree(P->d_trace);
   if (P->d_fctr) cudaFree(P->d_fctr);
+  if (P->e2e_sub) free_plan(P->e2e_sub);
+  for (cudaEvent_t e : P->e2e_ev) cudaEventDestroy(e);
+  if (P->e2e_h2d) cudaStreamDestroy(P->e2e_h2d);
+  if (P->e2e_d2h) cudaStreamDestroy(P->e2e_d2h);
   if (P->comm) ncclCommDestroy(P->comm);
   delete P;
 }
@@ -882,6 +886,50 @@ ctri_status ctri_solve_loopback(const ctri_plan* plans, int nparts, const double
   return solve_group(G, b, x, (cudaStream_t)stream);
 }
 
+// Choose the e2e pipeline for a one-partition plan: column chunks that are independent
+// problems of the same method (a sub-plan of the chunk's shape solves each).
+static ctri_status e2e_setup(Plan* P, cudaStream_t s) {
+  P->e2e_mode = 0;
+  const int64_t outer = P->lay.outer, n = P->lay.n, inner = P->lay.inner;
+  const size_t bytes = (size_t)P->lay.elems() * sizeof(double);
+  int nch = 8;
+  if (const char* e = std::getenv("CTRI_E2E_CHUNKS")) nch = std::atoi(e);  // measurement knob
+  if (P->p != 1 || P->loopback || nch < 2 || bytes < ((size_t)256 << 20)) return CTRI_OK;
+  int64_t dims[3];
+  int mode = 0;
+  if (outer % nch == 0) {
+    mode = 1;
+    dims[0] = outer / nch, dims[1] = n, dims[2] = inner;
+  } else if (outer == 1 && inner % nch == 0 && (inner / nch) % 2 == 0) {
+    mode = 2;
+    dims[0] = 1, dims[1] = n, dims[2] = inner / nch;
+  } else {
+    return CTRI_OK;
+  }
+  Plan* S = new Plan();
+  const uint32_t fl = P->flags & (CTRI_FLAG_FULL_BACKSUB | CTRI_FLAG_GENERIC_LOCAL);
+  ctri_status st;
+  if (P->r == 2) {
+    st = penta_init(S, dims, 1, 1, 0, P->bands5, P->cyclic, fl, s);
+  } else {
+    const double bd[3] = {P->bands.l, P->bands.d, P->bands.u};
+    st = plan_init(S, dims, 1, 1, 0, bd, P->cyclic, fl, s);
+  }
+  if (st != CTRI_OK) {
+    free_plan(S);
+    g_err.clear();
+    return CTRI_OK;  // no pipeline for this shape: sequential copies
+  }
+  P->e2e_sub = S;
+  CUDA_TRY(cudaStreamCreateWithFlags(&P->e2e_h2d, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&P->e2e_d2h, cudaStreamNonBlocking));
+  P->e2e_ev.resize(2 + 2 * (size_t)nch);
+  for (auto& e : P->e2e_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  P->e2e_nch = nch;
+  P->e2e_mode = mode;
+  return CTRI_OK;
+}
+
 ctri_status ctri_solve_host(ctri_plan plan, const double* b_host, double* x_host,
                             ctri_stream stream) {
   if (!plan || !b_host || !x_host) return fail(CTRI_ERR_INVALID_ARG, "NULL argument");
@@ -892,9 +940,57 @@ ctri_status ctri_solve_host(ctri_plan plan, const double* b_host, double* x_host
     CUDA_TRY(cudaMalloc(&P->d_stage_x, bytes));
   }
   cudaStream_t s = (cudaStream_t)stream;
-  CUDA_TRY(cudaMemcpyAsync(P->d_stage_b, b_host, bytes, cudaMemcpyHostToDevice, s));
-  TRY(ctri_solve(plan, P->d_stage_b, P->d_stage_x, stream));
-  CUDA_TRY(cudaMemcpyAsync(x_host, P->d_stage_x, bytes, cudaMemcpyDeviceToHost, s));
+  if (P->e2e_mode < 0) TRY(e2e_setup(P, s));
+  if (P->e2e_mode == 0) {
+    CUDA_TRY(cudaMemcpyAsync(P->d_stage_b, b_host, bytes, cudaMemcpyHostToDevice, s));
+    TRY(ctri_solve(plan, P->d_stage_b, P->d_stage_x, stream));
+    CUDA_TRY(cudaMemcpyAsync(x_host, P->d_stage_x, bytes, cudaMemcpyDeviceToHost, s));
+    return CTRI_OK;
+  }
+  // pipelined: H2D of chunk k+1 and D2H of chunk k-1 overlap the solve of chunk k
+  const int nch = P->e2e_nch;
+  const int64_t outer = P->lay.outer, n = P->lay.n, inner = P->lay.inner;
+  const int64_t celems = P->lay.elems() / nch;  // elements per chunk (contiguous on the device)
+  cudaEvent_t* ev = P->e2e_ev.data();
+  cudaEvent_t *e_h2d = ev + 2, *e_sol = ev + 2 + nch;
+  P->solves++;
+  CUDA_TRY(cudaEventRecord(ev[0], s));
+  CUDA_TRY(cudaStreamWaitEvent(P->e2e_h2d, ev[0], 0));
+  CUDA_TRY(cudaStreamWaitEvent(P->e2e_d2h, ev[0], 0));
+  const int64_t ic = inner / nch;
+  for (int k = 0; k < nch; ++k) {
+    double* db = P->d_stage_b + (size_t)k * celems;
+    if (P->e2e_mode == 1) {
+      CUDA_TRY(cudaMemcpyAsync(db, b_host + (size_t)k * celems, celems * sizeof(double),
+                               cudaMemcpyHostToDevice, P->e2e_h2d));
+    } else {  // columns [k*ic, (k+1)*ic) of every row (outer == 1)
+      CUDA_TRY(cudaMemcpy2DAsync(db, ic * sizeof(double), b_host + (size_t)k * ic, inner * sizeof(double),
+                                 ic * sizeof(double), n, cudaMemcpyHostToDevice, P->e2e_h2d));
+    }
+    CUDA_TRY(cudaEventRecord(e_h2d[k], P->e2e_h2d));
+  }
+  for (int k = 0; k < nch; ++k) {
+    CUDA_TRY(cudaStreamWaitEvent(s, e_h2d[k], 0));
+    std::vector<Plan*> G{P->e2e_sub};
+    const double* bk = P->d_stage_b + (size_t)k * celems;
+    double* xk = P->d_stage_x + (size_t)k * celems;
+    TRY(solve_group(G, &bk, &xk, s));
+    CUDA_TRY(cudaEventRecord(e_sol[k], s));
+  }
+  for (int k = 0; k < nch; ++k) {
+    CUDA_TRY(cudaStreamWaitEvent(P->e2e_d2h, e_sol[k], 0));
+    const double* dx = P->d_stage_x + (size_t)k * celems;
+    if (P->e2e_mode == 1) {
+      CUDA_TRY(cudaMemcpyAsync(x_host + (size_t)k * celems, dx, celems * sizeof(double),
+                               cudaMemcpyDeviceToHost, P->e2e_d2h));
+    } else {
+      CUDA_TRY(cudaMemcpy2DAsync(x_host + (size_t)k * ic, inner * sizeof(double), dx, ic * sizeof(double),
+                                 ic * sizeof(double), n, cudaMemcpyDeviceToHost, P->e2e_d2h));
+    }
+  }
+  CUDA_TRY(cudaEventRecord(ev[1], P->e2e_d2h));
+  CUDA_TRY(cudaStreamWaitEvent(s, ev[1], 0));
+  (void)outer;
   return CTRI_OK;
 }
 

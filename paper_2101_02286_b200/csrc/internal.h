@@ -211,9 +211,15 @@ struct Plan {
   int local_kernel = 0;  // 0 generic, 1 tile (strided axis)
   TileConfig tile;
 
-  // e2e staging
+  // e2e staging (ctri_solve_host); with one partition and a large slab the copies and the
+  // solve are pipelined over column chunks, each solved by a sub-plan of the chunk's shape
   double* d_stage_b = nullptr;
   double* d_stage_x = nullptr;
+  Plan* e2e_sub = nullptr;
+  int e2e_mode = -1;   // -1 undecided, 0 sequential, 1 chunks along outer, 2 chunks along inner
+  int e2e_nch = 0;
+  cudaStream_t e2e_h2d = nullptr, e2e_d2h = nullptr;
+  std::vector<cudaEvent_t> e2e_ev;  // [start, end, h2d[nch], solved[nch]]
 
   // fused P2P reduced phase
   bool p2p = false;
