@@ -374,7 +374,7 @@ def main():
         e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": nbytes,
                "d2h_bytes_per_step": nbytes, "steps": args.e2e_steps,
                "path": "ctri_solve_host: pinned host -> HBM, solve, HBM -> pinned host; one "
-                       "partition pipelines copies and solves over 8 column chunks"}
+                       "partition pipelines copies and solves over 16 column chunks"}
         del bh, xh
 
     if rank == 0:

@@ -337,7 +337,7 @@ def test_solve_host_e2e():
                                             ((64, 1024, 512), 1, NONSYM),        # chunks along outer
                                             ((64, 2, 256 * 1024), 2, SYM)])      # contiguous axis
 def test_solve_host_pipelined(shape, sd, bands):
-    """Arrays >= 256 MB: ctri_solve_host overlaps H2D / solve / D2H over 8 column chunks,
+    """Arrays >= 256 MB: ctri_solve_host overlaps H2D / solve / D2H over 16 column chunks,
     each solved by a sub-plan of the chunk's shape; same result as the device solve."""
     import torch
 
