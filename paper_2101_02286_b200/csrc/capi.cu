@@ -523,7 +523,14 @@ ctri_status exchange_loopback(std::vector<Plan*>& G, RoundFn fn, cudaStream_t s)
 }
 
 void record(Plan& P, int slot, cudaStream_t s) {
-  if (!P.ev.empty()) cudaEventRecord(P.ev[slot], s);
+  if (P.ev.empty()) return;
+  // inside a CUDA-graph capture the phase events become external event-record nodes, so
+  // ctri_get_stats can still read them after a replay
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(P.ev[slot], s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(P.ev[slot], s);
 }
 
 // (a1) local solve; with `deriv` the tile kernel reads f and forms the stencil RHS itself (a0).
