@@ -171,6 +171,16 @@ def test_virtual_partitions_contiguous_axis(shape, sd):
     assert st["vparts"] == 4 and st["local_kernel"] == 2
 
 
+@pytest.mark.parametrize("shape,sd", [((8192, 1, 1), 0), ((1, 1, 8192), 2), ((3, 4096, 5), 1),
+                                      ((1, 2, 100000), 2), ((6, 1, 4094), 2), ((4096, 3, 7), 0)])
+def test_odd_shapes(shape, sd):
+    """Single column, tiny / odd batch, n not a power of two: whichever kernel the plan picks
+    (tile, contiguous tile with virtual partitions, column-serial) matches the oracle."""
+    b = workloads.uniform(shape, 8)
+    check(b, sd, 1, NONSYM, True)
+    check(b, sd, 1, SYM, False)
+
+
 def test_p_independence():
     b = workloads.uniform((1024, 2, 16), 6)
     xs = [gpu_solve(b, 0, p) for p in (1, 2, 4, 8)]
