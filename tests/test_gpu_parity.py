@@ -423,3 +423,53 @@ def test_cfg2_full_size_sampled():
     r = a * torch.roll(x, 1, 0) + x + a * torch.roll(x, -1, 0) - b
     res = (r.abs().amax(0) / b.abs().amax(0)).max().item()
     assert res < TOL_RES
+
+
+def _sampled_columns(b, x, sd, n_cols=192, seed=0, fn=None):
+    """Oracle on sampled batch columns of a full-size device solve (columns are independent)."""
+    import torch
+    bc = torch.movedim(b, sd, 0).reshape(b.shape[sd], -1)
+    xc = torch.movedim(x, sd, 0).reshape(x.shape[sd], -1)
+    m = bc.shape[1]
+    cols = np.random.default_rng(seed).choice(m, size=min(n_cols, m), replace=False)
+    cols = np.unique(np.r_[cols, [0, m - 1]])
+    idx = torch.as_tensor(cols, device=b.device)
+    bs = bc[:, idx].cpu().numpy()
+    xs = xc[:, idx].cpu().numpy()
+    ref = (fn or (lambda a: oracle.cyclic_solve(a, 0)))(bs.reshape(bs.shape[0], -1, 1)).reshape(bs.shape[0], -1)
+    return rel_err(xs[:, :, None], ref[:, :, None], 0)
+
+
+@pytest.mark.parametrize("cfg", ["cfg4_d1", "cfg4_d2", "cfg3"])
+def test_full_size_sampled_directions(cfg):
+    """BASELINE direction sweep (256x8192x256 index 1, 256x256x8192 index 2) and the weak-scaling
+    slab, launched as bench.py does (default kernel choice), oracle on sampled columns."""
+    import torch
+
+    from paper_2101_02286_b200 import ctri
+    dims, sd = workloads.config(cfg)
+    b = workloads.device_uniform(dims, 3, torch.device("cuda:0"))
+    x = torch.empty_like(b)
+    plan = ctri.Plan(dims, sd)
+    plan.solve(b, x)
+    torch.cuda.synchronize()
+    st = plan.stats()
+    plan.close()
+    assert st["local_kernel"] in (1, 2)
+    assert _sampled_columns(b, x, sd) < TOL_REL
+
+
+def test_cfg5_full_size_sampled():
+    """cfg5 (1024x512^2 compact derivative, stencil fused into the tile kernel) at full size."""
+    import torch
+
+    from paper_2101_02286_b200 import CTRI_FLAG_DERIV, ctri
+    dims, sd = workloads.config("cfg5", 1)
+    f = workloads.device_uniform(dims, 5, torch.device("cuda:0"))
+    df = torch.empty_like(f)
+    plan = ctri.Plan(dims, sd, flags=CTRI_FLAG_DERIV)
+    plan.deriv(f, df)
+    torch.cuda.synchronize()
+    plan.close()
+    assert _sampled_columns(f, df, sd, fn=lambda a: oracle.deriv(a, 0, h=2 * math.pi / dims[sd])) < TOL_REL
+
