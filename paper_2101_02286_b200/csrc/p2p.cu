@@ -26,6 +26,7 @@
 #include <cstring>
 
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace ctri {
 
@@ -164,15 +165,35 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
       for (int i = 0; i < kMaxCpt; ++i)
         if (i < nc) ll_send(dst + 2 * col[i], bh[i], ep);
     }
+    // batched receive: every pending (column, source) word is loaded in one sweep before any
+    // is tested, so the two partners' (and the columns') poll latencies overlap
+    double u[2][kMaxCpt];
+    uint32_t pend = 0;
 #pragma unroll
     for (int i = 0; i < kMaxCpt; ++i) {
-      if (i >= nc || !ok) continue;
-      const int64_t j = col[i];
-      double u0 = 0.0, u1 = 0.0;
-      if (S.src0 >= 0) ok = ok && ll_recv(mine + OFF_S(s, 0) + 2 * j, ep, deadline, &u0);
-      if (S.src1 >= 0) ok = ok && ll_recv(mine + OFF_S(s, 1) + 2 * j, ep, deadline, &u1);
-      bh[i] = S.w * bh[i] - S.c0 * u0 - S.c1 * u1;
+      u[0][i] = u[1][i] = 0.0;
+      if (i < nc) pend |= (S.src0 >= 0 ? 1u : 0u) << (2 * i) | (S.src1 >= 0 ? 2u : 0u) << (2 * i);
     }
+    int spins = 0;
+    while (pend && ok) {
+      unsigned long long w0[2 * kMaxCpt], w1[2 * kMaxCpt];
+#pragma unroll
+      for (int k = 0; k < 2 * kMaxCpt; ++k)
+        if (pend & (1u << k)) dev::ll_load(mine + OFF_S(s, k & 1) + 2 * col[k >> 1], &w0[k], &w1[k]);
+#pragma unroll
+      for (int k = 0; k < 2 * kMaxCpt; ++k)
+        if ((pend & (1u << k)) && dev::ll_ready(w0[k], w1[k], ep)) {
+          u[k & 1][k >> 1] = dev::ll_value(w0[k], w1[k]);
+          pend &= ~(1u << k);
+        }
+      if (pend && ++spins == 64) {
+        spins = 0;
+        if (globaltimer() > deadline) ok = false;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kMaxCpt; ++i)
+      if (i < nc) bh[i] = S.w * bh[i] - S.c0 * u[0][i] - S.c1 * u[1][i];
   }
   stamp(3);
   // ---- (a4) x~_i -> left neighbour; back-substitution on the window ----
