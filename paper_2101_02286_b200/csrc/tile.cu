@@ -276,21 +276,26 @@ __global__ void __launch_bounds__(NT, MINB)
         xa += f_red[q * C + j];
         xb += f_red[NT + q * C + j];
       }
-      double* stp = f_stash + (size_t)slotp * A.f_srw * C;
+      // the stash and the S / R table share shared memory but never overlap: restrict lets the
+      // compiler batch the loads instead of serialising every row on a possible alias
+      double* __restrict__ stp = f_stash + (size_t)slotp * A.f_srw * C;
+      const double* __restrict__ sS = f_sr;
+      const double* __restrict__ sR = f_sr + A.f_srw;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int64_t r = (int64_t)c * K + k;
         int si = -1;
         if (f_top && r <= f_W) si = (int)r;
         else if (f_bot && r >= f_b0) si = f_bbase + (int)(r - f_b0);
-        if (si >= 0) {  // Eq. xi_app on the window (R15), in place; row 0 is x~_i
-          const double y = stp[si * C + j];
-          stp[si * C + j] = (r == 0) ? xa : y - f_sr[si] * xa - f_sr[A.f_srw + si] * xb;
-        }
+        if (si >= 0)  // Eq. xi_app on the window (R15), in place; row 0 is x~_i
+          stp[si * C + j] = (r == 0) ? xa : stp[si * C + j] - sS[si] * xa - sR[si] * xb;
       }
     }
+    stamp(it, 12);
     dev::fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA store
+    stamp(it, 13);
     __syncthreads();
+    stamp(it, 14);
     if (tid == 0) {  // the corrected window blocks go out through TMA (off the LSU store path)
       const uint32_t sb = dev::smem_u32(f_stash + (size_t)slotp * A.f_srw * C);
       if (f_top) dev::tma_store_3d(&xmap, sb, (int)colp, 0, (int)op);
@@ -423,8 +428,6 @@ __global__ void __launch_bounds__(NT, MINB)
     dev::st_async_f64(r_bt, btv, r_exbar);
     dev::st_async_f64(r_yf, v[1], r_exbar);
     dev::st_async_f64(r_yl, v[K - 1], r_exbar);
-    // FUSED: finalise the previous tile while the cluster exchange is in flight
-    if (FUSED && (f_top || f_bot) && it > 0) f_finalize(t - ncl, (it - 1) & 1);
     // ---- owner: head system b^_c (Eq. bi_hat at chunk level), then PCR stages ----
     {
       dev::mbar_wait(dev::smem_u32(mbar_ex), (uint32_t)it & 1u);
@@ -461,6 +464,9 @@ __global__ void __launch_bounds__(NT, MINB)
     v[0] = (A.mode == 1 && c == 0) ? btv : xa;  // mode 1: slab row 0 keeps b~ (scratch)
 #pragma unroll
     for (int k = 1; k < K; ++k) v[k] = v[k] - T.S[k - 1] * xa - T.R[k - 1] * xb;
+    // FUSED: finalise the previous tile here, a whole tile after its stores were issued, so
+    // the TMA store of its window rows does not queue behind them
+    if (FUSED && (f_top || f_bot) && it > 0) f_finalize(t - ncl, (it - 1) & 1);
     store_chunk();
     stamp(it, 6);
     if (valid && FUSED) {  // (a2) planes of this tile -> every rank's mailbox (all-gather, R21)
@@ -962,9 +968,14 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
         for (int k = 0; k < 3; ++k) fw[k] += (double)(h[i * 16 + 9 + k] - h[i * 16 + 8 + k]);
         ++fcnt;
       }
+    double fz[3] = {0, 0, 0};
+    for (int i = 4; i < 60; ++i)
+      if (h[i * 16 + 10] && h[i * 16 + 14])
+        for (int k = 0; k < 3; ++k) fz[k] += (double)(h[i * 16 + 12 + k] - h[i * 16 + 11 + k - (k == 0 ? 1 : 0)]);
     if (fcnt)
-      std::fprintf(stderr, "[tile trace] fused finalise (ns): LL %.0f reduce %.0f correct+store %.0f\n",
-                   fw[0] / fcnt, fw[1] / fcnt, fw[2] / fcnt);
+      std::fprintf(stderr, "[tile trace] fused finalise (ns): LL %.0f reduce %.0f correct+store %.0f "
+                   "(correct %.0f fence %.0f sync %.0f)\n",
+                   fw[0] / fcnt, fw[1] / fcnt, fw[2] / fcnt, fz[0] / fcnt, fz[1] / fcnt, fz[2] / fcnt);
     if (cnt)
       std::fprintf(stderr,
                    "[tile trace] per tile (ns): ring_wait+lds %.0f thomas %.0f ex_wait %.0f pcr %.0f "
