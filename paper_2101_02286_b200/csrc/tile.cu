@@ -85,8 +85,10 @@ __global__ void __launch_bounds__(NT, MINB)
   uint64_t* mbar_ex = mbar + SLOTS;
   uint64_t* mbar_rx = mbar_ex + 1;
   // FUSED: [2][f_srw][C] window rows (128-byte aligned: TMA-store source)
+  // (offset arithmetic on smem_raw, not on an integer address: the compiler must keep seeing
+  // a shared-memory pointer, or every stash access becomes a generic LD/ST)
   double* f_stash = reinterpret_cast<double*>(
-      (reinterpret_cast<uintptr_t>(mbar_rx + 1) + 127) & ~static_cast<uintptr_t>(127));
+      smem_raw + ((reinterpret_cast<unsigned char*>(mbar_rx + 1) - smem_raw + 127) & ~(ptrdiff_t)127));
   double* f_red = FUSED ? f_stash + (size_t)2 * A.f_srw * C : nullptr;  // [2][NT] partial x~
   double* f_sr = FUSED ? f_red + 2 * NT : nullptr;  // [2][f_srw]: S, R of the stashed rows
 
@@ -206,6 +208,21 @@ __global__ void __launch_bounds__(NT, MINB)
   const int f_W = FUSED ? A.f_W : 0;
   const int f_bbase = (G == 1) ? f_W + 1 : 0;  // stash row of slab row n - W - 1
   const int64_t f_b0 = f_n - f_W - 1;           // first stashed row of the bottom block
+  // rows k in [f_kb, f_ke) of this thread's chunk are stashed, at stash row k + f_soff (a chunk
+  // never holds both window blocks: tile_configure requires n >= 2(W+1) + K)
+  int f_kb = K, f_ke = 0, f_soff = 0;
+  if (FUSED) {
+    const int64_t rc0 = (int64_t)c * K;
+    if (f_top && rc0 <= f_W) {
+      f_kb = 0;
+      f_ke = (int)std::min<int64_t>(K, f_W + 1 - rc0);
+      f_soff = (int)rc0;
+    } else if (f_bot && rc0 + K > f_b0) {
+      f_kb = (int)std::max<int64_t>(0, f_b0 - rc0);
+      f_ke = K;
+      f_soff = f_bbase + (int)(rc0 - f_b0);
+    }
+  }
   uint32_t f_ep = 0;
   unsigned long long f_deadline = 0;
   if (FUSED) {
@@ -268,27 +285,32 @@ __global__ void __launch_bounds__(NT, MINB)
     f_red[NT + tid] = a1;
     __syncthreads();
     stamp(it, 10);
-    const int64_t colj = colp + j;
-    if (colj < A.lay.inner) {
-      double xa = 0.0, xb = 0.0;
+    double* f_x = f_red;  // [2][C] x~_i, x~_{i+1} per column (f_red's first 2C are read first)
+    double xa_j = 0.0, xb_j = 0.0;
+    if (tid < C) {
 #pragma unroll
       for (int q = 0; q < NT / C; ++q) {  // fixed order: deterministic
-        xa += f_red[q * C + j];
-        xb += f_red[NT + q * C + j];
+        xa_j += f_red[q * C + tid];
+        xb_j += f_red[NT + q * C + tid];
       }
-      // the stash and the S / R table share shared memory but never overlap: restrict lets the
-      // compiler batch the loads instead of serialising every row on a possible alias
+    }
+    __syncthreads();
+    if (tid < C) {
+      f_x[tid] = xa_j;
+      f_x[C + tid] = xb_j;
+    }
+    __syncthreads();
+    {  // Eq. xi_app on the stashed window rows (R15), spread over all threads; row 0 is x~_i
       double* __restrict__ stp = f_stash + (size_t)slotp * A.f_srw * C;
       const double* __restrict__ sS = f_sr;
       const double* __restrict__ sR = f_sr + A.f_srw;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int64_t r = (int64_t)c * K + k;
-        int si = -1;
-        if (f_top && r <= f_W) si = (int)r;
-        else if (f_bot && r >= f_b0) si = f_bbase + (int)(r - f_b0);
-        if (si >= 0)  // Eq. xi_app on the window (R15), in place; row 0 is x~_i
-          stp[si * C + j] = (r == 0) ? xa : stp[si * C + j] - sS[si] * xa - sR[si] * xb;
+      const double* __restrict__ fx = f_x;
+      for (int e = tid; e < A.f_srw * C; e += NT) {
+        const int si = e / C, jj = e - (e / C) * C;
+        const bool used = (f_top && si <= f_W) || (f_bot && si >= f_bbase && si <= f_bbase + f_W);
+        if (!used) continue;
+        const double xa = fx[jj], xb = fx[C + jj];
+        stp[e] = (f_top && si == 0) ? xa : stp[e] - sS[si] * xa - sR[si] * xb;
       }
     }
     stamp(it, 12);
@@ -387,12 +409,10 @@ __global__ void __launch_bounds__(NT, MINB)
       if (!valid) return;
       double* xp = A.x + (o * A.lay.n + (int64_t)c * K) * A.lay.inner + col;
       if (FUSED) {  // window rows wait in shared memory for x~ (finalised one tile later)
-        double* stp = f_stash + (size_t)(it & 1) * A.f_srw * C;
+        double* stp = f_stash + (size_t)(it & 1) * A.f_srw * C + (size_t)f_soff * C + j;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          const int64_t r = (int64_t)c * K + k;
-          if (f_top && r <= f_W) stp[r * C + j] = v[k];
-          else if (f_bot && r >= f_b0) stp[(f_bbase + (int)(r - f_b0)) * C + j] = v[k];
+          if (k >= f_kb && k < f_ke) stp[k * C] = v[k];
           else dev::st_global_cs(xp + (int64_t)k * A.lay.inner, v[k]);
         }
         return;
@@ -795,7 +815,7 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
       P.window > 0) {
     const int64_t W = P.window;
     const int srw = (int)(G == 1 ? 2 * (W + 1) : W + 1);
-    if (W + 1 <= 256 && ((G == 1 && 2 * (W + 1) <= L.n) || (G > 1 && W + 1 <= rows_cta))) {
+    if (W + 1 <= 256 && ((G == 1 && 2 * (W + 1) + K <= L.n) || (G > 1 && W + 1 + K <= rows_cta))) {
       tc.fused_srw = srw;
       tc.smem_fused = tc.smem_bytes + 128 +
                       (int)(sizeof(double) * (2 * (size_t)srw * V.C + 2 * (size_t)V.NT + 2 * (size_t)srw));
