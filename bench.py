@@ -362,6 +362,8 @@ def main():
     yx = pdist.max_over_ranks(st["t_yexchange_us"], dev) if world > 1 else st["t_yexchange_us"]
     xx = pdist.max_over_ranks(st["t_xexchange_us"], dev) if world > 1 else st["t_xexchange_us"]
     back = pdist.max_over_ranks(st["t_backsub_us"], dev) if world > 1 else st["t_backsub_us"]
+    p2p_k = pdist.max_over_ranks(st["t_reduced_kernel_us"], dev) if world > 1 else st["t_reduced_kernel_us"]
+    win_k = pdist.max_over_ranks(st["t_window_us"], dev) if world > 1 else st["t_window_us"]
 
     # e2e through ctri_solve_host with pinned host buffers
     e2e = None
@@ -423,11 +425,17 @@ def main():
                 "cpu_baseline": cpu,
                 "e2e": e2e,
                 "gpu_launches": launches,
-                "comm_us": ({"fused_reduced_kernel_us": back,
+                "comm_us": ({"reduced_phase_us": back,
+                             "p2p_kernel_us": p2p_k, "window_kernel_us": win_k,
+                             "per_round_median_us": {"y_exchange": st["t_p2p_y_us"],
+                                                     "schedule_steps": st["t_p2p_step_us"],
+                                                     "x_exchange": st["t_p2p_x_us"]},
                              "note": "device-initiated (a2)-(a4): LL P2P stores over NVLink "
-                                     "(pairwise schedule, or one all-gather round) + the window "
-                                     "back-substitution kernel; includes waiting for the slowest "
-                                     "peer's local solve"}
+                                     "(pairwise schedule, or one all-gather round), then the "
+                                     "window back-substitution kernel; kernel times are CUDA "
+                                     "events (max over ranks), rounds are medians over rank 0's "
+                                     "CTAs of %globaltimer stamps; the y round includes waiting "
+                                     "for the slowest peer's local solve"}
                             if st["reduced_path"] in (1, 2) else
                             {"fused_into_tile_kernel": True,
                              "note": "(a2)-(a4) inside the local-solve kernel: LL all-gather of the "

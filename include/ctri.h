@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define CTRI_ABI_VERSION 3
+#define CTRI_ABI_VERSION 4
 
 typedef struct ctri_plan_s* ctri_plan;
 typedef struct CUstream_st* ctri_stream; /* == cudaStream_t */
@@ -113,6 +113,13 @@ typedef struct ctri_stats {
   int32_t detach_stages;        /* nparts > 1 cyclic, not a power of two: detach stages */
   int32_t detached_rows;        /* rows detached and reattached: nparts - 2^floor(log2 nparts) */
   int32_t band_halfwidth;       /* r: 1 tridiagonal plan, 2 pentadiagonal plan */
+  /* device-initiated reduced phase (reduced_path 1 / 2, CTRI_FLAG_TIMING): CUDA-event times of
+     the P2P kernel and of the window kernel, and per-round medians over the kernel's CTAs of
+     %globaltimer stamps (y round incl. waiting for the left neighbour, each schedule step, x~
+     round); -1 where not applicable */
+  float t_reduced_kernel_us, t_window_us;
+  float t_p2p_y_us, t_p2p_step_us[CTRI_MAX_STAGES], t_p2p_x_us;
+  int32_t p2p_steps;            /* schedule steps timed in t_p2p_step_us */
 } ctri_stats;
 
 /* Human-readable status name; never NULL. */

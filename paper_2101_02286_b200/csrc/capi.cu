@@ -596,27 +596,33 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
     P2PArgs A;
     p2p_args(P0, &A);
     const int grid = A.nslices * (int)G.size();
-    if (std::getenv("CTRI_P2P_TRACE") && !P0.d_trace)
-      CUDA_TRY(cudaMalloc(&P0.d_trace, sizeof(unsigned long long) * 8 * grid));
+    const bool env_trace = std::getenv("CTRI_P2P_TRACE") != nullptr;
+    if ((env_trace || !P0.ev.empty()) && !P0.d_trace) {  // per-round stamps (CTRI_FLAG_TIMING)
+      CUDA_TRY(cudaMalloc(&P0.d_trace, sizeof(unsigned long long) * kP2PTrace * grid));
+      CUDA_TRY(cudaMemsetAsync(P0.d_trace, 0, sizeof(unsigned long long) * kP2PTrace * grid, s));
+      P0.trace_ctas = grid;
+    }
     A.trace = P0.d_trace;
     for (size_t r = 0; r < G.size(); ++r) p2p_fill_rank(*G[r], x[r], &A.rk[r]);
     cudaError_t e = launch_reduced_p2p(A, (int)G.size(), s);
     if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("p2p reduced kernel: ") + cudaGetErrorString(e));
+    record(P0, EV_XX, s);
     for (size_t r = 0; r < G.size(); ++r) {  // (a4) window pass of every rank
       e = launch_window(*G[r], x[r], G[r]->xt_next, s);
       if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("window: ") + cudaGetErrorString(e));
     }
-    if (P0.d_trace) {  // measurement only: per-phase durations across CTAs
-      std::vector<unsigned long long> t(8 * (size_t)grid);
+    if (P0.d_trace && env_trace) {  // measurement only: per-phase spread across CTAs on stderr
+      std::vector<unsigned long long> t((size_t)kP2PTrace * grid);
       CUDA_TRY(cudaMemcpyAsync(t.data(), P0.d_trace, t.size() * 8, cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaStreamSynchronize(s));
       unsigned long long t0 = ~0ull;
-      for (int b = 0; b < grid; ++b) t0 = std::min(t0, t[8 * b]);
+      for (int b = 0; b < grid; ++b) t0 = std::min(t0, t[(size_t)kP2PTrace * b]);
       std::fprintf(stderr, "[p2p trace rank %d solve %llu]", P0.rank, (unsigned long long)P0.solves);
-      const char* nm[6] = {"start", "y_sent", "y_recv", "stages", "x_recv", "end"};
-      for (int k = 0; k < 6; ++k) {
+      const int slots[5] = {kTrStart, kTrYSent, kTrYRecv, kTrXRecv, kTrEnd};
+      const char* nm[5] = {"start", "y_sent", "y_recv", "x_recv", "end"};
+      for (int k = 0; k < 5; ++k) {
         std::vector<double> v;
-        for (int b = 0; b < grid; ++b) v.push_back((t[8 * b + k] - t0) * 1e-3);
+        for (int b = 0; b < grid; ++b) v.push_back((t[(size_t)kP2PTrace * b + slots[k]] - t0) * 1e-3);
         std::sort(v.begin(), v.end());
         std::fprintf(stderr, " %s %.1f/%.1f/%.1f", nm[k], v.front(), v[v.size() / 2], v.back());
       }
@@ -1098,14 +1104,43 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
   float* ts[] = {&out->t_total_us, &out->t_local_us, &out->t_yexchange_us, &out->t_bhat_us,
                  &out->t_xexchange_us, &out->t_backsub_us};
   for (float* t : ts) *t = -1.f;
-  for (int k = 0; k < CTRI_MAX_STAGES; ++k) out->t_stage_us[k] = -1.f;
+  for (int k = 0; k < CTRI_MAX_STAGES; ++k) out->t_stage_us[k] = out->t_p2p_step_us[k] = -1.f;
+  out->t_reduced_kernel_us = out->t_window_us = out->t_p2p_y_us = out->t_p2p_x_us = -1.f;
   if (P->timed_valid || (!P->ev.empty() && P->solves > 0)) {
     const bool two = P->p > 1 || P->vp > 1 || P->r == 2;
     CUDA_TRY(cudaEventSynchronize(P->ev[two ? EV_BACK : EV_LOCAL]));
     out->t_local_us = elapsed(*P, EV_START, EV_LOCAL);
-    if (P->p > 1 && P->p2p) {
-      out->t_backsub_us = elapsed(*P, EV_LOCAL, EV_BACK);  // the whole fused (a2)-(a4) kernel
+    if (P->p > 1 && P->p2p && !P->fused) {
+      out->t_backsub_us = elapsed(*P, EV_LOCAL, EV_BACK);  // (a2)-(a4): P2P kernel + window pass
       out->t_total_us = elapsed(*P, EV_START, EV_BACK);
+      if (P->r == 1) {
+        out->t_reduced_kernel_us = elapsed(*P, EV_LOCAL, EV_XX);
+        out->t_window_us = elapsed(*P, EV_XX, EV_BACK);
+      }
+      if (P->d_trace && P->trace_ctas > 0) {  // per-round medians over the CTAs of this rank
+        const int grid = P->trace_ctas;
+        std::vector<unsigned long long> t((size_t)kP2PTrace * grid);
+        CUDA_TRY(cudaMemcpy(t.data(), P->d_trace, t.size() * 8, cudaMemcpyDeviceToHost));
+        auto med = [&](int a, int b) -> float {
+          std::vector<double> v;
+          for (int k = 0; k < grid; ++k) {
+            const unsigned long long* tk = t.data() + (size_t)kP2PTrace * k;
+            if (tk[a] && tk[b] >= tk[a]) v.push_back((double)(tk[b] - tk[a]) * 1e-3);
+          }
+          if (v.empty()) return -1.f;
+          std::nth_element(v.begin(), v.begin() + v.size() / 2, v.end());
+          return (float)v[v.size() / 2];
+        };
+        const int q = P->allgather ? 0 : (int)P->sched.steps.size();
+        out->p2p_steps = q;
+        out->t_p2p_y_us = med(kTrStart, kTrYRecv);
+        int prev = kTrYRecv;
+        for (int k = 0; k < q && k < CTRI_MAX_STAGES; ++k) {
+          out->t_p2p_step_us[k] = med(prev, kTrStep0 + k);
+          prev = kTrStep0 + k;
+        }
+        out->t_p2p_x_us = med(prev, kTrXRecv);
+      }
     } else if (P->p > 1) {
       out->t_yexchange_us = elapsed(*P, EV_LOCAL, EV_YX);
       out->t_bhat_us = elapsed(*P, EV_YX, EV_BHAT);

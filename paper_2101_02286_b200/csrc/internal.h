@@ -131,6 +131,10 @@ struct TileConfig {
 // ---- fused device-initiated reduced phase (p2p.cu) ----
 constexpr int kMaxP2PRanks = 16;  // real multi-GPU: <= 8 per box; loopback tests up to 16
 constexpr int kMaxP2PSteps = 16;
+// %globaltimer stamps of the P2P kernels, per CTA: start, y sent, y received, after schedule
+// step s (3 + s), x~ received, end
+constexpr int kP2PTrace = 24, kTrStart = 0, kTrYSent = 1, kTrYRecv = 2, kTrStep0 = 3,
+              kTrXRecv = 3 + kMaxP2PSteps, kTrEnd = 4 + kMaxP2PSteps;
 constexpr int kMaxAG = 8;  // all-gather reduced solve (CTRI_FLAG_ALLGATHER): nparts <= 8
 // One rank's part of a reduced-system schedule step (factor.h Schedule):
 //   v <- w v - c0 u0 - c1 u1, u_k received in mailbox slot k from rank src_k;
@@ -164,7 +168,7 @@ struct P2PArgs {
   double l, u;
   const double *S, *R;
   int* err;
-  unsigned long long* trace;  // measurement only (CTRI_P2P_TRACE): [grid][8] globaltimer stamps
+  unsigned long long* trace;  // CTRI_FLAG_TIMING / CTRI_P2P_TRACE: [grid][kP2PTrace] stamps
   P2PRank rk[kMaxP2PRanks];
 };
 cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s);
@@ -236,7 +240,8 @@ struct Plan {
   std::vector<void*> peer_alloc;       // peer allocations as mapped here (IPC) or direct
   std::vector<bool> peer_ipc;          // opened with cudaIpcOpenMemHandle
   int* d_err = nullptr;                // device error word (p2p deadline)
-  unsigned long long* d_trace = nullptr;  // CTRI_P2P_TRACE stamps
+  unsigned long long* d_trace = nullptr;  // P2P per-round stamps (CTRI_FLAG_TIMING / CTRI_P2P_TRACE)
+  int trace_ctas = 0;
   unsigned long long epoch = 0;
 
   // comm

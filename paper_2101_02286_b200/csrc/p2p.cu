@@ -116,11 +116,11 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
   const int left = cyc ? (rank + p - 1) % p : (rank > 0 ? rank - 1 : -1);
   unsigned long long* const mine = R.mbox + copy_off;
 
-  unsigned long long* tr = A.trace ? A.trace + (size_t)blockIdx.x * 8 : nullptr;
+  unsigned long long* tr = A.trace ? A.trace + (size_t)blockIdx.x * kP2PTrace : nullptr;
   auto stamp = [&](int k) {
     if (tr && threadIdx.x == 0) tr[k] = globaltimer();
   };
-  stamp(0);
+  stamp(kTrStart);
   double bh[kMaxCpt];
   int64_t col[kMaxCpt];
   int nc = 0;
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
     for (int i = 0; i < kMaxCpt; ++i)
       if (i < nc) ll_send(dst + 2 * col[i], R.yl[col[i]], ep);
   }
-  stamp(1);
+  stamp(kTrYSent);
 #pragma unroll
   for (int i = 0; i < kMaxCpt; ++i) {
     if (i >= nc) continue;
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
     if (left >= 0) ok = ok && ll_recv(mine + OFF_Y + 2 * j, ep, deadline, &ylp);
     bh[i] = R.bt[j] - A.l * ylp - A.u * R.yf[j];
   }
-  stamp(2);
+  stamp(kTrYRecv);
   // ---- (a3) reduced-system schedule: PCR stages, or detach / PCR / fold /
   //      reattach for cyclic non-power-of-two p; the fold is the last PCR step ----
   for (int s = 0; s < q && ok; ++s) {
@@ -194,8 +194,9 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
 #pragma unroll
     for (int i = 0; i < kMaxCpt; ++i)
       if (i < nc) bh[i] = S.w * bh[i] - S.c0 * u[0][i] - S.c1 * u[1][i];
+    stamp(kTrStep0 + s);
   }
-  stamp(3);
+  // (per-step stamps inside the loop)
   // ---- (a4) x~_i -> left neighbour; back-substitution on the window ----
   if (ok && left >= 0) {
     unsigned long long* dst = R.peer_mbox[left] + copy_off + OFF_X;
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
     if (threadIdx.x == 0) R.epoch[slice] = ep;
     return;
   }
-  stamp(4);
+  stamp(kTrXRecv);
   // x~_i into row 0 of this slab and x~_{i+1} into the next-plane; the window pass (k_window)
   // follows as its own high-occupancy launch
 #pragma unroll
@@ -228,7 +229,7 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
   }
   __syncthreads();  // every thread has read this solve's epoch
   if (threadIdx.x == 0) R.epoch[slice] = ep;
-  if (tr) stamp(5);
+  if (tr) stamp(kTrEnd);
 }
 
 // All-gather variant of (a2)-(a3) (CTRI_FLAG_ALLGATHER): one exchange round
@@ -247,11 +248,11 @@ __global__ void __launch_bounds__(kP2PThreads, 1)
   const int64_t copy_off = (int64_t)(ep & 1u) * A.copy_words;
   const bool cyc = A.cyclic != 0;
   unsigned long long* const mine = R.mbox + copy_off;
-  unsigned long long* tr = A.trace ? A.trace + (size_t)blockIdx.x * 8 : nullptr;
+  unsigned long long* tr = A.trace ? A.trace + (size_t)blockIdx.x * kP2PTrace : nullptr;
   auto stamp = [&](int k) {
     if (tr && threadIdx.x == 0) tr[k] = globaltimer();
   };
-  stamp(0);
+  stamp(kTrStart);
   bool ok = true;
   const int64_t n = A.lay.n, inner = A.lay.inner;
   // ---- (a2)+(a3) as ONE round: c_i = b~_i - u y_i[first] and y_i[last] go to
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(kP2PThreads, 1)
       ll_send(dst + (int64_t)(p + rank) * 2 * m + 2 * j, yl, ep);
     }
   }
-  stamp(1);
+  stamp(kTrYSent);
 #pragma unroll 1
   for (int64_t j = c0 + threadIdx.x; j < c1 && ok; j += kP2PThreads) {  // 2 x 8 loads in flight
     double c[kMaxAG], y[kMaxAG];
@@ -302,7 +303,9 @@ __global__ void __launch_bounds__(kP2PThreads, 1)
   if (!ok) atomicExch(A.err, 1);
   __syncthreads();
   if (threadIdx.x == 0) R.epoch[slice] = ep;
-  for (int k = 2; k < 6; ++k) stamp(k);
+  stamp(kTrYRecv);
+  stamp(kTrXRecv);
+  stamp(kTrEnd);
 }
 
 // Pentadiagonal (r = 2) reduced phase, all-gather form (SURVEY 8(f) N3 + N4): per column every

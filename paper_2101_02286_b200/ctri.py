@@ -26,7 +26,7 @@ CTRI_FLAG_NCCL_ROUNDS = 1 << 4
 CTRI_FLAG_ALLGATHER = 1 << 5
 CTRI_FLAG_FUSED_REDUCED = 1 << 6
 CTRI_MAX_STAGES = 16
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 STATUS = {0: "CTRI_OK", 1: "CTRI_ERR_INVALID_ARG", 2: "CTRI_ERR_UNSUPPORTED", 3: "CTRI_ERR_SINGULAR",
           4: "CTRI_ERR_PARTITION_TOO_SMALL", 5: "CTRI_ERR_CUDA", 6: "CTRI_ERR_NCCL",
@@ -70,7 +70,10 @@ class ctri_stats(ctypes.Structure):
                 ("reduced_path", ctypes.c_int32), ("device_error", ctypes.c_int32),
                 ("vparts", ctypes.c_int32), ("grid_ctas", ctypes.c_int32),
                 ("detach_stages", ctypes.c_int32), ("detached_rows", ctypes.c_int32),
-                ("band_halfwidth", ctypes.c_int32)]
+                ("band_halfwidth", ctypes.c_int32),
+                ("t_reduced_kernel_us", ctypes.c_float), ("t_window_us", ctypes.c_float),
+                ("t_p2p_y_us", ctypes.c_float), ("t_p2p_step_us", ctypes.c_float * CTRI_MAX_STAGES),
+                ("t_p2p_x_us", ctypes.c_float), ("p2p_steps", ctypes.c_int32)]
 
     def as_dict(self):
         d = {}
@@ -80,6 +83,7 @@ class ctri_stats(ctypes.Structure):
                 v = list(v)
             d[name] = v
         d["t_stage_us"] = d["t_stage_us"][: max(0, self.pcr_stages)]
+        d["t_p2p_step_us"] = d["t_p2p_step_us"][: max(0, self.p2p_steps)]
         return d
 
 
