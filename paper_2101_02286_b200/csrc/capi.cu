@@ -354,6 +354,7 @@ void p2p_args(const Plan& P0, P2PArgs* A) {
   A->p = P0.p;
   A->q = (int)P0.sched.steps.size();
   A->allgather = P0.allgather ? 1 : 0;
+  A->pdl = (!P0.loopback && std::getenv("CTRI_NO_PDL") == nullptr) ? 1 : 0;
   A->copy_words = p2p_copy_words(P0.lay.m(), A->q, P0.p, P0.allgather || P0.r == 2, P0.r == 2 ? 4 : 2);
   A->cyclic = P0.cyclic;
   A->nslices = P0.p2p_nslices;

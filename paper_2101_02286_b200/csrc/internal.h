@@ -162,6 +162,7 @@ struct P2PRank {
 struct P2PArgs {
   int p, q, cyclic, nslices, full;  // q = number of schedule steps
   int allgather;                    // 1: one all-gather round + A^{-1} rows instead of the schedule
+  int pdl;                          // launched with programmatic stream serialization
   int64_t slice_cols, m, W;
   int64_t copy_words;               // mailbox words of one epoch copy of the reduced-phase region
   Layout lay;

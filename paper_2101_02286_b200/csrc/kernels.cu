@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -125,8 +126,9 @@ struct WindowArgs {
   const double *S, *R, *next;
   int64_t outer, nv, inner, W, rows;
   int vp, full, wrap;
+  int pdl;  // launched with programmatic stream serialization: wait for the previous kernel
 };
-constexpr int kWinRows = 8;
+constexpr int kWinRows = 8, kWinBatches = 3;
 
 __device__ __forceinline__ int64_t window_row(const WindowArgs& A, int64_t ry) {
   return A.full ? ry + 1 : (ry < A.W ? ry + 1 : A.nv - 2 * A.W + ry);
@@ -134,6 +136,7 @@ __device__ __forceinline__ int64_t window_row(const WindowArgs& A, int64_t ry) {
 
 // strided axis (inner > 1): block = 256 consecutive columns x kWinRows rows of one slab
 __global__ void __launch_bounds__(256) k_window(const WindowArgs A) {
+  if (A.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");  // launched early (PDL)
   const int64_t j = blockIdx.x * 256ll + threadIdx.x;
   const int64_t m = A.outer * A.inner;
   if (j >= m) return;
@@ -146,17 +149,21 @@ __global__ void __launch_bounds__(256) k_window(const WindowArgs A) {
   if (s + 1 < A.vp) xn = xs[sl];
   else if (A.next) xn = A.next[j];
   else if (A.wrap) xn = A.x[o * A.vp * sl + c];
-  const int64_t r0 = (int64_t)blockIdx.y * kWinRows;
-  double v[kWinRows];
+  // kWinBatches batches of kWinRows rows per thread: the grid stays within about one wave
+  for (int bt = 0; bt < kWinBatches; ++bt) {
+    const int64_t r0 = ((int64_t)blockIdx.y * kWinBatches + bt) * kWinRows;
+    if (r0 >= A.rows) break;
+    double v[kWinRows];
 #pragma unroll
-  for (int u = 0; u < kWinRows; ++u)
-    if (r0 + u < A.rows) v[u] = xs[window_row(A, r0 + u) * A.inner];
+    for (int u = 0; u < kWinRows; ++u)
+      if (r0 + u < A.rows) v[u] = xs[window_row(A, r0 + u) * A.inner];
 #pragma unroll
-  for (int u = 0; u < kWinRows; ++u)
-    if (r0 + u < A.rows) {
-      const int64_t r = window_row(A, r0 + u);
-      dev::st_global_cs(xs + r * A.inner, v[u] - __ldg(A.S + r - 1) * xa - __ldg(A.R + r - 1) * xn);
-    }
+    for (int u = 0; u < kWinRows; ++u)
+      if (r0 + u < A.rows) {
+        const int64_t r = window_row(A, r0 + u);
+        dev::st_global_cs(xs + r * A.inner, v[u] - __ldg(A.S + r - 1) * xa - __ldg(A.R + r - 1) * xn);
+      }
+  }
 }
 
 // contiguous axis (inner == 1): one warp per column, lanes along the (contiguous) rows
@@ -204,14 +211,28 @@ cudaError_t launch_window(const Plan& P, double* x, const double* next, cudaStre
   A.rows = A.full ? A.nv - 1 : 2 * A.W;
   A.vp = P.vp;
   A.wrap = (P.p == 1 && P.cyclic) ? 1 : 0;
+  A.pdl = 0;
   if (A.rows <= 0) return cudaSuccess;
   if (A.inner == 1) {
     const int64_t warps = A.outer * A.vp;
     k_window_contig<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(A);
   } else {
     const int64_t m = P.lay.m();
-    dim3 grid((unsigned)((m + 255) / 256), (unsigned)((A.rows + kWinRows - 1) / kWinRows), (unsigned)A.vp);
-    k_window<<<grid, 256, 0, s>>>(A);
+    const int64_t rpb = (int64_t)kWinRows * kWinBatches;
+    dim3 grid((unsigned)((m + 255) / 256), (unsigned)((A.rows + rpb - 1) / rpb), (unsigned)A.vp);
+    // after the P2P kernel (nparts > 1): programmatic dependent launch, so the window grid is
+    // staged while the reduced-phase kernel drains (the kernel waits before touching x)
+    A.pdl = (P.p > 1 && std::getenv("CTRI_NO_PDL") == nullptr) ? 1 : 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = A.pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k_window, A);
   }
   return cudaGetLastError();
 }

@@ -96,6 +96,7 @@ __device__ __forceinline__ bool ll_recv_batch(const unsigned long long* src, int
 
 __global__ void __launch_bounds__(kP2PThreads, 2)
     k_reduced_p2p(const P2PArgs A) {
+  if (A.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");  // launched early (PDL)
   const int r_local = blockIdx.x / A.nslices;
   const int slice = blockIdx.x - r_local * A.nslices;
   const P2PRank& R = A.rk[r_local];
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
 // instead of 2 + log2 p dependent ones; its own kernel so each variant keeps its registers.
 __global__ void __launch_bounds__(kP2PThreads, 1)
     k_reduced_allgather(const P2PArgs A) {
+  if (A.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");  // launched early (PDL)
   const int r_local = blockIdx.x / A.nslices;
   const int slice = blockIdx.x - r_local * A.nslices;
   const P2PRank& R = A.rk[r_local];
@@ -408,10 +410,16 @@ cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t
   cfg.blockDim = dim3(kP2PThreads, 1, 1);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (they wait on each other)
-  attr[0].val.cooperative = 1;
+  if (nranks_launch > 1) {  // loopback: all CTAs co-resident (they wait on each other)
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.numAttrs = 1;
+  } else if (A.pdl) {  // one rank per launch: staged while the tile kernel drains (PDL)
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 1;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = nranks_launch > 1 ? 1 : 0;  // one rank per launch: the grid fits anyway
   return A.allgather ? cudaLaunchKernelEx(&cfg, k_reduced_allgather, A)
                      : cudaLaunchKernelEx(&cfg, k_reduced_p2p, A);
 }
