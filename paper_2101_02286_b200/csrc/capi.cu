@@ -354,7 +354,7 @@ void p2p_args(const Plan& P0, P2PArgs* A) {
   A->p = P0.p;
   A->q = (int)P0.sched.steps.size();
   A->allgather = P0.allgather ? 1 : 0;
-  A->pdl = (!P0.loopback && std::getenv("CTRI_NO_PDL") == nullptr) ? 1 : 0;
+  A->pdl = (!P0.loopback && !knob_no_pdl()) ? 1 : 0;
   A->copy_words = p2p_copy_words(P0.lay.m(), A->q, P0.p, P0.allgather || P0.r == 2, P0.r == 2 ? 4 : 2);
   A->cyclic = P0.cyclic;
   A->nslices = P0.p2p_nslices;
@@ -597,7 +597,7 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
     P2PArgs A;
     p2p_args(P0, &A);
     const int grid = A.nslices * (int)G.size();
-    const bool env_trace = std::getenv("CTRI_P2P_TRACE") != nullptr;
+    const bool env_trace = knob_p2p_trace();
     if ((env_trace || !P0.ev.empty()) && !P0.d_trace) {  // per-round stamps (CTRI_FLAG_TIMING)
       CUDA_TRY(cudaMalloc(&P0.d_trace, sizeof(unsigned long long) * kP2PTrace * grid));
       CUDA_TRY(cudaMemsetAsync(P0.d_trace, 0, sizeof(unsigned long long) * kP2PTrace * grid, s));

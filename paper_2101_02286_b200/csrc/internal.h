@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -266,6 +267,14 @@ struct Plan {
   bool timed_valid = false;
   int launches_per_solve = 0;
 };
+
+// Measurement / experiment knobs read once per process (the per-solve launch path must not
+// scan the environment): CTRI_NO_PDL, CTRI_P2P_TRACE, CTRI_TILE_TRACE, CTRI_TILE_COPY_ONLY.
+inline bool env_knob(const char* name) { return std::getenv(name) != nullptr; }
+inline bool knob_no_pdl() { static const bool v = env_knob("CTRI_NO_PDL"); return v; }
+inline bool knob_p2p_trace() { static const bool v = env_knob("CTRI_P2P_TRACE"); return v; }
+inline bool knob_tile_trace() { static const bool v = env_knob("CTRI_TILE_TRACE"); return v; }
+inline bool knob_copy_only() { static const bool v = env_knob("CTRI_TILE_COPY_ONLY"); return v; }
 
 // kernels.cu launchers (return cudaError_t of the launch)
 cudaError_t launch_local_generic(const Plan& P, const double* b, double* x, cudaStream_t s);

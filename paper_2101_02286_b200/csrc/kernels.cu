@@ -222,7 +222,7 @@ cudaError_t launch_window(const Plan& P, double* x, const double* next, cudaStre
     dim3 grid((unsigned)((m + 255) / 256), (unsigned)((A.rows + rpb - 1) / rpb), (unsigned)A.vp);
     // after the P2P kernel (nparts > 1): programmatic dependent launch, so the window grid is
     // staged while the reduced-phase kernel drains (the kernel waits before touching x)
-    A.pdl = (P.p > 1 && std::getenv("CTRI_NO_PDL") == nullptr) ? 1 : 0;
+    A.pdl = (P.p > 1 && !knob_no_pdl()) ? 1 : 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(256, 1, 1);

@@ -883,12 +883,15 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
     cuuint32_t box[3] = {(cuuint32_t)tc.C, (cuuint32_t)std::min(rows_cta / tc.SUB, 256), 1};
     cuuint32_t hbox[3] = {(cuuint32_t)tc.C, 2, 1};  // stencil halo rows (fused derivative)
     cuuint32_t estr[3] = {1, 1, 1};
-    CUtensorMapL2promotion prom = CU_TENSOR_MAP_L2_PROMOTION_NONE;
-    if (const char* e = std::getenv("CTRI_TMA_L2_PROMOTION")) {  // measurement knob
-      if (!std::strcmp(e, "64")) prom = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
-      if (!std::strcmp(e, "128")) prom = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-      if (!std::strcmp(e, "256")) prom = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-    }
+    static const CUtensorMapL2promotion prom = [] {  // measurement knob, read once
+      CUtensorMapL2promotion v = CU_TENSOR_MAP_L2_PROMOTION_NONE;
+      if (const char* e = std::getenv("CTRI_TMA_L2_PROMOTION")) {
+        if (!std::strcmp(e, "64")) v = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+        if (!std::strcmp(e, "128")) v = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+        if (!std::strcmp(e, "256")) v = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+      }
+      return v;
+    }();
     CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(b), gdim,
                       gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                       CU_TENSOR_MAP_SWIZZLE_NONE, prom, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -912,7 +915,7 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   A.rows_box = std::min(rows_cta / tc.SUB, 256);
   A.stages = tc.pcr.stages;
   A.mode = (P.p > 1 || P.vp > 1) ? 1 : (P.cyclic ? 0 : 2);
-  if (std::getenv("CTRI_TILE_COPY_ONLY")) A.mode = 3;  // measurement knob: memory ceiling
+  if (knob_copy_only()) A.mode = 3;  // measurement knob: memory ceiling
   A.pcr_uniform = tc.pcr_uniform ? 1 : 0;
   for (int k = 0; k < kMaxUniformStages; ++k) {
     A.ualpha[k] = (tc.pcr_uniform && k < tc.pcr.stages) ? tc.pcr.alpha[(size_t)k * tc.Q] : 0.0;
@@ -920,7 +923,7 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   }
   A.uinv = tc.pcr.inv[0];
   A.trace = nullptr;
-  if (std::getenv("CTRI_TILE_TRACE")) {  // measurement only
+  if (knob_tile_trace()) {  // measurement only
     static unsigned long long* d_tr = nullptr;
     if (!d_tr) cudaMalloc(&d_tr, 64 * 16 * sizeof(unsigned long long));
     A.trace = d_tr;
