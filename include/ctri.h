@@ -279,6 +279,14 @@ ctri_status ctri_reduced_schedule(int P, int cyclic, const double* L, const doub
 ctri_status ctri_penta_factor_query(int64_t n, const double bands[5], double* SR, double* hat,
                                    int* window);
 
+/* Host-only: the 2x2-block PCR tables of the pentadiagonal reduced system (P partitions of n
+ * rows, cyclic P a power of two, acyclic any P >= 2): alpha / gamma [stages][P][4] and the final
+ * fold / diagonal inverse [P][4], row-major 2x2 (factor.h PentaPcr).  Arrays hold
+ * max_stages*P*4 (alpha, gamma) and P*4 (fold) doubles.  UNSUPPORTED for cyclic
+ * non-power-of-two P. */
+ctri_status ctri_penta_block_pcr(int P, int cyclic, int64_t n, const double bands[5], int max_stages,
+                                 double* alpha, double* gamma, double* fold, int* stages);
+
 /* Dense inverse of the P x P reduced matrix A^ (bands L, D, U per row; cyclic corners;
  * couplings that coincide for P <= 2 add up) into inv[P*P], row-major: the plan-time table of
  * the all-gather reduced solve (CTRI_FLAG_ALLGATHER).  Gauss-Jordan with

@@ -1262,6 +1262,24 @@ ctri_status ctri_penta_factor_query(int64_t n, const double bands[5], double* SR
   return CTRI_OK;
 }
 
+ctri_status ctri_penta_block_pcr(int P, int cyclic, int64_t n, const double bands[5], int max_stages,
+                                 double* alpha, double* gamma, double* fold, int* stages) {
+  if (!bands || !alpha || !gamma || !fold || !stages) return fail(CTRI_ERR_INVALID_ARG, "NULL argument");
+  Penta pt;
+  FactorError fe;
+  if (!penta_factor(n - 2, bands, &pt, &fe)) return fail((ctri_status)fe.code, fe.detail);
+  double mx = 0;
+  for (int k = 0; k < 5; ++k) mx = std::max(mx, std::fabs(bands[k]));
+  PentaPcr t;
+  if (!penta_block_pcr(P, cyclic != 0, pt, 1e-13 * mx, &t, &fe)) return fail((ctri_status)fe.code, fe.detail);
+  if (t.stages > max_stages) return fail(CTRI_ERR_INVALID_ARG, "max_stages too small");
+  std::memcpy(alpha, t.alpha.data(), sizeof(double) * t.alpha.size());
+  std::memcpy(gamma, t.gamma.data(), sizeof(double) * t.gamma.size());
+  std::memcpy(fold, t.fold.data(), sizeof(double) * t.fold.size());
+  *stages = t.stages;
+  return CTRI_OK;
+}
+
 ctri_status ctri_reduced_inverse(int P, int cyclic, const double* L, const double* D,
                                  const double* U, double* inv) {
   if (P < 1 || !L || !D || !U || !inv) return fail(CTRI_ERR_INVALID_ARG, "bad arguments");

@@ -276,6 +276,96 @@ bool penta_reduced_inverse(int P, bool cyclic, const Penta& pt, double guard, st
   return dense_inverse(n, a, guard, inv, err, "penta_reduced_inverse");
 }
 
+// 2x2 helpers (row-major)
+static void mm2(const double* a, const double* b, double* o) {
+  const double t0 = a[0] * b[0] + a[1] * b[2], t1 = a[0] * b[1] + a[1] * b[3];
+  const double t2 = a[2] * b[0] + a[3] * b[2], t3 = a[2] * b[1] + a[3] * b[3];
+  o[0] = t0, o[1] = t1, o[2] = t2, o[3] = t3;
+}
+static bool inv2(const double* a, double guard, double* o) {
+  const double det = a[0] * a[3] - a[1] * a[2];
+  const double sc = std::max(std::max(std::fabs(a[0]), std::fabs(a[1])), std::max(std::fabs(a[2]), std::fabs(a[3])));
+  if (!(std::fabs(det) >= guard * sc)) return false;
+  const double r = 1.0 / det;
+  const double t0 = a[3] * r, t1 = -a[1] * r, t2 = -a[2] * r, t3 = a[0] * r;
+  o[0] = t0, o[1] = t1, o[2] = t2, o[3] = t3;
+  return true;
+}
+
+bool penta_block_pcr(int P, bool cyclic, const Penta& pt, double guard, PentaPcr* out, FactorError* err) {
+  if (P < 2) return fail(err, kInvalid, "penta_block_pcr: P < 2");
+  if (cyclic && !is_pow2(P)) return fail(err, kUnsupported, "penta_block_pcr: cyclic P must be a power of two");
+  PentaPcr t;
+  t.P = P;
+  t.cyclic = cyclic;
+  std::vector<double> L(4 * (size_t)P), D(4 * (size_t)P), U(4 * (size_t)P);
+  for (int i = 0; i < P; ++i) {
+    const bool lft = cyclic || i > 0, rgt = cyclic || i < P - 1;
+    for (int e = 0; e < 4; ++e) {
+      L[4 * i + e] = lft ? pt.Lh[e] : 0.0;
+      D[4 * i + e] = lft ? pt.Dh[e] : pt.DhFirst[e];
+      U[4 * i + e] = rgt ? pt.Uh[e] : 0.0;
+    }
+  }
+  const int q = ilog2(P);  // cyclic: log2 P; acyclic: ceil(log2 P)
+  for (int k = 0; k < q; ++k) {
+    const int s = 1 << k;
+    std::vector<double> nL(L.size()), nD(D.size()), nU(U.size()), al(4 * (size_t)P, 0.0), ga(4 * (size_t)P, 0.0);
+    for (int i = 0; i < P; ++i) {
+      int im = i - s, ip = i + s;
+      if (cyclic) {
+        im = ((im % P) + P) % P;
+        ip = ip % P;
+      } else {
+        if (im < 0) im = -1;
+        if (ip >= P) ip = -1;
+      }
+      double Di[4], a[4] = {0, 0, 0, 0}, g[4] = {0, 0, 0, 0}, tmp[4];
+      for (int e = 0; e < 4; ++e) Di[e] = D[4 * i + e];
+      double Ln[4] = {0, 0, 0, 0}, Un[4] = {0, 0, 0, 0};
+      if (im >= 0) {
+        double inv[4];
+        if (!inv2(&D[4 * im], guard, inv)) return fail(err, kSingular, "penta_block_pcr: pivot guard");
+        mm2(&L[4 * i], inv, a);
+        mm2(a, &U[4 * im], tmp);
+        for (int e = 0; e < 4; ++e) Di[e] -= tmp[e];
+        mm2(a, &L[4 * im], Ln);
+        for (int e = 0; e < 4; ++e) Ln[e] = -Ln[e];
+      }
+      if (ip >= 0) {
+        double inv[4];
+        if (!inv2(&D[4 * ip], guard, inv)) return fail(err, kSingular, "penta_block_pcr: pivot guard");
+        mm2(&U[4 * i], inv, g);
+        mm2(g, &L[4 * ip], tmp);
+        for (int e = 0; e < 4; ++e) Di[e] -= tmp[e];
+        mm2(g, &U[4 * ip], Un);
+        for (int e = 0; e < 4; ++e) Un[e] = -Un[e];
+      }
+      for (int e = 0; e < 4; ++e) {
+        nD[4 * i + e] = Di[e];
+        nL[4 * i + e] = Ln[e];
+        nU[4 * i + e] = Un[e];
+        al[4 * i + e] = a[e];
+        ga[4 * i + e] = g[e];
+      }
+    }
+    L.swap(nL);
+    D.swap(nD);
+    U.swap(nU);
+    t.alpha.insert(t.alpha.end(), al.begin(), al.end());
+    t.gamma.insert(t.gamma.end(), ga.begin(), ga.end());
+  }
+  t.stages = q;
+  t.fold.assign(4 * (size_t)P, 0.0);
+  for (int i = 0; i < P; ++i) {
+    double m[4];
+    for (int e = 0; e < 4; ++e) m[e] = D[4 * i + e] + (cyclic ? L[4 * i + e] + U[4 * i + e] : 0.0);
+    if (!inv2(m, guard, &t.fold[4 * (size_t)i])) return fail(err, kSingular, "penta_block_pcr: fold pivot guard");
+  }
+  *out = std::move(t);
+  return true;
+}
+
 bool reduced_inverse(int P, bool cyclic, const std::vector<double>& L, const std::vector<double>& D,
                      const std::vector<double>& U, double guard, std::vector<double>* inv,
                      FactorError* err) {

@@ -115,6 +115,20 @@ int64_t penta_window(const Penta& p);
 bool penta_reduced_inverse(int P, bool cyclic, const Penta& pt, double guard, std::vector<double>* inv,
                            FactorError* err);
 
+// Block (2x2) PCR on the pentadiagonal reduced system (P:346 with r = 2): for stage k, s = 2^k,
+//   alpha_i = L_i D_{i-s}^{-1},  gamma_i = U_i D_{i+s}^{-1}   (partners i -+ s, mod P if cyclic)
+//   b_i <- b_i - alpha_i b_{i-s} - gamma_i b_{i+s}
+//   D_i <- D_i - alpha_i U_{i-s} - gamma_i L_{i+s},  L_i <- -alpha_i L_{i-s},  U_i <- -gamma_i U_{i+s}
+// Cyclic P = 2^q: after q stages the couplings point back at row i and are folded,
+// x~_i = (L_i + D_i + U_i)^{-1} b_i (reading R3 in block form); acyclic: ceil(log2 P) stages,
+// x~_i = D_i^{-1} b_i.  Tables are row-major 2x2: alpha / gamma [stage][row][4], fold [row][4].
+struct PentaPcr {
+  int P = 0, stages = 0;
+  bool cyclic = true;
+  std::vector<double> alpha, gamma, fold;
+};
+bool penta_block_pcr(int P, bool cyclic, const Penta& pt, double guard, PentaPcr* out, FactorError* err);
+
 inline bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 inline int ilog2(int64_t v) {
   int q = 0;

@@ -39,7 +39,7 @@ ABI_SYMBOLS = ("ctri_status_string", "ctri_last_error", "ctri_abi_version", "ctr
                "ctri_plan_destroy", "ctri_factor_query", "ctri_pcr_coefficients",
                "ctri_reduced_schedule", "ctri_compact_apply", "ctri_compact_apply_loopback",
                "ctri_reduced_inverse", "ctri_plan_create_penta", "ctri_plan_create_penta_loopback",
-               "ctri_penta_factor_query")
+               "ctri_penta_factor_query", "ctri_penta_block_pcr")
 
 
 class CtriError(RuntimeError):
@@ -130,6 +130,8 @@ def load(build_if_missing: bool = False):
         "ctri_plan_create_penta_loopback": (st, [ctypes.POINTER(P), ctypes.c_int, i64p, ctypes.c_int, dp,
                                                  ctypes.c_int, ctypes.c_uint32, P]),
         "ctri_penta_factor_query": (st, [ctypes.c_int64, dp, dp, dp, ctypes.POINTER(ctypes.c_int)]),
+        "ctri_penta_block_pcr": (st, [ctypes.c_int, ctypes.c_int, ctypes.c_int64, dp, ctypes.c_int, dp, dp, dp,
+                                      ctypes.POINTER(ctypes.c_int)]),
         "ctri_compact_apply_loopback": (st, [ctypes.POINTER(P), ctypes.c_int, dp, ctypes.POINTER(P),
                                              ctypes.POINTER(P), P]),
         "ctri_get_stats": (st, [P, ctypes.POINTER(ctri_stats)]),
@@ -257,6 +259,20 @@ def ctri_penta_factor_query(n: int, bands):
     blocks = hat.reshape(4, 2, 2)
     return {"S": S, "R": R, "Lh": blocks[0], "Dh": blocks[1], "Uh": blocks[2], "Dh_first": blocks[3],
             "window": w.value}
+
+
+def ctri_penta_block_pcr(P: int, n: int, bands, cyclic=True, max_stages=16):
+    """Host-only: 2x2-block PCR tables of the pentadiagonal reduced system (alpha, gamma, fold)."""
+    a = np.zeros(max_stages * P * 4)
+    g = np.zeros(max_stages * P * 4)
+    f = np.zeros(P * 4)
+    q = ctypes.c_int()
+    dp = ctypes.POINTER(ctypes.c_double)
+    _check(load().ctri_penta_block_pcr(int(P), int(bool(cyclic)), int(n), _dbl5(bands), int(max_stages),
+                                       a.ctypes.data_as(dp), g.ctypes.data_as(dp), f.ctypes.data_as(dp),
+                                       ctypes.byref(q)), "ctri_penta_block_pcr")
+    k = q.value
+    return a[:k * P * 4].reshape(k, P, 2, 2), g[:k * P * 4].reshape(k, P, 2, 2), f.reshape(P, 2, 2)
 
 
 def ctri_solve(plan: int, b, x, stream=None):

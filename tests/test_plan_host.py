@@ -349,3 +349,52 @@ def test_penta_window(bands):
 def test_penta_singular_guard():
     with pytest.raises(pk.CtriError, match="SINGULAR"):
         pk.ctri_penta_factor_query(20, (0.0, 1.0, 1.0, 1.0, 0.0))  # mu_1 = d - l u / d = 0
+
+
+def _run_block_pcr(alpha, gamma, fold, b, cyclic):
+    P, q = b.shape[0], alpha.shape[0]
+    b = b.copy()
+    for k in range(q):
+        s = 1 << k
+        nb = b.copy()
+        for i in range(P):
+            im, ip = i - s, i + s
+            if cyclic:
+                im, ip = im % P, ip % P
+            if im >= 0 and im < P:
+                nb[i] -= alpha[k, i] @ b[im]
+            if ip >= 0 and ip < P:
+                nb[i] -= gamma[k, i] @ b[ip]
+        b = nb
+    return np.stack([fold[i] @ b[i] for i in range(P)])
+
+
+@pytest.mark.parametrize("bands", PENTA_BANDS)
+@pytest.mark.parametrize("P,cyclic", [(2, True), (4, True), (8, True), (16, True), (2, False), (3, False),
+                                      (5, False), (8, False)])
+def test_penta_block_pcr_vs_dense(bands, P, cyclic):
+    """2x2-block PCR (+ fold) on the reduced system equals the dense solve of the Schur complement
+    (the block matrix [L^, D^, U^] of the plan tables), for wide and narrow partitions."""
+    for n in (8, 40):
+        t = pk.ctri_penta_factor_query(n, bands)
+        A = np.zeros((2 * P, 2 * P))
+        for i in range(P):
+            A[2 * i:2 * i + 2, 2 * i:2 * i + 2] += t["Dh"] if (cyclic or i > 0) else t["Dh_first"]
+            if cyclic or i > 0:
+                j = (i - 1) % P
+                A[2 * i:2 * i + 2, 2 * j:2 * j + 2] += t["Lh"]
+            if cyclic or i < P - 1:
+                j = (i + 1) % P
+                A[2 * i:2 * i + 2, 2 * j:2 * j + 2] += t["Uh"]
+        a, g, f = pk.ctri_penta_block_pcr(P, n, bands, cyclic)
+        assert a.shape[0] == math.ceil(math.log2(P))
+        rng = np.random.default_rng(P + n)
+        for _ in range(2):
+            b = rng.uniform(-1, 1, (P, 2))
+            x = _run_block_pcr(a, g, f, b, cyclic)
+            assert np.max(np.abs(x.ravel() - np.linalg.solve(A, b.ravel()))) < 1e-13
+
+
+def test_penta_block_pcr_rejects_cyclic_non_pow2():
+    with pytest.raises(pk.CtriError, match="UNSUPPORTED"):
+        pk.ctri_penta_block_pcr(3, 20, PENTA_BANDS[0], True)
