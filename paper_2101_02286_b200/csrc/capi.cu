@@ -70,7 +70,7 @@ void free_plan(Plan* P) {
                     P->bt,      P->yl_prev,   P->bh,       P->recv_m,    P->recv_p,  P->xt,
                     P->xt_next, P->halo_lo,   P->halo_hi,  P->send_lo,   P->send_hi, P->tile.d_pcr,
                     P->d_stage_b, P->d_stage_x, P->d_plu,    P->d_pSR,     P->d_ainv,  P->d_planes4,
-                    P->d_xnext2};
+                    P->d_xnext2, P->d_ppcr};
   for (double* b : bufs)
     if (b) cudaFree(b);
   for (cudaEvent_t e : P->ev) cudaEventDestroy(e);
@@ -297,9 +297,63 @@ ctri_status penta_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, co
   if (st != CTRI_OK) return fail(st, "pentadiagonal tables: " + why);
   const int64_t m = P->lay.m();
   if (p > 1) {
-    P->p2p_nslices = p2p_slices(m, P->loopback ? p : 1, P->num_sms, 2);
-    P->mbox_bytes = sizeof(unsigned long long) *
-                    p2p_mailbox_words(p2p_copy_words(m, 0, p, true, 4), m, false);
+    // pairwise 2x2-block PCR where it applies, else the one-round all-gather (R20)
+    P->ppcr = (!cyclic || is_pow2(p)) && !(flags & CTRI_FLAG_ALLGATHER);
+    int64_t copy_words = p2p_copy_words(m, 0, p, true, 4);
+    if (P->ppcr) {
+      double mx = 0;
+      for (int k = 0; k < 5; ++k) mx = std::max(mx, std::fabs(bands[k]));
+      PentaPcr t;
+      FactorError fe;
+      if (!penta_block_pcr(p, cyclic != 0, P->pt, 1e-13 * mx, &t, &fe)) return fail((ctri_status)fe.code, fe.detail);
+      const int q = t.stages;
+      P->ppcr_steps = q;
+      auto srcs = [&](int i, int k, int* s0, int* s1) {  // partners of row i in step k
+        const int sh = 1 << k;
+        int im = i - sh, ip = i + sh;
+        if (cyclic) {
+          im = ((im % p) + p) % p;
+          ip = ip % p;
+        } else {
+          if (im < 0) im = -1;
+          if (ip >= p) ip = -1;
+        }
+        if (im >= 0 && im == ip) ip = -1;  // single partner: A0 = alpha + gamma
+        *s0 = im;
+        *s1 = ip;
+      };
+      std::vector<double> tab;
+      P->pstep.assign(kMaxP2PSteps, P2PStep{1.0, 0.0, 0.0, -1, -1, -1, -1, 0, 0});
+      for (int k = 0; k < q; ++k) {
+        int s0, s1;
+        srcs(rank, k, &s0, &s1);
+        const double* al = &t.alpha[((size_t)k * p + rank) * 4];
+        const double* ga = &t.gamma[((size_t)k * p + rank) * 4];
+        for (int e = 0; e < 4; ++e) tab.push_back(s1 < 0 && s0 >= 0 && (cyclic && (1 << k) * 2 == p) ? al[e] + ga[e] : al[e]);
+        for (int e = 0; e < 4; ++e) tab.push_back(s1 >= 0 ? ga[e] : 0.0);
+        P2PStep& stp = P->pstep[k];
+        stp.src0 = (int8_t)s0;
+        stp.src1 = (int8_t)s1;
+        int nd = 0;
+        for (int r = 0; r < p; ++r) {
+          int r0, r1;
+          srcs(r, k, &r0, &r1);
+          for (int sl = 0; sl < 2; ++sl)
+            if ((sl ? r1 : r0) == rank) {
+              if (nd == 0) { stp.dst0 = (int8_t)r; stp.dslot0 = (int8_t)sl; }
+              else { stp.dst1 = (int8_t)r; stp.dslot1 = (int8_t)sl; }
+              ++nd;
+            }
+        }
+      }
+      for (int e = 0; e < 4; ++e) tab.push_back(t.fold[(size_t)rank * 4 + e]);
+      CUDA_TRY(cudaMalloc(&P->d_ppcr, sizeof(double) * tab.size()));
+      CUDA_TRY(cudaMemcpyAsync(P->d_ppcr, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice, s));
+      copy_words = (int64_t)(4 + 4 * q) * 2 * m;
+    }
+    P->p2p_nslices = p2p_slices(m, P->loopback ? p : 1, P->num_sms, P->ppcr ? 3 : 2);
+    P->p2p_copy = copy_words;
+    P->mbox_bytes = sizeof(unsigned long long) * p2p_mailbox_words(copy_words, m, false);
     CUDA_TRY(cudaMalloc(&P->mbox_alloc, P->mbox_bytes));
     CUDA_TRY(cudaMemsetAsync(P->mbox_alloc, 0, P->mbox_bytes, s));
     CUDA_TRY(cudaMalloc(&P->d_err, sizeof(int)));
@@ -356,6 +410,10 @@ void p2p_args(const Plan& P0, P2PArgs* A) {
   A->allgather = P0.allgather ? 1 : 0;
   A->pdl = (!P0.loopback && !knob_no_pdl()) ? 1 : 0;
   A->copy_words = p2p_copy_words(P0.lay.m(), A->q, P0.p, P0.allgather || P0.r == 2, P0.r == 2 ? 4 : 2);
+  if (P0.r == 2) {
+    A->copy_words = P0.p2p_copy;
+    A->q = P0.ppcr ? P0.ppcr_steps : 0;
+  }
   A->cyclic = P0.cyclic;
   A->nslices = P0.p2p_nslices;
   A->m = P0.lay.m();
@@ -394,6 +452,12 @@ void p2p_fill_rank(const Plan& P, double* x, P2PRank* R) {
     R->ag0[r] = P.ainv[(size_t)P.rank * P.p + r];
     if (nx < P.p || P.cyclic) R->ag1[r] = P.ainv[(size_t)(nx % P.p) * P.p + r];
   }
+  R->ppcr = P.d_ppcr;
+  if (P.r == 2) {
+    for (int s = 0; s < kMaxP2PSteps; ++s)
+      R->step[s] = s < (int)P.pstep.size() ? P.pstep[s] : P2PStep{1.0, 0.0, 0.0, -1, -1, -1, -1, 0, 0};
+    return;
+  }
   const Schedule& sc = P.sched;
   for (int s = 0; s < kMaxP2PSteps; ++s) {
     P2PStep& t = R->step[s];
@@ -418,6 +482,17 @@ void p2p_fill_rank(const Plan& P, double* x, P2PRank* R) {
 
 // messages this rank sends per solve, and dependent exchange rounds, from the schedule
 void schedule_counts(const Plan& P, int* sends, int* rounds) {
+  if (P.r == 2 && P.ppcr) {  // y, block-PCR steps (2 planes per message), x
+    int sd = (has_right(P) ? 2 : 0) + (has_left(P) ? 2 : 0), rd = 2;
+    for (int k = 0; k < P.ppcr_steps; ++k) {
+      const P2PStep& t = P.pstep[k];
+      sd += 2 * ((t.dst0 >= 0 ? 1 : 0) + (t.dst1 >= 0 ? 1 : 0));
+      ++rd;
+    }
+    *sends = sd;
+    *rounds = rd;
+    return;
+  }
   if (P.allgather || P.r == 2) {  // one round: 2 (4 for r = 2) planes to each of the p - 1 peers
     *sends = 2 * P.r * (P.p - 1);
     *rounds = 1;
@@ -680,7 +755,8 @@ ctri_status penta_solve_group(std::vector<Plan*>& G, const double* const* b, dou
     P2PArgs A;
     p2p_args(P0, &A);
     for (size_t r = 0; r < G.size(); ++r) p2p_fill_rank(*G[r], x[r], &A.rk[r]);
-    cudaError_t e = launch_reduced_allgather_r2(A, (int)G.size(), s);
+    cudaError_t e = P0.ppcr ? launch_reduced_penta_pcr(A, (int)G.size(), s)
+                            : launch_reduced_allgather_r2(A, (int)G.size(), s);
     if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("penta reduced: ") + cudaGetErrorString(e));
   }
   for (size_t r = 0; r < G.size(); ++r) {
@@ -1080,7 +1156,7 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
   out->tile_columns = P->local_kernel ? P->tile.C : 1;
   out->tile_variant = P->local_kernel ? P->tile.variant : -1;
   out->tile_stages = P->local_kernel ? P->tile.STAGES : 0;
-  out->reduced_path = P->fused ? 3 : (P->p > 1 && P->p2p) ? ((P->allgather || P->r == 2) ? 2 : 1) : 0;
+  out->reduced_path = P->fused ? 3 : (P->p > 1 && P->p2p) ? ((P->allgather || (P->r == 2 && !P->ppcr)) ? 2 : 1) : 0;
   out->band_halfwidth = P->r;
   out->vparts = P->vp;
   out->grid_ctas = P->local_kernel ? P->tile.grid : (int32_t)((P->tlay.m() + 127) / 128);

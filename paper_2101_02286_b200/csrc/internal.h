@@ -159,6 +159,7 @@ struct P2PRank {
   double ag0[kMaxAG], ag1[kMaxAG];  // all-gather mode: rows i and i+1 of A^{-1} (zeros past p)
   const double* planes4;         // pentadiagonal all-gather: [4][m] c0 | c1 | w0 | w1
   const double* ainv;            // pentadiagonal all-gather: [2p][2p] reduced inverse
+  const double* ppcr;            // pentadiagonal pairwise: this rank's [step][8] A0 | A1, fold [4]
 };
 struct P2PArgs {
   int p, q, cyclic, nslices, full;  // q = number of schedule steps
@@ -174,8 +175,10 @@ struct P2PArgs {
   P2PRank rk[kMaxP2PRanks];
 };
 cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s);
-int p2p_slices(int64_t m, int nranks_launch, int num_sms, int kind);  // 0 schedule, 1 all-gather, 2 penta
+int p2p_slices(int64_t m, int nranks_launch, int num_sms, int kind);  // 0 schedule, 1 all-gather,
+                                                                       // 2 penta all-gather, 3 penta PCR
 cudaError_t launch_reduced_allgather_r2(const P2PArgs& A, int nranks_launch, cudaStream_t s);
+cudaError_t launch_reduced_penta_pcr(const P2PArgs& A, int nranks_launch, cudaStream_t s);
 int64_t p2p_copy_words(int64_t m, int q, int p, bool allgather, int planes = 2);
 size_t p2p_mailbox_words(int64_t copy_words, int64_t m, bool halo);
 cudaError_t launch_halo_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s);
@@ -260,6 +263,11 @@ struct Plan {
   double *d_ainv = nullptr;        // [2p][2p] reduced inverse (p > 1)
   double *d_planes4 = nullptr;     // [4][m]: c0 | c1 | w0 | w1  (c = b~ - U~ y_i, w = L~ y_i)
   double *d_xnext2 = nullptr;      // [2][m]: x~_{i+1}
+  bool ppcr = false;               // pairwise 2x2-block PCR reduced solve (else all-gather)
+  int ppcr_steps = 0;
+  double *d_ppcr = nullptr;        // this rank's [step][8] A0 | A1 and fold [4]
+  std::vector<P2PStep> pstep;      // this rank's partners per block-PCR step
+  int64_t p2p_copy = 0;            // mailbox words per epoch copy (pentadiagonal plans)
 
   // stats
   uint64_t solves = 0;

@@ -391,6 +391,193 @@ __global__ void __launch_bounds__(kP2PThreads, 1)
   if (threadIdx.x == 0) R.epoch[slice] = ep;
 }
 
+// Pentadiagonal (r = 2) reduced phase, pairwise (P:346 with 2x2 blocks, reading R20): the
+// y round sends w = L~ y_i[last two] right, b^_i = c_i - w_{i-1}; then ceil(log2 p) block-PCR
+// steps b^_i <- b^_i - A0 b^_{src0} - A1 b^_{src1} (2x2 matrices from factor.h PentaPcr; a single
+// partner when i - s = i + s), the fold x~_i = F_i b^_i, and the x~ round from the right.
+// Every message is a 2-vector of LL words; R.step[] carries the partners, R.ppcr the matrices
+// ([step][8]: A0 | A1, then the fold [4]).
+__global__ void __launch_bounds__(kP2PThreads, 2)
+    k_reduced_penta_pcr(const P2PArgs A) {
+  if (A.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");  // launched early (PDL)
+  const int r_local = blockIdx.x / A.nslices;
+  const int slice = blockIdx.x - r_local * A.nslices;
+  const P2PRank& R = A.rk[r_local];
+  const int p = A.p, q = A.q, rank = R.rank;
+  const int64_t m = A.m;
+  const int64_t c0 = (int64_t)slice * A.slice_cols;
+  const int64_t c1 = std::min<int64_t>(m, c0 + A.slice_cols);
+  const uint32_t ep = R.epoch[slice] + 1u;
+  const unsigned long long deadline = globaltimer() + 20ull * 1000000000ull;  // 20 s
+  const int64_t copy_off = (int64_t)(ep & 1u) * A.copy_words;
+  // copy: [y: 2 planes][step k: 2 slots x 2 planes][x: 2 planes] of 2m LL words
+  auto OFF_Y = [&](int pl) -> int64_t { return (int64_t)pl * 2 * m; };
+  auto OFF_S = [&](int k, int slot, int pl) -> int64_t { return (int64_t)(2 + 4 * k + 2 * slot + pl) * 2 * m; };
+  auto OFF_X = [&](int pl) -> int64_t { return (int64_t)(2 + 4 * q + pl) * 2 * m; };
+  const bool cyc = A.cyclic != 0;
+  const int right = cyc ? (rank + 1) % p : (rank + 1 < p ? rank + 1 : -1);
+  const int left = cyc ? (rank + p - 1) % p : (rank > 0 ? rank - 1 : -1);
+  unsigned long long* const mine = R.mbox + copy_off;
+  unsigned long long* tr = A.trace ? A.trace + (size_t)blockIdx.x * kP2PTrace : nullptr;
+  auto stamp = [&](int k) {
+    if (tr && threadIdx.x == 0) tr[k] = globaltimer();
+  };
+  stamp(kTrStart);
+  double b0[kMaxCpt], b1[kMaxCpt];
+  int64_t col[kMaxCpt];
+  int nc = 0;
+#pragma unroll
+  for (int i = 0; i < kMaxCpt; ++i) {
+    const int64_t j = c0 + threadIdx.x + (int64_t)i * kP2PThreads;
+    col[i] = j;
+    if (j < c1) nc = i + 1;
+  }
+  bool ok = true;
+  // receive the 2-vectors of `nc` columns from mailbox offsets o0 / o1 (batched sweep)
+  auto recv2 = [&](int64_t o0, int64_t o1, double (&v0)[kMaxCpt], double (&v1)[kMaxCpt]) {
+    uint32_t pend = 0;
+#pragma unroll
+    for (int i = 0; i < kMaxCpt; ++i)
+      if (i < nc) pend |= 3u << (2 * i);
+    int spins = 0;
+    while (pend && ok) {
+      unsigned long long w0[2 * kMaxCpt], w1[2 * kMaxCpt];
+#pragma unroll
+      for (int k = 0; k < 2 * kMaxCpt; ++k)
+        if (pend & (1u << k)) dev::ll_load(mine + ((k & 1) ? o1 : o0) + 2 * col[k >> 1], &w0[k], &w1[k]);
+#pragma unroll
+      for (int k = 0; k < 2 * kMaxCpt; ++k)
+        if ((pend & (1u << k)) && dev::ll_ready(w0[k], w1[k], ep)) {
+          const double v = dev::ll_value(w0[k], w1[k]);
+          if (k & 1) v1[k >> 1] = v;
+          else v0[k >> 1] = v;
+          pend &= ~(1u << k);
+        }
+      if (pend && ++spins == 64) {
+        spins = 0;
+        if (globaltimer() > deadline) ok = false;
+      }
+    }
+  };
+  // ---- (a2) w_i = L~ y_i[last two] -> right neighbour; b^_i = c_i - w_{i-1} ----
+  if (right >= 0) {
+    unsigned long long* dst = R.peer_mbox[right] + copy_off;
+#pragma unroll
+    for (int i = 0; i < kMaxCpt; ++i)
+      if (i < nc) {
+        dev::ll_store(dst + OFF_Y(0) + 2 * col[i], R.planes4[2 * m + col[i]], ep);
+        dev::ll_store(dst + OFF_Y(1) + 2 * col[i], R.planes4[3 * m + col[i]], ep);
+      }
+  }
+  stamp(kTrYSent);
+  {
+    double w0[kMaxCpt], w1[kMaxCpt];
+#pragma unroll
+    for (int i = 0; i < kMaxCpt; ++i) w0[i] = w1[i] = 0.0;
+    if (left >= 0) recv2(OFF_Y(0), OFF_Y(1), w0, w1);
+#pragma unroll
+    for (int i = 0; i < kMaxCpt; ++i)
+      if (i < nc) {
+        b0[i] = R.planes4[col[i]] - w0[i];
+        b1[i] = R.planes4[m + col[i]] - w1[i];
+      }
+  }
+  stamp(kTrYRecv);
+  // ---- (a3) block PCR steps ----
+  for (int st = 0; st < q && ok; ++st) {
+    const P2PStep& S = R.step[st];
+    for (int d = 0; d < 2; ++d) {
+      const int dst = d ? S.dst1 : S.dst0, slot = d ? S.dslot1 : S.dslot0;
+      if (dst < 0) continue;
+      unsigned long long* dp = R.peer_mbox[dst] + copy_off;
+#pragma unroll
+      for (int i = 0; i < kMaxCpt; ++i)
+        if (i < nc) {
+          dev::ll_store(dp + OFF_S(st, slot, 0) + 2 * col[i], b0[i], ep);
+          dev::ll_store(dp + OFF_S(st, slot, 1) + 2 * col[i], b1[i], ep);
+        }
+    }
+    double u0[kMaxCpt], u1[kMaxCpt], v0[kMaxCpt], v1[kMaxCpt];
+#pragma unroll
+    for (int i = 0; i < kMaxCpt; ++i) u0[i] = u1[i] = v0[i] = v1[i] = 0.0;
+    if (S.src0 >= 0) recv2(OFF_S(st, 0, 0), OFF_S(st, 0, 1), u0, u1);
+    if (S.src1 >= 0) recv2(OFF_S(st, 1, 0), OFF_S(st, 1, 1), v0, v1);
+    const double* M = R.ppcr + 8 * st;  // A0 (row-major 2x2) | A1
+    const double a00 = M[0], a01 = M[1], a10 = M[2], a11 = M[3];
+    const double g00 = M[4], g01 = M[5], g10 = M[6], g11 = M[7];
+#pragma unroll
+    for (int i = 0; i < kMaxCpt; ++i)
+      if (i < nc) {
+        const double n0 = b0[i] - (a00 * u0[i] + a01 * u1[i]) - (g00 * v0[i] + g01 * v1[i]);
+        const double n1 = b1[i] - (a10 * u0[i] + a11 * u1[i]) - (g10 * v0[i] + g11 * v1[i]);
+        b0[i] = n0;
+        b1[i] = n1;
+      }
+    stamp(kTrStep0 + st);
+  }
+  // fold: x~_i = F_i b^_i
+  {
+    const double* F = R.ppcr + 8 * q;
+#pragma unroll
+    for (int i = 0; i < kMaxCpt; ++i)
+      if (i < nc) {
+        const double x0 = F[0] * b0[i] + F[1] * b1[i];
+        const double x1 = F[2] * b0[i] + F[3] * b1[i];
+        b0[i] = x0;
+        b1[i] = x1;
+      }
+  }
+  // ---- (a4) x~_i -> left neighbour; x~_{i+1} from the right ----
+  if (ok && left >= 0) {
+    unsigned long long* dst = R.peer_mbox[left] + copy_off;
+#pragma unroll
+    for (int i = 0; i < kMaxCpt; ++i)
+      if (i < nc) {
+        dev::ll_store(dst + OFF_X(0) + 2 * col[i], b0[i], ep);
+        dev::ll_store(dst + OFF_X(1) + 2 * col[i], b1[i], ep);
+      }
+  }
+  double xn0[kMaxCpt], xn1[kMaxCpt];
+#pragma unroll
+  for (int i = 0; i < kMaxCpt; ++i) xn0[i] = xn1[i] = 0.0;
+  if (ok && right >= 0) recv2(OFF_X(0), OFF_X(1), xn0, xn1);
+  stamp(kTrXRecv);
+  if (!ok) atomicExch(A.err, 1);
+  const int64_t n = A.lay.n, inner = A.lay.inner;
+#pragma unroll
+  for (int i = 0; i < kMaxCpt; ++i)
+    if (i < nc) {
+      const int64_t j = col[i];
+      const int64_t o = j / inner, cc = j - o * inner;
+      R.x[o * n * inner + cc] = b0[i];
+      R.x[(o * n + 1) * inner + cc] = b1[i];
+      R.xnext[j] = xn0[i];
+      R.xnext[m + j] = xn1[i];
+    }
+  __syncthreads();
+  if (threadIdx.x == 0) R.epoch[slice] = ep;
+  if (tr) stamp(kTrEnd);
+}
+
+cudaError_t launch_reduced_penta_pcr(const P2PArgs& A, int nranks_launch, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(A.nslices * nranks_launch), 1, 1);
+  cfg.blockDim = dim3(kP2PThreads, 1, 1);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  if (nranks_launch > 1) {
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.numAttrs = 1;
+  } else if (A.pdl) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 1;
+  }
+  cfg.attrs = attr;
+  return cudaLaunchKernelEx(&cfg, k_reduced_penta_pcr, A);
+}
+
 cudaError_t launch_reduced_allgather_r2(const P2PArgs& A, int nranks_launch, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(A.nslices * nranks_launch), 1, 1);
@@ -426,9 +613,10 @@ cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t
 
 int p2p_slices(int64_t m, int nranks_launch, int num_sms, int kind) {
   // one wave: <= resident CTAs in total, <= kMaxCpt columns per thread
-  const bool allgather = kind != 0;
+  const bool allgather = kind == 1 || kind == 2;  // 0 and 3 keep <= kMaxCpt columns per thread
   const void* fn = kind == 0 ? (const void*)k_reduced_p2p
-                 : kind == 1 ? (const void*)k_reduced_allgather : (const void*)k_reduced_allgather_r2;
+                 : kind == 1 ? (const void*)k_reduced_allgather
+                 : kind == 2 ? (const void*)k_reduced_allgather_r2 : (const void*)k_reduced_penta_pcr;
   int per_sm = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kP2PThreads, 0) !=
           cudaSuccess || per_sm < 1) {

@@ -65,6 +65,8 @@ def test_penta_matches_oracle(p, cyclic, bands):
     x, st = penta_gpu(b, 0, p, bands, cyclic, return_stats=True)
     ref = oracle.penta_solve(b, 0, bands, cyclic)
     assert st["band_halfwidth"] == 2
+    if p > 1:  # pairwise block PCR where it applies (power-of-two or acyclic), else all-gather
+        assert st["reduced_path"] == (1 if (not cyclic or (p & (p - 1)) == 0) else 2), st
     assert rel_err(x, ref, 0) < TOL_REL
     assert penta_residual(x, b, 0, bands, cyclic) < 1e-13
 
@@ -113,3 +115,15 @@ def test_penta_unsupported():
         ctri.LoopbackGroup((64, 2, 8), 0, 2, BANDS[0], True, CTRI_FLAG_NCCL_ROUNDS)
     with pytest.raises(ctri.CtriError, match="PARTITION_TOO_SMALL"):
         ctri.LoopbackGroup((20, 2, 8), 0, 4, BANDS[0])
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_penta_pairwise_equals_allgather(p):
+    """The two reduced-system solvers (2x2-block PCR, A^-1 all-gather) agree to rounding."""
+    from paper_2101_02286_b200 import CTRI_FLAG_ALLGATHER
+    b = workloads.uniform((16 * p, 2, 24), 120 + p)
+    x1, s1 = penta_gpu(b, 0, p, BANDS[2], True, return_stats=True)
+    x2, s2 = penta_gpu(b, 0, p, BANDS[2], True, CTRI_FLAG_ALLGATHER, return_stats=True)
+    assert s1["reduced_path"] == 1 and s2["reduced_path"] == 2
+    assert np.max(np.abs(x1 - x2)) < 1e-13 * np.max(np.abs(x2))
+
