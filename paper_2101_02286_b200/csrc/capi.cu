@@ -754,10 +754,18 @@ ctri_status penta_solve_group(std::vector<Plan*>& G, const double* const* b, dou
   if (P0.p > 1) {
     P2PArgs A;
     p2p_args(P0, &A);
+    const int grid = A.nslices * (int)G.size();
+    if (!P0.ev.empty() && !P0.d_trace) {  // per-round stamps (CTRI_FLAG_TIMING)
+      CUDA_TRY(cudaMalloc(&P0.d_trace, sizeof(unsigned long long) * kP2PTrace * grid));
+      CUDA_TRY(cudaMemsetAsync(P0.d_trace, 0, sizeof(unsigned long long) * kP2PTrace * grid, s));
+      P0.trace_ctas = grid;
+    }
+    A.trace = P0.d_trace;
     for (size_t r = 0; r < G.size(); ++r) p2p_fill_rank(*G[r], x[r], &A.rk[r]);
     cudaError_t e = P0.ppcr ? launch_reduced_penta_pcr(A, (int)G.size(), s)
                             : launch_reduced_allgather_r2(A, (int)G.size(), s);
     if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("penta reduced: ") + cudaGetErrorString(e));
+    record(P0, EV_XX, s);
   }
   for (size_t r = 0; r < G.size(); ++r) {
     cudaError_t e = launch_penta_window(*G[r], x[r], s);
@@ -1190,10 +1198,8 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
     if (P->p > 1 && P->p2p && !P->fused) {
       out->t_backsub_us = elapsed(*P, EV_LOCAL, EV_BACK);  // (a2)-(a4): P2P kernel + window pass
       out->t_total_us = elapsed(*P, EV_START, EV_BACK);
-      if (P->r == 1) {
-        out->t_reduced_kernel_us = elapsed(*P, EV_LOCAL, EV_XX);
-        out->t_window_us = elapsed(*P, EV_XX, EV_BACK);
-      }
+      out->t_reduced_kernel_us = elapsed(*P, EV_LOCAL, EV_XX);
+      out->t_window_us = elapsed(*P, EV_XX, EV_BACK);
       if (P->d_trace && P->trace_ctas > 0) {  // per-round medians over the CTAs of this rank
         const int grid = P->trace_ctas;
         std::vector<unsigned long long> t((size_t)kP2PTrace * grid);
@@ -1208,7 +1214,8 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
           std::nth_element(v.begin(), v.begin() + v.size() / 2, v.end());
           return (float)v[v.size() / 2];
         };
-        const int q = P->allgather ? 0 : (int)P->sched.steps.size();
+        const int q = P->r == 2 ? (P->ppcr ? P->ppcr_steps : 0)
+                                : (P->allgather ? 0 : (int)P->sched.steps.size());
         out->p2p_steps = q;
         out->t_p2p_y_us = med(kTrStart, kTrYRecv);
         int prev = kTrYRecv;
