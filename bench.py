@@ -405,6 +405,7 @@ def main():
                            "k_penta_local (column-serial, 32 B/pt moved)" if st["local_kernel"] == 3
                            else "k_local_generic"),
                 "algorithmic_bytes_per_launch": bytes_local, "launch_us": t_local,
+                "frac_nominal_8tbs": achieved / 8000.0,
                 "peak_source": peak_src}
         cpu = None if args.no_cpu_baseline else cpu_oracle_sample(args.config)
         launches = st["launches_per_solve"] * args.steps + (args.steps * 0)
@@ -420,6 +421,7 @@ def main():
                            "local_kernel": roof["kernel"],
                            "launch": "host launches" if args.no_graph else "one CUDA graph per solve"},
                 "pct_hbm_roofline": 100.0 * step_gbs / peak,
+                "pct_nominal_8tbs": 100.0 * step_gbs / 8000.0,  # north star: >= 60% of ~8 TB/s
                 "step_gbs": step_gbs,
                 "roofline": roof,
                 "cpu_baseline": cpu,
