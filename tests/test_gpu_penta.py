@@ -127,3 +127,17 @@ def test_penta_pairwise_equals_allgather(p):
     assert s1["reduced_path"] == 1 and s2["reduced_path"] == 2
     assert np.max(np.abs(x1 - x2)) < 1e-13 * np.max(np.abs(x2))
 
+
+
+@pytest.mark.parametrize("r", [0, 1, 2, 15, 16, 17, 18, 63])
+@pytest.mark.parametrize("cyclic", [True, False])
+def test_penta_delta_at_partition_edges(r, cyclic):
+    """A unit impulse on (and next to) the interface rows of a partition: the couplings through
+    S, R, L~, U~ and the 2x2 reduced blocks are all exercised (p = 4, n = 16)."""
+    N, p = 64, 4
+    b = np.zeros((N, 1, 8))
+    b[r] = 1.0
+    for bands in BANDS:
+        x = penta_gpu(b, 0, p, bands, cyclic)
+        ref = oracle.penta_solve(b, 0, bands, cyclic)
+        assert np.max(np.abs(x - ref)) < 1e-14 * max(1.0, np.max(np.abs(ref)))
