@@ -139,11 +139,26 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
     if (vp_env) want = std::atoi(vp_env);
     if (want > 1 && want <= 8 && is_pow2(want) && n % want == 0 && n / want >= 512) P->vp = want;
   }
+  // nparts > 1: "virtual rows" -- every rank's slab is solved as vp partitions too and the
+  // reduced system has nparts * vp rows, exchanged over the same LL P2P path (rows on the same
+  // GPU exchange through its own mailbox).  Strided axis with outer == 1 (solve index 0),
+  // slabs of >= 4096 rows -> partitions of 2048 rows (clusters of 8 with 256-byte rows).
+  if (p > 1 && !(flags & (CTRI_FLAG_DERIV | CTRI_FLAG_NCCL_ROUNDS | CTRI_FLAG_ALLGATHER |
+                          CTRI_FLAG_FUSED_REDUCED)) &&
+      P->lay.outer == 1 && P->lay.inner >= 16) {
+    int want = n >= 4096 ? (int)std::min<int64_t>(4, n / 2048) : 1;
+    if (vp_env) want = std::atoi(vp_env);
+    // (the knob may go down to 16-row partitions: tests use them to make the reduced couplings
+    // between virtual rows large enough to see)
+    if (want > 1 && want <= 8 && is_pow2(want) && n % want == 0 && n / want >= (vp_env ? 16 : 512) &&
+        p * want <= kMaxP2PRanks)
+      P->vp = want;
+  }
   P->tlay = P->lay;
   P->tlay.outer = P->lay.outer * P->vp;
   P->tlay.n = n / P->vp;
   const int64_t nv = P->tlay.n;
-  const int pr = (p > 1) ? p : P->vp;  // rows of the reduced system
+  const int pr = p * P->vp;  // rows of the reduced system (virtual partitions included)
 
   // ---- pre-factorisation ----
   FactorError fe;
@@ -225,16 +240,18 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   if (p > 1 && p <= kMaxP2PRanks && !(flags & CTRI_FLAG_NCCL_ROUNDS)) {
     // device-initiated reduced phase: double-buffered mailbox + epoch flags
     const int q = (int)P->sched.steps.size();
-    P->p2p_nslices = p2p_slices(m, P->loopback ? p : 1, P->num_sms, P->allgather ? 1 : 0);
+    // one mailbox (two epoch copies) per virtual row of this rank
+    P->p2p_nslices = p2p_slices(m, (P->loopback ? p : 1) * P->vp, P->num_sms, P->allgather ? 1 : 0);
+    P->p2p_vrow_words = 2 * p2p_copy_words(m, q, pr, P->allgather);
     P->mbox_bytes = sizeof(unsigned long long) *
-                    ((size_t)P->p2p_off +
-                     p2p_mailbox_words(p2p_copy_words(m, q, p, P->allgather), m, (flags & CTRI_FLAG_DERIV) != 0));
+                    ((size_t)P->p2p_off + (size_t)P->vp * P->p2p_vrow_words +
+                     ((flags & CTRI_FLAG_DERIV) ? p2p_mailbox_words(0, m, true) : 0));
     CUDA_TRY(cudaMalloc(&P->mbox_alloc, P->mbox_bytes));
     CUDA_TRY(cudaMemsetAsync(P->mbox_alloc, 0, P->mbox_bytes, s));
     CUDA_TRY(cudaMalloc(&P->d_err, sizeof(int)));
     CUDA_TRY(cudaMemsetAsync(P->d_err, 0, sizeof(int), s));
-    CUDA_TRY(cudaMalloc(&P->d_epoch, sizeof(unsigned int) * P->p2p_nslices));
-    CUDA_TRY(cudaMemsetAsync(P->d_epoch, 0, sizeof(unsigned int) * P->p2p_nslices, s));
+    CUDA_TRY(cudaMalloc(&P->d_epoch, sizeof(unsigned int) * P->p2p_nslices * P->vp));
+    CUDA_TRY(cudaMemsetAsync(P->d_epoch, 0, sizeof(unsigned int) * P->p2p_nslices * P->vp, s));
     P->p2p = true;
   }
   if (flags & CTRI_FLAG_DERIV) {
@@ -405,11 +422,11 @@ ctri_status p2p_connect_ipc(Plan* P, cudaStream_t s) {
 
 void p2p_args(const Plan& P0, P2PArgs* A) {
   std::memset(A, 0, sizeof(*A));
-  A->p = P0.p;
+  A->p = P0.p * P0.vp;  // reduced rows: nparts x virtual partitions
   A->q = (int)P0.sched.steps.size();
   A->allgather = P0.allgather ? 1 : 0;
-  A->pdl = (!P0.loopback && !knob_no_pdl()) ? 1 : 0;
-  A->copy_words = p2p_copy_words(P0.lay.m(), A->q, P0.p, P0.allgather || P0.r == 2, P0.r == 2 ? 4 : 2);
+  A->pdl = (!P0.loopback && P0.vp == 1 && !knob_no_pdl()) ? 1 : 0;
+  A->copy_words = p2p_copy_words(P0.lay.m(), A->q, A->p, P0.allgather || P0.r == 2, P0.r == 2 ? 4 : 2);
   if (P0.r == 2) {
     A->copy_words = P0.p2p_copy;
     A->q = P0.ppcr ? P0.ppcr_steps : 0;
@@ -428,23 +445,30 @@ void p2p_args(const Plan& P0, P2PArgs* A) {
   A->err = P0.d_err;
 }
 
-void p2p_fill_rank(const Plan& P, double* x, P2PRank* R) {
-  R->rank = P.rank;
-  R->x = x;
-  R->yf = P.yf;
-  R->yl = P.yl;
-  R->bt = P.bt;
-  R->xnext = P.r == 2 ? P.d_xnext2 : P.xt_next;
+// Row `v` of this rank's virtual partitions (v = 0 without them): global reduced row
+// rank * vp + v, its slab at row v * n_v (outer == 1 whenever vp > 1 with nparts > 1), its
+// plane segment, mailbox and epochs.
+void p2p_fill_rank(const Plan& P, double* x, P2PRank* R, int v = 0) {
+  const int vp = P.vp, pr = P.p * vp;
+  const int64_t m = P.lay.m();
+  const int g = P.rank * vp + v;
+  R->rank = g;
+  R->x = x ? x + (int64_t)v * P.tlay.n * P.lay.inner : nullptr;
+  R->yf = P.yf + (int64_t)v * m;
+  R->yl = P.yl + (int64_t)v * m;
+  R->bt = P.bt + (int64_t)v * m;
+  R->xnext = P.r == 2 ? P.d_xnext2 : P.xt_next + (int64_t)v * m;
   R->planes4 = P.d_planes4;
   R->ainv = P.d_ainv;
-  R->mbox = reinterpret_cast<unsigned long long*>(P.mbox_alloc) + P.p2p_off;
-  R->epoch = P.d_epoch;
+  R->mbox = reinterpret_cast<unsigned long long*>(P.mbox_alloc) + P.p2p_off + (int64_t)v * P.p2p_vrow_words;
+  R->epoch = P.d_epoch + (int64_t)v * P.p2p_nslices;
   R->f = nullptr;
   R->halo_lo = P.halo_lo;
   R->halo_hi = P.halo_hi;
   for (int r = 0; r < kMaxP2PRanks; ++r) R->peer_mbox[r] = nullptr;
-  for (int r = 0; r < P.p; ++r)
-    R->peer_mbox[r] = reinterpret_cast<unsigned long long*>(P.peer_alloc[r]) + P.p2p_off;
+  for (int r = 0; r < pr; ++r)
+    R->peer_mbox[r] = reinterpret_cast<unsigned long long*>(P.peer_alloc[r / vp]) + P.p2p_off +
+                      (int64_t)(r % vp) * P.p2p_vrow_words;
   for (int r = 0; r < kMaxAG; ++r) {
     R->ag0[r] = R->ag1[r] = 0.0;
     if (!P.allgather || r >= P.p) continue;
@@ -463,16 +487,16 @@ void p2p_fill_rank(const Plan& P, double* x, P2PRank* R) {
     P2PStep& t = R->step[s];
     t = P2PStep{1.0, 0.0, 0.0, -1, -1, -1, -1, 0, 0};
     if (s >= (int)sc.steps.size()) continue;
-    const SchedEntry& e = sc.steps[s][P.rank];
+    const SchedEntry& e = sc.steps[s][g];
     t.w = e.w;
     t.c0 = e.c[0];
     t.c1 = e.c[1];
     t.src0 = (int8_t)e.src[0];
     t.src1 = (int8_t)e.src[1];
-    int nd = 0;  // ranks that read this rank's value in step s, and their slot
-    for (int i = 0; i < P.p; ++i)
+    int nd = 0;  // rows that read this row's value in step s, and their slot
+    for (int i = 0; i < pr; ++i)
       for (int k = 0; k < 2; ++k)
-        if (sc.steps[s][i].src[k] == P.rank) {
+        if (sc.steps[s][i].src[k] == g) {
           if (nd == 0) { t.dst0 = (int8_t)i; t.dslot0 = (int8_t)k; }
           else { t.dst1 = (int8_t)i; t.dslot1 = (int8_t)k; }
           ++nd;
@@ -498,14 +522,25 @@ void schedule_counts(const Plan& P, int* sends, int* rounds) {
     *rounds = 1;
     return;
   }
+  // messages leaving this GPU (its vp virtual rows to rows of other ranks), dependent rounds
   const Schedule& sc = P.sched;
-  int sd = (has_right(P) ? 1 : 0) + (has_left(P) ? 1 : 0), rd = 2;
+  const int vp = P.vp, pr = P.p * vp;
+  auto owner = [&](int row) { return row / vp; };
+  int sd = 0, rd = 2;
+  for (int v = 0; v < vp; ++v) {
+    const int g = P.rank * vp + v;
+    const int rt = P.cyclic ? (g + 1) % pr : (g + 1 < pr ? g + 1 : -1);
+    const int lt = P.cyclic ? (g + pr - 1) % pr : (g > 0 ? g - 1 : -1);
+    if (rt >= 0 && owner(rt) != P.rank) ++sd;  // y round
+    if (lt >= 0 && owner(lt) != P.rank) ++sd;  // x~ round
+  }
   for (size_t s = 0; s < sc.steps.size(); ++s) {
     bool any = false;
-    for (int i = 0; i < P.p; ++i)
+    for (int i = 0; i < pr; ++i)
       for (int k = 0; k < 2; ++k) {
-        if (sc.steps[s][i].src[k] >= 0) any = true;
-        if (sc.steps[s][i].src[k] == P.rank) ++sd;
+        const int src = sc.steps[s][i].src[k];
+        if (src >= 0) any = true;
+        if (src >= 0 && owner(src) == P.rank && owner(i) != P.rank) ++sd;
       }
     rd += any ? 1 : 0;
   }
@@ -671,7 +706,8 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
   if (P0.p2p) {  // fused device-initiated (a2)-(a4)
     P2PArgs A;
     p2p_args(P0, &A);
-    const int grid = A.nslices * (int)G.size();
+    const int nrows = (int)G.size() * P0.vp;  // rows launched together (ranks x virtual rows)
+    const int grid = A.nslices * nrows;
     const bool env_trace = knob_p2p_trace();
     if ((env_trace || !P0.ev.empty()) && !P0.d_trace) {  // per-round stamps (CTRI_FLAG_TIMING)
       CUDA_TRY(cudaMalloc(&P0.d_trace, sizeof(unsigned long long) * kP2PTrace * grid));
@@ -679,12 +715,13 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
       P0.trace_ctas = grid;
     }
     A.trace = P0.d_trace;
-    for (size_t r = 0; r < G.size(); ++r) p2p_fill_rank(*G[r], x[r], &A.rk[r]);
-    cudaError_t e = launch_reduced_p2p(A, (int)G.size(), s);
+    for (size_t r = 0; r < G.size(); ++r)
+      for (int v = 0; v < P0.vp; ++v) p2p_fill_rank(*G[r], x[r], &A.rk[r * P0.vp + v], v);
+    cudaError_t e = launch_reduced_p2p(A, nrows, s);
     if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("p2p reduced kernel: ") + cudaGetErrorString(e));
     record(P0, EV_XX, s);
-    for (size_t r = 0; r < G.size(); ++r) {  // (a4) window pass of every rank
-      e = launch_window(*G[r], x[r], G[r]->xt_next, s);
+    for (size_t r = 0; r < G.size(); ++r) {  // (a4) window pass of every rank (all its slabs)
+      e = launch_window(*G[r], x[r], G[r]->xt_next + (int64_t)(G[r]->vp - 1) * G[r]->lay.m(), s);
       if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("window: ") + cudaGetErrorString(e));
     }
     if (P0.d_trace && env_trace) {  // measurement only: per-phase spread across CTAs on stderr

@@ -239,6 +239,7 @@ struct Plan {
   double fg0[8] = {0}, fg1[8] = {0};   // fused: rows rank, rank + 1 of A^{-1}
   unsigned int* d_fctr = nullptr;      // fused: [epoch, CTA completion count]
   int64_t p2p_off = 0;                 // words before the P2P-kernel region of the mailbox
+  int64_t p2p_vrow_words = 0;          // mailbox words per virtual row (both epoch copies)
   void* mbox_alloc = nullptr;          // own LL mailbox (cudaMalloc, IPC-exported)
   unsigned int* d_epoch = nullptr;     // per-slice solve epochs of the fused P2P kernel
   size_t mbox_bytes = 0;

@@ -473,3 +473,30 @@ def test_cfg5_full_size_sampled():
     plan.close()
     assert _sampled_columns(f, df, sd, fn=lambda a: oracle.deriv(a, 0, h=2 * math.pi / dims[sd])) < TOL_REL
 
+
+
+@pytest.mark.parametrize("p,vp", [(2, 2), (2, 4), (3, 2), (4, 2), (4, 4)])
+@pytest.mark.parametrize("bands,cyclic", [((0.45, 1.0, 0.45), True), (NONSYM, False), (SYM, True)])
+def test_virtual_rows_multi_partition(p, vp, bands, cyclic, monkeypatch):
+    """nparts > 1 with virtual partitions: nparts * vp reduced rows over the LL P2P path (rows
+    of one GPU through its own mailbox), 16-row partitions so every coupling matters; p = 3
+    with vp = 2 is the cyclic 6-row detach / reattach schedule."""
+    monkeypatch.setenv("CTRI_VPARTS", str(vp))
+    b = workloads.uniform((16 * vp * p, 1, 40), 11 + p)
+    x, st = check(b, 0, p, bands, cyclic)
+    assert st["vparts"] == vp and st["reduced_path"] == 1
+
+
+@pytest.mark.parametrize("r", [0, 15, 16, 17, 31, 32, 63, 64, 127])
+def test_virtual_rows_green_function(r, monkeypatch):
+    """Unit impulse at virtual and real partition edges (p = 2, vp = 4, 16-row partitions)."""
+    monkeypatch.setenv("CTRI_VPARTS", "4")
+    N, p, alpha = 128, 2, 0.45
+    b = np.zeros((N, 1, 16))
+    b[r] = 1.0
+    x = gpu_solve(b, 0, p, (alpha, 1.0, alpha))[:, 0, 0]
+    s = math.sqrt(1 - 4 * alpha * alpha)
+    lam = (-1 + s) / (2 * alpha)
+    d = (np.arange(N) - r) % N
+    expect = (lam ** d + lam ** (N - d)) / (s * (1 - lam ** N))
+    assert np.max(np.abs(x - expect)) < 1e-13
