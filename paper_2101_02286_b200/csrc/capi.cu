@@ -130,6 +130,7 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   // local-solve clusters are small enough to occupy every GPC
   P->vp = 1;
   const char* vp_env = std::getenv("CTRI_VPARTS");  // measurement knob (any axis)
+  if (vp_env && !*vp_env) vp_env = nullptr;        // set but empty: default rule
   if (p == 1 && !(flags & CTRI_FLAG_DERIV) && (P->lay.inner >= 16 || P->lay.inner == 1 || vp_env)) {
     // measured: virtual slabs of 1024 rows (clusters of 4) are fastest for n >= 4096 on a
     // strided axis; 2048 rows (clusters of 2, 4 partitions at n = 8192) on the contiguous axis
@@ -141,12 +142,14 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   }
   // nparts > 1: "virtual rows" -- every rank's slab is solved as vp partitions too and the
   // reduced system has nparts * vp rows, exchanged over the same LL P2P path (rows on the same
-  // GPU exchange through its own mailbox).  Strided axis with outer == 1 (solve index 0),
-  // slabs of >= 4096 rows -> partitions of 2048 rows (clusters of 8 with 256-byte rows).
+  // GPU exchange through its own mailbox).  Strided axis with outer == 1 (solve index 0): as
+  // with one partition, partitions of 1024 rows (measured cfg2: N = 2 0.967 -> 0.890 ms with
+  // vp = 4, N = 4 0.478 -> 0.466 ms with vp = 2).
   if (p > 1 && !(flags & (CTRI_FLAG_DERIV | CTRI_FLAG_NCCL_ROUNDS | CTRI_FLAG_ALLGATHER |
                           CTRI_FLAG_FUSED_REDUCED)) &&
       P->lay.outer == 1 && P->lay.inner >= 16) {
-    int want = n >= 4096 ? (int)std::min<int64_t>(4, n / 2048) : 1;
+    int want = n >= 2048 ? (int)std::min<int64_t>(8, n / 1024) : 1;
+    while (want > 1 && p * want > kMaxP2PRanks) want /= 2;
     if (vp_env) want = std::atoi(vp_env);
     // (the knob may go down to 16-row partitions: tests use them to make the reduced couplings
     // between virtual rows large enough to see)
