@@ -428,7 +428,7 @@ void p2p_args(const Plan& P0, P2PArgs* A) {
   A->p = P0.p * P0.vp;  // reduced rows: nparts x virtual partitions
   A->q = (int)P0.sched.steps.size();
   A->allgather = P0.allgather ? 1 : 0;
-  A->pdl = (!P0.loopback && P0.vp == 1 && !knob_no_pdl()) ? 1 : 0;
+  A->pdl = (!P0.loopback && !knob_no_pdl()) ? 1 : 0;
   A->copy_words = p2p_copy_words(P0.lay.m(), A->q, A->p, P0.allgather || P0.r == 2, P0.r == 2 ? 4 : 2);
   if (P0.r == 2) {
     A->copy_words = P0.p2p_copy;
@@ -720,7 +720,9 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
     A.trace = P0.d_trace;
     for (size_t r = 0; r < G.size(); ++r)
       for (int v = 0; v < P0.vp; ++v) p2p_fill_rank(*G[r], x[r], &A.rk[r * P0.vp + v], v);
-    cudaError_t e = launch_reduced_p2p(A, nrows, s);
+    // loopback: one cooperative grid for all ranks; real ranks: the virtual rows' CTAs are
+    // co-resident by construction (p2p_slices sizes one wave), launched with PDL
+    cudaError_t e = launch_reduced_p2p(A, P0.loopback ? nrows : 1, s, nrows);
     if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("p2p reduced kernel: ") + cudaGetErrorString(e));
     record(P0, EV_XX, s);
     for (size_t r = 0; r < G.size(); ++r) {  // (a4) window pass of every rank (all its slabs)

@@ -174,7 +174,8 @@ struct P2PArgs {
   unsigned long long* trace;  // CTRI_FLAG_TIMING / CTRI_P2P_TRACE: [grid][kP2PTrace] stamps
   P2PRank rk[kMaxP2PRanks];
 };
-cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s);
+// nranks_launch > 1: cooperative (loopback); nrows: rows launched (ranks x virtual rows)
+cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s, int nrows = 1);
 int p2p_slices(int64_t m, int nranks_launch, int num_sms, int kind);  // 0 schedule, 1 all-gather,
                                                                        // 2 penta all-gather, 3 penta PCR
 cudaError_t launch_reduced_allgather_r2(const P2PArgs& A, int nranks_launch, cudaStream_t s);

@@ -591,9 +591,9 @@ cudaError_t launch_reduced_allgather_r2(const P2PArgs& A, int nranks_launch, cud
   return cudaLaunchKernelEx(&cfg, k_reduced_allgather_r2, A);
 }
 
-cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s) {
+cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t s, int nrows) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(A.nslices * nranks_launch), 1, 1);
+  cfg.gridDim = dim3((unsigned)(A.nslices * std::max(nranks_launch, nrows)), 1, 1);
   cfg.blockDim = dim3(kP2PThreads, 1, 1);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
