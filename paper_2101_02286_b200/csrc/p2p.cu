@@ -122,17 +122,21 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
     if (tr && threadIdx.x == 0) tr[k] = globaltimer();
   };
   stamp(kTrStart);
+  bool ok = true;
+  const int64_t n = A.lay.n, inner = A.lay.inner;
+  // the slice's columns in batches of kMaxCpt per thread (one batch unless the grid had to be
+  // capped to a single wave of co-resident CTAs)
+  for (int64_t b0 = c0; b0 < c1 && ok; b0 += (int64_t)kP2PThreads * kMaxCpt) {
+  const int64_t b1 = std::min<int64_t>(c1, b0 + (int64_t)kP2PThreads * kMaxCpt);
   double bh[kMaxCpt];
   int64_t col[kMaxCpt];
   int nc = 0;
 #pragma unroll
   for (int i = 0; i < kMaxCpt; ++i) {
-    const int64_t j = c0 + threadIdx.x + (int64_t)i * kP2PThreads;
+    const int64_t j = b0 + threadIdx.x + (int64_t)i * kP2PThreads;
     col[i] = j;
-    if (j < c1) nc = i + 1;
+    if (j < b1) nc = i + 1;
   }
-  bool ok = true;
-  const int64_t n = A.lay.n, inner = A.lay.inner;
   // ---- (a2) y_i[last] -> right neighbour; b^ ----
   if (right >= 0) {
     unsigned long long* dst = R.peer_mbox[right] + copy_off + OFF_Y;
@@ -213,9 +217,7 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
   }
   if (!ok) {
     atomicExch(A.err, 1);
-    __syncthreads();
-    if (threadIdx.x == 0) R.epoch[slice] = ep;
-    return;
+    break;
   }
   stamp(kTrXRecv);
   // x~_i into row 0 of this slab and x~_{i+1} into the next-plane; the window pass (k_window)
@@ -228,6 +230,7 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
     R.x[o * n * inner + c] = bh[i];
     R.xnext[j] = xb[i];
   }
+  }  // column batches
   __syncthreads();  // every thread has read this solve's epoch
   if (threadIdx.x == 0) R.epoch[slice] = ep;
   if (tr) stamp(kTrEnd);
@@ -423,16 +426,19 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
     if (tr && threadIdx.x == 0) tr[k] = globaltimer();
   };
   stamp(kTrStart);
+  bool ok = true;
+  // the slice's columns in batches of kMaxCpt per thread (see k_reduced_p2p)
+  for (int64_t cb0 = c0; cb0 < c1 && ok; cb0 += (int64_t)kP2PThreads * kMaxCpt) {
+  const int64_t cb1 = std::min<int64_t>(c1, cb0 + (int64_t)kP2PThreads * kMaxCpt);
   double b0[kMaxCpt], b1[kMaxCpt];
   int64_t col[kMaxCpt];
   int nc = 0;
 #pragma unroll
   for (int i = 0; i < kMaxCpt; ++i) {
-    const int64_t j = c0 + threadIdx.x + (int64_t)i * kP2PThreads;
+    const int64_t j = cb0 + threadIdx.x + (int64_t)i * kP2PThreads;
     col[i] = j;
-    if (j < c1) nc = i + 1;
+    if (j < cb1) nc = i + 1;
   }
-  bool ok = true;
   // receive the 2-vectors of `nc` columns from mailbox offsets o0 / o1 (batched sweep)
   auto recv2 = [&](int64_t o0, int64_t o1, double (&v0)[kMaxCpt], double (&v1)[kMaxCpt]) {
     uint32_t pend = 0;
@@ -554,6 +560,7 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
       R.xnext[j] = xn0[i];
       R.xnext[m + j] = xn1[i];
     }
+  }  // column batches
   __syncthreads();
   if (threadIdx.x == 0) R.epoch[slice] = ep;
   if (tr) stamp(kTrEnd);
@@ -612,8 +619,7 @@ cudaError_t launch_reduced_p2p(const P2PArgs& A, int nranks_launch, cudaStream_t
 }
 
 int p2p_slices(int64_t m, int nranks_launch, int num_sms, int kind) {
-  // one wave: <= resident CTAs in total, <= kMaxCpt columns per thread
-  const bool allgather = kind == 1 || kind == 2;  // 0 and 3 keep <= kMaxCpt columns per thread
+  // one wave: <= resident CTAs in total (the schedule kernels batch wider slices)
   const void* fn = kind == 0 ? (const void*)k_reduced_p2p
                  : kind == 1 ? (const void*)k_reduced_allgather
                  : kind == 2 ? (const void*)k_reduced_allgather_r2 : (const void*)k_reduced_penta_pcr;
@@ -625,8 +631,8 @@ int p2p_slices(int64_t m, int nranks_launch, int num_sms, int kind) {
   }
   const int64_t cap = std::max<int64_t>(1, (int64_t)per_sm * num_sms / nranks_launch);
   int64_t ns = std::min<int64_t>(cap, (m + kP2PThreads - 1) / kP2PThreads);
-  if (!allgather)  // the schedule kernel keeps <= kMaxCpt columns per thread in registers
-    while ((m + ns - 1) / ns > (int64_t)kP2PThreads * kMaxCpt) ++ns;
+  // one wave of co-resident CTAs always (rows of one GPU wait on each other); the schedule
+  // kernels loop over batches of kMaxCpt columns per thread when a slice is wider
   return (int)std::max<int64_t>(1, ns);
 }
 

@@ -500,3 +500,26 @@ def test_virtual_rows_green_function(r, monkeypatch):
     d = (np.arange(N) - r) % N
     expect = (lam ** d + lam ** (N - d)) / (s * (1 - lam ** N))
     assert np.max(np.abs(x - expect)) < 1e-13
+
+
+@pytest.mark.parametrize("p", [8, 6])
+def test_cfg2_full_size_loopback_partitions(p):
+    """The BASELINE grid split into p partitions (loopback on one GPU: the driver's N = 8
+    scaling run, and a non-power-of-two split), sampled columns vs the oracle."""
+    import torch
+
+    from paper_2101_02286_b200 import ctri
+    dims = (8192 if p == 8 else 6144, 256, 256)
+    dev = torch.device("cuda:0")
+    b = workloads.device_uniform(dims, 2, dev)
+    n = dims[0] // p
+    bs = [b[r * n:(r + 1) * n].contiguous() for r in range(p)]
+    xs = [torch.empty_like(t) for t in bs]
+    g = ctri.LoopbackGroup(dims, 0, p)
+    g.solve(bs, xs)
+    torch.cuda.synchronize()
+    st = g.stats(0)
+    g.close()
+    x = torch.cat(xs, 0)
+    assert st["reduced_path"] == 1 and st["device_error"] == 0
+    assert _sampled_columns(b, x, 0, n_cols=128) < TOL_REL
