@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(kP2PThreads, 1)
 // partner when i - s = i + s), the fold x~_i = F_i b^_i, and the x~ round from the right.
 // Every message is a 2-vector of LL words; R.step[] carries the partners, R.ppcr the matrices
 // ([step][8]: A0 | A1, then the fold [4]).
-__global__ void __launch_bounds__(kP2PThreads, 2)
+__global__ void __launch_bounds__(kP2PThreads, 1)
     k_reduced_penta_pcr(const P2PArgs A) {
   if (A.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");  // launched early (PDL)
   const int r_local = blockIdx.x / A.nslices;
