@@ -333,6 +333,11 @@ __global__ void __launch_bounds__(kP2PThreads, 1)
   unsigned long long* const mine = R.mbox + copy_off;
   const int64_t n = A.lay.n, inner = A.lay.inner;
   const int nx = rank + 1 < p ? rank + 1 : (cyc ? 0 : -1);  // owner of x~_{i+1}
+  unsigned long long* tr = A.trace ? A.trace + (size_t)blockIdx.x * kP2PTrace : nullptr;
+  auto stamp = [&](int k) {
+    if (tr && threadIdx.x == 0) tr[k] = globaltimer();
+  };
+  stamp(kTrStart);
   bool ok = true;
 #pragma unroll 1
   for (int64_t j = c0 + threadIdx.x; j < c1; j += kP2PThreads) {
@@ -390,8 +395,11 @@ __global__ void __launch_bounds__(kP2PThreads, 1)
     R.xnext[m + j] = xn1;
   }
   if (!ok) atomicExch(A.err, 1);
+  stamp(kTrYRecv);  // the single all-gather round
+  stamp(kTrXRecv);
   __syncthreads();
   if (threadIdx.x == 0) R.epoch[slice] = ep;
+  stamp(kTrEnd);
 }
 
 // Pentadiagonal (r = 2) reduced phase, pairwise (P:346 with 2x2 blocks, reading R20): the
