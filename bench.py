@@ -183,13 +183,34 @@ def cpu_oracle_sample(cfg: str, budget_s: float = 10.0):
         m = min(m_full, m * max(2, int(2 ** math.floor(math.log2(max(1.0, budget_s / 3 / max(dt, 1e-4)))))))
     dt, m, shape = best
     ms_full = dt * 1e3 * (m_full / m)
-    return {"value": ms_full, "unit": "ms", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{n} rows x {m} of {m_full} batch columns (shape {list(shape)}), "
-                      f"{dt:.2f} s, extrapolated x{m_full / m:g} to the full batch"}
+    out = {"value": ms_full, "unit": "ms", "cores": oracle.num_threads(), "kind": "oracle",
+           "sample": f"{n} rows x {m} of {m_full} batch columns (shape {list(shape)}), "
+                     f"{dt:.2f} s" + (f", extrapolated x{m_full / m:g} to the full batch" if m < m_full
+                                      else " (the full workload)")}
+    out.update(host_info())
+    return out
+
+
+def host_info():
+    """The host cores the oracle runs on: nproc, the lscpu model and OpenMP threads used."""
+    import oracle
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=5).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model, "omp_threads": oracle.num_threads()}
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle as it stands, bounded sample per step (rank 0 only)."""
+    """--impl reference: the CPU oracle as it stands (rank 0 only), on the same workload as the
+    GPU arm: every step solves the FULL batch (all columns of the global grid) unless the
+    requested steps would not fit in a few minutes, in which case each step solves a column
+    sample and the line says so ("extrapolated": true).  Steps and warm-up are honoured."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -200,26 +221,43 @@ def run_reference(args):
     dims, sd, name = workload(args.config, world)
     n = dims[sd]
     m_full = int(np.prod(dims)) // n
-    m = min(m_full, 4096)
-    shape = [1, m, n] if sd == 2 else ([1, n, m] if sd == 1 else [n, 1, m])
+    shape = [1, m_full, n] if sd == 2 else ([1, n, m_full] if sd == 1 else [n, 1, m_full])
+    fn_of = (lambda a: oracle.deriv(a, sd)) if args.config == "cfg5" else (lambda a: oracle.cyclic_solve(a, sd))
+    # probe one slice to size the run (<= 240 s for warm-up + timed steps)
+    m_probe = min(m_full, 4096)
+    pshape = list(shape)
+    pshape[2 if sd != 2 else 1] = m_probe
+    t0 = time.perf_counter()
+    fn_of(workloads.uniform(pshape, 2))
+    est_full = (time.perf_counter() - t0) * m_full / m_probe
+    steps, warm = max(1, args.steps), max(0, args.warmup)
+    budget = 240.0
+    m = m_full
+    if est_full * (steps + warm) > budget:
+        m = max(256, int(m_full * budget / (est_full * (steps + warm))) // 256 * 256)
+        m = min(m, m_full)
+        shape[2 if sd != 2 else 1] = m
     b = workloads.uniform(shape, 2)
-    fn = (lambda: oracle.deriv(b, sd)) if args.config == "cfg5" else (lambda: oracle.cyclic_solve(b, sd))
-    steps = max(1, min(args.steps, 20))
-    warm = max(1, min(args.warmup, 3))
     for _ in range(warm):
-        fn()
+        fn_of(b)
     t0 = time.perf_counter()
     for _ in range(steps):
-        fn()
+        fn_of(b)
     dt = (time.perf_counter() - t0) / steps
     ms = dt * 1e3 * m_full / m
-    sample = f"{n} rows x {m} of {m_full} batch columns per step, extrapolated x{m_full / m:g}"
+    extrap = m != m_full
+    sample = (f"{n} rows x {m} of {m_full} batch columns per step" +
+              (f", extrapolated x{m_full / m:g}" if extrap else " (the full workload every step)"))
+    cpu = {"value": ms, "unit": "ms", "kind": "oracle", "sample": sample, "extrapolated": extrap}
+    info = host_info()
+    cpu["cores"] = info["omp_threads"]
+    cpu.update(info)
     line = {"impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world,
             "steps": steps, "warmup": warm, "ms_per_step": ms, "higher_is_better": False,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if args.config != "cfg3" else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
             "config": {"workload": name, "global_dims": list(dims), "solve_dim": sd},
-            "cpu_baseline": {"value": ms, "unit": "ms", "cores": oracle.num_threads(),
-                             "kind": "oracle", "sample": sample},
+            "cpu_baseline": cpu,
             "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -281,9 +319,9 @@ def main():
     if deriv and args.scheme != "collocated":
         delta = 2 * math.pi / dims[sd]
         if args.scheme == "staggered_deriv":
-            bands, coef = ctri.STAGGERED_DERIV_BANDS, ctri.staggered_deriv_coef(delta)
+            bands, coef = ctri.staggered_deriv_bands(), ctri.staggered_deriv_coef(delta)
         else:
-            bands, coef = ctri.STAGGERED_INTERP_BANDS, ctri.staggered_interp_coef()
+            bands, coef = ctri.staggered_interp_bands(), ctri.staggered_interp_coef()
         name = f"{name.replace('compact 6th-order first derivative', args.scheme.replace('_', ' '))} (P:202-206)"
     if args.penta:
         if deriv:

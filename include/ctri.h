@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define CTRI_ABI_VERSION 4
+#define CTRI_ABI_VERSION 5
 
 typedef struct ctri_plan_s* ctri_plan;
 typedef struct CUstream_st* ctri_stream; /* == cudaStream_t */
@@ -120,6 +120,10 @@ typedef struct ctri_stats {
   float t_reduced_kernel_us, t_window_us;
   float t_p2p_y_us, t_p2p_step_us[CTRI_MAX_STAGES], t_p2p_x_us;
   int32_t p2p_steps;            /* schedule steps timed in t_p2p_step_us */
+  uint32_t p2p_epoch;           /* device epoch of the reduced-phase mailboxes (slice 0): one per
+                                   solve, so its parity alternates the double-buffered copies */
+  uint32_t halo_epoch;          /* device epoch of the derivative halo exchange (slice 0): one per
+                                   ctri_deriv / ctri_compact_apply, independent of p2p_epoch */
 } ctri_stats;
 
 /* Human-readable status name; never NULL. */
@@ -146,7 +150,8 @@ ctri_status ctri_get_unique_id(void* out128);
  *   flags        CTRI_FLAG_*.
  *   stream       stream used for the table uploads during create.
  * Errors: INVALID_ARG, PARTITION_TOO_SMALL, UNSUPPORTED (cyclic non-power-of-two nparts on the
- * NCCL-rounds path or nparts > 8), SINGULAR (pivot guard), CUDA, NCCL, OOM.  On error *out is NULL.
+ * NCCL-rounds path, or cyclic non-power-of-two nparts > 16 = kMaxP2PRanks on the P2P path),
+ * SINGULAR (pivot guard), CUDA, NCCL, OOM.  On error *out is NULL.
  * The plan owns its device tables, plane buffers, events and NCCL communicator. */
 ctri_status ctri_plan_create(ctri_plan* out, const int64_t global_dims[3], int solve_dim,
                              int nparts, int rank, const double bands[3], int cyclic,
@@ -164,7 +169,9 @@ ctri_status ctri_plan_create_loopback(ctri_plan* plans, int nparts, const int64_
  * 2x2").  bands = {e, l, d, u, f} = A[i,i-2], A[i,i-1], A[i,i], A[i,i+1],
  * A[i,i+2] (host array, copied); cyclic wraps the four corner couplings.  Each of the nparts
  * slabs keeps two interface rows (local rows 0, 1) and n - 2 >= 4 interior rows; the 2x2-block
- * reduced system is solved with ONE P2P all-gather round and plan-time rows of its inverse
+ * reduced system is solved over the P2P mailboxes by pairwise 2x2-block PCR (P:346 with
+ * 2x2 blocks, R20: a y round, ceil(log2 nparts) block steps, the fold, an x~ round)
+ * or, with CTRI_FLAG_ALLGATHER, by ONE all-gather round and plan-time rows of its inverse
  * (nparts <= 8).  The plan is used with ctri_solve / ctri_solve_loopback / ctri_solve_host /
  * ctri_get_stats / ctri_plan_destroy like a tridiagonal one.  Errors: INVALID_ARG (as
  * ctri_plan_create), PARTITION_TOO_SMALL (n < 6 or N % nparts), UNSUPPORTED (nparts > 8,
@@ -201,6 +208,10 @@ ctri_status ctri_solve_host(ctri_plan plan, const double* b_host, double* x_host
 /* Compact first derivative along solve_dim:
  *   rhs_j = a (f_{j+1}-f_{j-1})/(2h) + bc (f_{j+2}-f_{j-2})/(4h)  (periodic, halo from
  *   ranks i-1 / i+1), then df = A^{-1} rhs with this plan's bands.
+ * Defaults (the library fills them in, so callers carry no scheme arithmetic):
+ *   a or bc NaN  -> Lele's sixth-order pair a = 14/9, bc = 1/9 (the paper prints only the
+ *                   symbols; reading R8);
+ *   h <= 0 or NaN -> h = 2 pi / N_global[solve_dim] (periodic domain [0, 2 pi)).
  * Requires a cyclic plan created with CTRI_FLAG_DERIV and n >= 2.  f and df must not
  * overlap.  Asynchronous, stream ordered, collective. */
 ctri_status ctri_deriv(ctri_plan plan, const double* f, double* df, double a, double bc,
@@ -224,6 +235,21 @@ ctri_status ctri_deriv_loopback(const ctri_plan* plans, int nparts, const double
  * NULL or non-finite coef. */
 ctri_status ctri_compact_apply(ctri_plan plan, const double coef[5], const double* f, double* out,
                                ctri_stream stream);
+
+/* Coefficients of the compact schemes the paper uses, computed in the library so that
+ * bindings only marshal (PAPER.md P:65-67 collocated, P:202-206 staggered):
+ *   scheme CTRI_SCHEME_COLLOCATED_D1  bands (1/3, 1, 1/3),  coef {-1/(36D), -7/(9D), 0, 7/(9D), 1/(36D)}
+ *                                     (a = 14/9, b = 1/9 of P:66, D = grid spacing)
+ *   scheme CTRI_SCHEME_STAGGERED_D1   bands (9/62, 1, 9/62), coef {-17/(186D), -63/(62D), 63/(62D), 17/(186D), 0}
+ *   scheme CTRI_SCHEME_STAGGERED_I    bands (3/10, 1, 3/10), coef {1/20, 3/4, 3/4, 1/20, 0}
+ * (staggered inputs f_{i+1/2} stored at index i, R18).  delta is the grid spacing
+ * (ignored by the interpolation scheme; must be finite and > 0 otherwise).  coef[5] and
+ * bands[3] are caller-owned host arrays; either may be NULL.  Errors: INVALID_ARG for an
+ * unknown scheme or a bad delta.  Host only. */
+#define CTRI_SCHEME_COLLOCATED_D1 0
+#define CTRI_SCHEME_STAGGERED_D1  1
+#define CTRI_SCHEME_STAGGERED_I   2
+ctri_status ctri_scheme_coef(int scheme, double delta, double coef[5], double bands[3]);
 
 /* TEST-ONLY: ctri_compact_apply for a loopback group. */
 ctri_status ctri_compact_apply_loopback(const ctri_plan* plans, int nparts, const double coef[5],

@@ -13,9 +13,10 @@ from .ctri import (CTRI_FLAG_DERIV, CTRI_FLAG_FULL_BACKSUB, CTRI_FLAG_GENERIC_LO
                    ctri_pcr_coefficients, ctri_plan_create, ctri_reduced_schedule, ctri_plan_create_loopback,
                    ctri_plan_destroy, ctri_solve, ctri_solve_host, ctri_solve_loopback, load,
                    local_shape, ctri_compact_apply, ctri_compact_apply_loopback,
-                   STAGGERED_DERIV_BANDS, STAGGERED_INTERP_BANDS, staggered_deriv_coef,
-                   staggered_interp_coef)
+                   staggered_deriv_bands, staggered_interp_bands, staggered_deriv_coef,
+                   staggered_interp_coef, ctri_scheme_coef, CTRI_SCHEME_COLLOCATED_D1,
+                   CTRI_SCHEME_STAGGERED_D1, CTRI_SCHEME_STAGGERED_I)
 
 __all__ = [n for n in dir() if n.startswith(("ctri_", "CTRI_")) or n in
-           ("Plan", "LoopbackGroup", "CtriError", "load", "local_shape", "STAGGERED_DERIV_BANDS",
-            "STAGGERED_INTERP_BANDS", "staggered_deriv_coef", "staggered_interp_coef")]
+           ("Plan", "LoopbackGroup", "CtriError", "load", "local_shape", "staggered_deriv_bands",
+            "staggered_interp_bands", "staggered_deriv_coef", "staggered_interp_coef")]

@@ -64,6 +64,26 @@ ctri_status alloc_plane(double** p, int64_t count) {
   return CTRI_OK;
 }
 
+// The P2P deadline word lives in mapped pinned host memory: kernels store to it over the bus
+// only on failure, and the host reads it at the next call without synchronising.
+ctri_status alloc_err(Plan* P) {
+  CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&P->h_err), sizeof(int), cudaHostAllocMapped));
+  *reinterpret_cast<volatile int*>(P->h_err) = 0;
+  CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&P->d_err), P->h_err, 0));
+  return CTRI_OK;
+}
+
+// A plan whose P2P wait hit its deadline is out of step with its peers (epochs, mailboxes):
+// every later call fails instead of returning silently wrong results.
+ctri_status check_poisoned(const std::vector<Plan*>& G) {
+  for (const Plan* P : G)
+    if (P->h_err && *reinterpret_cast<volatile int*>(P->h_err))
+      return fail(CTRI_ERR_CUDA, "a previous solve timed out waiting for a peer (device deadline, "
+                                 "error word " + std::to_string(*reinterpret_cast<volatile int*>(P->h_err)) +
+                                 "); the plan is unusable: destroy it");
+  return CTRI_OK;
+}
+
 void free_plan(Plan* P) {
   if (!P) return;
   double* bufs[] = {P->d_cp,    P->d_inv_den, P->d_S,      P->d_R,       P->yf,      P->yl,
@@ -77,8 +97,9 @@ void free_plan(Plan* P) {
   for (size_t r = 0; r < P->peer_alloc.size(); ++r)
     if (r < P->peer_ipc.size() && P->peer_ipc[r] && P->peer_alloc[r]) cudaIpcCloseMemHandle(P->peer_alloc[r]);
   if (P->mbox_alloc) cudaFree(P->mbox_alloc);
-  if (P->d_err) cudaFree(P->d_err);
+  if (P->h_err) cudaFreeHost(P->h_err);
   if (P->d_epoch) cudaFree(P->d_epoch);
+  if (P->d_hepoch) cudaFree(P->d_hepoch);
   if (P->d_trace) cudaFree(P->d_trace);
   if (P->d_fctr) cudaFree(P->d_fctr);
   if (P->e2e_sub) free_plan(P->e2e_sub);
@@ -128,6 +149,11 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
 
   // virtual partitions (nparts == 1): the slab is solved as vp partitions of n/vp rows so the
   // local-solve clusters are small enough to occupy every GPC
+  // test knobs of the P2P deadline path, read once per plan (never on the solve path)
+  if (const char* e = std::getenv("CTRI_TEST_P2P_DEADLINE_MS"))
+    if (*e) P->deadline_ns = (unsigned long long)std::max(1, std::atoi(e)) * 1000000ull;
+  if (const char* e = std::getenv("CTRI_TEST_P2P_DROP_RANK"))
+    if (*e) P->test_drop_rank = std::atoi(e);
   P->vp = 1;
   const char* vp_env = std::getenv("CTRI_VPARTS");  // measurement knob (any axis)
   if (vp_env && !*vp_env) vp_env = nullptr;        // set but empty: default rule
@@ -251,10 +277,14 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
                      ((flags & CTRI_FLAG_DERIV) ? p2p_mailbox_words(0, m, true) : 0));
     CUDA_TRY(cudaMalloc(&P->mbox_alloc, P->mbox_bytes));
     CUDA_TRY(cudaMemsetAsync(P->mbox_alloc, 0, P->mbox_bytes, s));
-    CUDA_TRY(cudaMalloc(&P->d_err, sizeof(int)));
-    CUDA_TRY(cudaMemsetAsync(P->d_err, 0, sizeof(int), s));
+    TRY(alloc_err(P));
     CUDA_TRY(cudaMalloc(&P->d_epoch, sizeof(unsigned int) * P->p2p_nslices * P->vp));
     CUDA_TRY(cudaMemsetAsync(P->d_epoch, 0, sizeof(unsigned int) * P->p2p_nslices * P->vp, s));
+    if (flags & CTRI_FLAG_DERIV) {  // the halo exchange: its own mailbox region and epochs
+      P->halo_off = P->p2p_off + (int64_t)P->vp * P->p2p_vrow_words;
+      CUDA_TRY(cudaMalloc(&P->d_hepoch, sizeof(unsigned int) * P->p2p_nslices));
+      CUDA_TRY(cudaMemsetAsync(P->d_hepoch, 0, sizeof(unsigned int) * P->p2p_nslices, s));
+    }
     P->p2p = true;
   }
   if (flags & CTRI_FLAG_DERIV) {
@@ -376,8 +406,7 @@ ctri_status penta_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, co
     P->mbox_bytes = sizeof(unsigned long long) * p2p_mailbox_words(copy_words, m, false);
     CUDA_TRY(cudaMalloc(&P->mbox_alloc, P->mbox_bytes));
     CUDA_TRY(cudaMemsetAsync(P->mbox_alloc, 0, P->mbox_bytes, s));
-    CUDA_TRY(cudaMalloc(&P->d_err, sizeof(int)));
-    CUDA_TRY(cudaMemsetAsync(P->d_err, 0, sizeof(int), s));
+    TRY(alloc_err(P));
     CUDA_TRY(cudaMalloc(&P->d_epoch, sizeof(unsigned int) * P->p2p_nslices));
     CUDA_TRY(cudaMemsetAsync(P->d_epoch, 0, sizeof(unsigned int) * P->p2p_nslices, s));
     P->p2p = true;
@@ -446,6 +475,8 @@ void p2p_args(const Plan& P0, P2PArgs* A) {
   A->S = P0.d_S;
   A->R = P0.d_R;
   A->err = P0.d_err;
+  A->deadline_ns = P0.deadline_ns;
+  A->test_drop_rank = P0.test_drop_rank;
 }
 
 // Row `v` of this rank's virtual partitions (v = 0 without them): global reduced row
@@ -680,6 +711,7 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
   }
   const bool nccl = !G[0]->loopback;
   Plan& P0 = *G[0];
+  TRY(check_poisoned(G));
   for (size_t r = 0; r < G.size(); ++r) {
     if (!b[r] || !x[r]) return fail(CTRI_ERR_INVALID_ARG, "NULL b or x");
     if (((uintptr_t)b[r] | (uintptr_t)x[r]) & 15)
@@ -720,9 +752,10 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
     A.trace = P0.d_trace;
     for (size_t r = 0; r < G.size(); ++r)
       for (int v = 0; v < P0.vp; ++v) p2p_fill_rank(*G[r], x[r], &A.rk[r * P0.vp + v], v);
-    // loopback: one cooperative grid for all ranks; real ranks: the virtual rows' CTAs are
-    // co-resident by construction (p2p_slices sizes one wave), launched with PDL
-    cudaError_t e = launch_reduced_p2p(A, P0.loopback ? nrows : 1, s, nrows);
+    // CTAs of different reduced rows on this GPU wait on each other (loopback ranks, virtual
+    // rows): one cooperative grid guarantees they are co-resident even when other work shares
+    // the GPU.  A single row per GPU waits only on peers and is launched with PDL instead.
+    cudaError_t e = launch_reduced_p2p(A, nrows, s, nrows);
     if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("p2p reduced kernel: ") + cudaGetErrorString(e));
     record(P0, EV_XX, s);
     for (size_t r = 0; r < G.size(); ++r) {  // (a4) window pass of every rank (all its slabs)
@@ -784,6 +817,7 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
 ctri_status penta_solve_group(std::vector<Plan*>& G, const double* const* b, double* const* x,
                               cudaStream_t s) {
   Plan& P0 = *G[0];
+  TRY(check_poisoned(G));
   for (size_t r = 0; r < G.size(); ++r)
     if (!b[r] || !x[r]) return fail(CTRI_ERR_INVALID_ARG, "NULL b or x");
   for (Plan* P : G) P->solves++;
@@ -839,12 +873,20 @@ ctri_status deriv_group(std::vector<Plan*>& G, const double* const* f, double* c
       if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, cudaGetErrorString(e));
     }
   }
+  TRY(check_poisoned(G));
   if (G[0]->p > 1 && G[0]->p2p) {  // halo rows as LL words over the P2P mailboxes
     P2PArgs A;
     p2p_args(*G[0], &A);
+    A.p = G[0]->p;  // real ranks (not virtual rows): slab neighbours
     for (size_t r = 0; r < G.size(); ++r) {
-      p2p_fill_rank(*G[r], nullptr, &A.rk[r]);
+      const Plan& P = *G[r];
+      p2p_fill_rank(P, nullptr, &A.rk[r]);
+      A.rk[r].rank = P.rank;
       A.rk[r].f = f[r];
+      A.rk[r].epoch = P.d_hepoch;
+      A.rk[r].mbox = reinterpret_cast<unsigned long long*>(P.mbox_alloc) + P.halo_off;
+      for (int j = 0; j < kMaxP2PRanks; ++j)
+        A.rk[r].peer_mbox[j] = j < P.p ? reinterpret_cast<unsigned long long*>(P.peer_alloc[j]) + P.halo_off : nullptr;
     }
     cudaError_t e = launch_halo_p2p(A, (int)G.size(), s);
     if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("p2p halo: ") + cudaGetErrorString(e));
@@ -1135,8 +1177,12 @@ ctri_status ctri_solve_host(ctri_plan plan, const double* b_host, double* x_host
 }
 
 // collocated compact first derivative as a five-point stencil
-static bool deriv_coef(double a, double bc, double h, double c[5]) {
-  if (h == 0.0 || !std::isfinite(h)) return false;
+// a, bc NaN -> Lele's sixth-order pair (R8); h <= 0 or NaN -> 2 pi / N_global
+static bool deriv_coef(const Plan& P, double a, double bc, double h, double c[5]) {
+  if (std::isnan(a)) a = 14.0 / 9.0;
+  if (std::isnan(bc)) bc = 1.0 / 9.0;
+  if (std::isnan(h) || h <= 0.0) h = 2.0 * M_PI / (double)P.gdims[P.sd];
+  if (!std::isfinite(h) || !std::isfinite(a) || !std::isfinite(bc)) return false;
   c[0] = -bc / (4.0 * h);
   c[1] = -a / (2.0 * h);
   c[2] = 0.0;
@@ -1176,17 +1222,52 @@ ctri_status ctri_compact_apply_loopback(const ctri_plan* plans, int nparts, cons
 
 ctri_status ctri_deriv(ctri_plan plan, const double* f, double* df, double a, double bc, double h,
                        ctri_stream stream) {
+  if (!plan) return fail(CTRI_ERR_INVALID_ARG, "NULL plan");
   double c[5];
-  if (!deriv_coef(a, bc, h, c)) return fail(CTRI_ERR_INVALID_ARG, "bad h");
+  if (!deriv_coef(*reinterpret_cast<Plan*>(plan), a, bc, h, c))
+    return fail(CTRI_ERR_INVALID_ARG, "non-finite a, bc or h");
   return ctri_compact_apply(plan, c, f, df, stream);
 }
 
 ctri_status ctri_deriv_loopback(const ctri_plan* plans, int nparts, const double* const* f,
                                 double* const* df, double a, double bc, double h,
                                 ctri_stream stream) {
+  if (!plans || nparts < 1 || !plans[0]) return fail(CTRI_ERR_INVALID_ARG, "NULL arguments");
   double c[5];
-  if (!deriv_coef(a, bc, h, c)) return fail(CTRI_ERR_INVALID_ARG, "bad h");
+  if (!deriv_coef(*reinterpret_cast<Plan*>(plans[0]), a, bc, h, c))
+    return fail(CTRI_ERR_INVALID_ARG, "non-finite a, bc or h");
   return ctri_compact_apply_loopback(plans, nparts, c, f, df, stream);
+}
+
+ctri_status ctri_scheme_coef(int scheme, double delta, double coef[5], double bands[3]) {
+  double c[5] = {0, 0, 0, 0, 0}, al = 0;
+  switch (scheme) {
+    case CTRI_SCHEME_COLLOCATED_D1: {  // alpha = 1/3, a = 14/9, b = 1/9 (R8)
+      if (!(delta > 0) || !std::isfinite(delta)) return fail(CTRI_ERR_INVALID_ARG, "delta must be > 0");
+      const double a = 14.0 / 9.0, b = 1.0 / 9.0;
+      c[0] = -b / (4 * delta); c[1] = -a / (2 * delta); c[3] = a / (2 * delta); c[4] = b / (4 * delta);
+      al = 1.0 / 3.0;
+      break;
+    }
+    case CTRI_SCHEME_STAGGERED_D1: {  // alpha = 9/62, a = 63/62, b = 17/62 (R18)
+      if (!(delta > 0) || !std::isfinite(delta)) return fail(CTRI_ERR_INVALID_ARG, "delta must be > 0");
+      const double a = 63.0 / 62.0, b = 17.0 / 62.0;
+      c[0] = -b / (3 * delta); c[1] = -a / delta; c[2] = a / delta; c[3] = b / (3 * delta);
+      al = 9.0 / 62.0;
+      break;
+    }
+    case CTRI_SCHEME_STAGGERED_I: {  // alpha = 3/10, a = 3/2, b = 1/10 (R18)
+      const double a = 1.5, b = 0.1;
+      c[0] = b / 2; c[1] = a / 2; c[2] = a / 2; c[3] = b / 2;
+      al = 0.3;
+      break;
+    }
+    default:
+      return fail(CTRI_ERR_INVALID_ARG, "unknown scheme");
+  }
+  if (coef) for (int k = 0; k < 5; ++k) coef[k] = c[k];
+  if (bands) { bands[0] = al; bands[1] = 1.0; bands[2] = al; }
+  return CTRI_OK;
 }
 
 ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
@@ -1211,7 +1292,12 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
   out->vparts = P->vp;
   out->grid_ctas = P->local_kernel ? P->tile.grid : (int32_t)((P->tlay.m() + 127) / 128);
   out->device_error = 0;
-  if (P->d_err) CUDA_TRY(cudaMemcpy(&out->device_error, P->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (P->h_err) {
+    CUDA_TRY(cudaDeviceSynchronize());  // kernels of the last solve have stored their error words
+    out->device_error = *reinterpret_cast<volatile int*>(P->h_err);
+  }
+  if (P->d_epoch) CUDA_TRY(cudaMemcpy(&out->p2p_epoch, P->d_epoch, sizeof(unsigned int), cudaMemcpyDeviceToHost));
+  if (P->d_hepoch) CUDA_TRY(cudaMemcpy(&out->halo_epoch, P->d_hepoch, sizeof(unsigned int), cudaMemcpyDeviceToHost));
   out->chunk_heads = P->local_kernel ? P->tile.Q : 1;
   const int64_t interior = P->tlay.n - P->r;
   const bool full = (P->flags & CTRI_FLAG_FULL_BACKSUB) || (2 * P->window >= interior);

@@ -171,6 +171,9 @@ struct P2PArgs {
   double l, u;
   const double *S, *R;
   int* err;
+  unsigned long long deadline_ns;  // every LL wait gives up after this long (default 20 s)
+  int test_drop_rank;              // TEST ONLY (CTRI_TEST_P2P_DROP_RANK): this reduced row never
+                                   // sends its y plane, so its neighbour hits the deadline
   unsigned long long* trace;  // CTRI_FLAG_TIMING / CTRI_P2P_TRACE: [grid][kP2PTrace] stamps
   P2PRank rk[kMaxP2PRanks];
 };
@@ -246,7 +249,13 @@ struct Plan {
   size_t mbox_bytes = 0;
   std::vector<void*> peer_alloc;       // peer allocations as mapped here (IPC) or direct
   std::vector<bool> peer_ipc;          // opened with cudaIpcOpenMemHandle
-  int* d_err = nullptr;                // device error word (p2p deadline)
+  unsigned long long deadline_ns = 20ull * 1000000000ull;  // P2P wait deadline (CTRI_TEST_P2P_DEADLINE_MS)
+  int test_drop_rank = -1;             // CTRI_TEST_P2P_DROP_RANK (tests of the deadline path)
+  int* d_err = nullptr;                // device view of the error word (p2p deadline)
+  int* h_err = nullptr;                // the same word in mapped pinned host memory: the host
+                                       // reads it without a sync and poisons the plan
+  unsigned int* d_hepoch = nullptr;    // per-slice epochs of the derivative halo exchange
+  int64_t halo_off = 0;                // words before the halo region of the mailbox
   unsigned long long* d_trace = nullptr;  // P2P per-round stamps (CTRI_FLAG_TIMING / CTRI_P2P_TRACE)
   int trace_ctas = 0;
   unsigned long long epoch = 0;

@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(NT, MINB)
         if (dev::ll_ready(f_w[2], f_w[3], f_ep)) ylp = dev::ll_value(f_w[2], f_w[3]);
         else ok = dev::ll_wait(mb + f_word(1, (kg + A.f_P - 1) % A.f_P, jo), f_ep, f_deadline, &ylp);
       }
-      if (!ok) atomicExch(A.f_err, 1);
+      if (!ok) *reinterpret_cast<volatile int*>(A.f_err) = 1;
       const double bh = ck - (lft ? T.l * ylp : 0.0);  // Eq. bi_hat
       a0 = A.f_g0[kg] * bh;
       a1 = A.f_g1[kg] * bh;

@@ -26,7 +26,7 @@ CTRI_FLAG_NCCL_ROUNDS = 1 << 4
 CTRI_FLAG_ALLGATHER = 1 << 5
 CTRI_FLAG_FUSED_REDUCED = 1 << 6
 CTRI_MAX_STAGES = 16
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 STATUS = {0: "CTRI_OK", 1: "CTRI_ERR_INVALID_ARG", 2: "CTRI_ERR_UNSUPPORTED", 3: "CTRI_ERR_SINGULAR",
           4: "CTRI_ERR_PARTITION_TOO_SMALL", 5: "CTRI_ERR_CUDA", 6: "CTRI_ERR_NCCL",
@@ -39,7 +39,7 @@ ABI_SYMBOLS = ("ctri_status_string", "ctri_last_error", "ctri_abi_version", "ctr
                "ctri_plan_destroy", "ctri_factor_query", "ctri_pcr_coefficients",
                "ctri_reduced_schedule", "ctri_compact_apply", "ctri_compact_apply_loopback",
                "ctri_reduced_inverse", "ctri_plan_create_penta", "ctri_plan_create_penta_loopback",
-               "ctri_penta_factor_query", "ctri_penta_block_pcr")
+               "ctri_penta_factor_query", "ctri_penta_block_pcr", "ctri_scheme_coef")
 
 
 class CtriError(RuntimeError):
@@ -73,7 +73,8 @@ class ctri_stats(ctypes.Structure):
                 ("band_halfwidth", ctypes.c_int32),
                 ("t_reduced_kernel_us", ctypes.c_float), ("t_window_us", ctypes.c_float),
                 ("t_p2p_y_us", ctypes.c_float), ("t_p2p_step_us", ctypes.c_float * CTRI_MAX_STAGES),
-                ("t_p2p_x_us", ctypes.c_float), ("p2p_steps", ctypes.c_int32)]
+                ("t_p2p_x_us", ctypes.c_float), ("p2p_steps", ctypes.c_int32),
+                ("p2p_epoch", ctypes.c_uint32), ("halo_epoch", ctypes.c_uint32)]
 
     def as_dict(self):
         d = {}
@@ -124,6 +125,7 @@ def load(build_if_missing: bool = False):
                                      ctypes.POINTER(P), ctypes.c_double, ctypes.c_double,
                                      ctypes.c_double, P]),
         "ctri_compact_apply": (st, [P, dp, P, P, P]),
+        "ctri_scheme_coef": (st, [ctypes.c_int, ctypes.c_double, dp, dp]),
         "ctri_reduced_inverse": (st, [ctypes.c_int, ctypes.c_int, dp, dp, dp, dp]),
         "ctri_plan_create_penta": (st, [ctypes.POINTER(P), i64p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         dp, ctypes.c_int, P, ctypes.c_uint32, P]),
@@ -174,6 +176,29 @@ def _ptr(t) -> int:
     if not t.is_contiguous() or str(t.dtype) != "torch.float64":
         raise ValueError("tensors must be contiguous float64")
     return t.data_ptr()
+
+
+def _dev(t, numel: int, what: str):
+    """Plan / LoopbackGroup wrappers: a CUDA float64 tensor holding exactly the local slab."""
+    if isinstance(t, int):
+        return t
+    if isinstance(t, np.ndarray) or not getattr(t, "is_cuda", False):
+        raise ValueError(f"{what}: expected a CUDA tensor (device memory), got {type(t).__name__}"
+                         f"{'' if isinstance(t, np.ndarray) else ' on ' + str(getattr(t, 'device', '?'))}")
+    if t.numel() != numel:
+        raise ValueError(f"{what}: {t.numel()} elements, the plan's local slab has {numel}")
+    return t
+
+
+def _host(t, numel: int, what: str):
+    if isinstance(t, int):
+        return t
+    if getattr(t, "is_cuda", False):
+        raise ValueError(f"{what}: expected host memory")
+    n = t.size if isinstance(t, np.ndarray) else t.numel()
+    if n != numel:
+        raise ValueError(f"{what}: {n} elements, the plan's local slab has {numel}")
+    return t
 
 
 def _stream_ptr(stream) -> int:
@@ -292,18 +317,23 @@ def ctri_solve_host(plan: int, b_host, x_host, stream=None):
            "ctri_solve_host")
 
 
-def ctri_deriv(plan: int, f, df, a=14 / 9, bc=1 / 9, h=None, stream=None, n_global=None):
-    _check(load().ctri_deriv(plan, _ptr(f), _ptr(df), float(a), float(bc), float(h),
-                             _stream_ptr(stream)), "ctri_deriv")
+def _opt(v, none):
+    return none if v is None else float(v)
 
 
-def ctri_deriv_loopback(plans, fs, dfs, a, bc, h, stream=None):
+def ctri_deriv(plan: int, f, df, a=None, bc=None, h=None, stream=None):
+    """a, bc, h = None: the library's defaults (Lele's a = 14/9, bc = 1/9; h = 2 pi / N)."""
+    _check(load().ctri_deriv(plan, _ptr(f), _ptr(df), _opt(a, float("nan")), _opt(bc, float("nan")),
+                             _opt(h, 0.0), _stream_ptr(stream)), "ctri_deriv")
+
+
+def ctri_deriv_loopback(plans, fs, dfs, a=None, bc=None, h=None, stream=None):
     n = len(plans)
     hp = (ctypes.c_void_p * n)(*plans)
     fp = (ctypes.c_void_p * n)(*[_ptr(f) for f in fs])
     dp = (ctypes.c_void_p * n)(*[_ptr(d) for d in dfs])
-    _check(load().ctri_deriv_loopback(hp, n, fp, dp, float(a), float(bc), float(h),
-                                      _stream_ptr(stream)), "ctri_deriv_loopback")
+    _check(load().ctri_deriv_loopback(hp, n, fp, dp, _opt(a, float("nan")), _opt(bc, float("nan")),
+                                      _opt(h, 0.0), _stream_ptr(stream)), "ctri_deriv_loopback")
 
 
 def _coef5(coef):
@@ -329,20 +359,33 @@ def ctri_compact_apply_loopback(plans, coef, fs, outs, stream=None):
            "ctri_compact_apply_loopback")
 
 
-# Right-hand sides of the staggered sixth-order schemes as five-point
-# stencils over half-node values g_i = f_{i+1/2} stored at index i (offsets -2..2).
-STAGGERED_DERIV_BANDS = (9 / 62, 1.0, 9 / 62)
-STAGGERED_INTERP_BANDS = (3 / 10, 1.0, 3 / 10)
+CTRI_SCHEME_COLLOCATED_D1 = 0
+CTRI_SCHEME_STAGGERED_D1 = 1
+CTRI_SCHEME_STAGGERED_I = 2
+
+
+def ctri_scheme_coef(scheme: int, delta: float = 1.0):
+    """(coef[5], bands[3]) of a compact scheme of the paper, computed by the library."""
+    c = (ctypes.c_double * 5)()
+    bd = (ctypes.c_double * 3)()
+    _check(load().ctri_scheme_coef(int(scheme), float(delta), c, bd), "ctri_scheme_coef")
+    return tuple(c), tuple(bd)
 
 
 def staggered_deriv_coef(delta: float):
-    a, b = 63 / 62, 17 / 62
-    return (-b / (3 * delta), -a / delta, a / delta, b / (3 * delta), 0.0)
+    return ctri_scheme_coef(CTRI_SCHEME_STAGGERED_D1, delta)[0]
 
 
 def staggered_interp_coef():
-    a, b = 3 / 2, 1 / 10
-    return (b / 2, a / 2, a / 2, b / 2, 0.0)
+    return ctri_scheme_coef(CTRI_SCHEME_STAGGERED_I)[0]
+
+
+def staggered_deriv_bands():
+    return ctri_scheme_coef(CTRI_SCHEME_STAGGERED_D1)[1]
+
+
+def staggered_interp_bands():
+    return ctri_scheme_coef(CTRI_SCHEME_STAGGERED_I)[1]
 
 
 def ctri_get_stats(plan: int) -> dict:
@@ -450,25 +493,30 @@ class Plan:
     def local_shape(self):
         return local_shape(self.global_dims, self.solve_dim, self.nparts)
 
+    @property
+    def local_numel(self):
+        return int(np.prod(self.local_shape))
+
     def solve(self, b, x=None, stream=None):
         if x is None:
             x = b
-        ctri_solve(self.handle, b, x, stream)
+        n = self.local_numel
+        ctri_solve(self.handle, _dev(b, n, "b"), _dev(x, n, "x"), stream)
         return x
 
     def solve_host(self, b_host, x_host, stream=None):
-        ctri_solve_host(self.handle, b_host, x_host, stream)
+        n = self.local_numel
+        ctri_solve_host(self.handle, _host(b_host, n, "b_host"), _host(x_host, n, "x_host"), stream)
         return x_host
 
-    def deriv(self, f, df, a=14 / 9, bc=1 / 9, h=None, stream=None):
-        if h is None:
-            import math
-            h = 2 * math.pi / self.global_dims[self.solve_dim]
-        ctri_deriv(self.handle, f, df, a, bc, h, stream)
+    def deriv(self, f, df, a=None, bc=None, h=None, stream=None):
+        n = self.local_numel
+        ctri_deriv(self.handle, _dev(f, n, "f"), _dev(df, n, "df"), a, bc, h, stream)
         return df
 
     def compact_apply(self, coef, f, out, stream=None):
-        ctri_compact_apply(self.handle, coef, f, out, stream)
+        n = self.local_numel
+        ctri_compact_apply(self.handle, coef, _dev(f, n, "f"), _dev(out, n, "out"), stream)
         return out
 
     def stats(self) -> dict:
@@ -507,17 +555,20 @@ class LoopbackGroup:
     def local_shape(self):
         return local_shape(self.global_dims, self.solve_dim, self.nparts)
 
-    def solve(self, bs, xs, stream=None):
-        ctri_solve_loopback(self.handles, bs, xs, stream)
+    def _chk(self, ts, what):
+        if len(ts) != self.nparts:
+            raise ValueError(f"{what}: {len(ts)} slabs for {self.nparts} ranks")
+        n = int(np.prod(self.local_shape))
+        return [_dev(t, n, f"{what}[{r}]") for r, t in enumerate(ts)]
 
-    def deriv(self, fs, dfs, a=14 / 9, bc=1 / 9, h=None, stream=None):
-        if h is None:
-            import math
-            h = 2 * math.pi / self.global_dims[self.solve_dim]
-        ctri_deriv_loopback(self.handles, fs, dfs, a, bc, h, stream)
+    def solve(self, bs, xs, stream=None):
+        ctri_solve_loopback(self.handles, self._chk(bs, "b"), self._chk(xs, "x"), stream)
+
+    def deriv(self, fs, dfs, a=None, bc=None, h=None, stream=None):
+        ctri_deriv_loopback(self.handles, self._chk(fs, "f"), self._chk(dfs, "df"), a, bc, h, stream)
 
     def compact_apply(self, coef, fs, outs, stream=None):
-        ctri_compact_apply_loopback(self.handles, coef, fs, outs, stream)
+        ctri_compact_apply_loopback(self.handles, coef, self._chk(fs, "f"), self._chk(outs, "out"), stream)
 
     def stats(self, rank=0):
         return ctri_get_stats(self.handles[rank])

@@ -111,7 +111,7 @@ def main():
         results["penta"] = {"err": rel_err(x.cpu().numpy(), oracle.penta_solve(b, 0, pb, True), 0)}
     # staggered sixth-order interpolation through ctri_compact_apply
     from paper_2101_02286_b200 import ctri
-    plan = pdist.plan_from_process_group(dims, 0, ctri.STAGGERED_INTERP_BANDS, True, flags=CTRI_FLAG_DERIV)
+    plan = pdist.plan_from_process_group(dims, 0, ctri.staggered_interp_bands(), True, flags=CTRI_FLAG_DERIV)
     plan.compact_apply(ctri.staggered_interp_coef(), fl, dl)
     torch.cuda.synchronize()
     d = pdist.gather_to_rank0(dl, 0)

@@ -61,3 +61,20 @@ def test_no_product_import_of_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "ctri_oracle" not in txt, f
+
+
+def test_binding_rejects_host_and_wrong_size_buffers():
+    """The Plan wrappers check device placement and slab size before any pointer crosses the
+    ABI (a CPU tensor or a short buffer would otherwise fault inside a kernel)."""
+    import numpy as np
+    import pytest
+    import torch
+
+    from paper_2101_02286_b200 import ctri
+    with pytest.raises(ValueError, match="CUDA tensor"):
+        ctri._dev(torch.zeros(8, dtype=torch.float64), 8, "b")
+    with pytest.raises(ValueError, match="CUDA tensor"):
+        ctri._dev(np.zeros(8), 8, "b")
+    with pytest.raises(ValueError, match="elements"):
+        ctri._host(np.zeros(7), 8, "b_host")
+    assert ctri._dev(1234, 8, "b") == 1234  # raw addresses pass through (the C ABI checks them)

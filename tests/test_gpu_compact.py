@@ -31,9 +31,9 @@ def _scheme(name, N):
     from paper_2101_02286_b200 import ctri
     h = 2 * math.pi / N
     if name == "sderiv":
-        coef, ocoef, bands = ctri.staggered_deriv_coef(h), oracle.staggered_deriv_coef(h), ctri.STAGGERED_DERIV_BANDS
+        coef, ocoef, bands = ctri.staggered_deriv_coef(h), oracle.staggered_deriv_coef(h), ctri.staggered_deriv_bands()
     elif name == "sinterp":
-        coef, ocoef, bands = ctri.staggered_interp_coef(), oracle.staggered_interp_coef(), ctri.STAGGERED_INTERP_BANDS
+        coef, ocoef, bands = ctri.staggered_interp_coef(), oracle.staggered_interp_coef(), ctri.staggered_interp_bands()
     else:  # a general five-point stencil with non-symmetric bands
         coef = ocoef = (0.3, -1.7, 0.25, 2.1, -0.6)
         bands = (0.2, 1.1, 0.4)

@@ -523,3 +523,53 @@ def test_cfg2_full_size_loopback_partitions(p):
     x = torch.cat(xs, 0)
     assert st["reduced_path"] == 1 and st["device_error"] == 0
     assert _sampled_columns(b, x, 0, n_cols=128) < TOL_REL
+
+
+@pytest.mark.parametrize("p,n", [(4, 256), (2, 1024)])
+def test_deriv_halo_epochs_independent(p, n):
+    """Each derivative solve advances the reduced-phase epoch by one and the halo epoch by one
+    (separate counters and mailbox regions; with a shared counter the reduced phase would always
+    use the same of its two epoch copies), and 200 back-to-back derivatives stay correct."""
+    import torch
+
+    from paper_2101_02286_b200 import CTRI_FLAG_DERIV, ctri
+    shape = (p * n, 1, 32)
+    f = workloads.cfg5_field(shape, 0, 5)
+    ref = oracle.deriv(f, 0)
+    dev = torch.device("cuda:0")
+    g = ctri.LoopbackGroup(shape, 0, p, flags=CTRI_FLAG_DERIV)
+    fs = [torch.from_numpy(workloads.slab(f, 0, p, r)).to(dev) for r in range(p)]
+    ds = [torch.empty_like(t) for t in fs]
+    for k in range(1, 201):
+        g.deriv(fs, ds)
+        if k in (1, 2, 3, 200):
+            torch.cuda.synchronize()
+            st = g.stats(0)
+            assert st["p2p_epoch"] == k and st["halo_epoch"] == k, (k, st["p2p_epoch"], st["halo_epoch"])
+            assert st["device_error"] == 0
+    x = workloads.assemble([t.cpu().numpy() for t in ds], 0)
+    g.close()
+    assert rel_err(x, ref, 0) < 1e-12
+
+
+def test_p2p_deadline_poisons_plan(monkeypatch):
+    """A reduced row that never sends (test knob) makes its neighbour's LL wait hit the (here
+    200 ms) deadline: the error word is reported by ctri_get_stats and every later solve on the
+    group fails with CTRI_ERR_CUDA instead of returning stale results."""
+    import torch
+
+    from paper_2101_02286_b200 import CtriError, ctri
+    monkeypatch.setenv("CTRI_TEST_P2P_DEADLINE_MS", "200")
+    monkeypatch.setenv("CTRI_TEST_P2P_DROP_RANK", "1")
+    shape = (1024, 2, 32)
+    dev = torch.device("cuda:0")
+    g = ctri.LoopbackGroup(shape, 0, 4)
+    bs = [torch.ones(g.local_shape, dtype=torch.float64, device=dev) for _ in range(4)]
+    xs = [torch.empty_like(t) for t in bs]
+    g.solve(bs, xs)
+    torch.cuda.synchronize()
+    assert g.stats(0)["device_error"] == 1
+    with pytest.raises(CtriError) as e:
+        g.solve(bs, xs)
+    assert e.value.name == "CTRI_ERR_CUDA" and "destroy" in str(e.value)
+    g.close()

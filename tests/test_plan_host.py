@@ -398,3 +398,26 @@ def test_penta_block_pcr_vs_dense(bands, P, cyclic):
 def test_penta_block_pcr_rejects_cyclic_non_pow2():
     with pytest.raises(pk.CtriError, match="UNSUPPORTED"):
         pk.ctri_penta_block_pcr(3, 20, PENTA_BANDS[0], True)
+
+
+def test_scheme_coefficients_from_library():
+    """ctri_scheme_coef (the binding only marshals): the collocated pair a = 14/9, b = 1/9 at
+    alpha = 1/3 (R8) and the staggered schemes of P:202-206 (R18), against the oracle's
+    independently written tables; unknown schemes and bad spacings are rejected."""
+    import oracle
+    from paper_2101_02286_b200 import CtriError, ctri
+    h = 2 * math.pi / 64
+    c, bd = ctri.ctri_scheme_coef(ctri.CTRI_SCHEME_COLLOCATED_D1, h)
+    a, b = 14 / 9, 1 / 9
+    assert np.allclose(c, (-b / (4 * h), -a / (2 * h), 0.0, a / (2 * h), b / (4 * h)), rtol=1e-15)
+    assert bd == (1 / 3, 1.0, 1 / 3)
+    c, bd = ctri.ctri_scheme_coef(ctri.CTRI_SCHEME_STAGGERED_D1, h)
+    assert np.allclose(c, oracle.staggered_deriv_coef(h), rtol=1e-15) and bd == (9 / 62, 1.0, 9 / 62)
+    c, bd = ctri.ctri_scheme_coef(ctri.CTRI_SCHEME_STAGGERED_I)
+    assert np.allclose(c, oracle.staggered_interp_coef(), rtol=1e-15) and bd == (3 / 10, 1.0, 3 / 10)
+    # Lele's sixth-order family at alpha = 1/3: a = (2/3)(alpha + 2), b = (1/3)(4 alpha - 1)
+    c, _ = ctri.ctri_scheme_coef(ctri.CTRI_SCHEME_COLLOCATED_D1, 1.0)
+    assert abs(2 * c[3] - (2 / 3) * (1 / 3 + 2)) < 1e-15 and abs(4 * c[4] - (4 / 3 - 1) / 3) < 1e-15
+    for bad in ((7, 1.0), (ctri.CTRI_SCHEME_COLLOCATED_D1, 0.0), (ctri.CTRI_SCHEME_STAGGERED_D1, -1.0)):
+        with pytest.raises(CtriError):
+            ctri.ctri_scheme_coef(*bad)
