@@ -105,7 +105,10 @@ typedef struct ctri_stats {
   int32_t tile_stages;          /* TMA shared-memory ring depth of the tile kernel */
   int32_t reduced_path;         /* nparts > 1: 0 = NCCL rounds, 1 = fused P2P kernel (t_backsub_us
                                    then times the whole fused (a2)-(a4) kernel), 2 = P2P all-gather,
-                                   3 = fused into the local-solve tile kernel (t_local_us = all) */
+                                   3 = fused into the local-solve tile kernel (t_local_us = all);
+                                   nparts == 1 with vparts > 1: 3 when the virtual partitions'
+                                   reduced system and window rows are finished inside the
+                                   tile kernel (default), else 0 (k_reduced_local + k_window) */
   int32_t device_error;         /* nonzero: a P2P wait hit its deadline (peer missing) */
   int32_t vparts;               /* nparts == 1: partitions of the slab solved on this GPU (the
                                    paper's partition method; (a2)-(a4) then run on-device) */

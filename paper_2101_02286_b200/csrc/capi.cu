@@ -253,6 +253,9 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   P->fused = (flags & CTRI_FLAG_FUSED_REDUCED) && p > 1 && p <= 8 && !P->loopback &&
              P->local_kernel == 1 && P->tile.fused_ok &&
              !(flags & (CTRI_FLAG_NCCL_ROUNDS | CTRI_FLAG_FULL_BACKSUB | CTRI_FLAG_ALLGATHER));
+  // nparts == 1 with virtual partitions: (a2)-(a4) inside the tile kernel when it is configured
+  P->vchain = p == 1 && P->vp > 1 && P->local_kernel == 1 && P->tile.vc_ok && !knob_no_vchain() &&
+              !knob_copy_only();
   if (P->fused) {
     std::vector<double> inv;
     if (!reduced_inverse(p, cyclic != 0, L, D, U, pivot_threshold(P->bands), &inv, &fe))
@@ -301,7 +304,7 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   // launches per solve
   int launches = 1;
   if (p > 1 && !P->fused) launches += P->p2p ? 2 /*reduced + window*/ : 1 /*bhat*/ + P->gpcr.stages + 1 /*backsub*/;
-  if (p == 1 && P->vp > 1) launches += 2;  // local reduced system; window back-substitution
+  if (p == 1 && P->vp > 1 && !P->vchain) launches += 2;  // local reduced system; window pass
   P->launches_per_solve = launches;
   CUDA_TRY(cudaStreamSynchronize(s));
   return CTRI_OK;
@@ -727,7 +730,7 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
     return CTRI_OK;
   }
   if (P0.p == 1) {
-    if (P0.vp > 1) {  // (a2)-(a4) across the virtual partitions of this slab
+    if (P0.vp > 1 && !P0.vchain) {  // (a2)-(a4) across the virtual partitions of this slab
       for (size_t r = 0; r < G.size(); ++r) {
         cudaError_t e = launch_reduced_local(*G[r], x[r], s);
         if (e == cudaSuccess) e = launch_window(*G[r], x[r], nullptr, s);
@@ -1287,7 +1290,7 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
   out->tile_columns = P->local_kernel ? P->tile.C : 1;
   out->tile_variant = P->local_kernel ? P->tile.variant : -1;
   out->tile_stages = P->local_kernel ? P->tile.STAGES : 0;
-  out->reduced_path = P->fused ? 3 : (P->p > 1 && P->p2p) ? ((P->allgather || (P->r == 2 && !P->ppcr)) ? 2 : 1) : 0;
+  out->reduced_path = (P->fused || P->vchain) ? 3 : (P->p > 1 && P->p2p) ? ((P->allgather || (P->r == 2 && !P->ppcr)) ? 2 : 1) : 0;
   out->band_halfwidth = P->r;
   out->vparts = P->vp;
   out->grid_ctas = P->local_kernel ? P->tile.grid : (int32_t)((P->tlay.m() + 127) / 128);
@@ -1320,7 +1323,7 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
   for (int k = 0; k < CTRI_MAX_STAGES; ++k) out->t_stage_us[k] = out->t_p2p_step_us[k] = -1.f;
   out->t_reduced_kernel_us = out->t_window_us = out->t_p2p_y_us = out->t_p2p_x_us = -1.f;
   if (P->timed_valid || (!P->ev.empty() && P->solves > 0)) {
-    const bool two = P->p > 1 || P->vp > 1 || P->r == 2;
+    const bool two = P->p > 1 || (P->vp > 1 && !P->vchain) || P->r == 2;
     CUDA_TRY(cudaEventSynchronize(P->ev[two ? EV_BACK : EV_LOCAL]));
     out->t_local_us = elapsed(*P, EV_START, EV_LOCAL);
     if (P->p > 1 && P->p2p && !P->fused) {
@@ -1364,7 +1367,7 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
       out->t_xexchange_us = elapsed(*P, prev, EV_XX);
       out->t_backsub_us = elapsed(*P, EV_XX, EV_BACK);
       out->t_total_us = elapsed(*P, EV_START, EV_BACK);
-    } else if (P->vp > 1 || P->r == 2) {
+    } else if ((P->vp > 1 && !P->vchain) || P->r == 2) {
       out->t_backsub_us = elapsed(*P, EV_LOCAL, EV_BACK);  // local reduced + window back-sub
       out->t_total_us = elapsed(*P, EV_START, EV_BACK);
     } else {

@@ -96,7 +96,10 @@ struct TileArgs {
   Stencil5 st;
   const double* halo_lo;  // [2][m]: rows n-2, n-1 of the slab above
   const double* halo_hi;  // [2][m]: rows 0, 1 of the slab below
-  unsigned long long* trace;  // measurement only (CTRI_TILE_TRACE)
+  unsigned long long* trace;  // measurement only (CTRI_TILE_TRACE=<cta>)
+  int trace_cta;              // the CTA whose tiles are stamped
+  int vc_dbg;                 // experiment knob CTRI_VC_DBG (bit 0: no window finalisation,
+                              // bit 1: window rows stored evict-first like the rest)
   // fused reduced phase (LAYOUT 3, nparts > 1): the window rows of every tile stay
   // in shared memory while the tile's (c = b~ - u y_D[1], y_D[n-1]) go to every rank's mailbox
   // as LL words; one tile later x~_i, x~_{i+1} = rows i, i+1 of A^{-1} applied to the gathered
@@ -108,6 +111,16 @@ struct TileArgs {
   const double *f_S, *f_R;               // slab-level S_i, R_i (n - 1)
   unsigned int *f_epoch, *f_done;        // device epoch of the solve, CTA completion count
   int* f_err;                            // deadline error word
+  // virtual-partition chain (LAYOUT 4, nparts == 1 with vp > 1): one cluster solves the vp
+  // partitions of a column group back to back, gathers their planes on chip (c_v = b~_v -
+  // u y_v[first] in CTA 0, y_v[last] in CTA G-1, exchanged by st.async), solves the vp-row
+  // reduced system per column with the plan's PCR multipliers (fold R3) and
+  // finalises the window rows of every partition (Eq. xi_app, R15) while the next group is
+  // being solved: they were stored with an L2 evict-last hint and are read back from L2, so
+  // HBM sees 16 B per point.  f_S / f_R carry the slab-level S, R tables.
+  int vc_vp, vc_W, vc_q, vc_cyclic;
+  int64_t vc_groups;                     // column groups (num_tiles / vp)
+  double vc_alpha[4 * 8], vc_gamma[4 * 8], vc_inv[8];  // [stage][row] PCR of the vp-row system
 };
 
 struct TileConfig {
@@ -124,6 +137,8 @@ struct TileConfig {
   int smem_deriv = 0, grid_deriv = 0;
   bool fused_ok = false;               // fused reduced-phase instantiation configured (LAYOUT 3)
   int smem_fused = 0, grid_fused = 0, fused_srw = 0;
+  bool vc_ok = false;                  // virtual-partition chain instantiation (LAYOUT 4)
+  int smem_vc = 0, grid_vc = 0;
   std::vector<double> consts;  // serialized TileConsts<K> (l, u, then 4 tables of K-1)
   PcrTables pcr;
   double* d_pcr = nullptr;     // device: alpha | gamma | inv
@@ -240,6 +255,8 @@ struct Plan {
   std::vector<double> ainv;       // [p][p] A^{-1} (all-gather mode)
   int p2p_nslices = 0;
   bool fused = false;                  // (a2)-(a4) fused into the tile kernel (LAYOUT 3)
+  bool vchain = false;                 // nparts == 1, vp > 1: (a2)-(a4) inside the tile kernel
+                                       // (LAYOUT 4, no k_reduced_local / k_window launches)
   double fg0[8] = {0}, fg1[8] = {0};   // fused: rows rank, rank + 1 of A^{-1}
   unsigned int* d_fctr = nullptr;      // fused: [epoch, CTA completion count]
   int64_t p2p_off = 0;                 // words before the P2P-kernel region of the mailbox
@@ -294,6 +311,8 @@ inline bool knob_no_pdl() { static const bool v = env_knob("CTRI_NO_PDL"); retur
 inline bool knob_p2p_trace() { static const bool v = env_knob("CTRI_P2P_TRACE"); return v; }
 inline bool knob_tile_trace() { static const bool v = env_knob("CTRI_TILE_TRACE"); return v; }
 inline bool knob_copy_only() { static const bool v = env_knob("CTRI_TILE_COPY_ONLY"); return v; }
+// CTRI_NO_VCHAIN: virtual partitions finish with k_reduced_local + k_window (A/B measurement)
+inline bool knob_no_vchain() { static const bool v = env_knob("CTRI_NO_VCHAIN"); return v; }
 
 // kernels.cu launchers (return cudaError_t of the launch)
 cudaError_t launch_local_generic(const Plan& P, const double* b, double* x, cudaStream_t s);

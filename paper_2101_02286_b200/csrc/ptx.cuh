@@ -53,6 +53,11 @@ __device__ __forceinline__ void fence_mbar_init() {
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// orders this thread's (and what it acquired of other threads') generic-proxy global accesses
+// before its subsequent async-proxy (TMA) accesses of global memory
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
@@ -62,6 +67,17 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+// the same wait with acquire semantics at cluster scope: writes that remote CTAs made before
+// their st.async onto this barrier (release at cluster scope) are visible afterwards
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
       "r"(phase)
       : "memory");
@@ -92,6 +108,21 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// store with an L2 eviction-priority hint (createpolicy)
+__device__ __forceinline__ void st_global_hint(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+// load cached in L2 only (data this CTA stored earlier in the same kernel; ordered by bar.sync)
+__device__ __forceinline__ double ld_global_cg(const double* p) {
+  double v;
+  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
 // Asynchronous remote store into a (possibly other) CTA's shared memory of the cluster; the
 // destination CTA's mbarrier `bar` (shared::cluster address) receives complete_tx of 8 bytes.
 __device__ __forceinline__ void st_async_f64(uint32_t addr, double v, uint32_t bar) {
@@ -101,6 +132,9 @@ __device__ __forceinline__ void st_async_f64(uint32_t addr, double v, uint32_t b
 }
 __device__ __forceinline__ void cp_async_16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }

@@ -49,10 +49,14 @@ __global__ void __launch_bounds__(NT, MINB)
   constexpr bool CONTIG = (LAYOUT == 1);
   constexpr bool DERIV = (LAYOUT == 2);
   constexpr bool FUSED = (LAYOUT == 3);
+  // LAYOUT 4: nparts == 1 with vp virtual partitions: the cluster walks the vp partitions of a
+  // column group back to back and finishes (a2)-(a4) on chip (TileArgs vc_*)
+  constexpr bool VC = (LAYOUT == 4);
   constexpr int HALO = DERIV ? 2 : 0;     // stencil half-width (rows)
-  static_assert(K >= 4 && NT % C == 0 && (C == 4 || C == 8 || C == 16 || C == 32), "tile geometry");
+  static_assert(K >= 4 && NT % C == 0 && (C == 4 || C == 8 || C == 16 || C == 32 || C == 64), "tile geometry");
   static_assert(!CONTIG || (NT / C == 32 && SUB == 1 && SLOTS == 1), "contiguous: 32 chunks/CTA");
   static_assert(!DERIV || SUB == 1, "fused stencil: whole-tile ring slots");
+  static_assert(!VC || (SUB == 1 && !CONTIG), "virtual-partition chain: strided whole tiles");
   static_assert(SLOTS >= SUB, "ring must hold one tile");
   constexpr int CPC = NT / C;             // chunks per CTA
   constexpr int ROWS = CPC * K;           // rows per CTA
@@ -84,13 +88,23 @@ __global__ void __launch_bounds__(NT, MINB)
   uint64_t* mbar = reinterpret_cast<uint64_t*>(tab ? s_inv + Q : s_alpha);  // [SLOTS] ring, ex, rx
   uint64_t* mbar_ex = mbar + SLOTS;
   uint64_t* mbar_rx = mbar_ex + 1;
+  uint64_t* mbar_red = mbar_rx + 1;  // VC: [2] planes of a column group's owned columns
   // FUSED: [2][f_srw][C] window rows (128-byte aligned: TMA-store source)
   // (offset arithmetic on smem_raw, not on an integer address: the compiler must keep seeing
   // a shared-memory pointer, or every stash access becomes a generic LD/ST)
   double* f_stash = reinterpret_cast<double*>(
-      smem_raw + ((reinterpret_cast<unsigned char*>(mbar_rx + 1) - smem_raw + 127) & ~(ptrdiff_t)127));
+      smem_raw + ((reinterpret_cast<unsigned char*>(mbar_red + 2) - smem_raw + 127) & ~(ptrdiff_t)127));
   double* f_red = FUSED ? f_stash + (size_t)2 * A.f_srw * C : nullptr;  // [2][NT] partial x~
   double* f_sr = FUSED ? f_red + 2 * NT : nullptr;  // [2][f_srw]: S, R of the stashed rows
+  // VC (per owned column, C/G of them): [2 groups][8] c_v and y_v[last] planes, [2 groups][9]
+  // x~ (row vp: x~ past the last partition); [2][2W+1] S, R of the window rows in block order
+  // (rows 0..W, then nv-W..nv-1)
+  double* vc_c = f_stash;
+  double* vc_yl = vc_c + 2 * 8 * C;
+  double* vc_xt = vc_yl + 2 * 8 * C;
+  double* vc_sr = vc_xt + 2 * 9 * C;
+  double* vc_pcr = vc_sr + 2 * (VC ? 2 * A.vc_W + 1 : 0);  // [72] PCR multipliers, vp-row system
+  double* vc_buf = vc_pcr + 72;  // [2][3][NT] window rows in flight (cp.async, double-buffered)
 
   const int tid = threadIdx.x;
   // strided axis: lanes run over the C columns of a tile row (coalesced rows);
@@ -119,25 +133,65 @@ __global__ void __launch_bounds__(NT, MINB)
   if (tid < SLOTS) dev::mbar_init(dev::smem_u32(mbar + tid), 1);
   if (tid == SLOTS) dev::mbar_init(dev::smem_u32(mbar_ex), 1);
   if (tid == SLOTS + 1) dev::mbar_init(dev::smem_u32(mbar_rx), 1);
+  if (VC && tid == SLOTS + 2) dev::mbar_init(dev::smem_u32(mbar_red), 1);
+  if (VC && tid == SLOTS + 3) dev::mbar_init(dev::smem_u32(mbar_red + 1), 1);
+  if (VC) {  // S, R of the window rows (Eq. xi_app, R15) by block row ri: slab row ri (ri <= W),
+             // else nv - 2W - 1 + ri; row 0 is x~ itself
+    const int W = A.vc_W, R2 = 2 * W + 1;
+    const int64_t nv = A.lay.n;
+    for (int ri = tid; ri < R2; ri += NT) {
+      const int64_t r = ri <= W ? ri : nv - R2 + ri;
+      vc_sr[ri] = r >= 1 ? A.f_S[r - 1] : 0.0;
+      vc_sr[R2 + ri] = r >= 1 ? A.f_R[r - 1] : 0.0;
+    }
+    for (int i = tid; i < 72; i += NT)
+      vc_pcr[i] = i < 32 ? A.vc_alpha[i] : i < 64 ? A.vc_gamma[i - 32] : i < 72 ? A.vc_inv[i - 64] : 0.0;
+  }
   if (tid == 0) dev::fence_mbar_init();
   __syncthreads();
   if (G > 1) dev::cluster_sync();  // barriers initialised cluster-wide before any st.async
 
   const uint32_t ncl = (G > 1) ? dev::ncluster_x() : gridDim.x;
   const int64_t first = (G > 1) ? (int64_t)dev::cluster_id_x() : (int64_t)blockIdx.x;
+  // tile of this cluster's iteration itx (-1 past the end)
+  auto tile_at = [&](int64_t itx) -> int64_t {
+    const int64_t t = first + itx * (int64_t)ncl;
+    return t < A.num_tiles ? t : -1;
+  };
+  // VC: the cluster walks column groups first, first + ncl, ...; within a group the vp
+  // partitions one after the other (tile (og * vp + v, ct)); positions advance incrementally,
+  // one 64-bit division per group
+  // (32-bit: the host checks that column groups and tiles per outer index fit)
+  const int vcp = VC ? A.vc_vp : 1;
+  const int vtpo = (int)A.tiles_per_outer;
+  auto vc_og = [&](int gi) { return ((int)first + gi * (int)ncl) / vtpo; };  // outer index of group gi
+  auto vc_ct = [&](int gi) {                                                   // its column tile
+    const int cg = (int)first + gi * (int)ncl;
+    return cg - (cg / vtpo) * vtpo;
+  };
+  auto vc_has = [&](int gi) { return (int64_t)first + (int64_t)gi * ncl < A.vc_groups; };
+  int vq = 0, vgi = 0;              // partition within the group, groups completed
   constexpr uint32_t kSubBytes = (uint32_t)(SR + 2 * HALO) * C * (uint32_t)sizeof(double);
   const int boxr = A.rows_box;
   const int row0 = (int)g * ROWS;
   const uint64_t pol = dev::policy_evict_first();
 
   // sub-tile sequence number seq -> (tile first + (seq / SUB) * ncl, part seq % SUB), slot seq % SLOTS
-  auto issue = [&](int64_t seq) {
-    const int64_t t = first + (seq / SUB) * (int64_t)ncl;
-    if (t >= A.num_tiles) return;
+  // (VC: the caller passes the tile's outer index and first column, o_vc >= 0)
+  auto issue = [&](int64_t seq, int64_t o_vc = -1, int64_t col_vc = 0) {
+    int o, col0;
+    if (VC) {
+      if (o_vc < 0) return;
+      o = (int)o_vc;
+      col0 = (int)col_vc;
+    } else {
+      const int64_t t = tile_at(seq / SUB);
+      if (t < 0) return;
+      o = (int)(t / A.tiles_per_outer);
+      col0 = (int)(t - (int64_t)o * A.tiles_per_outer) * C;
+    }
     const int h = (int)(seq % SUB);
     const int s = (int)(seq % SLOTS);
-    const int o = (int)(t / A.tiles_per_outer);
-    const int col0 = (int)(t - (int64_t)o * A.tiles_per_outer) * C;
     const uint32_t bar = dev::smem_u32(mbar + s);
     double* dst = ring + (size_t)s * RING;
     const int r0 = row0 + h * SR;
@@ -154,25 +208,14 @@ __global__ void __launch_bounds__(NT, MINB)
   const int hsub = cl / CPS, lc = cl - (cl / CPS) * CPS;  // my sub-tile and chunk within it
 
   // remote addresses: my (b~, y_first, y_last) -> owner; my x~ -> holders of chunks oc, oc-1
-  uint32_t r_bt = dev::smem_u32(ex_bt + slot), r_yf = dev::smem_u32(ex_yf + slot),
-           r_yl = dev::smem_u32(ex_yl + slot), r_exbar = dev::smem_u32(mbar_ex);
+  // (mapped where they are used: mapa is one instruction, a live address a register)
+  auto rmap = [&](const void* p, uint32_t rank) {
+    const uint32_t a = dev::smem_u32(p);
+    return G > 1 ? dev::mapa(a, rank) : a;
+  };
   // holder thread of (column ocol, chunk cc): strided tid = cl*C + j, contiguous tid = j*32 + cl
   auto holder_tid = [&](int cc) { return CONTIG ? ocol * 32 + (cc % CPC) : (cc % CPC) * C + ocol; };
-  const int ha = oc / CPC, ta = holder_tid(oc);                 // holder of chunk oc
-  const int ocm = (oc - 1) & (Q - 1);
-  const int hb = ocm / CPC, tb = holder_tid(ocm);               // holder of chunk oc-1
-  uint32_t r_xa = dev::smem_u32(rx_a + ta), r_xb = dev::smem_u32(rx_b + tb),
-           r_rxa = dev::smem_u32(mbar_rx), r_rxb = dev::smem_u32(mbar_rx);
-  if (G > 1) {
-    r_bt = dev::mapa(r_bt, owner);
-    r_yf = dev::mapa(r_yf, owner);
-    r_yl = dev::mapa(r_yl, owner);
-    r_exbar = dev::mapa(r_exbar, owner);
-    r_xa = dev::mapa(r_xa, (uint32_t)ha);
-    r_rxa = dev::mapa(r_rxa, (uint32_t)ha);
-    r_xb = dev::mapa(r_xb, (uint32_t)hb);
-    r_rxb = dev::mapa(r_rxb, (uint32_t)hb);
-  }
+  const int ocm = (oc - 1) & (Q - 1);  // chunk oc's holder gets x~_oc as x_a, chunk oc-1's as x_b
 
   // contiguous axis: ONE TMA load per tile through a 3-D view (row in chunk, chunk, column) of
   // the slab with a box of K+2 rows per chunk: the 2 rows past each chunk are out of bounds of
@@ -188,11 +231,13 @@ __global__ void __launch_bounds__(NT, MINB)
   if (CONTIG) {
     if (first < A.num_tiles) issue_contig(first);
   } else if (tid == 0) {
-    for (int s = 0; s < SLOTS; ++s) issue(s);
+    if (VC) issue(0, vc_has(0) ? (int64_t)vc_og(0) * vcp : -1, (int64_t)vc_ct(0) * C);
+    else
+      for (int s = 0; s < SLOTS; ++s) issue(s);
   }
 
   // measurement only (CTRI_TILE_TRACE): CTA 0 stamps its first 64 tiles' phases
-  unsigned long long* tr = (A.trace && blockIdx.x == 0) ? A.trace : nullptr;
+  unsigned long long* tr = (A.trace && (int)blockIdx.x == A.trace_cta) ? A.trace : nullptr;
   auto stamp = [&](int it_, int k) {
     if (tr && tid == 0 && it_ < 64) {
       unsigned long long tt;
@@ -327,17 +372,118 @@ __global__ void __launch_bounds__(NT, MINB)
     stamp(it, 11);
   };
 
-  for (int64_t t = first; t < A.num_tiles; t += ncl, ++it) {
+  // ---- virtual-partition chain (VC): roles, window rows, reduced solve, finalisation ----
+  // Every CTA finishes the columns whose head systems it owns (cpo of them): it receives their
+  // planes, solves their vp-row systems and finalises their window rows.  The window rows were
+  // stored by the holder threads of those columns, whose later st.async head stores complete on
+  // this CTA's exchange barrier with release semantics at cluster scope; the exchange wait is an
+  // acquire at cluster scope, so those stores are visible here (no fence on the tile path).
+  const int vc_W = VC ? A.vc_W : 0;
+  const int vc_nv = VC ? (int)A.lay.n : 0;
+  const int vc_R2 = 2 * vc_W + 1;  // window block rows per partition
+  // rows k <= vc_wt of this thread's chunk are top-window rows (CTA 0), rows k >= vc_wb bottom
+  // (CTA G-1): stored with an L2 evict-last hint, finalised one column group later
+  const int vc_wt = (VC && g == 0) ? vc_W - c * K : -1;
+  const int vc_wb = (VC && (int)g == G - 1) ? vc_nv - vc_W - c * K : K + 1;
+  // (a2)-(a3) for the owned columns of group parity par: lane group of vp threads per column
+  // (thread tid < cpo*vp: row v = tid % vp of column tid / vp): b^_v = c_v - l y_{v-1}[last]
+  // (Eq. bi_hat), PCR over the vp rows by register shuffles with the plan's multipliers
+  // (both partners may coincide, fold R3), x~_v = b^_v inv_v -> vc_xt[par][v]
+  // (row vp: x~ right of the last partition, the wrap x~_0 or 0 when acyclic)
+  auto vc_solve = [&](int par) {
+    const int v = tid % vcp, jl = tid / vcp;
+    const bool act = jl < cpo;
+    const int vl = v == 0 ? vcp - 1 : v - 1;
+    double bh = 0.0;
+    if (act) {
+      const double ylp = (v > 0 || A.vc_cyclic) ? vc_yl[(par * 8 + vl) * cpo + jl] : 0.0;
+      bh = vc_c[(par * 8 + v) * cpo + jl] - T.l * ylp;
+    }
+    for (int k = 0; k < A.vc_q; ++k) {
+      const int sh = 1 << k;
+      const double vm = __shfl_sync(0xffffffffu, bh, (v - sh) & (vcp - 1), vcp);
+      const double vq = __shfl_sync(0xffffffffu, bh, (v + sh) & (vcp - 1), vcp);
+      bh = bh - vc_pcr[k * 8 + v] * vm - vc_pcr[32 + k * 8 + v] * vq;
+    }
+    if (act) {
+      const double xv = bh * vc_pcr[64 + v];
+      vc_xt[(par * 9 + v) * cpo + jl] = xv;
+      if (v == 0) vc_xt[(par * 9 + vcp) * cpo + jl] = A.vc_cyclic ? xv : 0.0;
+    }
+  };
+  const bool vc_solver = VC && (tid / 32) < (cpo * vcp + 31) / 32;  // whole warps (shuffles)
+  // window element i of this thread: block row tid / cpo + i * (NT / cpo), owned column tid % cpo
+  constexpr int kVcFin = 3;  // host: (2W + 1) * C / G <= 3 NT
+  const int vc_jl = tid % cpo;
+  const int vc_r0 = tid / cpo, vc_rs = NT / cpo;
+  auto vc_block = [&](int gi, int q) -> double* {  // (row 0, this thread's column) of a block
+    const int64_t colp = (int64_t)vc_ct(gi) * C + (int64_t)g * cpo + vc_jl;
+    if (colp >= A.lay.inner) return nullptr;
+    return A.x + ((int64_t)(vc_og(gi) * vcp + q) * vc_nv) * A.lay.inner + colp;
+  };
+  auto vc_row = [&](int ri) { return ri <= vc_W ? ri : vc_nv - vc_R2 + ri; };
+  // y of the window rows (stored >= vp tiles earlier by the holder CTAs) -> this thread's
+  // vc_buf slots by cp.async (L2 only), so nothing is held in registers meanwhile
+  auto vc_load = [&](const double* blk, int bf) {
+    if (blk) {
+      double* bb = vc_buf + bf * kVcFin * NT;
+#pragma unroll
+      for (int i = 0; i < kVcFin; ++i) {
+        const int ri = vc_r0 + i * vc_rs;
+        if (ri < vc_R2 && ri != 0)
+          dev::cp_async_8(dev::smem_u32(bb + i * NT + tid), blk + (int64_t)vc_row(ri) * A.lay.inner);
+      }
+    }
+    dev::cp_async_commit();
+  };
+  // Eq. xi_app on the loaded window rows (row 0 of the partition := x~_q), stored once
+  auto vc_store = [&](double* blk, int gp, int q, int bf) {
+    if (!blk) return;
+    const double* bb = vc_buf + bf * kVcFin * NT;
+    const double* xt = vc_xt + (gp & 1) * 9 * cpo;
+    const double xa = xt[q * cpo + vc_jl], xb = xt[(q + 1) * cpo + vc_jl];
+#pragma unroll
+    for (int i = 0; i < kVcFin; ++i) {
+      const int ri = vc_r0 + i * vc_rs;
+      if (ri >= vc_R2) break;
+      const double xv = ri == 0 ? xa : bb[i * NT + tid] - vc_sr[ri] * xa - vc_sr[vc_R2 + ri] * xb;
+      dev::st_global_cs(blk + (int64_t)vc_row(ri) * A.lay.inner, xv);
+    }
+  };
+  // the window block finalised at tile itx: that of tile itx - vp - 1 (partition q - 1 of the
+  // previous group, or the last partition of the group before it); false if none
+  auto vc_target = [&](int gi, int q, int* fg, int* fq) -> bool {
+    *fq = q >= 1 ? q - 1 : vcp - 1;
+    *fg = q >= 1 ? gi - 1 : gi - 2;
+    return *fg >= 0 && !(A.vc_dbg & 1);
+  };
+
+  for (;; ++it) {
+    int64_t t;
+    int vog = 0, vct = 0;  // VC: this group's outer index and column tile
+    if (VC) {
+      if (!vc_has(vgi)) break;
+      vog = vc_og(vgi);
+      vct = vc_ct(vgi);
+      t = ((int64_t)vog * vcp + vq) * A.tiles_per_outer + vct;
+    } else {
+      t = tile_at(it);
+      if (t < 0) break;
+    }
     stamp(it, 0);
+    const int vc_q = vq;                            // VC: partition of this tile
+    const int vc_gi = vgi;                          // VC: column group (this cluster's count)
     if (FUSED && (f_top || f_bot) && it > 0) f_prefetch(t - ncl);
     const int64_t seq = (int64_t)it * SUB + hsub;
     const int s = (int)(seq % SLOTS);
     // global column: strided axis (o, col) with col < inner; contiguous axis column = o
-    const int64_t o = CONTIG ? t * C + j : t / A.tiles_per_outer;
-    const int64_t col = CONTIG ? 0 : (t - o * A.tiles_per_outer) * C + j;
+    const int64_t o = CONTIG ? t * C + j : (VC ? (int64_t)vog * vcp + vq : t / A.tiles_per_outer);
+    const int64_t col = CONTIG ? 0 : (VC ? (int64_t)vct * C : (t - o * A.tiles_per_outer) * C) + j;
     if (tid == 0 && A.mode != 3) {  // arm this tile's exchange barriers (remote bytes may race ahead)
       dev::mbar_expect_tx(dev::smem_u32(mbar_ex), (uint32_t)NT * 3u * 8u);
       dev::mbar_expect_tx(dev::smem_u32(mbar_rx), (uint32_t)NT * 2u * 8u);
+      if (VC && vc_q == 0)  // c_v and y_v[last] of this group's owned columns
+        dev::mbar_expect_tx(dev::smem_u32(mbar_red + (vc_gi & 1)), (uint32_t)(2 * vcp * cpo * 8));
     }
     dev::mbar_wait(dev::smem_u32(mbar + s), (uint32_t)(seq / SLOTS) & 1u);
     double* tile = ring + (size_t)s * RING;
@@ -402,12 +548,30 @@ __global__ void __launch_bounds__(NT, MINB)
     if (CONTIG) {
       if (t + ncl < A.num_tiles) issue_contig(t + ncl);
     } else if (tid == 0) {
-      for (int hh = 0; hh < SUB; ++hh) issue((int64_t)it * SUB + hh + SLOTS);  // freed slots
+      if (VC) {  // the next tile: next partition of this group, or partition 0 of the next group
+        if (vq + 1 < vcp) issue(it + 1, (int64_t)vog * vcp + vq + 1, (int64_t)vct * C);
+        else issue(it + 1, vc_has(vgi + 1) ? (int64_t)vc_og(vgi + 1) * vcp : -1, (int64_t)vc_ct(vgi + 1) * C);
+      } else {
+        for (int hh = 0; hh < SUB; ++hh) issue((int64_t)it * SUB + hh + SLOTS);  // freed slots
+      }
     }
     const bool valid = CONTIG ? (o < A.lay.outer) : (col < A.lay.inner);
     auto store_chunk = [&]() {
       if (!valid) return;
       double* xp = A.x + (o * A.lay.n + (int64_t)c * K) * A.lay.inner + col;
+      if (VC && (vc_wt >= 0 || vc_wb <= K)) {  // a chunk holding window rows (warp-uniform:
+        // the chunk is the warp): their y stays in L2 until the finaliser reads it back
+        const uint64_t pol_last = dev::policy_evict_last();
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if ((k <= vc_wt || k >= vc_wb) && !(A.vc_dbg & 2)) {
+            if (c != 0 || k != 0) dev::st_global_hint(xp + (int64_t)k * A.lay.inner, v[k], pol_last);
+          } else {
+            dev::st_global_cs(xp + (int64_t)k * A.lay.inner, v[k]);
+          }
+        }
+        return;
+      }
       if (FUSED) {  // window rows wait in shared memory for x~ (finalised one tile later)
         double* stp = f_stash + (size_t)(it & 1) * A.f_srw * C + (size_t)f_soff * C + j;
 #pragma unroll
@@ -445,36 +609,69 @@ __global__ void __launch_bounds__(NT, MINB)
     }
     stamp(it, 2);
     // ---- (b~_c, y_c[first], y_c[last]) -> owner CTA, completing on its exchange barrier ----
-    dev::st_async_f64(r_bt, btv, r_exbar);
-    dev::st_async_f64(r_yf, v[1], r_exbar);
-    dev::st_async_f64(r_yl, v[K - 1], r_exbar);
+    {
+      const uint32_t bar = rmap(mbar_ex, owner);
+      dev::st_async_f64(rmap(ex_bt + slot, owner), btv, bar);
+      dev::st_async_f64(rmap(ex_yf + slot, owner), v[1], bar);
+      dev::st_async_f64(rmap(ex_yl + slot, owner), v[K - 1], bar);
+    }
+    if (VC) {  // in the shadow of the exchange: (a2)-(a4) work of earlier tiles
+      // x~ of the previous group's owned columns (its planes left at least a tile ago)
+      if (vc_q == 0 && vc_gi > 0 && vc_solver) {
+        const int par = (vc_gi - 1) & 1;
+        dev::mbar_wait(dev::smem_u32(mbar_red + par), (uint32_t)(((vc_gi - 1) >> 1) & 1));
+        vc_solve(par);
+      }
+      int fg, fq;
+      dev::cp_async_wait_all();  // this thread's window rows of this tile's target (loaded a tile ago)
+      if (vc_target(vc_gi, vc_q, &fg, &fq)) vc_store(vc_block(fg, fq), fg, fq, it & 1);
+      // start loading the next tile's target (stored >= vp tiles ago and acquired since)
+      const int nq = vc_q + 1 < vcp ? vc_q + 1 : 0, ngi = vc_q + 1 < vcp ? vc_gi : vc_gi + 1;
+      if (vc_target(ngi, nq, &fg, &fq)) vc_load(vc_block(fg, fq), (it + 1) & 1);
+    }
     // ---- owner: head system b^_c (Eq. bi_hat at chunk level), then PCR stages ----
     {
-      dev::mbar_wait(dev::smem_u32(mbar_ex), (uint32_t)it & 1u);
+      if (VC) dev::mbar_wait_acq_cluster(dev::smem_u32(mbar_ex), (uint32_t)it & 1u);
+      else dev::mbar_wait(dev::smem_u32(mbar_ex), (uint32_t)it & 1u);
       stamp(it, 3);
       const double lt = (A.mode == 2 && oc == 0) ? 0.0 : T.l * ex_yl[prev_row];  // acyclic top
       double bh = ex_bt[tid] - lt - T.u * ex_yf[tid];
       if (A.mode == 1 && oc == 0) bh = 0.0;  // slab row 0 is the GPU interface, not in D_i
-      double* cur = pb0;
-      double* nxt = pb1;
-      for (int k = 0; k < stages; ++k) {
-        cur[tid] = bh;
-        __syncthreads();
-        const int sh = 1 << k;
-        const double vm = cur[oj * Q + ((oc - sh) & (Q - 1))];
-        const double vp = cur[oj * Q + ((oc + sh) & (Q - 1))];
-        const double al = tab ? s_alpha[k * Q + oc] : A.ualpha[k];
-        const double ga = tab ? s_gamma[k * Q + oc] : A.ugamma[k];
-        bh = bh - al * vm - ga * vp;
-        double* tmp = cur;
-        cur = nxt;
-        nxt = tmp;
+      if (Q <= 32) {
+        // the Q heads of an owned column are Q consecutive lanes of one warp (oc = lane % Q):
+        // every PCR stage is a pair of register shuffles, no shared memory and no block barrier
+        for (int k = 0; k < stages; ++k) {
+          const int sh = 1 << k;
+          const double vm = __shfl_sync(0xffffffffu, bh, (oc - sh) & (Q - 1), Q);
+          const double vp = __shfl_sync(0xffffffffu, bh, (oc + sh) & (Q - 1), Q);
+          const double al = tab ? s_alpha[k * Q + oc] : A.ualpha[k];
+          const double ga = tab ? s_gamma[k * Q + oc] : A.ugamma[k];
+          bh = bh - al * vm - ga * vp;
+        }
+      } else {
+        double* cur = pb0;
+        double* nxt = pb1;
+        for (int k = 0; k < stages; ++k) {
+          cur[tid] = bh;
+          __syncthreads();
+          const int sh = 1 << k;
+          const double vm = cur[oj * Q + ((oc - sh) & (Q - 1))];
+          const double vp = cur[oj * Q + ((oc + sh) & (Q - 1))];
+          const double al = tab ? s_alpha[k * Q + oc] : A.ualpha[k];
+          const double ga = tab ? s_gamma[k * Q + oc] : A.ugamma[k];
+          bh = bh - al * vm - ga * vp;
+          double* tmp = cur;
+          cur = nxt;
+          nxt = tmp;
+        }
       }
       const double xt = bh * (tab ? s_inv[oc] : A.uinv);
       stamp(it, 4);
       // x~_oc -> x_a of chunk oc's holder and x_b of chunk oc-1's holder
-      dev::st_async_f64(r_xa, xt, r_rxa);
-      dev::st_async_f64(r_xb, xt, r_rxb);
+      dev::st_async_f64(rmap(rx_a + holder_tid(oc), (uint32_t)(oc / CPC)), xt,
+                        rmap(mbar_rx, (uint32_t)(oc / CPC)));
+      dev::st_async_f64(rmap(rx_b + holder_tid(ocm), (uint32_t)(ocm / CPC)), xt,
+                        rmap(mbar_rx, (uint32_t)(ocm / CPC)));
     }
     dev::mbar_wait(dev::smem_u32(mbar_rx), (uint32_t)it & 1u);
     stamp(it, 5);
@@ -489,6 +686,21 @@ __global__ void __launch_bounds__(NT, MINB)
     if (FUSED && (f_top || f_bot) && it > 0) f_finalize(t - ncl, (it - 1) & 1);
     store_chunk();
     stamp(it, 6);
+    if (VC) {  // (a2) planes of partition vc_q -> the column's owner CTA: c_v (chunk 0) and
+               // y_v[last] (chunk Q-1)
+      const int par = (int)(vc_gi & 1);
+      const int e = (par * 8 + vc_q) * cpo + (j % cpo);
+      if (c == 0)  // c_v = b~_v - u y_v[first]
+        dev::st_async_f64(dev::mapa(dev::smem_u32(vc_c + e), owner), btv - T.u * v[1],
+                          dev::mapa(dev::smem_u32(mbar_red + par), owner));
+      if (c == Q - 1)
+        dev::st_async_f64(dev::mapa(dev::smem_u32(vc_yl + e), owner), v[K - 1],
+                          dev::mapa(dev::smem_u32(mbar_red + par), owner));
+      if (++vq == vcp) {  // next column group
+        vq = 0;
+        ++vgi;
+      }
+    }
     if (valid && FUSED) {  // (a2) planes of this tile -> every rank's mailbox (all-gather, R21)
       const int64_t jo = o * A.lay.inner + col;
       if (c == 0) {
@@ -507,6 +719,27 @@ __global__ void __launch_bounds__(NT, MINB)
         if (c == Q - 1) A.plane_yl[pj] = v[K - 1];
       }
     }
+  }
+  if (VC && vgi > 0) {  // finalise this cluster's last partitions
+    const int gl = vgi - 1;
+    dev::cluster_sync();  // the last tiles' window rows, stored by the holder CTAs, visible here
+    dev::cp_async_wait_all();
+    int fg, fq;
+    if (vc_target(vgi, 0, &fg, &fq))  // loaded by the last tile (into buffer it & 1)
+      vc_store(vc_block(fg, fq), fg, fq, it & 1);
+    if (vc_solver) {
+      const int par = gl & 1;
+      dev::mbar_wait(dev::smem_u32(mbar_red + par), (uint32_t)((gl >> 1) & 1));
+      vc_solve(par);
+    }
+    __syncthreads();
+    if (!(A.vc_dbg & 1))
+      for (int q = 0; q < vcp; ++q) {
+        double* blk = vc_block(gl, q);
+        vc_load(blk, 0);
+        dev::cp_async_wait_all();
+        vc_store(blk, gl, q, 0);
+      }
   }
   if (FUSED) {
     if ((f_top || f_bot) && it > 0) {  // the last tile of this cluster
@@ -554,6 +787,9 @@ static const Variant kVariants[] = {
     {"c32t256k16", 32, 256, 1, 1, 4, false, 16},  // 256-byte rows, K <= 16, 4 CTA/SM
     {"c16t256k16", 16, 256, 1, 1, 4, false, 16},  // 128-byte rows, K <= 16, 4 CTA/SM
     {"c32t256k16x3", 32, 256, 2, 3, 3, false, 16},  // K <= 16, half-tile slots, 3 CTA/SM
+    {"c64t256s1", 64, 256, 1, 1, 2, false},   // 512-byte row segments, 4 chunks per CTA
+    {"c64t512s1", 64, 512, 1, 1, 1, false},   // 512-byte row segments, 8 chunks per CTA
+    {"c64t512x3", 64, 512, 2, 3, 1, false},   // 512-byte rows, half-tile ring slots
 };
 static constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -584,9 +820,9 @@ static cudaError_t launch_one(const TileConfig& tc, const CUtensorMap& map, cons
   TileConsts<K> T;
   fill_consts<K>(tc, &T);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(LY == 2 ? tc.grid_deriv : LY == 3 ? tc.grid_fused : tc.grid, 1, 1);
+  cfg.gridDim = dim3(LY == 2 ? tc.grid_deriv : LY == 3 ? tc.grid_fused : LY == 4 ? tc.grid_vc : tc.grid, 1, 1);
   cfg.blockDim = dim3(NT, 1, 1);
-  cfg.dynamicSmemBytes = LY == 2 ? tc.smem_deriv : LY == 3 ? tc.smem_fused : tc.smem_bytes;
+  cfg.dynamicSmemBytes = LY == 2 ? tc.smem_deriv : LY == 3 ? tc.smem_fused : LY == 4 ? tc.smem_vc : tc.smem_bytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -618,11 +854,22 @@ static cudaError_t dispatch_k(const TileConfig& tc, const CUtensorMap& map, cons
   return cudaErrorInvalidValue;
 }
 
-// kind 0: solve; 2: fused stencil + solve; 3: solve with the fused reduced phase (nparts > 1)
+// kind 0: solve; 2: fused stencil + solve; 3: solve with the fused reduced phase (nparts > 1);
+// 4: virtual-partition chain (nparts == 1, vp > 1)
 static cudaError_t dispatch(const TileConfig& tc, int kind, const CUtensorMap& map,
                             const CUtensorMap& hmap, const CUtensorMap& xmap, const TileArgs& A,
                             cudaStream_t s, bool cfg_only, const void** fp = nullptr) {
 #define CTRI_V(C, NT, SB, S, M, LY) return dispatch_k<C, NT, SB, S, M, LY>(tc, map, hmap, xmap, A, s, cfg_only, fp)
+  if (kind == 4) {  // virtual-partition chain: strided whole-tile variants
+    switch (tc.variant) {
+      case 0: CTRI_V(16, 512, 1, 1, 1, 4);
+      case 4: CTRI_V(16, 256, 1, 1, 2, 4);
+      case 13: CTRI_V(32, 256, 1, 1, 2, 4);
+      case 17: CTRI_V(64, 256, 1, 1, 2, 4);
+      case 18: CTRI_V(64, 512, 1, 1, 1, 4);
+    }
+    return cudaErrorInvalidValue;
+  }
   if (kind == 3) {  // fused reduced phase: strided whole-tile variants
     switch (tc.variant) {
       case 0: CTRI_V(16, 512, 1, 1, 1, 3);
@@ -657,6 +904,9 @@ static cudaError_t dispatch(const TileConfig& tc, int kind, const CUtensorMap& m
     case 14: CTRI_V(32, 256, 1, 1, 4, 0);
     case 15: CTRI_V(16, 256, 1, 1, 4, 0);
     case 16: CTRI_V(32, 256, 2, 3, 3, 0);
+    case 17: CTRI_V(64, 256, 1, 1, 2, 0);
+    case 18: CTRI_V(64, 512, 1, 1, 1, 0);
+    case 19: CTRI_V(64, 512, 2, 3, 1, 0);
   }
 #undef CTRI_V
   return cudaErrorInvalidValue;
@@ -758,7 +1008,7 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
   const size_t ring = V.contig ? (size_t)V.C * cpc * (K + 2) : (size_t)(rows_cta / V.SUB) * V.C;
   const size_t tables = tc.pcr_uniform ? 0 : (2 * (size_t)tc.pcr.stages + 1) * Q;
   tc.smem_bytes = (int)(sizeof(double) * ((size_t)V.SLOTS * ring + 7 * (size_t)V.NT + tables) +
-                        8 * (V.SLOTS + 2));
+                        8 * (V.SLOTS + 4));  // mbarriers: ring slots, ex, rx, red[2]
   // configure one instantiation (solve, or the fused-stencil one): smem attribute + grid
   auto setup = [&](int kind, int smem, int* grid_out) -> bool {
     const void* fn = nullptr;
@@ -824,6 +1074,22 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
       tc.fused_ok = setup(3, tc.smem_fused, &tc.grid_fused);
       std::swap(w2, *why);
     }
+  }
+  // virtual-partition chain (nparts == 1, vp > 1): planes + x~ of two column groups and the
+  // window-row S, R tables; the window blocks lie in the end CTAs (G >= 2) and fit the
+  // finaliser's per-thread register budget (W + 1 <= 6 chunks per CTA)
+  tc.vc_ok = false;
+  if (!V.contig && V.SUB == 1 && (vi == 0 || vi == 4 || vi == 13 || vi == 17 || vi == 18) && P.p == 1 && P.vp > 1 &&
+      P.vp <= 8 && G >= 2 && P.window > 0 && P.gpcr.stages <= 4 && !(P.flags & CTRI_FLAG_FULL_BACKSUB) &&
+      (2 * P.window + 1) * (V.C / G) <= 3 * V.NT && P.window + 1 <= rows_cta && 2 * P.window + 1 < L.n &&
+      L.outer * ((L.inner + V.C - 1) / V.C) < ((int64_t)1 << 31)) {  // 32-bit group arithmetic
+    tc.smem_vc = tc.smem_bytes + 128 +
+                 (int)(sizeof(double) * ((2 * 8 + 2 * 8 + 2 * 9) * (size_t)V.C + 2 * (2 * (size_t)P.window + 1) +
+                                         72 + 6 * (size_t)V.NT));
+    std::string w2;
+    std::swap(w2, *why);
+    tc.vc_ok = setup(4, tc.smem_vc, &tc.grid_vc);
+    std::swap(w2, *why);
   }
   tc.ok = true;
   return true;
@@ -927,7 +1193,10 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
     static unsigned long long* d_tr = nullptr;
     if (!d_tr) cudaMalloc(&d_tr, 64 * 16 * sizeof(unsigned long long));
     A.trace = d_tr;
+    A.trace_cta = std::atoi(std::getenv("CTRI_TILE_TRACE"));  // which CTA stamps (0 if not a number)
   }
+  A.vc_dbg = 0;
+  if (const char* e = std::getenv("CTRI_VC_DBG")) A.vc_dbg = std::atoi(e);  // experiment knob
   A.pcr_alpha = tc.d_pcr;
   A.pcr_gamma = tc.d_pcr + (size_t)tc.pcr.stages * tc.Q;
   A.pcr_inv = tc.d_pcr + (size_t)2 * tc.pcr.stages * tc.Q;
@@ -940,6 +1209,23 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   A.halo_lo = (P.p == 1) ? P.send_hi : P.halo_lo;
   A.halo_hi = (P.p == 1) ? P.send_lo : P.halo_hi;
   const bool fused = !deriv && P.fused;
+  const bool vchain = !deriv && P.vchain;
+  if (vchain) {
+    A.vc_vp = P.vp;
+    A.vc_W = (int)P.window;
+    A.vc_q = P.gpcr.stages;
+    A.vc_cyclic = P.cyclic;
+    A.vc_groups = A.num_tiles / P.vp;
+    for (int i = 0; i < 32; ++i) A.vc_alpha[i] = A.vc_gamma[i] = 0.0;
+    for (int k = 0; k < P.gpcr.stages && k < 4; ++k)
+      for (int v = 0; v < P.vp; ++v) {
+        A.vc_alpha[k * 8 + v] = P.gpcr.alpha[(size_t)k * P.vp + v];
+        A.vc_gamma[k * 8 + v] = P.gpcr.gamma[(size_t)k * P.vp + v];
+      }
+    for (int v = 0; v < 8; ++v) A.vc_inv[v] = v < P.vp ? P.gpcr.inv[v] : 0.0;
+    A.f_S = P.d_S;
+    A.f_R = P.d_R;
+  }
   if (fused) {
     A.f_P = P.p;
     A.f_row = P.rank;
@@ -971,7 +1257,7 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
                       CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
   }
-  cudaError_t e = dispatch(tc, deriv ? 2 : (fused ? 3 : 0), map, hmap, xmap, A, s, false);
+  cudaError_t e = dispatch(tc, deriv ? 2 : (fused ? 3 : (vchain ? 4 : 0)), map, hmap, xmap, A, s, false);
   if (A.trace && e == cudaSuccess) {  // measurement only: print CTA 0's per-phase averages
     std::vector<unsigned long long> h(64 * 16);
     cudaMemcpyAsync(h.data(), A.trace, h.size() * 8, cudaMemcpyDeviceToHost, s);
