@@ -311,8 +311,9 @@ inline bool knob_no_pdl() { static const bool v = env_knob("CTRI_NO_PDL"); retur
 inline bool knob_p2p_trace() { static const bool v = env_knob("CTRI_P2P_TRACE"); return v; }
 inline bool knob_tile_trace() { static const bool v = env_knob("CTRI_TILE_TRACE"); return v; }
 inline bool knob_copy_only() { static const bool v = env_knob("CTRI_TILE_COPY_ONLY"); return v; }
-// CTRI_NO_VCHAIN: virtual partitions finish with k_reduced_local + k_window (A/B measurement)
-inline bool knob_no_vchain() { static const bool v = env_knob("CTRI_NO_VCHAIN"); return v; }
+// CTRI_NO_VCHAIN: virtual partitions finish with k_reduced_local + k_window (A/B measurement;
+// read at plan creation, not on the solve path)
+inline bool knob_no_vchain() { return env_knob("CTRI_NO_VCHAIN"); }
 
 // kernels.cu launchers (return cudaError_t of the launch)
 cudaError_t launch_local_generic(const Plan& P, const double* b, double* x, cudaStream_t s);
