@@ -20,13 +20,22 @@ SYM = (1 / 3, 1.0, 1 / 3)
 NONSYM = (0.2, 1.1, 0.4)
 
 
-def check(b, sd, p=1, bands=SYM, cyclic=True, flags=0, inplace=False, tol=TOL_REL):
+def tolerances(bands):
+    """(relative error, residual) bars (DESIGN reading R22): the north-star 1e-12 / 1e-13, except
+    for the near-singular alpha = 0.499 (kappa_inf(A) = 999) where the oracle's own residual is
+    3.3e-14: 10x the largest values measured on B200 (2.1e-14 / 5.0e-14,
+    profiles/r2_tolerance_near_singular.log)."""
+    return (TOL_REL, TOL_RES) if bands[0] < 0.49 else (2e-13, 5e-13)
+
+
+def check(b, sd, p=1, bands=SYM, cyclic=True, flags=0, inplace=False, tol=None):
     x, st = gpu_solve(b, sd, p, bands, cyclic, flags, inplace, return_stats=True)
     ref = oracle.cyclic_solve(b, sd, bands) if cyclic else oracle.acyclic_solve(b, sd, bands)
     err = rel_err(x, ref, sd)
     res = residual(x, b, sd, bands, cyclic)
-    assert err <= tol, (err, st)
-    assert res <= max(TOL_RES, tol / 10), (res, st)
+    tol_rel, tol_res = tolerances(bands)
+    assert err <= (tol if tol is not None else tol_rel), (err, st)
+    assert res <= tol_res, (res, st)
     return x, st
 
 
@@ -65,8 +74,7 @@ def test_shapes_single_gpu(shape, sd, kernel):
 @pytest.mark.parametrize("cyclic", [True, False])
 def test_bands_single_gpu(bands, cyclic):
     b = workloads.uniform((512, 4, 32), 6)
-    tol = 1e-12 if bands[0] < 0.49 else 1e-11  # cond(A) ~ 1000 at alpha = 0.499 (oracle's error)
-    check(b, 0, 1, bands, cyclic, tol=tol)
+    check(b, 0, 1, bands, cyclic)
 
 
 @pytest.mark.parametrize("p", [2, 4, 8])
@@ -78,9 +86,8 @@ def test_loopback_partitions(p, shape, bands, path):
     both the fused device-initiated reduced kernel and the host-issued exchange rounds."""
     from paper_2101_02286_b200 import CTRI_FLAG_NCCL_ROUNDS
     b = workloads.uniform(shape, 6)
-    tol = 1e-12 if bands[0] < 0.49 else 1e-11
     flags = CTRI_FLAG_NCCL_ROUNDS if path == "rounds" else 0
-    x, st = check(b, 0, p, bands, flags=flags, tol=tol)
+    x, st = check(b, 0, p, bands, flags=flags)
     assert st["reduced_path"] == (1 if path == "p2p" else 0)
     assert st["device_error"] == 0
     assert st["pcr_stages"] == int(math.log2(p))
@@ -94,8 +101,7 @@ def test_loopback_cyclic_detach_reattach(p, bands):
     """Cyclic non-power-of-two partitions: detach / PCR / reattach (counts P:346)."""
     shape = (p * 16, 4, 16) if bands[0] > 0.4 else (p * 64, 4, 16)
     b = workloads.uniform(shape, 6)
-    tol = 1e-12 if bands[0] < 0.49 else 1e-11
-    x, st = check(b, 0, p, bands, tol=tol)
+    x, st = check(b, 0, p, bands)
     q = int(math.floor(math.log2(p)))
     assert st["reduced_path"] == 1 and st["device_error"] == 0
     assert st["pcr_stages"] == q
@@ -156,8 +162,7 @@ def test_virtual_partitions(vp, bands, cyclic, monkeypatch):
     """nparts == 1 solved as vp partitions of one slab (local reduced system + window back-sub)."""
     monkeypatch.setenv("CTRI_VPARTS", str(vp))
     b = workloads.uniform((4096, 2, 32), 6)
-    tol = 1e-12 if bands[0] < 0.49 else 1e-11
-    x, st = check(b, 0, 1, bands, cyclic, tol=tol)
+    x, st = check(b, 0, 1, bands, cyclic)
     assert st["vparts"] == vp
 
 
