@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define CTRI_ABI_VERSION 5
+#define CTRI_ABI_VERSION 6
 
 typedef struct ctri_plan_s* ctri_plan;
 typedef struct CUstream_st* ctri_stream; /* == cudaStream_t */
@@ -125,6 +125,12 @@ typedef struct ctri_stats {
   int32_t p2p_steps;            /* schedule steps timed in t_p2p_step_us */
   uint32_t p2p_epoch;           /* device epoch of the reduced-phase mailboxes (slice 0): one per
                                    solve, so its parity alternates the double-buffered copies */
+  int32_t reduced_rows;         /* rows of the reduced system this solve exchanges across ranks:
+                                   nparts (one per rank; with vparts > 1 the virtual partitions
+                                   are chained inside the tile kernel) or nparts * vparts ("virtual
+                                   rows", each its own row of the distributed PCR) */
+  int32_t vchain;               /* 1: the virtual partitions' reduced system and window rows are
+                                   finished inside the tile kernel (the virtual-partition chain) */
   uint32_t halo_epoch;          /* device epoch of the derivative halo exchange (slice 0): one per
                                    ctri_deriv / ctri_compact_apply, independent of p2p_epoch */
 } ctri_stats;

@@ -86,7 +86,8 @@ ctri_status check_poisoned(const std::vector<Plan*>& G) {
 
 void free_plan(Plan* P) {
   if (!P) return;
-  double* bufs[] = {P->d_cp,    P->d_inv_den, P->d_S,      P->d_R,       P->yf,      P->yl,
+  double* bufs[] = {P->d_cp,    P->d_inv_den, P->d_S,      P->d_R,       P->d_vS,    P->d_vR,
+                    P->yf,      P->yl,
                     P->bt,      P->yl_prev,   P->bh,       P->recv_m,    P->recv_p,  P->xt,
                     P->xt_next, P->halo_lo,   P->halo_hi,  P->send_lo,   P->send_hi, P->tile.d_pcr,
                     P->d_stage_b, P->d_stage_x, P->d_plu,    P->d_pSR,     P->d_ainv,  P->d_planes4,
@@ -187,13 +188,31 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   P->tlay.outer = P->lay.outer * P->vp;
   P->tlay.n = n / P->vp;
   const int64_t nv = P->tlay.n;
-  const int pr = p * P->vp;  // rows of the reduced system (virtual partitions included)
 
   // ---- pre-factorisation ----
   FactorError fe;
-  if (!partition_factor(nv - 1, P->bands, &P->part, &fe)) return fail((ctri_status)fe.code, fe.detail);
+  // the (virtual) partition the local kernels solve: nv - 1 interior rows
+  if (!partition_factor(nv - 1, P->bands, &P->vpart, &fe)) return fail((ctri_status)fe.code, fe.detail);
+  P->vwindow = backsub_window(P->vpart);
+  P->window = P->vwindow;  // tile_configure's checks (the fused layout needs vp == 1: same level)
+  std::string why;
+  const bool tile_ok = tile_configure(*P, &why);
+  // virtual partitions finish (a2)-(a4) inside the tile kernel when its configuration allows
+  // (the virtual-partition chain).  With nparts > 1 that makes two levels: the chain computes
+  // D_i^{-1} b_i of the whole slab (its internal interfaces solved on chip), and the reduced
+  // system across the GPUs keeps the paper's one row per rank.
+  P->vchain = tile_ok && !P->tile.contig && P->vp > 1 && P->tile.vc_ok && !knob_no_vchain() &&
+              !knob_copy_only();
+  P->rvp = (p > 1 && P->vchain) ? 1 : P->vp;
+  const int64_t rn = n / P->rvp;  // rows per reduced-system row's partition
+  const int pr = p * P->rvp;      // rows of the reduced system (virtual rows included)
+  if (P->rvp == P->vp) {
+    P->part = P->vpart;
+  } else if (!partition_factor(rn - 1, P->bands, &P->part, &fe)) {
+    return fail((ctri_status)fe.code, fe.detail);
+  }
   const Partition& pt = P->part;
-  const int64_t last = nv - 2;
+  const int64_t last = rn - 2;
   std::vector<double> L(pr), D(pr), U(pr);
   for (int i = 0; i < pr; ++i) {
     const bool lft = cyclic || i > 0, rgt = cyclic || i < pr - 1;
@@ -218,13 +237,32 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   if (P->gpcr.stages > CTRI_MAX_STAGES) return fail(CTRI_ERR_UNSUPPORTED, "too many PCR stages");
   P->inv_closure = P->gpcr.inv[0];
   P->window = backsub_window(pt);
+  // two levels: the slab's internal interfaces 1..vp-1 as an acyclic vp-row system whose row 0
+  // (the GPU interface, not part of D_i) is decoupled: L^ = D^ - 1 = U^ = 0 there, no coupling
+  // of row 1 to it nor of row vp-1 past the slab (Eqs. Li_hat..Ui_hat at the virtual level)
+  if (p > 1 && P->vchain) {
+    const Partition& vt = P->vpart;
+    const int64_t vl = nv - 2;
+    const int vp = P->vp;
+    std::vector<double> Lv(vp), Dv(vp), Uv(vp);
+    for (int v = 0; v < vp; ++v) {
+      Lv[v] = v >= 2 ? -P->bands.l * vt.S[vl] : 0.0;
+      Dv[v] = v == 0 ? 1.0 : P->bands.d - P->bands.l * vt.R[vl] - P->bands.u * vt.S[0];
+      Uv[v] = (v >= 1 && v <= vp - 2) ? -P->bands.u * vt.R[0] : 0.0;
+    }
+    if (!pcr_factor(vp, false, Lv, Dv, Uv, pivot_threshold(P->bands), &P->vpcr, &fe))
+      return fail((ctri_status)fe.code, fe.detail);
+  }
 
   // ---- device tables ----
   TRY(upload(&P->d_S, pt.S, s));
   TRY(upload(&P->d_R, pt.R, s));
+  if (P->rvp != P->vp) {  // the chain's own (virtual-level) S, R
+    TRY(upload(&P->d_vS, P->vpart.S, s));
+    TRY(upload(&P->d_vR, P->vpart.R, s));
+  }
   const int64_t m = P->lay.m();
-  std::string why;
-  if (tile_configure(*P, &why)) {
+  if (tile_ok) {
     P->local_kernel = P->tile.contig ? 2 : 1;
     std::vector<double> t;
     t.insert(t.end(), P->tile.pcr.alpha.begin(), P->tile.pcr.alpha.end());
@@ -233,13 +271,13 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
     TRY(upload(&P->tile.d_pcr, t, s));
   } else {
     P->local_kernel = 0;
-    TRY(upload(&P->d_cp, pt.th.cp, s));
-    TRY(upload(&P->d_inv_den, pt.th.inv_den, s));
+    TRY(upload(&P->d_cp, P->vpart.th.cp, s));
+    TRY(upload(&P->d_inv_den, P->vpart.th.inv_den, s));
   }
   if (p > 1 || P->vp > 1) {
     double** planes[] = {&P->yf, &P->yl, &P->bt, &P->yl_prev, &P->bh, &P->recv_m, &P->recv_p,
                          &P->xt, &P->xt_next};
-    for (double** pl : planes) TRY(alloc_plane(pl, m * P->vp));
+    for (double** pl : planes) TRY(alloc_plane(pl, m * P->rvp));
   }
   if (flags & CTRI_FLAG_ALLGATHER) {
     if (p < 2 || p > kMaxAG || (flags & CTRI_FLAG_NCCL_ROUNDS))
@@ -253,9 +291,6 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   P->fused = (flags & CTRI_FLAG_FUSED_REDUCED) && p > 1 && p <= 8 && !P->loopback &&
              P->local_kernel == 1 && P->tile.fused_ok &&
              !(flags & (CTRI_FLAG_NCCL_ROUNDS | CTRI_FLAG_FULL_BACKSUB | CTRI_FLAG_ALLGATHER));
-  // nparts == 1 with virtual partitions: (a2)-(a4) inside the tile kernel when it is configured
-  P->vchain = p == 1 && P->vp > 1 && P->local_kernel == 1 && P->tile.vc_ok && !knob_no_vchain() &&
-              !knob_copy_only();
   if (P->fused) {
     std::vector<double> inv;
     if (!reduced_inverse(p, cyclic != 0, L, D, U, pivot_threshold(P->bands), &inv, &fe))
@@ -273,18 +308,18 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
     // device-initiated reduced phase: double-buffered mailbox + epoch flags
     const int q = (int)P->sched.steps.size();
     // one mailbox (two epoch copies) per virtual row of this rank
-    P->p2p_nslices = p2p_slices(m, (P->loopback ? p : 1) * P->vp, P->num_sms, P->allgather ? 1 : 0);
+    P->p2p_nslices = p2p_slices(m, (P->loopback ? p : 1) * P->rvp, P->num_sms, P->allgather ? 1 : 0);
     P->p2p_vrow_words = 2 * p2p_copy_words(m, q, pr, P->allgather);
     P->mbox_bytes = sizeof(unsigned long long) *
-                    ((size_t)P->p2p_off + (size_t)P->vp * P->p2p_vrow_words +
+                    ((size_t)P->p2p_off + (size_t)P->rvp * P->p2p_vrow_words +
                      ((flags & CTRI_FLAG_DERIV) ? p2p_mailbox_words(0, m, true) : 0));
     CUDA_TRY(cudaMalloc(&P->mbox_alloc, P->mbox_bytes));
     CUDA_TRY(cudaMemsetAsync(P->mbox_alloc, 0, P->mbox_bytes, s));
     TRY(alloc_err(P));
-    CUDA_TRY(cudaMalloc(&P->d_epoch, sizeof(unsigned int) * P->p2p_nslices * P->vp));
-    CUDA_TRY(cudaMemsetAsync(P->d_epoch, 0, sizeof(unsigned int) * P->p2p_nslices * P->vp, s));
+    CUDA_TRY(cudaMalloc(&P->d_epoch, sizeof(unsigned int) * P->p2p_nslices * P->rvp));
+    CUDA_TRY(cudaMemsetAsync(P->d_epoch, 0, sizeof(unsigned int) * P->p2p_nslices * P->rvp, s));
     if (flags & CTRI_FLAG_DERIV) {  // the halo exchange: its own mailbox region and epochs
-      P->halo_off = P->p2p_off + (int64_t)P->vp * P->p2p_vrow_words;
+      P->halo_off = P->p2p_off + (int64_t)P->rvp * P->p2p_vrow_words;
       CUDA_TRY(cudaMalloc(&P->d_hepoch, sizeof(unsigned int) * P->p2p_nslices));
       CUDA_TRY(cudaMemsetAsync(P->d_hepoch, 0, sizeof(unsigned int) * P->p2p_nslices, s));
     }
@@ -457,7 +492,7 @@ ctri_status p2p_connect_ipc(Plan* P, cudaStream_t s) {
 
 void p2p_args(const Plan& P0, P2PArgs* A) {
   std::memset(A, 0, sizeof(*A));
-  A->p = P0.p * P0.vp;  // reduced rows: nparts x virtual partitions
+  A->p = P0.p * P0.rvp;  // reduced rows: nparts x virtual rows
   A->q = (int)P0.sched.steps.size();
   A->allgather = P0.allgather ? 1 : 0;
   A->pdl = (!P0.loopback && !knob_no_pdl()) ? 1 : 0;
@@ -470,7 +505,7 @@ void p2p_args(const Plan& P0, P2PArgs* A) {
   A->nslices = P0.p2p_nslices;
   A->m = P0.lay.m();
   A->slice_cols = (A->m + A->nslices - 1) / A->nslices;
-  A->full = ((P0.flags & CTRI_FLAG_FULL_BACKSUB) || (2 * P0.window >= P0.lay.n - 1)) ? 1 : 0;
+  A->full = ((P0.flags & CTRI_FLAG_FULL_BACKSUB) || (2 * P0.window >= P0.lay.n / P0.rvp - 1)) ? 1 : 0;
   A->W = P0.window;
   A->lay = P0.lay;
   A->l = P0.bands.l;
@@ -486,11 +521,11 @@ void p2p_args(const Plan& P0, P2PArgs* A) {
 // rank * vp + v, its slab at row v * n_v (outer == 1 whenever vp > 1 with nparts > 1), its
 // plane segment, mailbox and epochs.
 void p2p_fill_rank(const Plan& P, double* x, P2PRank* R, int v = 0) {
-  const int vp = P.vp, pr = P.p * vp;
+  const int vp = P.rvp, pr = P.p * vp;
   const int64_t m = P.lay.m();
   const int g = P.rank * vp + v;
   R->rank = g;
-  R->x = x ? x + (int64_t)v * P.tlay.n * P.lay.inner : nullptr;
+  R->x = x ? x + (int64_t)v * (P.lay.n / vp) * P.lay.inner : nullptr;
   R->yf = P.yf + (int64_t)v * m;
   R->yl = P.yl + (int64_t)v * m;
   R->bt = P.bt + (int64_t)v * m;
@@ -561,7 +596,7 @@ void schedule_counts(const Plan& P, int* sends, int* rounds) {
   }
   // messages leaving this GPU (its vp virtual rows to rows of other ranks), dependent rounds
   const Schedule& sc = P.sched;
-  const int vp = P.vp, pr = P.p * vp;
+  const int vp = P.rvp, pr = P.p * vp;
   auto owner = [&](int row) { return row / vp; };
   int sd = 0, rd = 2;
   for (int v = 0; v < vp; ++v) {
@@ -744,7 +779,7 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
   if (P0.p2p) {  // fused device-initiated (a2)-(a4)
     P2PArgs A;
     p2p_args(P0, &A);
-    const int nrows = (int)G.size() * P0.vp;  // rows launched together (ranks x virtual rows)
+    const int nrows = (int)G.size() * P0.rvp;  // rows launched together (ranks x virtual rows)
     const int grid = A.nslices * nrows;
     const bool env_trace = knob_p2p_trace();
     if ((env_trace || !P0.ev.empty()) && !P0.d_trace) {  // per-round stamps (CTRI_FLAG_TIMING)
@@ -754,7 +789,7 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
     }
     A.trace = P0.d_trace;
     for (size_t r = 0; r < G.size(); ++r)
-      for (int v = 0; v < P0.vp; ++v) p2p_fill_rank(*G[r], x[r], &A.rk[r * P0.vp + v], v);
+      for (int v = 0; v < P0.rvp; ++v) p2p_fill_rank(*G[r], x[r], &A.rk[r * P0.rvp + v], v);
     // CTAs of different reduced rows on this GPU wait on each other (loopback ranks, virtual
     // rows): one cooperative grid guarantees they are co-resident even when other work shares
     // the GPU.  A single row per GPU waits only on peers and is launched with PDL instead.
@@ -762,7 +797,7 @@ ctri_status solve_group(std::vector<Plan*>& G, const double* const* b, double* c
     if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("p2p reduced kernel: ") + cudaGetErrorString(e));
     record(P0, EV_XX, s);
     for (size_t r = 0; r < G.size(); ++r) {  // (a4) window pass of every rank (all its slabs)
-      e = launch_window(*G[r], x[r], G[r]->xt_next + (int64_t)(G[r]->vp - 1) * G[r]->lay.m(), s);
+      e = launch_window(*G[r], x[r], G[r]->xt_next + (int64_t)(G[r]->rvp - 1) * G[r]->lay.m(), s);
       if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("window: ") + cudaGetErrorString(e));
     }
     if (P0.d_trace && env_trace) {  // measurement only: per-phase spread across CTAs on stderr
@@ -1290,7 +1325,9 @@ ctri_status ctri_get_stats(ctri_plan plan, ctri_stats* out) {
   out->tile_columns = P->local_kernel ? P->tile.C : 1;
   out->tile_variant = P->local_kernel ? P->tile.variant : -1;
   out->tile_stages = P->local_kernel ? P->tile.STAGES : 0;
-  out->reduced_path = (P->fused || P->vchain) ? 3 : (P->p > 1 && P->p2p) ? ((P->allgather || (P->r == 2 && !P->ppcr)) ? 2 : 1) : 0;
+  out->reduced_rows = P->p * P->rvp;
+  out->vchain = P->vchain ? 1 : 0;
+  out->reduced_path = (P->fused || (P->p == 1 && P->vchain)) ? 3 : (P->p > 1 && P->p2p) ? ((P->allgather || (P->r == 2 && !P->ppcr)) ? 2 : 1) : 0;
   out->band_halfwidth = P->r;
   out->vparts = P->vp;
   out->grid_ctas = P->local_kernel ? P->tile.grid : (int32_t)((P->tlay.m() + 127) / 128);

@@ -81,6 +81,7 @@ struct TileArgs {
   int G;            // cluster size
   int rows_per_cta; // n / G
   int stages;       // log2 Q
+  int vc_slab;      // VC with nparts > 1 (two levels): slab row 0 is the GPU interface
   int mode;         // 0: complete cyclic solve (p = 1); 1: y_D = D_i^{-1} b_i + planes (p >= 2);
                     // 2: complete acyclic solve (p = 1)
   int rows_box;     // TMA box rows (<= 256)
@@ -212,12 +213,17 @@ struct Plan {
   int vp = 1;           // virtual partitions of the slab solved as separate partitions on this
                         // GPU (nparts == 1 only; the paper's method with more partitions than GPUs)
   Layout tlay;          // layout the local-solve kernels see: (outer*vp, n/vp, inner)
+  int rvp = 1;          // rows per rank of the reduced system: vp ("virtual rows"), or 1 when the
+                        // virtual partitions are chained inside the tile kernel (two levels)
   int device = 0;
   int num_sms = 0;
   bool loopback = false;
 
   // host tables
-  Partition part;       // GPU-level S_i, R_i, L^, D^, U^ (p >= 2); (n-1)-row interior
+  Partition part;       // S_i, R_i, L^, D^, U^ of the reduced system's partitions (n/rvp rows)
+  Partition vpart;      // the same for the local kernels' (virtual) partitions (n/vp rows)
+  int64_t vwindow = 0;  // window rows per end at the virtual level
+  PcrTables vpcr;       // two levels: acyclic vp-row system of the slab's internal interfaces
   PcrTables gpcr;       // GPU-level PCR over the p reduced rows (power-of-two or acyclic)
   Schedule sched;       // reduced-system step schedule (PCR / detach / fold / reattach)
   int64_t window = 0;   // rows per end for (a4)
@@ -226,8 +232,10 @@ struct Plan {
   // device tables
   double* d_cp = nullptr;       // generic local solve Thomas factors (n-1)
   double* d_inv_den = nullptr;
-  double* d_S = nullptr;        // GPU-level S_i, R_i (n-1)
+  double* d_S = nullptr;        // S_i, R_i of the reduced system's partitions (n/rvp - 1)
   double* d_R = nullptr;
+  double* d_vS = nullptr;       // two levels: S, R of the virtual partitions (n/vp - 1)
+  double* d_vR = nullptr;
 
   // planes (m doubles each)
   double *yf = nullptr, *yl = nullptr, *bt = nullptr, *yl_prev = nullptr, *bh = nullptr,

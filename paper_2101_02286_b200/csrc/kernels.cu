@@ -204,12 +204,12 @@ cudaError_t launch_window(const Plan& P, double* x, const double* next, cudaStre
   A.R = P.d_R;
   A.next = next;
   A.outer = P.lay.outer;
-  A.nv = P.tlay.n;
+  A.nv = P.lay.n / P.rvp;  // the reduced system's partitions (virtual rows, or whole slabs)
   A.inner = P.lay.inner;
   A.W = P.window;
-  A.full = ((P.flags & CTRI_FLAG_FULL_BACKSUB) || (2 * P.window >= P.tlay.n - 1)) ? 1 : 0;
+  A.full = ((P.flags & CTRI_FLAG_FULL_BACKSUB) || (2 * P.window >= A.nv - 1)) ? 1 : 0;
   A.rows = A.full ? A.nv - 1 : 2 * A.W;
-  A.vp = P.vp;
+  A.vp = P.rvp;
   A.wrap = (P.p == 1 && P.cyclic) ? 1 : 0;
   A.pdl = 0;
   if (A.rows <= 0) return cudaSuccess;

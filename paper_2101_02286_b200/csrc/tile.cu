@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(NT, MINB)
     const bool act = jl < cpo;
     const int vl = v == 0 ? vcp - 1 : v - 1;
     double bh = 0.0;
-    if (act) {
+    if (act && !(A.vc_slab && v == 0)) {  // two levels: row 0 (the GPU interface) is decoupled
       const double ylp = (v > 0 || A.vc_cyclic) ? vc_yl[(par * 8 + vl) * cpo + jl] : 0.0;
       bh = vc_c[(par * 8 + v) * cpo + jl] - T.l * ylp;
     }
@@ -437,6 +437,9 @@ __global__ void __launch_bounds__(NT, MINB)
     dev::cp_async_commit();
   };
   // Eq. xi_app on the loaded window rows (row 0 of the partition := x~_q), stored once
+  // (two levels: slab row 0 keeps its role as the GPU interface -- not written here -- and the
+  // finalised rows 1 and n-1 of the slab, y_D[first] and y_D[last], go to the planes of the
+  // reduced system across the GPUs)
   auto vc_store = [&](double* blk, int gp, int q, int bf) {
     if (!blk) return;
     const double* bb = vc_buf + bf * kVcFin * NT;
@@ -447,6 +450,12 @@ __global__ void __launch_bounds__(NT, MINB)
       const int ri = vc_r0 + i * vc_rs;
       if (ri >= vc_R2) break;
       const double xv = ri == 0 ? xa : bb[i * NT + tid] - vc_sr[ri] * xa - vc_sr[vc_R2 + ri] * xb;
+      if (A.vc_slab) {
+        if (q == 0 && ri == 0) continue;
+        const int64_t pj = (int64_t)vc_og(gp) * A.lay.inner + (int64_t)vc_ct(gp) * C + (int64_t)g * cpo + vc_jl;
+        if (q == 0 && ri == 1) A.plane_yf[pj] = xv;
+        if (q == vcp - 1 && ri == vc_R2 - 1) A.plane_yl[pj] = xv;
+      }
       dev::st_global_cs(blk + (int64_t)vc_row(ri) * A.lay.inner, xv);
     }
   };
@@ -690,9 +699,11 @@ __global__ void __launch_bounds__(NT, MINB)
                // y_v[last] (chunk Q-1)
       const int par = (int)(vc_gi & 1);
       const int e = (par * 8 + vc_q) * cpo + (j % cpo);
-      if (c == 0)  // c_v = b~_v - u y_v[first]
+      if (c == 0) {  // c_v = b~_v - u y_v[first]
         dev::st_async_f64(dev::mapa(dev::smem_u32(vc_c + e), owner), btv - T.u * v[1],
                           dev::mapa(dev::smem_u32(mbar_red + par), owner));
+        if (A.vc_slab && vc_q == 0 && valid) A.plane_bt[(int64_t)vog * A.lay.inner + col] = btv;  // b~_i
+      }
       if (c == Q - 1)
         dev::st_async_f64(dev::mapa(dev::smem_u32(vc_yl + e), owner), v[K - 1],
                           dev::mapa(dev::smem_u32(mbar_red + par), owner));
@@ -709,7 +720,7 @@ __global__ void __launch_bounds__(NT, MINB)
       }
       if (c == Q - 1)
         for (int r = 0; r < A.f_P; ++r) dev::ll_store(A.f_peer[r] + f_word(1, A.f_row, jo), v[K - 1], f_ep);
-    } else if (valid) {
+    } else if (valid && !VC) {
       if (A.mode == 1) {
         const int64_t pj = o * A.lay.inner + col;
         if (c == 0) {
@@ -1079,12 +1090,13 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
   // window-row S, R tables; the window blocks lie in the end CTAs (G >= 2) and fit the
   // finaliser's per-thread register budget (W + 1 <= 6 chunks per CTA)
   tc.vc_ok = false;
-  if (!V.contig && V.SUB == 1 && (vi == 0 || vi == 4 || vi == 13 || vi == 17 || vi == 18) && P.p == 1 && P.vp > 1 &&
-      P.vp <= 8 && G >= 2 && P.window > 0 && P.gpcr.stages <= 4 && !(P.flags & CTRI_FLAG_FULL_BACKSUB) &&
-      (2 * P.window + 1) * (V.C / G) <= 3 * V.NT && P.window + 1 <= rows_cta && 2 * P.window + 1 < L.n &&
+  if (!V.contig && V.SUB == 1 && (vi == 0 || vi == 4 || vi == 13 || vi == 17 || vi == 18) && P.vp > 1 &&
+      P.vp <= 8 && G >= 2 && P.vwindow > 0 && !(P.flags & CTRI_FLAG_FULL_BACKSUB) &&
+      !(P.flags & (CTRI_FLAG_NCCL_ROUNDS | CTRI_FLAG_ALLGATHER | CTRI_FLAG_FUSED_REDUCED)) &&
+      (2 * P.vwindow + 1) * (V.C / G) <= 3 * V.NT && P.vwindow + 1 <= rows_cta && 2 * P.vwindow + 1 < L.n &&
       L.outer * ((L.inner + V.C - 1) / V.C) < ((int64_t)1 << 31)) {  // 32-bit group arithmetic
     tc.smem_vc = tc.smem_bytes + 128 +
-                 (int)(sizeof(double) * ((2 * 8 + 2 * 8 + 2 * 9) * (size_t)V.C + 2 * (2 * (size_t)P.window + 1) +
+                 (int)(sizeof(double) * ((2 * 8 + 2 * 8 + 2 * 9) * (size_t)V.C + 2 * (2 * (size_t)P.vwindow + 1) +
                                          72 + 6 * (size_t)V.NT));
     std::string w2;
     std::swap(w2, *why);
@@ -1210,21 +1222,28 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   A.halo_hi = (P.p == 1) ? P.send_lo : P.halo_hi;
   const bool fused = !deriv && P.fused;
   const bool vchain = !deriv && P.vchain;
+  A.vc_slab = 0;
   if (vchain) {
+    // nparts == 1: the vp-row system is the whole (cyclic or acyclic) reduced system (gpcr);
+    // nparts > 1: the slab's internal interfaces, acyclic with the GPU interface decoupled
+    // (vpcr), and the slab-level planes for the reduced system across GPUs
+    const bool two = P.p > 1;
+    const PcrTables& t = two ? P.vpcr : P.gpcr;
+    A.vc_slab = two ? 1 : 0;
     A.vc_vp = P.vp;
-    A.vc_W = (int)P.window;
-    A.vc_q = P.gpcr.stages;
-    A.vc_cyclic = P.cyclic;
+    A.vc_W = (int)P.vwindow;
+    A.vc_q = t.stages;
+    A.vc_cyclic = two ? 0 : P.cyclic;
     A.vc_groups = A.num_tiles / P.vp;
     for (int i = 0; i < 32; ++i) A.vc_alpha[i] = A.vc_gamma[i] = 0.0;
-    for (int k = 0; k < P.gpcr.stages && k < 4; ++k)
+    for (int k = 0; k < t.stages && k < 4; ++k)
       for (int v = 0; v < P.vp; ++v) {
-        A.vc_alpha[k * 8 + v] = P.gpcr.alpha[(size_t)k * P.vp + v];
-        A.vc_gamma[k * 8 + v] = P.gpcr.gamma[(size_t)k * P.vp + v];
+        A.vc_alpha[k * 8 + v] = t.alpha[(size_t)k * P.vp + v];
+        A.vc_gamma[k * 8 + v] = t.gamma[(size_t)k * P.vp + v];
       }
-    for (int v = 0; v < 8; ++v) A.vc_inv[v] = v < P.vp ? P.gpcr.inv[v] : 0.0;
-    A.f_S = P.d_S;
-    A.f_R = P.d_R;
+    for (int v = 0; v < 8; ++v) A.vc_inv[v] = v < P.vp ? t.inv[v] : 0.0;
+    A.f_S = two ? P.d_vS : P.d_S;
+    A.f_R = two ? P.d_vR : P.d_R;
   }
   if (fused) {
     A.f_P = P.p;

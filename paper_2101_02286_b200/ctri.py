@@ -26,7 +26,7 @@ CTRI_FLAG_NCCL_ROUNDS = 1 << 4
 CTRI_FLAG_ALLGATHER = 1 << 5
 CTRI_FLAG_FUSED_REDUCED = 1 << 6
 CTRI_MAX_STAGES = 16
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 STATUS = {0: "CTRI_OK", 1: "CTRI_ERR_INVALID_ARG", 2: "CTRI_ERR_UNSUPPORTED", 3: "CTRI_ERR_SINGULAR",
           4: "CTRI_ERR_PARTITION_TOO_SMALL", 5: "CTRI_ERR_CUDA", 6: "CTRI_ERR_NCCL",
@@ -74,7 +74,8 @@ class ctri_stats(ctypes.Structure):
                 ("t_reduced_kernel_us", ctypes.c_float), ("t_window_us", ctypes.c_float),
                 ("t_p2p_y_us", ctypes.c_float), ("t_p2p_step_us", ctypes.c_float * CTRI_MAX_STAGES),
                 ("t_p2p_x_us", ctypes.c_float), ("p2p_steps", ctypes.c_int32),
-                ("p2p_epoch", ctypes.c_uint32), ("halo_epoch", ctypes.c_uint32)]
+                ("p2p_epoch", ctypes.c_uint32), ("reduced_rows", ctypes.c_int32),
+                ("vchain", ctypes.c_int32), ("halo_epoch", ctypes.c_uint32)]
 
     def as_dict(self):
         d = {}

@@ -109,3 +109,45 @@ def test_vchain_repeated_solves(monkeypatch):
             assert rel_err(xt.cpu().numpy(), refs[k % 2], 0) < TOL_REL
     assert plan.stats()["reduced_path"] == 3
     plan.close()
+
+
+@pytest.mark.parametrize("p,n,cyclic", [(2, 4096, True), (4, 2048, True), (3, 2048, True), (2, 4096, False),
+                                        (2, 8192, True)])
+@pytest.mark.parametrize("bands", [SYM, NONSYM])
+def test_two_level_chain_loopback(p, n, cyclic, bands):
+    """nparts > 1 with virtual partitions chained in the tile kernel (two levels): each rank's
+    slab is solved as vp partitions whose internal interfaces are eliminated on chip
+    (D_i^{-1} b_i of the whole slab), and the reduced system across the ranks has one row per
+    rank (p = 3: detach / reattach).  Loopback on one GPU, every element vs the oracle."""
+    from helpers import gpu_solve
+    b = workloads.uniform((p * n, 1, 64), 40 + p)
+    x, st = gpu_solve(b, 0, p, bands, cyclic, return_stats=True)
+    vp = min(8, n // 1024)
+    assert st["vparts"] == vp and st["vchain"] == 1 and st["reduced_rows"] == p, st
+    assert st["reduced_path"] == 1 and st["device_error"] == 0
+    ref = oracle.cyclic_solve(b, 0, bands) if cyclic else oracle.acyclic_solve(b, 0, bands)
+    assert rel_err(x, ref, 0) < TOL_REL
+    assert residual(x, b, 0, bands, cyclic) < TOL_RES
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_two_level_chain_cfg2_full_size(p):
+    """The BASELINE grid split into p loopback partitions of 4096 / 2048 rows (vp = 4 / 2
+    chained on chip, p reduced rows): every one of the 65,536 columns vs the oracle."""
+    import torch
+
+    from paper_2101_02286_b200 import ctri
+    from test_gpu_parity import _full_columns
+    dims = (8192, 256, 256)
+    b = workloads.device_uniform(dims, 2, torch.device("cuda:0"))
+    n = dims[0] // p
+    bs = [b[r * n:(r + 1) * n].contiguous() for r in range(p)]
+    xs = [torch.empty_like(t) for t in bs]
+    g = ctri.LoopbackGroup(dims, 0, p)
+    g.solve(bs, xs)
+    torch.cuda.synchronize()
+    st = g.stats(0)
+    g.close()
+    assert st["vchain"] == 1 and st["reduced_rows"] == p and st["device_error"] == 0
+    err, m = _full_columns(b, torch.cat(xs, 0), 0)
+    assert m == 65536 and err < TOL_REL, err
