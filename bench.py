@@ -461,6 +461,8 @@ def main():
                                                             if (p == 1 and st["reduced_path"] == 3) else "")
                            if st["local_kernel"] in (1, 2) else
                            "k_penta_local (column-serial, 32 B/pt moved)" if st["local_kernel"] == 3
+                           else "k_ptile (pentadiagonal on chip: register leaf + 2x2-block PCR, clusters)"
+                           if st["local_kernel"] == 4
                            else "k_local_generic"),
                 "algorithmic_bytes_per_launch": bytes_local, "launch_us": t_local,
                 "launch_us_isolated": t_local_iso,

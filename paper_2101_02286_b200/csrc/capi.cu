@@ -91,7 +91,7 @@ void free_plan(Plan* P) {
                     P->bt,      P->yl_prev,   P->bh,       P->recv_m,    P->recv_p,  P->xt,
                     P->xt_next, P->halo_lo,   P->halo_hi,  P->send_lo,   P->send_hi, P->tile.d_pcr,
                     P->d_stage_b, P->d_stage_x, P->d_plu,    P->d_pSR,     P->d_ainv,  P->d_planes4,
-                    P->d_xnext2, P->d_ppcr};
+                    P->d_xnext2, P->d_ppcr, P->d_vppcr, P->ptc.d_tab};
   for (double* b : bufs)
     if (b) cudaFree(b);
   for (cudaEvent_t e : P->ev) cudaEventDestroy(e);
@@ -201,8 +201,10 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   // (the virtual-partition chain).  With nparts > 1 that makes two levels: the chain computes
   // D_i^{-1} b_i of the whole slab (its internal interfaces solved on chip), and the reduced
   // system across the GPUs keeps the paper's one row per rank.
+  // (two levels are opt-in, CTRI_TWO_LEVEL=1: measured on 2 and 4 B200s the in-kernel window
+  // work cost more than the virtual rows' window pass it saves -- DESIGN.md section 5)
   P->vchain = tile_ok && !P->tile.contig && P->vp > 1 && P->tile.vc_ok && !knob_no_vchain() &&
-              !knob_copy_only();
+              !knob_copy_only() && (p == 1 || knob_two_level());
   P->rvp = (p > 1 && P->vchain) ? 1 : P->vp;
   const int64_t rn = n / P->rvp;  // rows per reduced-system row's partition
   const int pr = p * P->rvp;      // rows of the reduced system (virtual rows included)
@@ -376,13 +378,31 @@ ctri_status penta_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, co
   P->lay.inner = 1;
   for (int k = 0; k < sd; ++k) P->lay.outer *= gd[k];
   for (int k = sd + 1; k < 3; ++k) P->lay.inner *= gd[k];
+  // on-chip local solve (ptile.cu) where its geometry fits: one partition of 256..1024 rows, or
+  // with one GPU and a longer strided slab the paper's partition method with vp = n / 1024
+  // partitions on this GPU (reduced 2x2-block system over them, then the window pass)
+  P->vp = 1;
+  if (p == 1 && P->lay.inner >= 32 && n > 1024 && n % 1024 == 0 && n / 1024 <= 8 &&
+      is_pow2(n / 1024) && !knob_penta_serial())
+    P->vp = (int)(n / 1024);
+  P->rvp = 1;
   P->tlay = P->lay;
+  P->tlay.outer = P->lay.outer * P->vp;
+  P->tlay.n = n / P->vp;
   P->local_kernel = 3;
   CUDA_TRY(cudaGetDevice(&P->device));
   CUDA_TRY(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device));
   std::string why;
   ctri_status st = penta_plan_tables(P, s, &why);
   if (st != CTRI_OK) return fail(st, "pentadiagonal tables: " + why);
+  if (!knob_penta_serial() && ptile_configure(*P, &why)) {
+    P->local_kernel = 4;
+    if ((st = upload(&P->ptc.d_tab, P->ptc.tab, s)) != CTRI_OK) return fail(st, "penta tile tables");
+  } else if (P->vp > 1) {  // no on-chip solve: the slab as one partition, column-serial
+    P->vp = 1;
+    P->tlay = P->lay;
+    if ((st = penta_plan_tables(P, s, &why)) != CTRI_OK) return fail(st, "pentadiagonal tables: " + why);
+  }
   const int64_t m = P->lay.m();
   if (p > 1) {
     // pairwise 2x2-block PCR where it applies, else the one-round all-gather (R20)
@@ -453,7 +473,9 @@ ctri_status penta_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, co
     P->ev.resize(EV_COUNT);
     for (auto& e : P->ev) CUDA_TRY(cudaEventCreate(&e));
   }
-  P->launches_per_solve = 2 + (p > 1 ? 1 : 0);
+  // local solve; + window pass (one partition column-serial); + reduced kernel and window pass
+  // (nparts > 1, or the vp partitions of one GPU); the on-chip single partition is complete
+  P->launches_per_solve = 1 + (p > 1 || P->vp > 1 ? 2 : (P->local_kernel == 4 ? 0 : 1));
   CUDA_TRY(cudaStreamSynchronize(s));
   return CTRI_OK;
 }
@@ -861,10 +883,23 @@ ctri_status penta_solve_group(std::vector<Plan*>& G, const double* const* b, dou
   for (Plan* P : G) P->solves++;
   record(P0, EV_START, s);
   for (size_t r = 0; r < G.size(); ++r) {
-    cudaError_t e = launch_penta_local(*G[r], b[r], x[r], s);
+    cudaError_t e = G[r]->local_kernel == 4 ? launch_ptile(*G[r], b[r], x[r], s)
+                                            : launch_penta_local(*G[r], b[r], x[r], s);
     if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("penta local: ") + cudaGetErrorString(e));
   }
   record(P0, EV_LOCAL, s);
+  if (P0.p == 1 && P0.local_kernel == 4 && P0.vp == 1) {  // one partition solved completely on chip
+    record(P0, EV_BACK, s);
+    for (Plan* P : G) P->timed_valid = !P->ev.empty();
+    return CTRI_OK;
+  }
+  if (P0.p == 1 && P0.vp > 1) {  // (a2)+(a3) over this GPU's partitions: x~ into rows 0, 1 of each
+    for (size_t r = 0; r < G.size(); ++r) {
+      cudaError_t e = launch_penta_reduced_local(*G[r], x[r], s);
+      if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("penta reduced: ") + cudaGetErrorString(e));
+    }
+    record(P0, EV_XX, s);
+  }
   if (P0.p > 1) {
     P2PArgs A;
     p2p_args(P0, &A);

@@ -294,10 +294,6 @@ static bool inv2(const double* a, double guard, double* o) {
 
 bool penta_block_pcr(int P, bool cyclic, const Penta& pt, double guard, PentaPcr* out, FactorError* err) {
   if (P < 2) return fail(err, kInvalid, "penta_block_pcr: P < 2");
-  if (cyclic && !is_pow2(P)) return fail(err, kUnsupported, "penta_block_pcr: cyclic P must be a power of two");
-  PentaPcr t;
-  t.P = P;
-  t.cyclic = cyclic;
   std::vector<double> L(4 * (size_t)P), D(4 * (size_t)P), U(4 * (size_t)P);
   for (int i = 0; i < P; ++i) {
     const bool lft = cyclic || i > 0, rgt = cyclic || i < P - 1;
@@ -307,6 +303,16 @@ bool penta_block_pcr(int P, bool cyclic, const Penta& pt, double guard, PentaPcr
       U[4 * i + e] = rgt ? pt.Uh[e] : 0.0;
     }
   }
+  return penta_block_pcr_rows(P, cyclic, L, D, U, guard, out, err);
+}
+
+bool penta_block_pcr_rows(int P, bool cyclic, std::vector<double> L, std::vector<double> D,
+                          std::vector<double> U, double guard, PentaPcr* out, FactorError* err) {
+  if (P < 1) return fail(err, kInvalid, "penta_block_pcr: P < 1");
+  if (cyclic && !is_pow2(P)) return fail(err, kUnsupported, "penta_block_pcr: cyclic P must be a power of two");
+  PentaPcr t;
+  t.P = P;
+  t.cyclic = cyclic;
   const int q = ilog2(P);  // cyclic: log2 P; acyclic: ceil(log2 P)
   for (int k = 0; k < q; ++k) {
     const int s = 1 << k;

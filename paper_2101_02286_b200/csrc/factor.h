@@ -128,6 +128,11 @@ struct PentaPcr {
   std::vector<double> alpha, gamma, fold;
 };
 bool penta_block_pcr(int P, bool cyclic, const Penta& pt, double guard, PentaPcr* out, FactorError* err);
+// the same with per-row 2x2 blocks L, D, U ([P][4] row-major each; out-of-range couplings of an
+// acyclic system must be zero) -- e.g. the chunk-head systems of the on-chip pentadiagonal
+// solve, whose first row may be a decoupled dummy
+bool penta_block_pcr_rows(int P, bool cyclic, std::vector<double> L, std::vector<double> D,
+                          std::vector<double> U, double guard, PentaPcr* out, FactorError* err);
 
 inline bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 inline int ilog2(int64_t v) {

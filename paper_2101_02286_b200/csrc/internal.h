@@ -82,6 +82,7 @@ struct TileArgs {
   int rows_per_cta; // n / G
   int stages;       // log2 Q
   int vc_slab;      // VC with nparts > 1 (two levels): slab row 0 is the GPU interface
+  int l2_W;         // > 0: rows <= l2_W and >= n - l2_W of every slab stored evict-last (window)
   int mode;         // 0: complete cyclic solve (p = 1); 1: y_D = D_i^{-1} b_i + planes (p >= 2);
                     // 2: complete acyclic solve (p = 1)
   int rows_box;     // TMA box rows (<= 256)
@@ -122,6 +123,23 @@ struct TileArgs {
   int vc_vp, vc_W, vc_q, vc_cyclic;
   int64_t vc_groups;                     // column groups (num_tiles / vp)
   double vc_alpha[4 * 8], vc_gamma[4 * 8], vc_inv[8];  // [stage][row] PCR of the vp-row system
+};
+
+// on-chip pentadiagonal local solve (ptile.cu): kernel arguments and plan-time configuration
+struct PTileArgs {
+  double* x;
+  Layout lay;                 // the (virtual) slabs as the kernel sees them
+  int64_t tiles_per_outer, num_tiles;
+  int Q, G, stages, mode;     // chunk heads per column, cluster, head-system PCR stages, mode
+  const double* tab;          // [stages][Q][4] alpha | [stages][Q][4] gamma | [Q][4] fold
+  double* planes4;            // mode 1: [4][pm] c0 | c1 | w0 | w1 per (virtual) slab column
+  int64_t pm;
+};
+struct PTileConfig {
+  bool ok = false;
+  int G = 0, Q = 0, stages = 0, mode = 0, grid = 0, smem = 0;
+  std::vector<double> tab, consts;  // head-system tables; chunk LU, S0, S1, R0, R1 (30 each)
+  double* d_tab = nullptr;
 };
 
 struct TileConfig {
@@ -299,6 +317,9 @@ struct Plan {
   double *d_ainv = nullptr;        // [2p][2p] reduced inverse (p > 1)
   double *d_planes4 = nullptr;     // [4][m]: c0 | c1 | w0 | w1  (c = b~ - U~ y_i, w = L~ y_i)
   double *d_xnext2 = nullptr;      // [2][m]: x~_{i+1}
+  PTileConfig ptc;                 // on-chip local solve (local_kernel 4)
+  PentaPcr vppcr;                  // nparts == 1, vp > 1: 2x2-block PCR over the vp partitions
+  double *d_vppcr = nullptr;       // [stages][vp][4] alpha | gamma, [vp][4] fold
   bool ppcr = false;               // pairwise 2x2-block PCR reduced solve (else all-gather)
   int ppcr_steps = 0;
   double *d_ppcr = nullptr;        // this rank's [step][8] A0 | A1 and fold [4]
@@ -322,6 +343,8 @@ inline bool knob_copy_only() { static const bool v = env_knob("CTRI_TILE_COPY_ON
 // CTRI_NO_VCHAIN: virtual partitions finish with k_reduced_local + k_window (A/B measurement;
 // read at plan creation, not on the solve path)
 inline bool knob_no_vchain() { return env_knob("CTRI_NO_VCHAIN"); }
+// CTRI_TWO_LEVEL: nparts > 1 with virtual partitions chained in the tile kernel (plan creation)
+inline bool knob_two_level() { return env_knob("CTRI_TWO_LEVEL"); }
 
 // kernels.cu launchers (return cudaError_t of the launch)
 cudaError_t launch_local_generic(const Plan& P, const double* b, double* x, cudaStream_t s);
@@ -334,6 +357,11 @@ cudaError_t launch_window(const Plan& P, double* x, const double* next, cudaStre
 ctri_status penta_plan_tables(Plan* P, cudaStream_t s, std::string* why);
 cudaError_t launch_penta_local(const Plan& P, const double* b, double* x, cudaStream_t s);
 cudaError_t launch_penta_window(const Plan& P, double* x, cudaStream_t s);
+cudaError_t launch_penta_reduced_local(const Plan& P, double* x, cudaStream_t s);
+bool ptile_configure(Plan& P, std::string* why);
+cudaError_t launch_ptile(const Plan& P, const double* b, double* x, cudaStream_t s);
+// CTRI_PENTA_COLUMN_SERIAL: pentadiagonal plans keep the column-serial local solve (A/B)
+inline bool knob_penta_serial() { return env_knob("CTRI_PENTA_COLUMN_SERIAL"); }
 cudaError_t launch_pack_halo(const Plan& P, const double* f, cudaStream_t s);
 cudaError_t launch_stencil(const Plan& P, const double* f, double* rhs, const Stencil5& st,
                            cudaStream_t s);

@@ -280,8 +280,9 @@ struct PentaWinArgs {
   double* x;
   const double* SR;    // [4][N]: S0 | S1 | R0 | R1
   const double* next;  // [2][m] x~_{i+1} (p > 1), else nullptr
-  int64_t outer, n, inner, N, W, rows;
+  int64_t outer, n, inner, N, W, rows;  // n: rows of one partition (a slab, or 1/vp of it)
   int full, wrap;
+  int vp;              // partitions per slab (nparts == 1); the grid's z index is the partition
 };
 
 __device__ __forceinline__ int64_t penta_row(const PentaWinArgs& A, int64_t ry) {
@@ -303,15 +304,20 @@ __global__ void __launch_bounds__(256) k_penta_window(const PentaWinArgs A) {
   const int64_t m = A.outer * A.inner;
   if (j >= m) return;
   const int64_t o = j / A.inner, c = j - o * A.inner, st = A.inner;
-  double* xc = A.x + o * A.n * st + c;
+  const int s = blockIdx.z;  // partition of the slab
+  double* xc = A.x + (o * A.vp + s) * A.n * st + c;
   const double a0 = xc[0], a1 = xc[st];
   double n0 = 0.0, n1 = 0.0;
-  if (A.next) {
+  if (s + 1 < A.vp) {  // x~ of the next partition on this GPU
+    n0 = xc[A.n * st];
+    n1 = xc[(A.n + 1) * st];
+  } else if (A.next) {
     n0 = A.next[j];
     n1 = A.next[m + j];
-  } else if (A.wrap) {
-    n0 = a0;
-    n1 = a1;
+  } else if (A.wrap) {  // the first partition of the slab (itself when vp == 1)
+    const double* x0 = A.x + o * A.vp * A.n * st + c;
+    n0 = x0[0];
+    n1 = x0[st];
   }
   const int64_t r0 = (int64_t)blockIdx.y * kPentaRows;
   double v[kPentaRows];
@@ -359,7 +365,8 @@ static ctri_status upload_vec(double** d, const std::vector<double>& h, cudaStre
 }
 
 ctri_status penta_plan_tables(Plan* P, cudaStream_t s, std::string* why) {
-  const int64_t n = P->lay.n, N = n - 2, m = P->lay.m();
+  // the partitions the local kernel solves: the slab, or its vp partitions (nparts == 1)
+  const int64_t n = P->tlay.n, N = n - 2, m = P->lay.m();
   FactorError fe;
   if (!penta_factor(N, P->bands5, &P->pt, &fe)) {
     *why = fe.detail;
@@ -377,13 +384,35 @@ ctri_status penta_plan_tables(Plan* P, cudaStream_t s, std::string* why) {
   }
   P->ainv = inv;
   if (P->p == 1) std::memcpy(P->pcinv, inv.data(), sizeof(P->pcinv));
+  if (P->p == 1 && P->vp > 1) {  // 2x2-block PCR over the vp partitions of this GPU (R20)
+    if (!penta_block_pcr(P->vp, P->cyclic != 0, pt, guard, &P->vppcr, &fe)) {
+      *why = fe.detail;
+      return (ctri_status)fe.code;
+    }
+    std::vector<double> t;
+    t.insert(t.end(), P->vppcr.alpha.begin(), P->vppcr.alpha.end());
+    t.insert(t.end(), P->vppcr.gamma.begin(), P->vppcr.gamma.end());
+    t.insert(t.end(), P->vppcr.fold.begin(), P->vppcr.fold.end());
+    if (P->d_vppcr) cudaFree(P->d_vppcr);
+    P->d_vppcr = nullptr;
+    ctri_status st = upload_vec(&P->d_vppcr, t, s);
+    if (st != CTRI_OK) return st;
+  }
   std::vector<double> lu, sr;
   for (const std::vector<double>* v : {&pt.lam1, &pt.lam2, &pt.nu1, &pt.inv_mu}) lu.insert(lu.end(), v->begin(), v->end());
   for (const std::vector<double>* v : {&pt.S0, &pt.S1, &pt.R0, &pt.R1}) sr.insert(sr.end(), v->begin(), v->end());
   ctri_status st;
+  for (double** d : {&P->d_plu, &P->d_pSR, &P->d_ainv, &P->d_planes4})  // (called again when the
+    if (*d) {                                                            //  partition size changes)
+      cudaFree(*d);
+      *d = nullptr;
+    }
   if ((st = upload_vec(&P->d_plu, lu, s)) != CTRI_OK) return st;
   if ((st = upload_vec(&P->d_pSR, sr, s)) != CTRI_OK) return st;
   if ((st = upload_vec(&P->d_ainv, inv, s)) != CTRI_OK) return st;
+  if (P->p == 1 && P->vp > 1 &&
+      cudaMalloc(&P->d_planes4, sizeof(double) * 4 * m * P->vp) != cudaSuccess)
+    return CTRI_ERR_OOM;
   if (P->p > 1) {
     if (cudaMalloc(&P->d_planes4, sizeof(double) * 4 * m) != cudaSuccess) return CTRI_ERR_OOM;
     if (cudaMalloc(&P->d_xnext2, sizeof(double) * 2 * m) != cudaSuccess) return CTRI_ERR_OOM;
@@ -433,9 +462,10 @@ cudaError_t launch_penta_window(const Plan& P, double* x, cudaStream_t s) {
   A.SR = P.d_pSR;
   A.next = P.p > 1 ? P.d_xnext2 : nullptr;
   A.outer = P.lay.outer;
-  A.n = P.lay.n;
+  A.n = P.tlay.n;
   A.inner = P.lay.inner;
-  A.N = P.lay.n - 2;
+  A.N = P.tlay.n - 2;
+  A.vp = P.vp;
   A.W = P.window;
   A.full = ((P.flags & CTRI_FLAG_FULL_BACKSUB) || 2 * P.window >= A.N) ? 1 : 0;
   A.rows = A.full ? A.N : 2 * A.W;
@@ -445,9 +475,69 @@ cudaError_t launch_penta_window(const Plan& P, double* x, cudaStream_t s) {
     k_penta_window_contig<<<(unsigned)((A.outer + 7) / 8), 256, 0, s>>>(A);
   } else {
     const int64_t m = P.lay.m();
-    dim3 grid((unsigned)((m + 255) / 256), (unsigned)((A.rows + kPentaRows - 1) / kPentaRows));
+    dim3 grid((unsigned)((m + 255) / 256), (unsigned)((A.rows + kPentaRows - 1) / kPentaRows),
+              (unsigned)A.vp);
     k_penta_window<<<grid, 256, 0, s>>>(A);
   }
+  return cudaGetLastError();
+}
+
+// (a2)+(a3) across the vp partitions of one GPU (nparts == 1, local_kernel 4): per batch column
+// b^_v = c_v - w_{v-1} (Eq. bi_hat with 2x2 blocks; cyclic wrap or none), 2x2-block PCR
+// over the vp rows with the plan's multipliers (R20; fold R3) and x~_v into rows 0, 1 of
+// partition v; the window pass follows.
+__global__ void __launch_bounds__(128) k_penta_reduced_local(double* __restrict__ x,
+                                                             const double* __restrict__ planes4,
+                                                             const double* __restrict__ tab,
+                                                             int64_t outer, int64_t nv, int64_t inner,
+                                                             int vp, int stages, int cyclic) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t m = outer * inner;
+  if (j >= m) return;
+  const int64_t o = j / inner, c = j - o * inner, pm = m * vp;
+  double b0[8], b1[8];
+  for (int v = 0; v < vp; ++v) {
+    const int64_t pj = (o * vp + v) * inner + c;
+    const int vl = v == 0 ? vp - 1 : v - 1;
+    const int64_t pl = (o * vp + vl) * inner + c;
+    const bool lft = cyclic || v > 0;
+    b0[v] = planes4[pj] - (lft ? planes4[2 * pm + pl] : 0.0);
+    b1[v] = planes4[pm + pj] - (lft ? planes4[3 * pm + pl] : 0.0);
+  }
+  for (int k = 0; k < stages; ++k) {
+    const int sh = 1 << k;
+    double n0[8], n1[8];
+    for (int v = 0; v < vp; ++v) {
+      int im = v - sh, ip = v + sh;
+      double m0 = 0.0, m1 = 0.0, p0 = 0.0, p1 = 0.0;
+      if (cyclic) {
+        im = ((im % vp) + vp) % vp;
+        ip = ip % vp;
+      }
+      if (im >= 0) { m0 = b0[im]; m1 = b1[im]; }
+      if (ip < vp) { p0 = b0[ip]; p1 = b1[ip]; }
+      const double* a = tab + ((size_t)k * vp + v) * 4;
+      const double* g = tab + ((size_t)(stages + k) * vp + v) * 4;
+      n0[v] = b0[v] - (a[0] * m0 + a[1] * m1) - (g[0] * p0 + g[1] * p1);
+      n1[v] = b1[v] - (a[2] * m0 + a[3] * m1) - (g[2] * p0 + g[3] * p1);
+    }
+    for (int v = 0; v < vp; ++v) {
+      b0[v] = n0[v];
+      b1[v] = n1[v];
+    }
+  }
+  for (int v = 0; v < vp; ++v) {
+    const double* f = tab + ((size_t)2 * stages * vp + v) * 4;
+    double* xs = x + (o * vp + v) * nv * inner + c;
+    xs[0] = f[0] * b0[v] + f[1] * b1[v];
+    xs[inner] = f[2] * b0[v] + f[3] * b1[v];
+  }
+}
+
+cudaError_t launch_penta_reduced_local(const Plan& P, double* x, cudaStream_t s) {
+  const int64_t m = P.lay.m();
+  k_penta_reduced_local<<<(unsigned)((m + 127) / 128), 128, 0, s>>>(
+      x, P.d_planes4, P.d_vppcr, P.lay.outer, P.tlay.n, P.lay.inner, P.vp, P.vppcr.stages, P.cyclic);
   return cudaGetLastError();
 }
 

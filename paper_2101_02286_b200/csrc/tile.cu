@@ -593,6 +593,14 @@ __global__ void __launch_bounds__(NT, MINB)
       if (CONTIG) {
 #pragma unroll
         for (int k = 0; k < K; k += 4) dev::st_global_cs_v4(xp + k, v[k], v[k + 1], v[k + 2], v[k + 3]);
+      } else if (LAYOUT == 0 && A.l2_W > 0 &&
+                 ((g == 0 && c * K <= A.l2_W) || ((int)g == G - 1 && (c + 1) * K > (int)A.lay.n - A.l2_W))) {
+        // nparts > 1, window rows of the whole solve fit in L2: the chunks holding them (whole
+        // warps) store every row evict-last, so the window pass after the reduced phase reads
+        // them from L2 instead of HBM
+        const uint64_t pol_last = dev::policy_evict_last();
+#pragma unroll
+        for (int k = 0; k < K; ++k) dev::st_global_hint(xp + (int64_t)k * A.lay.inner, v[k], pol_last);
       } else {
 #pragma unroll
         for (int k = 0; k < K; ++k) dev::st_global_cs(xp + (int64_t)k * A.lay.inner, v[k]);
@@ -1222,6 +1230,13 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   A.halo_hi = (P.p == 1) ? P.send_lo : P.halo_hi;
   const bool fused = !deriv && P.fused;
   const bool vchain = !deriv && P.vchain;
+  // nparts > 1 without the chain: keep the window rows L2-resident for the window pass when all
+  // of them fit in a third of L2 (measured: HBM re-reads of the window were 20-70% of the
+  // reduced phase)
+  A.l2_W = 0;
+  if (P.p > 1 && !vchain && !fused && !deriv && !tc.contig && P.window > 0 &&
+      (2 * P.window + 1) * P.tlay.outer * P.lay.inner * 8 <= (int64_t)64 << 20)
+    A.l2_W = (int)P.window;
   A.vc_slab = 0;
   if (vchain) {
     // nparts == 1: the vp-row system is the whole (cyclic or acyclic) reduced system (gpcr);

@@ -141,3 +141,74 @@ def test_penta_delta_at_partition_edges(r, cyclic):
         x = penta_gpu(b, 0, p, bands, cyclic)
         ref = oracle.penta_solve(b, 0, bands, cyclic)
         assert np.max(np.abs(x - ref)) < 1e-14 * max(1.0, np.max(np.abs(ref)))
+
+
+@pytest.mark.parametrize("shape", [(256, 1, 64), (512, 2, 32), (1024, 1, 96), (8192, 1, 32), (4096, 2, 40)])
+@pytest.mark.parametrize("cyclic", [True, False])
+@pytest.mark.parametrize("bands", BANDS)
+def test_penta_on_chip_matches_oracle(shape, cyclic, bands, monkeypatch):
+    """The on-chip pentadiagonal local solve (ptile.cu): register leaf + 2x2-block PCR of the
+    chunk heads; one partition of 256 / 512 / 1024 rows solved completely, longer slabs as
+    n / 1024 partitions of one GPU (2x2-block PCR over them, then the window pass).  Every
+    element vs the oracle, and vs the column-serial kernel of the same plan."""
+    b = workloads.uniform(shape, 150 + shape[0] // 256)
+    x, st = penta_gpu(b, 0, 1, bands, cyclic, return_stats=True)
+    assert st["local_kernel"] == 4, st
+    assert st["vparts"] == max(1, shape[0] // 1024)
+    ref = oracle.penta_solve(b, 0, bands, cyclic)
+    assert rel_err(x, ref, 0) < TOL_REL
+    assert penta_residual(x, b, 0, bands, cyclic) < 1e-13
+    monkeypatch.setenv("CTRI_PENTA_COLUMN_SERIAL", "1")
+    xs, ss = penta_gpu(b, 0, 1, bands, cyclic, return_stats=True)
+    assert ss["local_kernel"] == 3
+    assert np.max(np.abs(x - xs)) < 1e-13 * np.max(np.abs(xs))
+
+
+@pytest.mark.parametrize("r", [0, 1, 2, 31, 32, 33, 255, 256, 257, 1023, 1024, 1025, 2047])
+def test_penta_on_chip_delta_at_chunk_and_partition_edges(r):
+    """Unit impulses on and next to the chunk heads (every 32 rows), the CTA boundaries (256)
+    and the on-GPU partition interfaces (1024) of the on-chip solve (p = 1, n = 2048: two
+    partitions, clusters of 4)."""
+    N = 2048
+    b = np.zeros((N, 1, 32))
+    b[r] = 1.0
+    for bands in BANDS:
+        for cyclic in (True, False):
+            x, st = penta_gpu(b, 0, 1, bands, cyclic, return_stats=True)
+            assert st["local_kernel"] == 4
+            ref = oracle.penta_solve(b, 0, bands, cyclic)
+            assert np.max(np.abs(x - ref)) < 1e-14 * max(1.0, np.max(np.abs(ref)))
+
+
+@pytest.mark.parametrize("p", [1, 8])
+def test_penta_cfg2_grid_full_size(p):
+    """The pentadiagonal solve on the BASELINE grid (8192 x 256^2, Lele's tenth-order LHS) as
+    bench.py --penta runs it (p = 1: 8 on-chip partitions; p = 8 loopback: 1024-row slabs on
+    chip, reduced system over the P2P path): every column vs the oracle."""
+    import torch
+
+    from paper_2101_02286_b200 import ctri
+    from test_gpu_parity import _full_columns
+    bands = BANDS[2]
+    dims = (8192, 256, 256)
+    b = workloads.device_uniform(dims, 2, torch.device("cuda:0"))
+    if p == 1:
+        x = torch.empty_like(b)
+        plan = ctri.Plan(dims, 0, 1, 0, bands)
+        plan.solve(b, x)
+        torch.cuda.synchronize()
+        st = plan.stats()
+        plan.close()
+    else:
+        n = dims[0] // p
+        bs = [b[r * n:(r + 1) * n].contiguous() for r in range(p)]
+        xs = [torch.empty_like(t) for t in bs]
+        g = ctri.LoopbackGroup(dims, 0, p, bands)
+        g.solve(bs, xs)
+        torch.cuda.synchronize()
+        st = g.stats(0)
+        g.close()
+        x = torch.cat(xs, 0)
+    assert st["local_kernel"] == 4 and st["device_error"] == 0
+    err, m = _full_columns(b, x, 0, fn=lambda a: oracle.penta_solve(a, 0, bands, True))
+    assert m == 65536 and err < TOL_REL, err

@@ -114,12 +114,13 @@ def test_vchain_repeated_solves(monkeypatch):
 @pytest.mark.parametrize("p,n,cyclic", [(2, 4096, True), (4, 2048, True), (3, 2048, True), (2, 4096, False),
                                         (2, 8192, True)])
 @pytest.mark.parametrize("bands", [SYM, NONSYM])
-def test_two_level_chain_loopback(p, n, cyclic, bands):
-    """nparts > 1 with virtual partitions chained in the tile kernel (two levels): each rank's
+def test_two_level_chain_loopback(p, n, cyclic, bands, monkeypatch):
+    """nparts > 1 with virtual partitions chained in the tile kernel (two levels, opt-in): each rank's
     slab is solved as vp partitions whose internal interfaces are eliminated on chip
     (D_i^{-1} b_i of the whole slab), and the reduced system across the ranks has one row per
     rank (p = 3: detach / reattach).  Loopback on one GPU, every element vs the oracle."""
     from helpers import gpu_solve
+    monkeypatch.setenv("CTRI_TWO_LEVEL", "1")
     b = workloads.uniform((p * n, 1, 64), 40 + p)
     x, st = gpu_solve(b, 0, p, bands, cyclic, return_stats=True)
     vp = min(8, n // 1024)
@@ -131,13 +132,14 @@ def test_two_level_chain_loopback(p, n, cyclic, bands):
 
 
 @pytest.mark.parametrize("p", [2, 4])
-def test_two_level_chain_cfg2_full_size(p):
+def test_two_level_chain_cfg2_full_size(p, monkeypatch):
     """The BASELINE grid split into p loopback partitions of 4096 / 2048 rows (vp = 4 / 2
     chained on chip, p reduced rows): every one of the 65,536 columns vs the oracle."""
     import torch
 
     from paper_2101_02286_b200 import ctri
     from test_gpu_parity import _full_columns
+    monkeypatch.setenv("CTRI_TWO_LEVEL", "1")
     dims = (8192, 256, 256)
     b = workloads.device_uniform(dims, 2, torch.device("cuda:0"))
     n = dims[0] // p
