@@ -378,9 +378,11 @@ ctri_status penta_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, co
   P->lay.inner = 1;
   for (int k = 0; k < sd; ++k) P->lay.outer *= gd[k];
   for (int k = sd + 1; k < 3; ++k) P->lay.inner *= gd[k];
-  // on-chip local solve (ptile.cu) where its geometry fits: one partition of 256..1024 rows, or
+  // on-chip local solve (ptile.cu) where its geometry fits: one partition of 256..2048 rows, or
   // with one GPU and a longer strided slab the paper's partition method with vp = n / 1024
-  // partitions on this GPU (reduced 2x2-block system over them, then the window pass)
+  // partitions on this GPU (reduced 2x2-block system over them, then the window pass).
+  // Measured on the cfg2 grid: 1024-row partitions (clusters of 4, shuffle PCR) 2.32 ms,
+  // 2048-row ones (clusters of 8, shared-memory PCR, half the window rows) 2.50 ms.
   P->vp = 1;
   if (p == 1 && P->lay.inner >= 32 && n > 1024 && n % 1024 == 0 && n / 1024 <= 8 &&
       is_pow2(n / 1024) && !knob_penta_serial())

@@ -33,7 +33,7 @@ namespace ctri {
 
 constexpr int kPK = 32, kPC = 32, kPNT = 256, kPCPC = kPNT / kPC;  // rows/chunk, cols, threads
 constexpr int kPN = kPK - 2;                                        // interior rows per chunk
-constexpr int kPMaxStages = 5;                                      // Q <= 32
+constexpr int kPMaxStages = 6, kPMaxQ = 64;                         // Q <= 64 (clusters <= 8)
 
 // chunk-level tables (kernel parameters: constant bank)
 struct PTileConsts {
@@ -50,9 +50,9 @@ __global__ void __launch_bounds__(kPNT, 2)
   double* ex = ring + ROWS * C;                          // owner: [NT][4] c0 c1 w0 w1 per head row
   double* rx = ex + 4 * NT;                              // holder: [NT][4] x~_c, x~_{c+1}
   double* s_al = rx + 4 * NT;                            // [stages][Q][4]
-  double* s_ga = s_al + kPMaxStages * 32 * 4;
-  double* s_fold = s_ga + kPMaxStages * 32 * 4;          // [Q][4]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(s_fold + 32 * 4);  // ring, ex, rx
+  double* s_ga = s_al + kPMaxStages * kPMaxQ * 4;
+  double* s_fold = s_ga + kPMaxStages * kPMaxQ * 4;      // [Q][4]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(s_fold + kPMaxQ * 4);  // ring, ex, rx
   uint64_t* mbar_ex = mbar + 1;
   uint64_t* mbar_rx = mbar + 2;
 
@@ -157,15 +157,38 @@ __global__ void __launch_bounds__(kPNT, 2)
         h0 -= ex[4 * prev_row + 2];
         h1 -= ex[4 * prev_row + 3];
       }
-      for (int k = 0; k < stages; ++k) {
-        const int sh = 1 << k;
-        const int lm = (oc - sh) & (Q - 1), lp = (oc + sh) & (Q - 1);
-        const double m0 = __shfl_sync(0xffffffffu, h0, lm, Q), m1 = __shfl_sync(0xffffffffu, h1, lm, Q);
-        const double p0 = __shfl_sync(0xffffffffu, h0, lp, Q), p1 = __shfl_sync(0xffffffffu, h1, lp, Q);
-        const double* a = s_al + (k * Q + oc) * 4;
-        const double* gm = s_ga + (k * Q + oc) * 4;
-        h0 = h0 - (a[0] * m0 + a[1] * m1) - (gm[0] * p0 + gm[1] * p1);
-        h1 = h1 - (a[2] * m0 + a[3] * m1) - (gm[2] * p0 + gm[3] * p1);
+      if (Q <= 32) {  // the Q heads of a column are Q lanes of one warp: register shuffles
+        for (int k = 0; k < stages; ++k) {
+          const int sh = 1 << k;
+          const int lm = (oc - sh) & (Q - 1), lp = (oc + sh) & (Q - 1);
+          const double m0 = __shfl_sync(0xffffffffu, h0, lm, Q), m1 = __shfl_sync(0xffffffffu, h1, lm, Q);
+          const double p0 = __shfl_sync(0xffffffffu, h0, lp, Q), p1 = __shfl_sync(0xffffffffu, h1, lp, Q);
+          const double* a = s_al + (k * Q + oc) * 4;
+          const double* gm = s_ga + (k * Q + oc) * 4;
+          h0 = h0 - (a[0] * m0 + a[1] * m1) - (gm[0] * p0 + gm[1] * p1);
+          h1 = h1 - (a[2] * m0 + a[3] * m1) - (gm[2] * p0 + gm[3] * p1);
+        }
+      } else {  // Q = 64: a column's heads span two warps; ping-pong through shared memory (the
+                // exchange buffer, free once every owner has read its rows)
+        __syncthreads();
+        double* cur = ex;
+        double* nxt = ex + 2 * NT;
+        for (int k = 0; k < stages; ++k) {
+          cur[2 * tid] = h0;
+          cur[2 * tid + 1] = h1;
+          __syncthreads();
+          const int sh = 1 << k;
+          const int rm = oj * Q + ((oc - sh) & (Q - 1)), rp = oj * Q + ((oc + sh) & (Q - 1));
+          const double m0 = cur[2 * rm], m1 = cur[2 * rm + 1], p0 = cur[2 * rp], p1 = cur[2 * rp + 1];
+          const double* a = s_al + (k * Q + oc) * 4;
+          const double* gm = s_ga + (k * Q + oc) * 4;
+          h0 = h0 - (a[0] * m0 + a[1] * m1) - (gm[0] * p0 + gm[1] * p1);
+          h1 = h1 - (a[2] * m0 + a[3] * m1) - (gm[2] * p0 + gm[3] * p1);
+          double* tmp = cur;
+          cur = nxt;
+          nxt = tmp;
+        }
+        __syncthreads();  // every read done before x~ leaves (the next tile's planes land here)
       }
       const double* fo = s_fold + oc * 4;
       const double x0 = fo[0] * h0 + fo[1] * h1, x1 = fo[2] * h0 + fo[3] * h1;
@@ -219,7 +242,7 @@ bool ptile_configure(Plan& P, std::string* why) {
   if (L.inner < kPC || (L.inner % 2) != 0) { *why = "on-chip penta: strided axis with >= 32 columns"; return false; }
   if (L.n % (kPCPC * kPK) != 0) { *why = "on-chip penta: n not a multiple of 256"; return false; }
   const int G = (int)(L.n / (kPCPC * kPK));
-  if (G < 1 || G > 4) { *why = "on-chip penta: n / 256 not in 1..4"; return false; }
+  if (G < 1 || G > 8) { *why = "on-chip penta: n / 256 not in 1..8"; return false; }
   if (L.outer > ((int64_t)1 << 30) || L.inner > ((int64_t)1 << 31)) { *why = "dims too large"; return false; }
   const int Q = kPCPC * G;
   Penta cp;
@@ -262,7 +285,7 @@ bool ptile_configure(Plan& P, std::string* why) {
   pc.Q = Q;
   pc.stages = t.stages;
   pc.mode = mode;
-  pc.smem = (int)(sizeof(double) * ((size_t)kPCPC * kPK * kPC + 8 * kPNT + (2 * kPMaxStages + 1) * 32 * 4) + 3 * 8);
+  pc.smem = (int)(sizeof(double) * ((size_t)kPCPC * kPK * kPC + 8 * kPNT + (2 * kPMaxStages + 1) * kPMaxQ * 4) + 3 * 8);
   if (cudaFuncSetAttribute(k_ptile, cudaFuncAttributeMaxDynamicSharedMemorySize, pc.smem) != cudaSuccess) {
     cudaGetLastError();
     *why = "cudaFuncSetAttribute(smem) failed";

@@ -212,3 +212,18 @@ def test_penta_cfg2_grid_full_size(p):
     assert st["local_kernel"] == 4 and st["device_error"] == 0
     err, m = _full_columns(b, x, 0, fn=lambda a: oracle.penta_solve(a, 0, bands, True))
     assert m == 65536 and err < TOL_REL, err
+
+
+@pytest.mark.parametrize("p", [2, 4])
+@pytest.mark.parametrize("cyclic", [True, False])
+def test_penta_on_chip_2048_row_slabs(p, cyclic):
+    """Slabs of 2048 rows per rank (the cfg2 grid at 4 GPUs): the on-chip solve with clusters of
+    8 (64 chunk heads per column, 2x2-block PCR through shared memory), then the reduced system
+    over the P2P path and the window pass; vs the oracle."""
+    b = workloads.uniform((2048 * p, 1, 64), 170 + p)
+    for bands in BANDS:
+        x, st = penta_gpu(b, 0, p, bands, cyclic, return_stats=True)
+        assert st["local_kernel"] == 4 and st["device_error"] == 0
+        ref = oracle.penta_solve(b, 0, bands, cyclic)
+        assert rel_err(x, ref, 0) < TOL_REL
+        assert penta_residual(x, b, 0, bands, cyclic) < 1e-13
