@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(NT, MINB)
       if (CONTIG) {
 #pragma unroll
         for (int k = 0; k < K; k += 4) dev::st_global_cs_v4(xp + k, v[k], v[k + 1], v[k + 2], v[k + 3]);
-      } else if (LAYOUT == 0 && A.l2_W > 0 &&
+      } else if ((LAYOUT == 0 || LAYOUT == 2) && A.l2_W > 0 &&
                  ((g == 0 && c * K <= A.l2_W) || ((int)g == G - 1 && (c + 1) * K > (int)A.lay.n - A.l2_W))) {
         // nparts > 1, window rows of the whole solve fit in L2: the chunks holding them (whole
         // warps) store every row evict-last, so the window pass after the reduced phase reads
@@ -1230,12 +1230,18 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   A.halo_hi = (P.p == 1) ? P.send_lo : P.halo_hi;
   const bool fused = !deriv && P.fused;
   const bool vchain = !deriv && P.vchain;
-  // nparts > 1 without the chain: keep the window rows L2-resident for the window pass when all
-  // of them fit in a third of L2 (measured: HBM re-reads of the window were 20-70% of the
-  // reduced phase)
+  // nparts > 1 without the chain: the window rows are stored with an L2 evict-last hint so the
+  // window pass after the reduced phase finds them in L2 (all of them when they fit, the most
+  // recent ones otherwise; the streaming rows are evict-first).  CTRI_L2_WINDOW_MB caps the
+  // window bytes it is used for (default 64 MB: measured on 4 B200s, cfg3 0.0997 -> 0.0968 ms at
+  // N = 4, while cfg5's 195 MB of window rows only slowed its tile kernel; 0 disables).
   A.l2_W = 0;
-  if (P.p > 1 && !vchain && !fused && !deriv && !tc.contig && P.window > 0 &&
-      (2 * P.window + 1) * P.tlay.outer * P.lay.inner * 8 <= (int64_t)64 << 20)
+  static const int64_t l2_cap = [] {
+    const char* e = std::getenv("CTRI_L2_WINDOW_MB");
+    return (int64_t)(e ? std::atoi(e) : 64) << 20;
+  }();
+  if (P.p > 1 && !vchain && !fused && !tc.contig && P.window > 0 &&
+      (2 * P.window + 1) * P.tlay.outer * P.lay.inner * 8 <= l2_cap)
     A.l2_W = (int)P.window;
   A.vc_slab = 0;
   if (vchain) {
