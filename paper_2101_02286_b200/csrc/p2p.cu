@@ -138,20 +138,52 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
     if (j < b1) nc = i + 1;
   }
   // ---- (a2) y_i[last] -> right neighbour; b^ ----
+  // the batch's planes into registers first: the LL stores are asm volatile with a memory
+  // clobber, so no load can move across them (a load per store would serialise HBM latencies)
+  double ylv[kMaxCpt], btv[kMaxCpt], yfv[kMaxCpt];
+#pragma unroll
+  for (int i = 0; i < kMaxCpt; ++i) {
+    ylv[i] = btv[i] = yfv[i] = 0.0;
+    if (i < nc) {
+      ylv[i] = R.yl[col[i]];
+      btv[i] = R.bt[col[i]];
+      yfv[i] = R.yf[col[i]];
+    }
+  }
   if (right >= 0 && rank != A.test_drop_rank) {  // (test knob: a rank that never sends)
     unsigned long long* dst = R.peer_mbox[right] + copy_off + OFF_Y;
 #pragma unroll
     for (int i = 0; i < kMaxCpt; ++i)
-      if (i < nc) ll_send(dst + 2 * col[i], R.yl[col[i]], ep);
+      if (i < nc) ll_send(dst + 2 * col[i], ylv[i], ep);
   }
   stamp(kTrYSent);
+  {  // batched receive: every pending column's word is loaded before any is tested
+    double ylp[kMaxCpt];
+    uint32_t pend = 0;
 #pragma unroll
-  for (int i = 0; i < kMaxCpt; ++i) {
-    if (i >= nc) continue;
-    const int64_t j = col[i];
-    double ylp = 0.0;
-    if (left >= 0) ok = ok && ll_recv(mine + OFF_Y + 2 * j, ep, deadline, &ylp);
-    bh[i] = R.bt[j] - A.l * ylp - A.u * R.yf[j];
+    for (int i = 0; i < kMaxCpt; ++i) {
+      ylp[i] = 0.0;
+      if (i < nc && left >= 0) pend |= 1u << i;
+    }
+    int spins = 0;
+    while (pend && ok) {
+      unsigned long long w0[kMaxCpt], w1[kMaxCpt];
+#pragma unroll
+      for (int i = 0; i < kMaxCpt; ++i)
+        if (pend & (1u << i)) dev::ll_load(mine + OFF_Y + 2 * col[i], &w0[i], &w1[i]);
+#pragma unroll
+      for (int i = 0; i < kMaxCpt; ++i)
+        if ((pend & (1u << i)) && dev::ll_ready(w0[i], w1[i], ep)) {
+          ylp[i] = dev::ll_value(w0[i], w1[i]);
+          pend &= ~(1u << i);
+        }
+      if (pend && ++spins == 64) {
+        spins = 0;
+        if (globaltimer() > deadline) ok = false;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kMaxCpt; ++i) bh[i] = btv[i] - A.l * ylp[i] - A.u * yfv[i];
   }
   stamp(kTrYRecv);
   // ---- (a3) reduced-system schedule: PCR stages, or detach / PCR / fold /
@@ -210,10 +242,30 @@ __global__ void __launch_bounds__(kP2PThreads, 2)
       if (i < nc) ll_send(dst + 2 * col[i], bh[i], ep);
   }
   double xb[kMaxCpt];
+  {  // batched receive of x~_{i+1}
+    uint32_t pend = 0;
 #pragma unroll
-  for (int i = 0; i < kMaxCpt; ++i) {
-    xb[i] = 0.0;
-    if (i < nc && ok && right >= 0) ok = ll_recv(mine + OFF_X + 2 * col[i], ep, deadline, &xb[i]);
+    for (int i = 0; i < kMaxCpt; ++i) {
+      xb[i] = 0.0;
+      if (i < nc && right >= 0) pend |= 1u << i;
+    }
+    int spins = 0;
+    while (pend && ok) {
+      unsigned long long w0[kMaxCpt], w1[kMaxCpt];
+#pragma unroll
+      for (int i = 0; i < kMaxCpt; ++i)
+        if (pend & (1u << i)) dev::ll_load(mine + OFF_X + 2 * col[i], &w0[i], &w1[i]);
+#pragma unroll
+      for (int i = 0; i < kMaxCpt; ++i)
+        if ((pend & (1u << i)) && dev::ll_ready(w0[i], w1[i], ep)) {
+          xb[i] = dev::ll_value(w0[i], w1[i]);
+          pend &= ~(1u << i);
+        }
+      if (pend && ++spins == 64) {
+        spins = 0;
+        if (globaltimer() > deadline) ok = false;
+      }
+    }
   }
   if (!ok) {
     *reinterpret_cast<volatile int*>(A.err) = 1;
@@ -474,13 +526,26 @@ __global__ void __launch_bounds__(kP2PThreads, 1)
     }
   };
   // ---- (a2) w_i = L~ y_i[last two] -> right neighbour; b^_i = c_i - w_{i-1} ----
+  // (the planes are loaded before the first LL store: the stores are asm volatile with a memory
+  // clobber, a load between two of them would serialise the HBM latencies)
+  double pw0[kMaxCpt], pw1[kMaxCpt], pc0[kMaxCpt], pc1[kMaxCpt];
+#pragma unroll
+  for (int i = 0; i < kMaxCpt; ++i) {
+    pw0[i] = pw1[i] = pc0[i] = pc1[i] = 0.0;
+    if (i < nc) {
+      pc0[i] = R.planes4[col[i]];
+      pc1[i] = R.planes4[m + col[i]];
+      pw0[i] = R.planes4[2 * m + col[i]];
+      pw1[i] = R.planes4[3 * m + col[i]];
+    }
+  }
   if (right >= 0) {
     unsigned long long* dst = R.peer_mbox[right] + copy_off;
 #pragma unroll
     for (int i = 0; i < kMaxCpt; ++i)
       if (i < nc) {
-        dev::ll_store(dst + OFF_Y(0) + 2 * col[i], R.planes4[2 * m + col[i]], ep);
-        dev::ll_store(dst + OFF_Y(1) + 2 * col[i], R.planes4[3 * m + col[i]], ep);
+        dev::ll_store(dst + OFF_Y(0) + 2 * col[i], pw0[i], ep);
+        dev::ll_store(dst + OFF_Y(1) + 2 * col[i], pw1[i], ep);
       }
   }
   stamp(kTrYSent);
@@ -492,8 +557,8 @@ __global__ void __launch_bounds__(kP2PThreads, 1)
 #pragma unroll
     for (int i = 0; i < kMaxCpt; ++i)
       if (i < nc) {
-        b0[i] = R.planes4[col[i]] - w0[i];
-        b1[i] = R.planes4[m + col[i]] - w1[i];
+        b0[i] = pc0[i] - w0[i];
+        b1[i] = pc1[i] - w1[i];
       }
   }
   stamp(kTrYRecv);
@@ -672,26 +737,70 @@ __global__ void __launch_bounds__(kP2PThreads) k_halo_p2p(const P2PArgs A) {
   const int64_t c0 = (int64_t)slice * A.slice_cols;
   const int64_t c1 = std::min<int64_t>(m, c0 + A.slice_cols);
   bool ok = true;
-  for (int64_t j = c0 + threadIdx.x; j < c1; j += kP2PThreads) {
-    const int64_t o = j / inner, c = j - o * inner;
-    const double* fc = R.f + o * n * inner + c;
-    unsigned long long* lo = R.peer_mbox[right] + hoff;  // right neighbour's rows -2, -1
-    unsigned long long* hi = R.peer_mbox[left] + hoff;   // left neighbour's rows n, n+1
-    ll_send(lo + 2 * j, fc[(n - 2) * inner], ep);
-    ll_send(lo + 2 * m + 2 * j, fc[(n - 1) * inner], ep);
-    ll_send(hi + 4 * m + 2 * j, fc[0], ep);
-    ll_send(hi + 6 * m + 2 * j, fc[inner], ep);
+  // kHU columns per thread and pass: every f row load is issued before the first LL store (the
+  // stores are asm volatile with a memory clobber: a load per store would serialise HBM
+  // latencies), and every pending word of the receive is loaded before any is tested
+  constexpr int kHU = 4;
+  unsigned long long* lo = R.peer_mbox[right] + hoff;  // right neighbour's rows -2, -1
+  unsigned long long* hi = R.peer_mbox[left] + hoff;   // left neighbour's rows n, n+1
+  for (int64_t jb = c0 + threadIdx.x; jb < c1; jb += (int64_t)kP2PThreads * kHU) {
+    double v[kHU][4];
+#pragma unroll
+    for (int u = 0; u < kHU; ++u) {
+      const int64_t j = jb + (int64_t)u * kP2PThreads;
+      if (j >= c1) continue;
+      const int64_t o = j / inner, c = j - o * inner;
+      const double* fc = R.f + o * n * inner + c;
+      v[u][0] = fc[(n - 2) * inner];
+      v[u][1] = fc[(n - 1) * inner];
+      v[u][2] = fc[0];
+      v[u][3] = fc[inner];
+    }
+#pragma unroll
+    for (int u = 0; u < kHU; ++u) {
+      const int64_t j = jb + (int64_t)u * kP2PThreads;
+      if (j >= c1) continue;
+      ll_send(lo + 2 * j, v[u][0], ep);
+      ll_send(lo + 2 * m + 2 * j, v[u][1], ep);
+      ll_send(hi + 4 * m + 2 * j, v[u][2], ep);
+      ll_send(hi + 6 * m + 2 * j, v[u][3], ep);
+    }
   }
   const unsigned long long* mine = R.mbox + hoff;
-  for (int64_t j = c0 + threadIdx.x; j < c1 && ok; j += kP2PThreads) {
-    double v[4];
+  for (int64_t jb = c0 + threadIdx.x; jb < c1 && ok; jb += (int64_t)kP2PThreads * kHU) {
+    double v[kHU][4];
+    uint32_t pend = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) ok = ok && ll_recv(mine + (int64_t)k * 2 * m + 2 * j, ep, deadline, &v[k]);
+    for (int u = 0; u < kHU; ++u)
+      if (jb + (int64_t)u * kP2PThreads < c1) pend |= 0xfu << (4 * u);
+    int spins = 0;
+    while (pend && ok) {
+      unsigned long long w0[4 * kHU], w1[4 * kHU];
+#pragma unroll
+      for (int k = 0; k < 4 * kHU; ++k)
+        if (pend & (1u << k))
+          dev::ll_load(mine + (int64_t)(k & 3) * 2 * m + 2 * (jb + (int64_t)(k >> 2) * kP2PThreads), &w0[k], &w1[k]);
+#pragma unroll
+      for (int k = 0; k < 4 * kHU; ++k)
+        if ((pend & (1u << k)) && dev::ll_ready(w0[k], w1[k], ep)) {
+          v[k >> 2][k & 3] = dev::ll_value(w0[k], w1[k]);
+          pend &= ~(1u << k);
+        }
+      if (pend && ++spins == 64) {
+        spins = 0;
+        if (globaltimer() > deadline) ok = false;
+      }
+    }
     if (!ok) break;
-    R.halo_lo[j] = v[0];
-    R.halo_lo[m + j] = v[1];
-    R.halo_hi[j] = v[2];
-    R.halo_hi[m + j] = v[3];
+#pragma unroll
+    for (int u = 0; u < kHU; ++u) {
+      const int64_t j = jb + (int64_t)u * kP2PThreads;
+      if (j >= c1) continue;
+      R.halo_lo[j] = v[u][0];
+      R.halo_lo[m + j] = v[u][1];
+      R.halo_hi[j] = v[u][2];
+      R.halo_hi[m + j] = v[u][3];
+    }
   }
   if (!ok) *reinterpret_cast<volatile int*>(A.err) = 2;
   __syncthreads();
