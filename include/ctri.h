@@ -329,6 +329,16 @@ ctri_status ctri_penta_block_pcr(int P, int cyclic, int64_t n, const double band
 ctri_status ctri_reduced_inverse(int P, int cyclic, const double* L, const double* D,
                                  const double* U, double* inv);
 
+/* HOST query (no device work): the pentadiagonal reduced system of P partitions of n rows
+ * (bands as ctri_plan_create_penta) solved by its step schedule -- 2x2-block PCR, or for
+ * cyclic non-power-of-two P the block detach / PCR / fold / reattach of P:271 / P:294 --
+ * applied serially to bhat[2P] (row-major: row i, component c at 2i + c) into xt[2P], exactly
+ * as the P2P kernel executes it rank by rank.  *steps, *detach_stages and *detached_rows
+ * (each may be NULL) receive the schedule's counts.  Errors: INVALID_ARG, SINGULAR. */
+ctri_status ctri_penta_reduced_schedule_apply(int P, int cyclic, int64_t n, const double bands[5],
+                                              const double* bhat, double* xt, int* steps,
+                                              int* detach_stages, int* detached_rows);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,7 +7,7 @@ built -- there is no CPU fallback.
 from .ctri import (CTRI_FLAG_DERIV, CTRI_FLAG_FULL_BACKSUB, CTRI_FLAG_GENERIC_LOCAL,  # noqa: F401
                    CTRI_FLAG_NCCL_ROUNDS, CTRI_FLAG_ALLGATHER, CTRI_FLAG_FUSED_REDUCED, ctri_reduced_inverse,
                    ctri_plan_create_penta, ctri_plan_create_penta_loopback, ctri_penta_factor_query,
-                   ctri_penta_block_pcr,
+                   ctri_penta_block_pcr, ctri_penta_reduced_schedule_apply,
                    CTRI_FLAG_TIMING, CtriError, LoopbackGroup, Plan, ctri_deriv,
                    ctri_deriv_loopback, ctri_factor_query, ctri_get_stats, ctri_get_unique_id,
                    ctri_pcr_coefficients, ctri_plan_create, ctri_reduced_schedule, ctri_plan_create_loopback,

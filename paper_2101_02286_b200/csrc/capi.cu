@@ -407,56 +407,44 @@ ctri_status penta_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, co
   }
   const int64_t m = P->lay.m();
   if (p > 1) {
-    // pairwise 2x2-block PCR where it applies, else the one-round all-gather (R20)
-    P->ppcr = (!cyclic || is_pow2(p)) && !(flags & CTRI_FLAG_ALLGATHER);
+    // the 2x2-block step schedule (P:346 in block form; detach / PCR / fold / reattach for
+    // cyclic non-power-of-two p, P:271 / P:294), or with CTRI_FLAG_ALLGATHER the one-round
+    // all-gather (R20)
+    P->ppcr = !(flags & CTRI_FLAG_ALLGATHER);
     int64_t copy_words = p2p_copy_words(m, 0, p, true, 4);
     if (P->ppcr) {
       double mx = 0;
       for (int k = 0; k < 5; ++k) mx = std::max(mx, std::fabs(bands[k]));
-      PentaPcr t;
+      BlockSchedule sc;
       FactorError fe;
-      if (!penta_block_pcr(p, cyclic != 0, P->pt, 1e-13 * mx, &t, &fe)) return fail((ctri_status)fe.code, fe.detail);
-      const int q = t.stages;
+      if (!penta_reduced_schedule(p, cyclic != 0, P->pt, 1e-13 * mx, &sc, &fe))
+        return fail((ctri_status)fe.code, fe.detail);
+      const int q = (int)sc.steps.size();
+      if (q > kMaxP2PSteps) return fail(CTRI_ERR_UNSUPPORTED, "pentadiagonal reduced schedule too long");
       P->ppcr_steps = q;
-      auto srcs = [&](int i, int k, int* s0, int* s1) {  // partners of row i in step k
-        const int sh = 1 << k;
-        int im = i - sh, ip = i + sh;
-        if (cyclic) {
-          im = ((im % p) + p) % p;
-          ip = ip % p;
-        } else {
-          if (im < 0) im = -1;
-          if (ip >= p) ip = -1;
-        }
-        if (im >= 0 && im == ip) ip = -1;  // single partner: A0 = alpha + gamma
-        *s0 = im;
-        *s1 = ip;
-      };
-      std::vector<double> tab;
+      P->sched.pcr_stages = sc.pcr_stages;  // (counts reported by ctri_get_stats)
+      P->sched.detach_stages = sc.detach_stages;
+      P->sched.detached_rows = sc.detached_rows;
+      std::vector<double> tab;  // [step][12]: W | C0 | C1 of this rank
       P->pstep.assign(kMaxP2PSteps, P2PStep{1.0, 0.0, 0.0, -1, -1, -1, -1, 0, 0});
       for (int k = 0; k < q; ++k) {
-        int s0, s1;
-        srcs(rank, k, &s0, &s1);
-        const double* al = &t.alpha[((size_t)k * p + rank) * 4];
-        const double* ga = &t.gamma[((size_t)k * p + rank) * 4];
-        for (int e = 0; e < 4; ++e) tab.push_back(s1 < 0 && s0 >= 0 && (cyclic && (1 << k) * 2 == p) ? al[e] + ga[e] : al[e]);
-        for (int e = 0; e < 4; ++e) tab.push_back(s1 >= 0 ? ga[e] : 0.0);
+        const BlockSchedEntry& e = sc.steps[k][rank];
+        tab.insert(tab.end(), e.W, e.W + 4);
+        tab.insert(tab.end(), e.C[0], e.C[0] + 4);
+        tab.insert(tab.end(), e.C[1], e.C[1] + 4);
         P2PStep& stp = P->pstep[k];
-        stp.src0 = (int8_t)s0;
-        stp.src1 = (int8_t)s1;
-        int nd = 0;
-        for (int r = 0; r < p; ++r) {
-          int r0, r1;
-          srcs(r, k, &r0, &r1);
+        stp.src0 = (int8_t)e.src[0];
+        stp.src1 = (int8_t)e.src[1];
+        int nd = 0;  // this rank's pre-step value goes to every row that reads it
+        for (int r = 0; r < p; ++r)
           for (int sl = 0; sl < 2; ++sl)
-            if ((sl ? r1 : r0) == rank) {
+            if (sc.steps[k][r].src[sl] == rank) {
               if (nd == 0) { stp.dst0 = (int8_t)r; stp.dslot0 = (int8_t)sl; }
-              else { stp.dst1 = (int8_t)r; stp.dslot1 = (int8_t)sl; }
+              else if (nd == 1) { stp.dst1 = (int8_t)r; stp.dslot1 = (int8_t)sl; }
               ++nd;
             }
-        }
+        if (nd > 2) return fail(CTRI_ERR_UNSUPPORTED, "pentadiagonal reduced schedule: > 2 readers");
       }
-      for (int e = 0; e < 4; ++e) tab.push_back(t.fold[(size_t)rank * 4 + e]);
       CUDA_TRY(cudaMalloc(&P->d_ppcr, sizeof(double) * tab.size()));
       CUDA_TRY(cudaMemcpyAsync(P->d_ppcr, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice, s));
       copy_words = (int64_t)(4 + 4 * q) * 2 * m;
@@ -607,7 +595,7 @@ void schedule_counts(const Plan& P, int* sends, int* rounds) {
     for (int k = 0; k < P.ppcr_steps; ++k) {
       const P2PStep& t = P.pstep[k];
       sd += 2 * ((t.dst0 >= 0 ? 1 : 0) + (t.dst1 >= 0 ? 1 : 0));
-      ++rd;
+      if (t.src0 >= 0 || t.src1 >= 0 || t.dst0 >= 0 || t.dst1 >= 0) ++rd;  // (the fold is local)
     }
     *sends = sd;
     *rounds = rd;
@@ -1565,6 +1553,42 @@ ctri_status ctri_penta_block_pcr(int P, int cyclic, int64_t n, const double band
   std::memcpy(gamma, t.gamma.data(), sizeof(double) * t.gamma.size());
   std::memcpy(fold, t.fold.data(), sizeof(double) * t.fold.size());
   *stages = t.stages;
+  return CTRI_OK;
+}
+
+ctri_status ctri_penta_reduced_schedule_apply(int P, int cyclic, int64_t n, const double bands[5],
+                                              const double* bhat, double* xt, int* steps,
+                                              int* detach_stages, int* detached_rows) {
+  if (P < 1 || !bands || !bhat || !xt) return fail(CTRI_ERR_INVALID_ARG, "bad arguments");
+  Penta pt;
+  FactorError fe;
+  if (!penta_factor(n - 2, bands, &pt, &fe)) return fail((ctri_status)fe.code, fe.detail);
+  double mx = 0;
+  for (int k = 0; k < 5; ++k) mx = std::max(mx, std::fabs(bands[k]));
+  BlockSchedule sc;
+  if (!penta_reduced_schedule(P, cyclic != 0, pt, 1e-13 * mx, &sc, &fe)) return fail((ctri_status)fe.code, fe.detail);
+  std::vector<double> v(bhat, bhat + 2 * P);
+  for (const auto& st : sc.steps) {  // every row reads its sources' pre-step values
+    std::vector<double> nv = v;
+    for (int i = 0; i < P; ++i) {
+      const BlockSchedEntry& e = st[i];
+      double r0 = e.W[0] * v[2 * i] + e.W[1] * v[2 * i + 1];
+      double r1 = e.W[2] * v[2 * i] + e.W[3] * v[2 * i + 1];
+      for (int k = 0; k < 2; ++k) {
+        if (e.src[k] < 0) continue;
+        const double u0 = v[2 * e.src[k]], u1 = v[2 * e.src[k] + 1];
+        r0 -= e.C[k][0] * u0 + e.C[k][1] * u1;
+        r1 -= e.C[k][2] * u0 + e.C[k][3] * u1;
+      }
+      nv[2 * i] = r0;
+      nv[2 * i + 1] = r1;
+    }
+    v.swap(nv);
+  }
+  std::memcpy(xt, v.data(), sizeof(double) * 2 * P);
+  if (steps) *steps = (int)sc.steps.size();
+  if (detach_stages) *detach_stages = sc.detach_stages;
+  if (detached_rows) *detached_rows = sc.detached_rows;
   return CTRI_OK;
 }
 

@@ -372,6 +372,194 @@ bool penta_block_pcr_rows(int P, bool cyclic, std::vector<double> L, std::vector
   return true;
 }
 
+bool penta_reduced_schedule(int P, bool cyclic, const Penta& pt, double guard, BlockSchedule* out,
+                            FactorError* err) {
+  *out = BlockSchedule();
+  out->P = P;
+  out->cyclic = cyclic;
+  if (P < 1) return fail(err, kInvalid, "penta_reduced_schedule: P < 1");
+  auto sub2 = [](double* a, const double* b) {
+    for (int e = 0; e < 4; ++e) a[e] -= b[e];
+  };
+  auto neg2 = [](double* a) {
+    for (int e = 0; e < 4; ++e) a[e] = -a[e];
+  };
+  if (!cyclic || is_pow2(P)) {  // block PCR stages, then the fold
+    if (P == 1) {
+      PentaPcr t;
+      std::vector<double> L(pt.Lh, pt.Lh + 4), D(cyclic ? pt.Dh : pt.DhFirst, (cyclic ? pt.Dh : pt.DhFirst) + 4),
+          U(pt.Uh, pt.Uh + 4);
+      if (!cyclic) L.assign(4, 0.0), U.assign(4, 0.0);
+      if (!penta_block_pcr_rows(1, cyclic, L, D, U, guard, &t, err)) return false;
+      std::vector<BlockSchedEntry> fold(1);
+      std::copy(t.fold.begin(), t.fold.begin() + 4, fold[0].W);
+      out->kind.push_back(kStepFold);
+      out->steps.push_back(fold);
+      return true;
+    }
+    PentaPcr t;
+    if (!penta_block_pcr(P, cyclic, pt, guard, &t, err)) return false;
+    for (int k = 0; k < t.stages; ++k) {
+      const int s = 1 << k;
+      std::vector<BlockSchedEntry> st(P);
+      for (int i = 0; i < P; ++i) {
+        int im = i - s, ip = i + s;
+        if (cyclic) {
+          im = ((im % P) + P) % P;
+          ip = ip % P;
+        } else {
+          if (im < 0) im = -1;
+          if (ip >= P) ip = -1;
+        }
+        const double* a = &t.alpha[((size_t)k * P + i) * 4];
+        const double* g = &t.gamma[((size_t)k * P + i) * 4];
+        if (im >= 0 && im == ip) {  // single partner (s = P/2)
+          st[i].src[0] = im;
+          for (int e = 0; e < 4; ++e) st[i].C[0][e] = a[e] + g[e];
+        } else {
+          if (im >= 0) { st[i].src[0] = im; std::copy(a, a + 4, st[i].C[0]); }
+          if (ip >= 0) { st[i].src[1] = ip; std::copy(g, g + 4, st[i].C[1]); }
+        }
+      }
+      out->kind.push_back(kStepPcr);
+      out->steps.push_back(st);
+    }
+    std::vector<BlockSchedEntry> fold(P);
+    for (int i = 0; i < P; ++i) std::copy(&t.fold[4 * (size_t)i], &t.fold[4 * (size_t)i] + 4, fold[i].W);
+    out->kind.push_back(kStepFold);
+    out->steps.push_back(fold);
+    out->pcr_stages = t.stages;
+    return true;
+  }
+  // ---- cyclic, P not a power of two: detach / PCR / fold / reattach with 2x2 blocks ----
+  std::vector<double> Lc(4 * (size_t)P), Dc(4 * (size_t)P), Uc(4 * (size_t)P);
+  for (int i = 0; i < P; ++i)
+    for (int e = 0; e < 4; ++e) {
+      Lc[4 * i + e] = pt.Lh[e];
+      Dc[4 * i + e] = pt.Dh[e];
+      Uc[4 * i + e] = pt.Uh[e];
+    }
+  std::vector<std::vector<int>> subs(1);
+  for (int i = 0; i < P; ++i) subs[0].push_back(i);
+  struct Det { int z, y, a; double Lz[4], Dz[4], Uz[4]; };
+  std::vector<std::vector<Det>> levels;
+  auto inv = [&](const double* m, double* o) -> bool {
+    if (!inv2(m, guard, o)) return fail(err, kSingular, "penta_reduced_schedule: pivot guard");
+    return true;
+  };
+  while (subs[0].size() > 1) {
+    const int d = (int)subs[0].size();
+    if (d % 2) {  // detach the last row of every sub-system
+      std::vector<BlockSchedEntry> st(P);
+      std::vector<Det> lv;
+      for (auto& sub : subs) {
+        const int z = sub[d - 1], y = sub[d - 2], a = sub[0];
+        double iz[4], cy[4], ca[4], tmp[4];
+        if (!inv(&Dc[4 * z], iz)) return false;
+        mm2(&Uc[4 * y], iz, cy);  // row y: upper block on z
+        mm2(&Lc[4 * a], iz, ca);  // row a: lower block on z (cyclic wrap)
+        st[y].src[0] = z;
+        std::copy(cy, cy + 4, st[y].C[0]);
+        st[a].src[0] = z;
+        std::copy(ca, ca + 4, st[a].C[0]);
+        Det t;
+        t.z = z, t.y = y, t.a = a;
+        std::copy(&Lc[4 * z], &Lc[4 * z] + 4, t.Lz);
+        std::copy(&Dc[4 * z], &Dc[4 * z] + 4, t.Dz);
+        std::copy(&Uc[4 * z], &Uc[4 * z] + 4, t.Uz);
+        lv.push_back(t);
+        mm2(cy, &Lc[4 * z], tmp);  // y - cy z: z's lower block sits on y, its upper on a
+        sub2(&Dc[4 * y], tmp);
+        double nUy[4];
+        mm2(cy, &Uc[4 * z], nUy);
+        neg2(nUy);
+        mm2(ca, &Uc[4 * z], tmp);  // a - ca z: z's upper block sits on a, its lower on y
+        sub2(&Dc[4 * a], tmp);
+        double nLa[4];
+        mm2(ca, &Lc[4 * z], nLa);
+        neg2(nLa);
+        std::copy(nUy, nUy + 4, &Uc[4 * y]);  // y's next row is now a
+        std::copy(nLa, nLa + 4, &Lc[4 * a]);  // a's previous row is now y
+        sub.pop_back();
+      }
+      levels.push_back(lv);
+      out->kind.push_back(kStepDetach);
+      out->steps.push_back(st);
+      out->detach_stages++;
+      out->detached_rows += (int)lv.size();
+      continue;
+    }
+    // one block PCR step on every (even) sub-system, then split into even / odd positions
+    std::vector<BlockSchedEntry> st(P);
+    std::vector<double> nL = Lc, nD = Dc, nU = Uc;
+    std::vector<std::vector<int>> next;
+    for (auto& sub : subs) {
+      for (int k = 0; k < d; ++k) {
+        const int i = sub[k], pm = sub[(k + d - 1) % d], pn = sub[(k + 1) % d];
+        double im[4], in[4], a[4], g[4], tmp[4];
+        if (!inv(&Dc[4 * pm], im) || !inv(&Dc[4 * pn], in)) return false;
+        mm2(&Lc[4 * i], im, a);
+        mm2(&Uc[4 * i], in, g);
+        if (pm == pn) {
+          st[i].src[0] = pm;
+          for (int e = 0; e < 4; ++e) st[i].C[0][e] = a[e] + g[e];
+        } else {
+          st[i].src[0] = pm;
+          std::copy(a, a + 4, st[i].C[0]);
+          st[i].src[1] = pn;
+          std::copy(g, g + 4, st[i].C[1]);
+        }
+        mm2(a, &Lc[4 * pm], &nL[4 * i]);
+        neg2(&nL[4 * i]);
+        mm2(g, &Uc[4 * pn], &nU[4 * i]);
+        neg2(&nU[4 * i]);
+        std::copy(&Dc[4 * i], &Dc[4 * i] + 4, &nD[4 * i]);
+        mm2(a, &Uc[4 * pm], tmp);
+        sub2(&nD[4 * i], tmp);
+        mm2(g, &Lc[4 * pn], tmp);
+        sub2(&nD[4 * i], tmp);
+      }
+      std::vector<int> ev, od;
+      for (int k = 0; k < d; ++k) (k % 2 ? od : ev).push_back(sub[k]);
+      next.push_back(ev);
+      next.push_back(od);
+    }
+    Lc.swap(nL);
+    Dc.swap(nD);
+    Uc.swap(nU);
+    subs.swap(next);
+    out->kind.push_back(kStepPcr);
+    out->steps.push_back(st);
+    out->pcr_stages++;
+  }
+  // fold the wrapped couplings of the 1x1-block sub-systems (reading R3 in block form)
+  std::vector<BlockSchedEntry> fold(P);
+  for (auto& sub : subs) {
+    const int i = sub[0];
+    double m[4];
+    for (int e = 0; e < 4; ++e) m[e] = Lc[4 * i + e] + Dc[4 * i + e] + Uc[4 * i + e];
+    if (!inv(m, fold[i].W)) return false;
+  }
+  out->kind.push_back(kStepFold);
+  out->steps.push_back(fold);
+  // reattach the detached rows, last level first
+  for (int lvl = (int)levels.size() - 1; lvl >= 0; --lvl) {
+    std::vector<BlockSchedEntry> st(P);
+    for (const Det& t : levels[lvl]) {
+      double iz[4];
+      if (!inv(t.Dz, iz)) return false;
+      std::copy(iz, iz + 4, st[t.z].W);
+      st[t.z].src[0] = t.y;
+      mm2(iz, t.Lz, st[t.z].C[0]);
+      st[t.z].src[1] = t.a;
+      mm2(iz, t.Uz, st[t.z].C[1]);
+    }
+    out->kind.push_back(kStepReattach);
+    out->steps.push_back(st);
+  }
+  return true;
+}
+
 bool reduced_inverse(int P, bool cyclic, const std::vector<double>& L, const std::vector<double>& D,
                      const std::vector<double>& U, double guard, std::vector<double>* inv,
                      FactorError* err) {

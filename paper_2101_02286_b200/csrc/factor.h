@@ -134,6 +134,28 @@ bool penta_block_pcr(int P, bool cyclic, const Penta& pt, double guard, PentaPcr
 bool penta_block_pcr_rows(int P, bool cyclic, std::vector<double> L, std::vector<double> D,
                           std::vector<double> U, double guard, PentaPcr* out, FactorError* err);
 
+// The pentadiagonal reduced system as a step schedule with 2x2 blocks (the block form of
+// reduced_schedule): every step is  v_i <- W v_i - C0 u_src0 - C1 u_src1  with 2x2 W, C0, C1
+// (row-major [4] each; W = I unless stated).  Power-of-two or acyclic P: the block PCR stages
+// of penta_block_pcr (a single partner C0 = alpha + gamma when i - s = i + s) and the fold
+// W = F_i.  Cyclic P not a power of two: the paper's detach / PCR / fold / reattach (P:271,
+// P:294) with 2x2 blocks -- detach: row y <- y - U_y D_z^-1 z, row a <- a - L_a D_z^-1 z;
+// reattach: x_z = D_z^-1 (b_z - L_z x_y - U_z x_a).
+struct BlockSchedEntry {
+  double W[4] = {1.0, 0.0, 0.0, 1.0};
+  int src[2] = {-1, -1};
+  double C[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+};
+struct BlockSchedule {
+  int P = 0;
+  bool cyclic = true;
+  std::vector<int> kind;                            // per step (StepKind)
+  std::vector<std::vector<BlockSchedEntry>> steps;  // [step][row]
+  int pcr_stages = 0, detach_stages = 0, detached_rows = 0;
+};
+bool penta_reduced_schedule(int P, bool cyclic, const Penta& pt, double guard, BlockSchedule* out,
+                            FactorError* err);
+
 inline bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
 inline int ilog2(int64_t v) {
   int q = 0;

@@ -455,11 +455,12 @@ __global__ void __launch_bounds__(kP2PThreads, 1)
 }
 
 // Pentadiagonal (r = 2) reduced phase, pairwise (P:346 with 2x2 blocks, reading R20): the
-// y round sends w = L~ y_i[last two] right, b^_i = c_i - w_{i-1}; then ceil(log2 p) block-PCR
-// steps b^_i <- b^_i - A0 b^_{src0} - A1 b^_{src1} (2x2 matrices from factor.h PentaPcr; a single
-// partner when i - s = i + s), the fold x~_i = F_i b^_i, and the x~ round from the right.
-// Every message is a 2-vector of LL words; R.step[] carries the partners, R.ppcr the matrices
-// ([step][8]: A0 | A1, then the fold [4]).
+// y round sends w = L~ y_i[last two] right, b^_i = c_i - w_{i-1}; then the steps of the block
+// schedule (factor.h penta_reduced_schedule): b^_i <- W b^_i - C0 b^_{src0} - C1 b^_{src1} with
+// 2x2 matrices -- block PCR stages (a single partner when i - s = i + s), the fold W = F_i, and
+// for cyclic non-power-of-two p the detach / reattach steps of P:271 / P:294 -- and the x~ round
+// from the right.  Every message is a 2-vector of LL words; R.step[] carries the partners,
+// R.ppcr the matrices ([step][12]: W | C0 | C1).
 __global__ void __launch_bounds__(kP2PThreads, 1)
     k_reduced_penta_pcr(const P2PArgs A) {
   if (A.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");  // launched early (PDL)
@@ -581,31 +582,21 @@ __global__ void __launch_bounds__(kP2PThreads, 1)
     for (int i = 0; i < kMaxCpt; ++i) u0[i] = u1[i] = v0[i] = v1[i] = 0.0;
     if (S.src0 >= 0) recv2(OFF_S(st, 0, 0), OFF_S(st, 0, 1), u0, u1);
     if (S.src1 >= 0) recv2(OFF_S(st, 1, 0), OFF_S(st, 1, 1), v0, v1);
-    const double* M = R.ppcr + 8 * st;  // A0 (row-major 2x2) | A1
-    const double a00 = M[0], a01 = M[1], a10 = M[2], a11 = M[3];
-    const double g00 = M[4], g01 = M[5], g10 = M[6], g11 = M[7];
+    const double* M = R.ppcr + 12 * st;  // W | C0 | C1 (row-major 2x2)
+    const double w00 = M[0], w01 = M[1], w10 = M[2], w11 = M[3];
+    const double a00 = M[4], a01 = M[5], a10 = M[6], a11 = M[7];
+    const double g00 = M[8], g01 = M[9], g10 = M[10], g11 = M[11];
 #pragma unroll
     for (int i = 0; i < kMaxCpt; ++i)
       if (i < nc) {
-        const double n0 = b0[i] - (a00 * u0[i] + a01 * u1[i]) - (g00 * v0[i] + g01 * v1[i]);
-        const double n1 = b1[i] - (a10 * u0[i] + a11 * u1[i]) - (g10 * v0[i] + g11 * v1[i]);
+        const double n0 = (w00 * b0[i] + w01 * b1[i]) - (a00 * u0[i] + a01 * u1[i]) - (g00 * v0[i] + g01 * v1[i]);
+        const double n1 = (w10 * b0[i] + w11 * b1[i]) - (a10 * u0[i] + a11 * u1[i]) - (g10 * v0[i] + g11 * v1[i]);
         b0[i] = n0;
         b1[i] = n1;
       }
     stamp(kTrStep0 + st);
   }
-  // fold: x~_i = F_i b^_i
-  {
-    const double* F = R.ppcr + 8 * q;
-#pragma unroll
-    for (int i = 0; i < kMaxCpt; ++i)
-      if (i < nc) {
-        const double x0 = F[0] * b0[i] + F[1] * b1[i];
-        const double x1 = F[2] * b0[i] + F[3] * b1[i];
-        b0[i] = x0;
-        b1[i] = x1;
-      }
-  }
+  // (the fold x~_i = F_i b^_i and the reattach steps are steps of the schedule)
   // ---- (a4) x~_i -> left neighbour; x~_{i+1} from the right ----
   if (ok && left >= 0) {
     unsigned long long* dst = R.peer_mbox[left] + copy_off;

@@ -39,7 +39,8 @@ ABI_SYMBOLS = ("ctri_status_string", "ctri_last_error", "ctri_abi_version", "ctr
                "ctri_plan_destroy", "ctri_factor_query", "ctri_pcr_coefficients",
                "ctri_reduced_schedule", "ctri_compact_apply", "ctri_compact_apply_loopback",
                "ctri_reduced_inverse", "ctri_plan_create_penta", "ctri_plan_create_penta_loopback",
-               "ctri_penta_factor_query", "ctri_penta_block_pcr", "ctri_scheme_coef")
+               "ctri_penta_factor_query", "ctri_penta_block_pcr", "ctri_scheme_coef",
+               "ctri_penta_reduced_schedule_apply")
 
 
 class CtriError(RuntimeError):
@@ -135,6 +136,9 @@ def load(build_if_missing: bool = False):
         "ctri_penta_factor_query": (st, [ctypes.c_int64, dp, dp, dp, ctypes.POINTER(ctypes.c_int)]),
         "ctri_penta_block_pcr": (st, [ctypes.c_int, ctypes.c_int, ctypes.c_int64, dp, ctypes.c_int, dp, dp, dp,
                                       ctypes.POINTER(ctypes.c_int)]),
+        "ctri_penta_reduced_schedule_apply": (st, [ctypes.c_int, ctypes.c_int, ctypes.c_int64, dp, dp, dp,
+                                                   ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                                   ctypes.POINTER(ctypes.c_int)]),
         "ctri_compact_apply_loopback": (st, [ctypes.POINTER(P), ctypes.c_int, dp, ctypes.POINTER(P),
                                              ctypes.POINTER(P), P]),
         "ctri_get_stats": (st, [P, ctypes.POINTER(ctri_stats)]),
@@ -299,6 +303,21 @@ def ctri_penta_block_pcr(P: int, n: int, bands, cyclic=True, max_stages=16):
                                        ctypes.byref(q)), "ctri_penta_block_pcr")
     k = q.value
     return a[:k * P * 4].reshape(k, P, 2, 2), g[:k * P * 4].reshape(k, P, 2, 2), f.reshape(P, 2, 2)
+
+
+def ctri_penta_reduced_schedule_apply(P: int, n: int, bands, bhat, cyclic=True):
+    """Host-only: the pentadiagonal reduced system's step schedule (block PCR, or block detach /
+    PCR / fold / reattach) applied to bhat [P, 2]; returns (x~ [P, 2], steps, detach stages,
+    detached rows)."""
+    b = np.ascontiguousarray(bhat, dtype=np.float64).reshape(2 * P)
+    x = np.zeros(2 * P)
+    k, ds, dr = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    dp = ctypes.POINTER(ctypes.c_double)
+    _check(load().ctri_penta_reduced_schedule_apply(int(P), int(bool(cyclic)), int(n), _dbl5(bands),
+                                                    b.ctypes.data_as(dp), x.ctypes.data_as(dp),
+                                                    ctypes.byref(k), ctypes.byref(ds), ctypes.byref(dr)),
+           "ctri_penta_reduced_schedule_apply")
+    return x.reshape(P, 2), k.value, ds.value, dr.value
 
 
 def ctri_solve(plan: int, b, x, stream=None):

@@ -56,7 +56,7 @@ def penta_residual(x, b, sd, bands, cyclic):
     return float(np.max(np.abs(r)) / np.max(np.abs(bc)))
 
 
-@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("cyclic", [True, False])
 @pytest.mark.parametrize("bands", BANDS)
 def test_penta_matches_oracle(p, cyclic, bands):
@@ -65,8 +65,11 @@ def test_penta_matches_oracle(p, cyclic, bands):
     x, st = penta_gpu(b, 0, p, bands, cyclic, return_stats=True)
     ref = oracle.penta_solve(b, 0, bands, cyclic)
     assert st["band_halfwidth"] == 2
-    if p > 1:  # pairwise block PCR where it applies (power-of-two or acyclic), else all-gather
-        assert st["reduced_path"] == (1 if (not cyclic or (p & (p - 1)) == 0) else 2), st
+    if p > 1:  # the pairwise block schedule; cyclic non-power-of-two p: block detach/reattach
+        assert st["reduced_path"] == 1, st
+        if cyclic and p & (p - 1):
+            q = int(math.floor(math.log2(p)))
+            assert st["detached_rows"] == p - 2 ** q and st["detach_stages"] == bin(p).count("1") - 1
     assert rel_err(x, ref, 0) < TOL_REL
     assert penta_residual(x, b, 0, bands, cyclic) < 1e-13
 

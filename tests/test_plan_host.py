@@ -400,6 +400,38 @@ def test_penta_block_pcr_rejects_cyclic_non_pow2():
         pk.ctri_penta_block_pcr(3, 20, PENTA_BANDS[0], True)
 
 
+@pytest.mark.parametrize("bands", PENTA_BANDS)
+@pytest.mark.parametrize("P,cyclic", [(3, True), (5, True), (6, True), (7, True), (11, True), (2, True),
+                                      (4, True), (8, True), (3, False), (6, False)])
+def test_penta_reduced_schedule_vs_dense(bands, P, cyclic):
+    """The block step schedule of the pentadiagonal reduced system -- block PCR, or for cyclic
+    non-power-of-two P the paper's detach / PCR / fold / reattach with 2x2
+    blocks -- equals the dense solve of the block matrix [L^, D^, U^]; its detach counts follow
+    P:346 (P - 2^floor(log2 P) rows, popcount(P) - 1 stages)."""
+    for n in (8, 40):
+        t = pk.ctri_penta_factor_query(n, bands)
+        A = np.zeros((2 * P, 2 * P))
+        for i in range(P):
+            A[2 * i:2 * i + 2, 2 * i:2 * i + 2] += t["Dh"] if (cyclic or i > 0) else t["Dh_first"]
+            if cyclic or i > 0:
+                j = (i - 1) % P
+                A[2 * i:2 * i + 2, 2 * j:2 * j + 2] += t["Lh"]
+            if cyclic or i < P - 1:
+                j = (i + 1) % P
+                A[2 * i:2 * i + 2, 2 * j:2 * j + 2] += t["Uh"]
+        rng = np.random.default_rng(3 * P + n)
+        for _ in range(2):
+            b = rng.uniform(-1, 1, (P, 2))
+            x, steps, ds, dr = pk.ctri_penta_reduced_schedule_apply(P, n, bands, b, cyclic)
+            assert np.max(np.abs(x.ravel() - np.linalg.solve(A, b.ravel()))) < 1e-13
+        if cyclic and P & (P - 1):
+            q = int(math.floor(math.log2(P)))
+            assert dr == P - 2 ** q and ds == bin(P).count("1") - 1
+            assert steps == q + 1 + 2 * ds  # PCR stages, fold, detach and reattach levels
+        else:
+            assert ds == 0 and dr == 0 and steps == math.ceil(math.log2(P)) + 1
+
+
 def test_scheme_coefficients_from_library():
     """ctri_scheme_coef (the binding only marshals): the collocated pair a = 14/9, b = 1/9 at
     alpha = 1/3 (R8) and the staggered schemes of P:202-206 (R18), against the oracle's
