@@ -178,10 +178,14 @@ ctri_status ctri_plan_create_loopback(ctri_plan* plans, int nparts, const int64_
  * 2x2").  bands = {e, l, d, u, f} = A[i,i-2], A[i,i-1], A[i,i], A[i,i+1],
  * A[i,i+2] (host array, copied); cyclic wraps the four corner couplings.  Each of the nparts
  * slabs keeps two interface rows (local rows 0, 1) and n - 2 >= 4 interior rows; the 2x2-block
- * reduced system is solved over the P2P mailboxes by pairwise 2x2-block PCR (P:346 with
- * 2x2 blocks, R20: a y round, ceil(log2 nparts) block steps, the fold, an x~ round)
- * or, with CTRI_FLAG_ALLGATHER, by ONE all-gather round and plan-time rows of its inverse
- * (nparts <= 8).  The plan is used with ctri_solve / ctri_solve_loopback / ctri_solve_host /
+ * reduced system is solved over the P2P mailboxes by its 2x2-block step schedule (P:346 with
+ * 2x2 blocks, R20: a y round, the block PCR steps -- with block detach / reattach
+ * for cyclic non-power-of-two nparts, P:271 / P:294 -- the fold, an x~ round) or, with
+ * CTRI_FLAG_ALLGATHER, by ONE all-gather round and plan-time rows of its inverse (nparts <= 8).
+ * The local solve runs on chip (2x2-block PCR of 32-row chunk heads in thread-block clusters)
+ * for strided slabs of 256..2048 rows, and with nparts == 1 for longer slabs as n/1024
+ * partitions of one GPU; column-serial otherwise (contiguous axis, other sizes).
+ * The plan is used with ctri_solve / ctri_solve_loopback / ctri_solve_host /
  * ctri_get_stats / ctri_plan_destroy like a tridiagonal one.  Errors: INVALID_ARG (as
  * ctri_plan_create), PARTITION_TOO_SMALL (n < 6 or N % nparts), UNSUPPORTED (nparts > 8,
  * CTRI_FLAG_NCCL_ROUNDS, CTRI_FLAG_DERIV or CTRI_FLAG_GENERIC_LOCAL), SINGULAR (pivot guard
