@@ -99,12 +99,18 @@ __global__ void __launch_bounds__(NT, MINB)
   // VC (per owned column, C/G of them): [2 groups][8] c_v and y_v[last] planes, [2 groups][9]
   // x~ (row vp: x~ past the last partition); [2][2W+1] S, R of the window rows in block order
   // (rows 0..W, then nv-W..nv-1)
+  const int vc_cpo = C / A.G;  // owned columns per CTA
   double* vc_c = f_stash;
-  double* vc_yl = vc_c + 2 * 8 * C;
-  double* vc_xt = vc_yl + 2 * 8 * C;
-  double* vc_sr = vc_xt + 2 * 9 * C;
+  double* vc_yl = vc_c + 2 * 8 * vc_cpo;
+  double* vc_xt = vc_yl + 2 * 8 * vc_cpo;
+  double* vc_sr = vc_xt + 2 * 9 * vc_cpo;
   double* vc_pcr = vc_sr + 2 * (VC ? 2 * A.vc_W + 1 : 0);  // [72] PCR multipliers, vp-row system
-  double* vc_buf = vc_pcr + 72;  // [2][3][NT] window rows in flight (cp.async, double-buffered)
+  // [4 groups][2]: outer index and column tile of the last column groups (written once per
+  // group by thread 0, so no thread divides on the tile path)
+  int* vc_gtab = reinterpret_cast<int*>(vc_pcr + 72);
+  // [2][kVcFin][NT] pairs of window values in flight (16-byte cp.async, double-buffered)
+  double* vc_buf = reinterpret_cast<double*>(
+      smem_raw + ((reinterpret_cast<unsigned char*>(vc_gtab + 8) - smem_raw + 15) & ~(ptrdiff_t)15));
 
   const int tid = threadIdx.x;
   // strided axis: lanes run over the C columns of a tile row (coalesced rows);
@@ -412,26 +418,30 @@ __global__ void __launch_bounds__(NT, MINB)
     }
   };
   const bool vc_solver = VC && (tid / 32) < (cpo * vcp + 31) / 32;  // whole warps (shuffles)
-  // window element i of this thread: block row tid / cpo + i * (NT / cpo), owned column tid % cpo
-  constexpr int kVcFin = 3;  // host: (2W + 1) * C / G <= 3 NT
-  const int vc_jl = tid % cpo;
-  const int vc_r0 = tid / cpo, vc_rs = NT / cpo;
-  auto vc_block = [&](int gi, int q) -> double* {  // (row 0, this thread's column) of a block
-    const int64_t colp = (int64_t)vc_ct(gi) * C + (int64_t)g * cpo + vc_jl;
-    if (colp >= A.lay.inner) return nullptr;
-    return A.x + ((int64_t)(vc_og(gi) * vcp + q) * vc_nv) * A.lay.inner + colp;
+  // window element i of this thread: block row tid / (cpo/2) + i * (NT / (cpo/2)), the pair of
+  // owned columns 2 (tid % (cpo/2)) and the next: 16-byte copies, loads and stores
+  constexpr int kVcFin = 2;  // host: (2W + 1) * C / G / 2 <= 2 NT
+  const int vc_hp = cpo / 2;
+  const int vc_jl = 2 * (tid % vc_hp);
+  const int vc_r0 = tid / vc_hp, vc_rs = NT / vc_hp;
+  auto gt_og = [&](int gi) { return vc_gtab[2 * (gi & 3)]; };
+  auto gt_ct = [&](int gi) { return vc_gtab[2 * (gi & 3) + 1]; };
+  auto vc_block = [&](int gi, int q) -> double* {  // (row 0, this thread's column pair) of a block
+    const int64_t colp = (int64_t)gt_ct(gi) * C + (int64_t)g * cpo + vc_jl;
+    if (colp >= A.lay.inner) return nullptr;  // (inner is even: the pair is whole or absent)
+    return A.x + ((int64_t)(gt_og(gi) * vcp + q) * vc_nv) * A.lay.inner + colp;
   };
   auto vc_row = [&](int ri) { return ri <= vc_W ? ri : vc_nv - vc_R2 + ri; };
   // y of the window rows (stored >= vp tiles earlier by the holder CTAs) -> this thread's
   // vc_buf slots by cp.async (L2 only), so nothing is held in registers meanwhile
   auto vc_load = [&](const double* blk, int bf) {
     if (blk) {
-      double* bb = vc_buf + bf * kVcFin * NT;
+      double* bb = vc_buf + bf * kVcFin * 2 * NT;
 #pragma unroll
       for (int i = 0; i < kVcFin; ++i) {
         const int ri = vc_r0 + i * vc_rs;
         if (ri < vc_R2 && ri != 0)
-          dev::cp_async_8(dev::smem_u32(bb + i * NT + tid), blk + (int64_t)vc_row(ri) * A.lay.inner);
+          dev::cp_async_16(dev::smem_u32(bb + 2 * (i * NT + tid)), blk + (int64_t)vc_row(ri) * A.lay.inner);
       }
     }
     dev::cp_async_commit();
@@ -442,21 +452,25 @@ __global__ void __launch_bounds__(NT, MINB)
   // reduced system across the GPUs)
   auto vc_store = [&](double* blk, int gp, int q, int bf) {
     if (!blk) return;
-    const double* bb = vc_buf + bf * kVcFin * NT;
+    const double* bb = vc_buf + bf * kVcFin * 2 * NT;
     const double* xt = vc_xt + (gp & 1) * 9 * cpo;
-    const double xa = xt[q * cpo + vc_jl], xb = xt[(q + 1) * cpo + vc_jl];
+    const double2 xa = *reinterpret_cast<const double2*>(xt + q * cpo + vc_jl);
+    const double2 xb = *reinterpret_cast<const double2*>(xt + (q + 1) * cpo + vc_jl);
 #pragma unroll
     for (int i = 0; i < kVcFin; ++i) {
       const int ri = vc_r0 + i * vc_rs;
       if (ri >= vc_R2) break;
-      const double xv = ri == 0 ? xa : bb[i * NT + tid] - vc_sr[ri] * xa - vc_sr[vc_R2 + ri] * xb;
+      const double s = vc_sr[ri], r = vc_sr[vc_R2 + ri];
+      const double2 y = *reinterpret_cast<const double2*>(bb + 2 * (i * NT + tid));
+      const double x0 = ri == 0 ? xa.x : y.x - s * xa.x - r * xb.x;
+      const double x1 = ri == 0 ? xa.y : y.y - s * xa.y - r * xb.y;
       if (A.vc_slab) {
         if (q == 0 && ri == 0) continue;
-        const int64_t pj = (int64_t)vc_og(gp) * A.lay.inner + (int64_t)vc_ct(gp) * C + (int64_t)g * cpo + vc_jl;
-        if (q == 0 && ri == 1) A.plane_yf[pj] = xv;
-        if (q == vcp - 1 && ri == vc_R2 - 1) A.plane_yl[pj] = xv;
+        const int64_t pj = (int64_t)gt_og(gp) * A.lay.inner + (int64_t)gt_ct(gp) * C + (int64_t)g * cpo + vc_jl;
+        if (q == 0 && ri == 1) { A.plane_yf[pj] = x0; A.plane_yf[pj + 1] = x1; }
+        if (q == vcp - 1 && ri == vc_R2 - 1) { A.plane_yl[pj] = x0; A.plane_yl[pj + 1] = x1; }
       }
-      dev::st_global_cs(blk + (int64_t)vc_row(ri) * A.lay.inner, xv);
+      dev::st_global_cs_v2(blk + (int64_t)vc_row(ri) * A.lay.inner, x0, x1);
     }
   };
   // the window block finalised at tile itx: that of tile itx - vp - 1 (partition q - 1 of the
@@ -469,12 +483,14 @@ __global__ void __launch_bounds__(NT, MINB)
 
   for (;; ++it) {
     int64_t t;
-    int vog = 0, vct = 0;  // VC: this group's outer index and column tile
+    int vog = 0, vct = 0;  // VC: this group's outer index and column tile (after the barrier)
     if (VC) {
       if (!vc_has(vgi)) break;
-      vog = vc_og(vgi);
-      vct = vc_ct(vgi);
-      t = ((int64_t)vog * vcp + vq) * A.tiles_per_outer + vct;
+      if (tid == 0 && vq == 0) {  // a new column group: its position into the table
+        vc_gtab[2 * (vgi & 3)] = vc_og(vgi);
+        vc_gtab[2 * (vgi & 3) + 1] = vc_ct(vgi);
+      }
+      t = 0;  // (VC addresses the tile through vog, vct)
     } else {
       t = tile_at(it);
       if (t < 0) break;
@@ -485,9 +501,6 @@ __global__ void __launch_bounds__(NT, MINB)
     if (FUSED && (f_top || f_bot) && it > 0) f_prefetch(t - ncl);
     const int64_t seq = (int64_t)it * SUB + hsub;
     const int s = (int)(seq % SLOTS);
-    // global column: strided axis (o, col) with col < inner; contiguous axis column = o
-    const int64_t o = CONTIG ? t * C + j : (VC ? (int64_t)vog * vcp + vq : t / A.tiles_per_outer);
-    const int64_t col = CONTIG ? 0 : (VC ? (int64_t)vct * C : (t - o * A.tiles_per_outer) * C) + j;
     if (tid == 0 && A.mode != 3) {  // arm this tile's exchange barriers (remote bytes may race ahead)
       dev::mbar_expect_tx(dev::smem_u32(mbar_ex), (uint32_t)NT * 3u * 8u);
       dev::mbar_expect_tx(dev::smem_u32(mbar_rx), (uint32_t)NT * 2u * 8u);
@@ -558,12 +571,19 @@ __global__ void __launch_bounds__(NT, MINB)
       if (t + ncl < A.num_tiles) issue_contig(t + ncl);
     } else if (tid == 0) {
       if (VC) {  // the next tile: next partition of this group, or partition 0 of the next group
-        if (vq + 1 < vcp) issue(it + 1, (int64_t)vog * vcp + vq + 1, (int64_t)vct * C);
+        if (vq + 1 < vcp) issue(it + 1, (int64_t)gt_og(vgi) * vcp + vq + 1, (int64_t)gt_ct(vgi) * C);
         else issue(it + 1, vc_has(vgi + 1) ? (int64_t)vc_og(vgi + 1) * vcp : -1, (int64_t)vc_ct(vgi + 1) * C);
       } else {
         for (int hh = 0; hh < SUB; ++hh) issue((int64_t)it * SUB + hh + SLOTS);  // freed slots
       }
     }
+    if (VC) {
+      vog = gt_og(vgi);
+      vct = gt_ct(vgi);
+    }
+    // global column: strided axis (o, col) with col < inner; contiguous axis column = o
+    const int64_t o = CONTIG ? t * C + j : (VC ? (int64_t)vog * vcp + vq : t / A.tiles_per_outer);
+    const int64_t col = CONTIG ? 0 : (VC ? (int64_t)vct * C : (t - o * A.tiles_per_outer) * C) + j;
     const bool valid = CONTIG ? (o < A.lay.outer) : (col < A.lay.inner);
     auto store_chunk = [&]() {
       if (!valid) return;
@@ -1101,11 +1121,12 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
   if (!V.contig && V.SUB == 1 && (vi == 0 || vi == 4 || vi == 13 || vi == 17 || vi == 18) && P.vp > 1 &&
       P.vp <= 8 && G >= 2 && P.vwindow > 0 && !(P.flags & CTRI_FLAG_FULL_BACKSUB) &&
       !(P.flags & (CTRI_FLAG_NCCL_ROUNDS | CTRI_FLAG_ALLGATHER | CTRI_FLAG_FUSED_REDUCED)) &&
-      (2 * P.vwindow + 1) * (V.C / G) <= 3 * V.NT && P.vwindow + 1 <= rows_cta && 2 * P.vwindow + 1 < L.n &&
+      (V.C / G) % 2 == 0 && (2 * P.vwindow + 1) * (V.C / G / 2) <= 2 * V.NT && P.vwindow + 1 <= rows_cta &&
+      2 * P.vwindow + 1 < L.n &&
       L.outer * ((L.inner + V.C - 1) / V.C) < ((int64_t)1 << 31)) {  // 32-bit group arithmetic
     tc.smem_vc = tc.smem_bytes + 128 +
-                 (int)(sizeof(double) * ((2 * 8 + 2 * 8 + 2 * 9) * (size_t)V.C + 2 * (2 * (size_t)P.vwindow + 1) +
-                                         72 + 6 * (size_t)V.NT));
+                 (int)(sizeof(double) * ((2 * 8 + 2 * 8 + 2 * 9) * (size_t)(V.C / G) + 2 * (2 * (size_t)P.vwindow + 1) +
+                                         72 + 6 + 8 * (size_t)V.NT));
     std::string w2;
     std::swap(w2, *why);
     tc.vc_ok = setup(4, tc.smem_vc, &tc.grid_vc);
