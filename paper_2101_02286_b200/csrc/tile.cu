@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(NT, MINB)
   // [2][kVcFin][NT] pairs of window values in flight (16-byte cp.async, double-buffered)
   double* vc_buf = reinterpret_cast<double*>(
       smem_raw + ((reinterpret_cast<unsigned char*>(vc_gtab + 8) - smem_raw + 15) & ~(ptrdiff_t)15));
+  double** vc_bptr = reinterpret_cast<double**>(vc_buf + 8 * NT);  // [NT]: the block in flight
 
   const int tid = threadIdx.x;
   // strided axis: lanes run over the C columns of a tile row (coalesced rows);
@@ -432,6 +433,13 @@ __global__ void __launch_bounds__(NT, MINB)
     return A.x + ((int64_t)(gt_og(gi) * vcp + q) * vc_nv) * A.lay.inner + colp;
   };
   auto vc_row = [&](int ri) { return ri <= vc_W ? ri : vc_nv - vc_R2 + ri; };
+  // this thread's window rows as element offsets (host: nv * inner < 2^31)
+  int vc_off[kVcFin];
+#pragma unroll
+  for (int i = 0; i < kVcFin; ++i) {
+    const int ri = vc_r0 + i * vc_rs;
+    vc_off[i] = ri < vc_R2 ? vc_row(ri) * (int)A.lay.inner : 0;
+  }
   // y of the window rows (stored >= vp tiles earlier by the holder CTAs) -> this thread's
   // vc_buf slots by cp.async (L2 only), so nothing is held in registers meanwhile
   auto vc_load = [&](const double* blk, int bf) {
@@ -441,7 +449,7 @@ __global__ void __launch_bounds__(NT, MINB)
       for (int i = 0; i < kVcFin; ++i) {
         const int ri = vc_r0 + i * vc_rs;
         if (ri < vc_R2 && ri != 0)
-          dev::cp_async_16(dev::smem_u32(bb + 2 * (i * NT + tid)), blk + (int64_t)vc_row(ri) * A.lay.inner);
+          dev::cp_async_16(dev::smem_u32(bb + 2 * (i * NT + tid)), blk + vc_off[i]);
       }
     }
     dev::cp_async_commit();
@@ -470,7 +478,7 @@ __global__ void __launch_bounds__(NT, MINB)
         if (q == 0 && ri == 1) { A.plane_yf[pj] = x0; A.plane_yf[pj + 1] = x1; }
         if (q == vcp - 1 && ri == vc_R2 - 1) { A.plane_yl[pj] = x0; A.plane_yl[pj + 1] = x1; }
       }
-      dev::st_global_cs_v2(blk + (int64_t)vc_row(ri) * A.lay.inner, x0, x1);
+      dev::st_global_cs_v2(blk + vc_off[i], x0, x1);
     }
   };
   // the window block finalised at tile itx: that of tile itx - vp - 1 (partition q - 1 of the
@@ -661,14 +669,22 @@ __global__ void __launch_bounds__(NT, MINB)
       }
       int fg, fq;
       dev::cp_async_wait_all();  // this thread's window rows of this tile's target (loaded a tile ago)
-      if (vc_target(vc_gi, vc_q, &fg, &fq)) vc_store(vc_block(fg, fq), fg, fq, it & 1);
+      if (vc_target(vc_gi, vc_q, &fg, &fq)) vc_store(vc_bptr[tid], fg, fq, it & 1);
       // start loading the next tile's target (stored >= vp tiles ago and acquired since)
       const int nq = vc_q + 1 < vcp ? vc_q + 1 : 0, ngi = vc_q + 1 < vcp ? vc_gi : vc_gi + 1;
-      if (vc_target(ngi, nq, &fg, &fq)) vc_load(vc_block(fg, fq), (it + 1) & 1);
+      if (vc_target(ngi, nq, &fg, &fq)) {
+        double* blk = vc_block(fg, fq);
+        vc_bptr[tid] = blk;  // (this thread's own slot: read back by it one tile later)
+        vc_load(blk, (it + 1) & 1);
+      }
     }
     // ---- owner: head system b^_c (Eq. bi_hat at chunk level), then PCR stages ----
     {
-      if (VC) dev::mbar_wait_acq_cluster(dev::smem_u32(mbar_ex), (uint32_t)it & 1u);
+      // VC: an acquire at cluster scope once per column group suffices -- the window rows read
+      // at tile it were stored at tile it - vp - 1 and released by the holders' head stores
+      // of every later tile, and a group's first tile lies within the last vp tiles (the
+      // acquire also invalidates L1: CCTL.IVALL in SASS, so not on every tile)
+      if (VC && vq == 0) dev::mbar_wait_acq_cluster(dev::smem_u32(mbar_ex), (uint32_t)it & 1u);
       else dev::mbar_wait(dev::smem_u32(mbar_ex), (uint32_t)it & 1u);
       stamp(it, 3);
       const double lt = (A.mode == 2 && oc == 0) ? 0.0 : T.l * ex_yl[prev_row];  // acyclic top
@@ -765,7 +781,7 @@ __global__ void __launch_bounds__(NT, MINB)
     dev::cp_async_wait_all();
     int fg, fq;
     if (vc_target(vgi, 0, &fg, &fq))  // loaded by the last tile (into buffer it & 1)
-      vc_store(vc_block(fg, fq), fg, fq, it & 1);
+      vc_store(vc_bptr[tid], fg, fq, it & 1);
     if (vc_solver) {
       const int par = gl & 1;
       dev::mbar_wait(dev::smem_u32(mbar_red + par), (uint32_t)((gl >> 1) & 1));
@@ -1123,10 +1139,11 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
       !(P.flags & (CTRI_FLAG_NCCL_ROUNDS | CTRI_FLAG_ALLGATHER | CTRI_FLAG_FUSED_REDUCED)) &&
       (V.C / G) % 2 == 0 && (2 * P.vwindow + 1) * (V.C / G / 2) <= 2 * V.NT && P.vwindow + 1 <= rows_cta &&
       2 * P.vwindow + 1 < L.n &&
-      L.outer * ((L.inner + V.C - 1) / V.C) < ((int64_t)1 << 31)) {  // 32-bit group arithmetic
+      L.outer * ((L.inner + V.C - 1) / V.C) < ((int64_t)1 << 31) &&  // 32-bit group arithmetic
+      L.n * L.inner < ((int64_t)1 << 31)) {                           // 32-bit row offsets
     tc.smem_vc = tc.smem_bytes + 128 +
                  (int)(sizeof(double) * ((2 * 8 + 2 * 8 + 2 * 9) * (size_t)(V.C / G) + 2 * (2 * (size_t)P.vwindow + 1) +
-                                         72 + 6 + 8 * (size_t)V.NT));
+                                         72 + 6 + 9 * (size_t)V.NT));
     std::string w2;
     std::swap(w2, *why);
     tc.vc_ok = setup(4, tc.smem_vc, &tc.grid_vc);
