@@ -109,6 +109,24 @@ def main():
     plan.close()
     if rank == 0:
         results["penta"] = {"err": rel_err(x.cpu().numpy(), oracle.penta_solve(b, 0, pb, True), 0)}
+    # pentadiagonal with the on-chip local solve (1024-row slabs) and the 2x2-block schedule
+    # (block detach / reattach at 3 GPUs), Lele's tenth-order LHS
+    pb2 = (1 / 20, 1 / 2, 1.0, 1 / 2, 1 / 20)
+    pdims = (1024 * world, 1, 64)
+    b = workloads.uniform(pdims, 96)
+    plan = pdist.plan_from_process_group(pdims, 0, pb2, True)
+    bl = torch.from_numpy(workloads.slab(b, 0, world, rank)).to(dev)
+    xl = torch.empty_like(bl)
+    plan.solve(bl, xl)
+    torch.cuda.synchronize()
+    st = plan.stats()
+    x = pdist.gather_to_rank0(xl, 0)
+    plan.close()
+    if rank == 0:
+        results["penta_chip"] = {"err": rel_err(x.cpu().numpy(), oracle.penta_solve(b, 0, pb2, True), 0),
+                                 "kernel": st["local_kernel"], "path": st["reduced_path"],
+                                 "detached": st["detached_rows"]}
+        assert st["local_kernel"] == 4 and st["reduced_path"] == 1, st
     # staggered sixth-order interpolation through ctri_compact_apply
     from paper_2101_02286_b200 import ctri
     plan = pdist.plan_from_process_group(dims, 0, ctri.staggered_interp_bands(), True, flags=CTRI_FLAG_DERIV)
