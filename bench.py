@@ -468,6 +468,9 @@ def main():
                 "launch_us_isolated": t_local_iso,
                 "launch_us_source": t_src,
                 "frac_nominal_8tbs": achieved / 8000.0,
+                # context: the strided access pattern's own copy ceiling on B200 (6.0 TB/s with
+                # every pipeline, profiles/r2_copy_ceiling_pattern.log; index-0/1 configs)
+                "frac_of_pattern_copy_ceiling": achieved / 6000.0,
                 "peak_source": peak_src}
         cpu = None if args.no_cpu_baseline else cpu_oracle_sample(args.config)
         launches = st["launches_per_solve"] * args.steps + (args.steps * 0)

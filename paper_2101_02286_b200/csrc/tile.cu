@@ -1253,8 +1253,11 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
     A.trace = d_tr;
     A.trace_cta = std::atoi(std::getenv("CTRI_TILE_TRACE"));  // which CTA stamps (0 if not a number)
   }
-  A.vc_dbg = 0;
-  if (const char* e = std::getenv("CTRI_VC_DBG")) A.vc_dbg = std::atoi(e);  // experiment knob
+  static const int vc_dbg = [] {  // experiment knob, read once per process
+    const char* e = std::getenv("CTRI_VC_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  A.vc_dbg = vc_dbg;
   A.pcr_alpha = tc.d_pcr;
   A.pcr_gamma = tc.d_pcr + (size_t)tc.pcr.stages * tc.Q;
   A.pcr_inv = tc.d_pcr + (size_t)2 * tc.pcr.stages * tc.Q;
