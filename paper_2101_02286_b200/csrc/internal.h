@@ -101,7 +101,8 @@ struct TileArgs {
   unsigned long long* trace;  // measurement only (CTRI_TILE_TRACE=<cta>)
   int trace_cta;              // the CTA whose tiles are stamped
   int vc_dbg;                 // experiment knob CTRI_VC_DBG (bit 0: no window finalisation,
-                              // bit 1: window rows stored evict-first like the rest)
+                              // bit 1: window rows stored evict-first like the rest; bits 2, 3:
+                              // finalisation without its stores / loads -- wrong results, timing only)
   // fused reduced phase (LAYOUT 3, nparts > 1): the window rows of every tile stay
   // in shared memory while the tile's (c = b~ - u y_D[1], y_D[n-1]) go to every rank's mailbox
   // as LL words; one tile later x~_i, x~_{i+1} = rows i, i+1 of A^{-1} applied to the gathered

@@ -38,6 +38,14 @@
 
 namespace ctri {
 
+// CTRI_VC_DBG experiment bits of the virtual-partition chain (timing studies only: they break
+// results) are compiled in only with -DCTRI_VC_EXPERIMENTS
+#ifdef CTRI_VC_EXPERIMENTS
+constexpr bool kVcExperiments = true;
+#else
+constexpr bool kVcExperiments = false;
+#endif
+
 template <int K, int C, int NT, int SUB, int SLOTS, int MINB, int LAYOUT>
 __global__ void __launch_bounds__(NT, MINB)
     k_tile(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap hmap,
@@ -51,7 +59,8 @@ __global__ void __launch_bounds__(NT, MINB)
   constexpr bool FUSED = (LAYOUT == 3);
   // LAYOUT 4: nparts == 1 with vp virtual partitions: the cluster walks the vp partitions of a
   // column group back to back and finishes (a2)-(a4) on chip (TileArgs vc_*)
-  constexpr bool VC = (LAYOUT == 4);
+  constexpr bool VC = (LAYOUT == 4 || LAYOUT == 5);
+  constexpr bool VC_SLAB = (LAYOUT == 5);  // two levels (nparts > 1): slab row 0 is the GPU interface
   constexpr int HALO = DERIV ? 2 : 0;     // stencil half-width (rows)
   static_assert(K >= 4 && NT % C == 0 && (C == 4 || C == 8 || C == 16 || C == 32 || C == 64), "tile geometry");
   static_assert(!CONTIG || (NT / C == 32 && SUB == 1 && SLOTS == 1), "contiguous: 32 chunks/CTA");
@@ -402,7 +411,7 @@ __global__ void __launch_bounds__(NT, MINB)
     const bool act = jl < cpo;
     const int vl = v == 0 ? vcp - 1 : v - 1;
     double bh = 0.0;
-    if (act && !(A.vc_slab && v == 0)) {  // two levels: row 0 (the GPU interface) is decoupled
+    if (act && !(VC_SLAB && v == 0)) {  // two levels: row 0 (the GPU interface) is decoupled
       const double ylp = (v > 0 || A.vc_cyclic) ? vc_yl[(par * 8 + vl) * cpo + jl] : 0.0;
       bh = vc_c[(par * 8 + v) * cpo + jl] - T.l * ylp;
     }
@@ -448,7 +457,7 @@ __global__ void __launch_bounds__(NT, MINB)
 #pragma unroll
       for (int i = 0; i < kVcFin; ++i) {
         const int ri = vc_r0 + i * vc_rs;
-        if (ri < vc_R2 && ri != 0)
+        if (ri < vc_R2 && ri != 0 && !(kVcExperiments && (A.vc_dbg & 8)))
           dev::cp_async_16(dev::smem_u32(bb + 2 * (i * NT + tid)), blk + vc_off[i]);
       }
     }
@@ -472,13 +481,13 @@ __global__ void __launch_bounds__(NT, MINB)
       const double2 y = *reinterpret_cast<const double2*>(bb + 2 * (i * NT + tid));
       const double x0 = ri == 0 ? xa.x : y.x - s * xa.x - r * xb.x;
       const double x1 = ri == 0 ? xa.y : y.y - s * xa.y - r * xb.y;
-      if (A.vc_slab) {
+      if (VC_SLAB) {
         if (q == 0 && ri == 0) continue;
         const int64_t pj = (int64_t)gt_og(gp) * A.lay.inner + (int64_t)gt_ct(gp) * C + (int64_t)g * cpo + vc_jl;
         if (q == 0 && ri == 1) { A.plane_yf[pj] = x0; A.plane_yf[pj + 1] = x1; }
         if (q == vcp - 1 && ri == vc_R2 - 1) { A.plane_yl[pj] = x0; A.plane_yl[pj + 1] = x1; }
       }
-      dev::st_global_cs_v2(blk + vc_off[i], x0, x1);
+      if (!(kVcExperiments && (A.vc_dbg & 4))) dev::st_global_cs_v2(blk + vc_off[i], x0, x1);
     }
   };
   // the window block finalised at tile itx: that of tile itx - vp - 1 (partition q - 1 of the
@@ -486,7 +495,7 @@ __global__ void __launch_bounds__(NT, MINB)
   auto vc_target = [&](int gi, int q, int* fg, int* fq) -> bool {
     *fq = q >= 1 ? q - 1 : vcp - 1;
     *fg = q >= 1 ? gi - 1 : gi - 2;
-    return *fg >= 0 && !(A.vc_dbg & 1);
+    return *fg >= 0 && !(kVcExperiments && (A.vc_dbg & 1));
   };
 
   for (;; ++it) {
@@ -601,7 +610,7 @@ __global__ void __launch_bounds__(NT, MINB)
         const uint64_t pol_last = dev::policy_evict_last();
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          if ((k <= vc_wt || k >= vc_wb) && !(A.vc_dbg & 2)) {
+          if ((k <= vc_wt || k >= vc_wb) && !(kVcExperiments && (A.vc_dbg & 2))) {
             if (c != 0 || k != 0) dev::st_global_hint(xp + (int64_t)k * A.lay.inner, v[k], pol_last);
           } else {
             dev::st_global_cs(xp + (int64_t)k * A.lay.inner, v[k]);
@@ -746,7 +755,7 @@ __global__ void __launch_bounds__(NT, MINB)
       if (c == 0) {  // c_v = b~_v - u y_v[first]
         dev::st_async_f64(dev::mapa(dev::smem_u32(vc_c + e), owner), btv - T.u * v[1],
                           dev::mapa(dev::smem_u32(mbar_red + par), owner));
-        if (A.vc_slab && vc_q == 0 && valid) A.plane_bt[(int64_t)vog * A.lay.inner + col] = btv;  // b~_i
+        if (VC_SLAB && vc_q == 0 && valid) A.plane_bt[(int64_t)vog * A.lay.inner + col] = btv;  // b~_i
       }
       if (c == Q - 1)
         dev::st_async_f64(dev::mapa(dev::smem_u32(vc_yl + e), owner), v[K - 1],
@@ -788,7 +797,7 @@ __global__ void __launch_bounds__(NT, MINB)
       vc_solve(par);
     }
     __syncthreads();
-    if (!(A.vc_dbg & 1))
+    if (!(kVcExperiments && (A.vc_dbg & 1)))
       for (int q = 0; q < vcp; ++q) {
         double* blk = vc_block(gl, q);
         vc_load(blk, 0);
@@ -875,9 +884,9 @@ static cudaError_t launch_one(const TileConfig& tc, const CUtensorMap& map, cons
   TileConsts<K> T;
   fill_consts<K>(tc, &T);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(LY == 2 ? tc.grid_deriv : LY == 3 ? tc.grid_fused : LY == 4 ? tc.grid_vc : tc.grid, 1, 1);
+  cfg.gridDim = dim3(LY == 2 ? tc.grid_deriv : LY == 3 ? tc.grid_fused : LY >= 4 ? tc.grid_vc : tc.grid, 1, 1);
   cfg.blockDim = dim3(NT, 1, 1);
-  cfg.dynamicSmemBytes = LY == 2 ? tc.smem_deriv : LY == 3 ? tc.smem_fused : LY == 4 ? tc.smem_vc : tc.smem_bytes;
+  cfg.dynamicSmemBytes = LY == 2 ? tc.smem_deriv : LY == 3 ? tc.smem_fused : LY >= 4 ? tc.smem_vc : tc.smem_bytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -922,6 +931,13 @@ static cudaError_t dispatch(const TileConfig& tc, int kind, const CUtensorMap& m
       case 13: CTRI_V(32, 256, 1, 1, 2, 4);
       case 17: CTRI_V(64, 256, 1, 1, 2, 4);
       case 18: CTRI_V(64, 512, 1, 1, 1, 4);
+    }
+    return cudaErrorInvalidValue;
+  }
+  if (kind == 5) {  // the chain with two levels (nparts > 1, opt-in)
+    switch (tc.variant) {
+      case 4: CTRI_V(16, 256, 1, 1, 2, 5);
+      case 13: CTRI_V(32, 256, 1, 1, 2, 5);
     }
     return cudaErrorInvalidValue;
   }
@@ -1135,6 +1151,7 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
   // finaliser's per-thread register budget (W + 1 <= 6 chunks per CTA)
   tc.vc_ok = false;
   if (!V.contig && V.SUB == 1 && (vi == 0 || vi == 4 || vi == 13 || vi == 17 || vi == 18) && P.vp > 1 &&
+      (P.p == 1 || vi == 4 || vi == 13) &&
       P.vp <= 8 && G >= 2 && P.vwindow > 0 && !(P.flags & CTRI_FLAG_FULL_BACKSUB) &&
       !(P.flags & (CTRI_FLAG_NCCL_ROUNDS | CTRI_FLAG_ALLGATHER | CTRI_FLAG_FUSED_REDUCED)) &&
       (V.C / G) % 2 == 0 && (2 * P.vwindow + 1) * (V.C / G / 2) <= 2 * V.NT && P.vwindow + 1 <= rows_cta &&
@@ -1146,7 +1163,7 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
                                          72 + 6 + 9 * (size_t)V.NT));
     std::string w2;
     std::swap(w2, *why);
-    tc.vc_ok = setup(4, tc.smem_vc, &tc.grid_vc);
+    tc.vc_ok = setup(P.p > 1 ? 5 : 4, tc.smem_vc, &tc.grid_vc);
     std::swap(w2, *why);
   }
   tc.ok = true;
@@ -1338,7 +1355,7 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
                       CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
   }
-  cudaError_t e = dispatch(tc, deriv ? 2 : (fused ? 3 : (vchain ? 4 : 0)), map, hmap, xmap, A, s, false);
+  cudaError_t e = dispatch(tc, deriv ? 2 : (fused ? 3 : (vchain ? (P.p > 1 ? 5 : 4) : 0)), map, hmap, xmap, A, s, false);
   if (A.trace && e == cudaSuccess) {  // measurement only: print CTA 0's per-phase averages
     std::vector<unsigned long long> h(64 * 16);
     cudaMemcpyAsync(h.data(), A.trace, h.size() * 8, cudaMemcpyDeviceToHost, s);
