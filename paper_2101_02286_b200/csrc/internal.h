@@ -100,9 +100,9 @@ struct TileArgs {
   const double* halo_hi;  // [2][m]: rows 0, 1 of the slab below
   unsigned long long* trace;  // measurement only (CTRI_TILE_TRACE=<cta>)
   int trace_cta;              // the CTA whose tiles are stamped
-  int vc_dbg;                 // experiment knob CTRI_VC_DBG (bit 0: no window finalisation,
-                              // bit 1: window rows stored evict-first like the rest; bits 2, 3:
-                              // finalisation without its stores / loads -- wrong results, timing only)
+  int vc_dbg;                 // experiment knob CTRI_VC_DBG, compiled in with -DCTRI_VC_EXPERIMENTS
+                              // (bit 0: no window finalisation; bits 2, 3: finalisation without its
+                              // stores / loads -- wrong results, timing only)
   // fused reduced phase (LAYOUT 3, nparts > 1): the window rows of every tile stay
   // in shared memory while the tile's (c = b~ - u y_D[1], y_D[n-1]) go to every rank's mailbox
   // as LL words; one tile later x~_i, x~_{i+1} = rows i, i+1 of A^{-1} applied to the gathered
@@ -135,6 +135,8 @@ struct PTileArgs {
   const double* tab;          // [stages][Q][4] alpha | [stages][Q][4] gamma | [Q][4] fold
   double* planes4;            // mode 1: [4][pm] c0 | c1 | w0 | w1 per (virtual) slab column
   int64_t pm;
+  unsigned long long* trace;  // measurement only (CTRI_TILE_TRACE): one CTA's phase stamps
+  int trace_cta;
 };
 struct PTileConfig {
   bool ok = false;

@@ -24,7 +24,10 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -101,8 +104,18 @@ __global__ void __launch_bounds__(kPNT, 2)
   };
   if (tid == 0) issue(first);
 
+  // measurement only (CTRI_TILE_TRACE): one CTA stamps the phases of its first 64 tiles
+  unsigned long long* tr = (A.trace && (int)blockIdx.x == A.trace_cta) ? A.trace : nullptr;
+  auto stamp = [&](int it_, int k) {
+    if (tr && tid == 0 && it_ < 64) {
+      unsigned long long tt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+      tr[it_ * 16 + k] = tt;
+    }
+  };
   int it = 0;
   for (int64_t t = first; t < A.num_tiles; t += ncl, ++it) {
+    stamp(it, 0);
     const int64_t o = t / A.tiles_per_outer;
     const int64_t col = (t - o * A.tiles_per_outer) * C + j;
     if (tid == 0) {
@@ -113,6 +126,7 @@ __global__ void __launch_bounds__(kPNT, 2)
     double v[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) v[k] = ring[(cl * K + k) * C + j];
+    stamp(it, 1);
     __syncthreads();  // the ring slot is free
     if (tid == 0) issue(t + ncl);
     const bool valid = col < A.lay.inner;
@@ -137,6 +151,7 @@ __global__ void __launch_bounds__(kPNT, 2)
         y1 = y;
       }
     }
+    stamp(it, 2);
     // chunk planes: c = b~ - U~ y, w = L~ y -> the owner of this column's head system
     {
       const uint32_t bar = rmap(mbar_ex, owner);
@@ -149,6 +164,7 @@ __global__ void __launch_bounds__(kPNT, 2)
     // ---- owner: b^_c = c_c - w_{c-1} (Eq. bi_hat), 2x2-block PCR over the Q heads ----
     {
       dev::mbar_wait(dev::smem_u32(mbar_ex), (uint32_t)it & 1u);
+      stamp(it, 3);
       double h0 = ex[4 * tid], h1 = ex[4 * tid + 1];
       if (A.mode == 1 && oc == 0) {  // the partition's interface: decoupled dummy row
         h0 = 0.0;
@@ -190,6 +206,7 @@ __global__ void __launch_bounds__(kPNT, 2)
         }
         __syncthreads();  // every read done before x~ leaves (the next tile's planes land here)
       }
+      stamp(it, 4);
       const double* fo = s_fold + oc * 4;
       const double x0 = fo[0] * h0 + fo[1] * h1, x1 = fo[2] * h0 + fo[3] * h1;
       // x~_oc -> x~_c of chunk oc's holder and x~_{c+1} of chunk oc-1's holder
@@ -203,6 +220,7 @@ __global__ void __launch_bounds__(kPNT, 2)
       dev::st_async_f64(rb + 8, x1, bb);
     }
     dev::mbar_wait(dev::smem_u32(mbar_rx), (uint32_t)it & 1u);
+    stamp(it, 5);
     const double xa0 = rx[4 * tid], xa1 = rx[4 * tid + 1];
     const bool last = (A.mode != 0 && c == Q - 1);  // x~_{c+1} lies outside D_i / acyclic end
     const double xb0 = last ? 0.0 : rx[4 * tid + 2], xb1 = last ? 0.0 : rx[4 * tid + 3];
@@ -228,6 +246,7 @@ __global__ void __launch_bounds__(kPNT, 2)
         }
       }
     }
+    stamp(it, 6);
   }
   if (G > 1) dev::cluster_sync();  // no CTA exits while peers may still address its smem
 }
@@ -382,7 +401,36 @@ cudaError_t launch_ptile(const Plan& P, const double* b, double* x, cudaStream_t
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_ptile, map, A, T);
+  A.trace = nullptr;
+  A.trace_cta = 0;
+  if (knob_tile_trace()) {  // measurement only
+    static unsigned long long* d_tr = nullptr;
+    if (!d_tr) cudaMalloc(&d_tr, 64 * 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(d_tr, 0, 64 * 16 * sizeof(unsigned long long), s);
+    A.trace = d_tr;
+    A.trace_cta = std::atoi(std::getenv("CTRI_TILE_TRACE"));
+  }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_ptile, map, A, T);
+  if (A.trace && e == cudaSuccess) {  // measurement only: the traced CTA's per-phase averages
+    std::vector<unsigned long long> h(64 * 16);
+    cudaMemcpyAsync(h.data(), A.trace, h.size() * 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double acc[8] = {0};
+    int cnt = 0;
+    for (int i = 4; i < 60; ++i) {
+      if (!h[i * 16 + 6] || !h[(i + 1) * 16]) break;
+      for (int k = 1; k <= 6; ++k) acc[k] += (double)(h[i * 16 + k] - h[i * 16 + k - 1]);
+      acc[7] += (double)(h[(i + 1) * 16] - h[i * 16 + 6]);
+      ++cnt;
+    }
+    if (cnt)
+      std::fprintf(stderr,
+                   "[ptile trace] per tile (ns): ring_wait+lds %.0f leaf %.0f ex_wait %.0f pcr %.0f "
+                   "rx_wait %.0f backsub+store %.0f loop %.0f total %.0f (%d tiles)\n",
+                   acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt, acc[6] / cnt,
+                   acc[7] / cnt, (acc[1] + acc[2] + acc[3] + acc[4] + acc[5] + acc[6] + acc[7]) / cnt, cnt);
+  }
+  return e;
 }
 
 }  // namespace ctri

@@ -606,16 +606,13 @@ __global__ void __launch_bounds__(NT, MINB)
       if (!valid) return;
       double* xp = A.x + (o * A.lay.n + (int64_t)c * K) * A.lay.inner + col;
       if (VC && (vc_wt >= 0 || vc_wb <= K)) {  // a chunk holding window rows (warp-uniform:
-        // the chunk is the warp): their y stays in L2 until the finaliser reads it back
+        // the chunk is the warp): its y stays in L2 until the finaliser reads the window rows
+        // back (the whole chunk: no per-row test on the store path); row 0 of the partition is
+        // left to the finaliser (x~)
         const uint64_t pol_last = dev::policy_evict_last();
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-          if ((k <= vc_wt || k >= vc_wb) && !(kVcExperiments && (A.vc_dbg & 2))) {
-            if (c != 0 || k != 0) dev::st_global_hint(xp + (int64_t)k * A.lay.inner, v[k], pol_last);
-          } else {
-            dev::st_global_cs(xp + (int64_t)k * A.lay.inner, v[k]);
-          }
-        }
+        for (int k = 0; k < K; ++k)
+          if (c != 0 || k != 0) dev::st_global_hint(xp + (int64_t)k * A.lay.inner, v[k], pol_last);
         return;
       }
       if (FUSED) {  // window rows wait in shared memory for x~ (finalised one tile later)
@@ -679,13 +676,6 @@ __global__ void __launch_bounds__(NT, MINB)
       int fg, fq;
       dev::cp_async_wait_all();  // this thread's window rows of this tile's target (loaded a tile ago)
       if (vc_target(vc_gi, vc_q, &fg, &fq)) vc_store(vc_bptr[tid], fg, fq, it & 1);
-      // start loading the next tile's target (stored >= vp tiles ago and acquired since)
-      const int nq = vc_q + 1 < vcp ? vc_q + 1 : 0, ngi = vc_q + 1 < vcp ? vc_gi : vc_gi + 1;
-      if (vc_target(ngi, nq, &fg, &fq)) {
-        double* blk = vc_block(fg, fq);
-        vc_bptr[tid] = blk;  // (this thread's own slot: read back by it one tile later)
-        vc_load(blk, (it + 1) & 1);
-      }
     }
     // ---- owner: head system b^_c (Eq. bi_hat at chunk level), then PCR stages ----
     {
@@ -734,6 +724,16 @@ __global__ void __launch_bounds__(NT, MINB)
                         rmap(mbar_rx, (uint32_t)(oc / CPC)));
       dev::st_async_f64(rmap(rx_b + holder_tid(ocm), (uint32_t)(ocm / CPC)), xt,
                         rmap(mbar_rx, (uint32_t)(ocm / CPC)));
+    }
+    if (VC) {  // in the shadow of the x~ return: start loading the next tile's target (stored
+               // >= vp tiles ago and acquired since)
+      int fg, fq;
+      const int nq = vq + 1 < vcp ? vq + 1 : 0, ngi = vq + 1 < vcp ? vgi : vgi + 1;
+      if (vc_target(ngi, nq, &fg, &fq)) {
+        double* blk = vc_block(fg, fq);
+        vc_bptr[tid] = blk;  // (this thread's own slot: read back by it one tile later)
+        vc_load(blk, (it + 1) & 1);
+      }
     }
     dev::mbar_wait(dev::smem_u32(mbar_rx), (uint32_t)it & 1u);
     stamp(it, 5);

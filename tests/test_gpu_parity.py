@@ -539,6 +539,57 @@ def test_cfg2_full_size_loopback_partitions(p):
     assert m == 65536 and err < TOL_REL, err
 
 
+@pytest.mark.parametrize("cfg", ["cfg4_d1", "cfg4_d2"])
+def test_direction_sweep_full_size_loopback_8(cfg):
+    """The BASELINE direction sweep (index 1 strided, index 2 contiguous) split into 8 slabs
+    along the solve index (the driver's N = 8 run, loopback on one GPU): every column vs the
+    oracle."""
+    import torch
+
+    from paper_2101_02286_b200 import ctri
+    p = 8
+    dims, sd = workloads.config(cfg)
+    b = workloads.device_uniform(dims, 3, torch.device("cuda:0"))
+    n = dims[sd] // p
+    bs = [b.narrow(sd, r * n, n).contiguous() for r in range(p)]
+    xs = [torch.empty_like(t) for t in bs]
+    g = ctri.LoopbackGroup(dims, sd, p)
+    g.solve(bs, xs)
+    torch.cuda.synchronize()
+    st = g.stats(0)
+    g.close()
+    x = torch.cat(xs, sd)
+    del bs, xs
+    assert st["device_error"] == 0
+    err, m = _full_columns(b, x, sd)
+    assert m == b.numel() // dims[sd] and err < TOL_REL, err
+
+
+def test_cfg5_full_size_loopback_8():
+    """cfg5 (1024 x 512^2 compact derivative, fused stencil) split into 8 slabs of 128 rows
+    (loopback on one GPU; halo planes and the reduced phase between every pair): every column
+    vs the oracle's derivative of the whole field."""
+    import torch
+
+    from paper_2101_02286_b200 import CTRI_FLAG_DERIV, ctri
+    p = 8
+    dims, sd = workloads.config("cfg5", 1)
+    f = workloads.device_uniform(dims, 5, torch.device("cuda:0"))
+    n = dims[sd] // p
+    fs = [f[r * n:(r + 1) * n].contiguous() for r in range(p)]
+    ds = [torch.empty_like(t) for t in fs]
+    g = ctri.LoopbackGroup(dims, sd, p, flags=CTRI_FLAG_DERIV)
+    g.deriv(fs, ds, h=2 * math.pi / dims[sd])
+    torch.cuda.synchronize()
+    st = g.stats(0)
+    g.close()
+    df = torch.cat(ds, 0)
+    del fs, ds
+    assert st["device_error"] == 0
+    err, m = _full_columns(f, df, sd, fn=lambda a: oracle.deriv(a, 0, h=2 * math.pi / dims[sd]))
+    assert m == 512 * 512 and err < TOL_REL, err
+
+
 @pytest.mark.parametrize("p,n", [(4, 256), (2, 1024)])
 def test_deriv_halo_epochs_independent(p, n):
     """Each derivative solve advances the reduced-phase epoch by one and the halo epoch by one
