@@ -166,6 +166,47 @@ __global__ void __launch_bounds__(256) k_window(const WindowArgs A) {
   }
 }
 
+// strided axis with an even row length (the usual case): a thread owns a PAIR of adjacent
+// columns (16-byte loads and stores) and kWinPairRows consecutive window rows of one slab, all
+// loads in flight before the first store; rows walk by pointer increments, so the per-element
+// work is one load, one store and four DFMA per pair (the per-element 64-bit index arithmetic of
+// k_window made that kernel issue-bound: ncu cfg3 slab, 60% issue slots busy at 2.5 TB/s)
+constexpr int kWinPairRows = 8;
+__global__ void __launch_bounds__(256) k_window_pairs(const WindowArgs A) {
+  if (A.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");  // launched early (PDL)
+  const int64_t j = 2 * (blockIdx.x * 256ll + threadIdx.x);        // first column of the pair
+  const int64_t m = A.outer * A.inner;
+  if (j >= m) return;
+  const int s = blockIdx.z;
+  const int64_t o = j / A.inner, c = j - o * A.inner;
+  const int64_t sl = A.nv * A.inner;  // one slab
+  double* xs = A.x + (o * A.vp + s) * sl + c;
+  const double2 xa = *reinterpret_cast<const double2*>(xs);
+  double2 xn = make_double2(0.0, 0.0);
+  if (s + 1 < A.vp) xn = *reinterpret_cast<const double2*>(xs + sl);
+  else if (A.next) xn = *reinterpret_cast<const double2*>(A.next + j);
+  else if (A.wrap) xn = *reinterpret_cast<const double2*>(A.x + o * A.vp * sl + c);
+  const int r0 = blockIdx.y * kWinPairRows;  // first window row index of this thread
+  double2 v[kWinPairRows];
+  double* pr[kWinPairRows];
+#pragma unroll
+  for (int u = 0; u < kWinPairRows; ++u) {
+    const int ry = r0 + u;
+    const int64_t r = window_row(A, ry);
+    pr[u] = xs + r * A.inner;
+    if (ry < A.rows) v[u] = *reinterpret_cast<const double2*>(pr[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < kWinPairRows; ++u) {
+    const int ry = r0 + u;
+    if (ry < A.rows) {
+      const int64_t r = window_row(A, ry);
+      const double sv = __ldg(A.S + r - 1), rv = __ldg(A.R + r - 1);
+      dev::st_global_cs_v2(pr[u], v[u].x - sv * xa.x - rv * xn.x, v[u].y - sv * xa.y - rv * xn.y);
+    }
+  }
+}
+
 // contiguous axis (inner == 1): one warp per column, lanes along the (contiguous) rows
 __global__ void __launch_bounds__(256) k_window_contig(const WindowArgs A) {
   const int64_t w = blockIdx.x * 8ll + (threadIdx.x >> 5);
@@ -218,8 +259,10 @@ cudaError_t launch_window(const Plan& P, double* x, const double* next, cudaStre
     k_window_contig<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(A);
   } else {
     const int64_t m = P.lay.m();
-    const int64_t rpb = (int64_t)kWinRows * kWinBatches;
-    dim3 grid((unsigned)((m + 255) / 256), (unsigned)((A.rows + rpb - 1) / rpb), (unsigned)A.vp);
+    const bool pairs = (A.inner % 2) == 0;  // (ncu, cold: cfg3 slab 18.1 -> 16.7 us, cfg2 N=2 62 -> 57 us)
+    const int64_t rpb = pairs ? (int64_t)kWinPairRows : (int64_t)kWinRows * kWinBatches;
+    const int64_t cpb = pairs ? 512 : 256;  // columns per block
+    dim3 grid((unsigned)((m + cpb - 1) / cpb), (unsigned)((A.rows + rpb - 1) / rpb), (unsigned)A.vp);
     // after the P2P kernel (nparts > 1): programmatic dependent launch, so the window grid is
     // staged while the reduced-phase kernel drains (the kernel waits before touching x)
     A.pdl = (P.p > 1 && !knob_no_pdl()) ? 1 : 0;
@@ -232,7 +275,7 @@ cudaError_t launch_window(const Plan& P, double* x, const double* next, cudaStre
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = A.pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k_window, A);
+    return pairs ? cudaLaunchKernelEx(&cfg, k_window_pairs, A) : cudaLaunchKernelEx(&cfg, k_window, A);
   }
   return cudaGetLastError();
 }
