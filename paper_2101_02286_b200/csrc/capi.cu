@@ -383,11 +383,22 @@ ctri_status penta_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, co
   // partitions on this GPU (reduced 2x2-block system over them, then the window pass).
   // Measured on the cfg2 grid: 1024-row partitions (clusters of 4, shuffle PCR) 2.32 ms,
   // 2048-row ones (clusters of 8, shared-memory PCR, half the window rows) 2.50 ms.
+  // nparts > 1 (solve index 0, outer == 1): the same 1024-row partitions as "virtual rows" --
+  // the reduced 2x2-block system has nparts * vp block rows, exchanged over the LL P2P path
+  // (rows of one GPU through its own mailbox), as for the tridiagonal solve.  CTRI_VPARTS
+  // overrides the count (measurement and test knob; 1: the slab as one partition).
   P->vp = 1;
-  if (p == 1 && P->lay.inner >= 32 && n > 1024 && n % 1024 == 0 && n / 1024 <= 8 &&
-      is_pow2(n / 1024) && !knob_penta_serial())
+  const bool vp_fit = P->lay.inner >= 32 && n > 1024 && n % 1024 == 0 && n / 1024 <= 8 &&
+                      is_pow2(n / 1024) && !knob_penta_serial();
+  if (vp_fit && (p == 1 || (P->lay.outer == 1 && !(flags & CTRI_FLAG_ALLGATHER) &&
+                            p * (n / 1024) <= kMaxP2PRanks)))
     P->vp = (int)(n / 1024);
-  P->rvp = 1;
+  if (const char* e = std::getenv("CTRI_VPARTS"))
+    if (*e && P->vp > 1) {
+      const int want = std::atoi(e);
+      if (want >= 1 && want <= P->vp && is_pow2(want)) P->vp = want;
+    }
+  P->rvp = p > 1 ? P->vp : 1;
   P->tlay = P->lay;
   P->tlay.outer = P->lay.outer * P->vp;
   P->tlay.n = n / P->vp;
@@ -402,6 +413,7 @@ ctri_status penta_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, co
     if ((st = upload(&P->ptc.d_tab, P->ptc.tab, s)) != CTRI_OK) return fail(st, "penta tile tables");
   } else if (P->vp > 1) {  // no on-chip solve: the slab as one partition, column-serial
     P->vp = 1;
+    P->rvp = 1;
     P->tlay = P->lay;
     if ((st = penta_plan_tables(P, s, &why)) != CTRI_OK) return fail(st, "pentadiagonal tables: " + why);
   }
@@ -417,7 +429,8 @@ ctri_status penta_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, co
       for (int k = 0; k < 5; ++k) mx = std::max(mx, std::fabs(bands[k]));
       BlockSchedule sc;
       FactorError fe;
-      if (!penta_reduced_schedule(p, cyclic != 0, P->pt, 1e-13 * mx, &sc, &fe))
+      const int pr = p * P->rvp;  // block rows of the reduced system (virtual rows included)
+      if (!penta_reduced_schedule(pr, cyclic != 0, P->pt, 1e-13 * mx, &sc, &fe))
         return fail((ctri_status)fe.code, fe.detail);
       const int q = (int)sc.steps.size();
       if (q > kMaxP2PSteps) return fail(CTRI_ERR_UNSUPPORTED, "pentadiagonal reduced schedule too long");
@@ -425,38 +438,44 @@ ctri_status penta_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, co
       P->sched.pcr_stages = sc.pcr_stages;  // (counts reported by ctri_get_stats)
       P->sched.detach_stages = sc.detach_stages;
       P->sched.detached_rows = sc.detached_rows;
-      std::vector<double> tab;  // [step][12]: W | C0 | C1 of this rank
-      P->pstep.assign(kMaxP2PSteps, P2PStep{1.0, 0.0, 0.0, -1, -1, -1, -1, 0, 0});
-      for (int k = 0; k < q; ++k) {
-        const BlockSchedEntry& e = sc.steps[k][rank];
-        tab.insert(tab.end(), e.W, e.W + 4);
-        tab.insert(tab.end(), e.C[0], e.C[0] + 4);
-        tab.insert(tab.end(), e.C[1], e.C[1] + 4);
-        P2PStep& stp = P->pstep[k];
-        stp.src0 = (int8_t)e.src[0];
-        stp.src1 = (int8_t)e.src[1];
-        int nd = 0;  // this rank's pre-step value goes to every row that reads it
-        for (int r = 0; r < p; ++r)
-          for (int sl = 0; sl < 2; ++sl)
-            if (sc.steps[k][r].src[sl] == rank) {
-              if (nd == 0) { stp.dst0 = (int8_t)r; stp.dslot0 = (int8_t)sl; }
-              else if (nd == 1) { stp.dst1 = (int8_t)r; stp.dslot1 = (int8_t)sl; }
-              ++nd;
-            }
-        if (nd > 2) return fail(CTRI_ERR_UNSUPPORTED, "pentadiagonal reduced schedule: > 2 readers");
+      std::vector<double> tab;  // [virtual row][step][12]: W | C0 | C1 of this rank's rows
+      P->pstep.assign((size_t)P->rvp * kMaxP2PSteps, P2PStep{1.0, 0.0, 0.0, -1, -1, -1, -1, 0, 0});
+      for (int v = 0; v < P->rvp; ++v) {
+        const int g = rank * P->rvp + v;  // global block row
+        for (int k = 0; k < q; ++k) {
+          const BlockSchedEntry& e = sc.steps[k][g];
+          tab.insert(tab.end(), e.W, e.W + 4);
+          tab.insert(tab.end(), e.C[0], e.C[0] + 4);
+          tab.insert(tab.end(), e.C[1], e.C[1] + 4);
+          P2PStep& stp = P->pstep[(size_t)v * kMaxP2PSteps + k];
+          stp.src0 = (int8_t)e.src[0];
+          stp.src1 = (int8_t)e.src[1];
+          int nd = 0;  // this row's pre-step value goes to every row that reads it
+          for (int r = 0; r < pr; ++r)
+            for (int sl = 0; sl < 2; ++sl)
+              if (sc.steps[k][r].src[sl] == g) {
+                if (nd == 0) { stp.dst0 = (int8_t)r; stp.dslot0 = (int8_t)sl; }
+                else if (nd == 1) { stp.dst1 = (int8_t)r; stp.dslot1 = (int8_t)sl; }
+                ++nd;
+              }
+          if (nd > 2) return fail(CTRI_ERR_UNSUPPORTED, "pentadiagonal reduced schedule: > 2 readers");
+        }
       }
       CUDA_TRY(cudaMalloc(&P->d_ppcr, sizeof(double) * tab.size()));
       CUDA_TRY(cudaMemcpyAsync(P->d_ppcr, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice, s));
       copy_words = (int64_t)(4 + 4 * q) * 2 * m;
     }
-    P->p2p_nslices = p2p_slices(m, P->loopback ? p : 1, P->num_sms, P->ppcr ? 3 : 2);
+    P->p2p_nslices = p2p_slices(m, (P->loopback ? p : 1) * P->rvp, P->num_sms, P->ppcr ? 3 : 2);
     P->p2p_copy = copy_words;
-    P->mbox_bytes = sizeof(unsigned long long) * p2p_mailbox_words(copy_words, m, false);
+    // one mailbox (two epoch copies) per virtual row of this rank
+    P->p2p_off = 0;
+    P->p2p_vrow_words = (int64_t)p2p_mailbox_words(copy_words, m, false);
+    P->mbox_bytes = sizeof(unsigned long long) * (size_t)P->rvp * (size_t)P->p2p_vrow_words;
     CUDA_TRY(cudaMalloc(&P->mbox_alloc, P->mbox_bytes));
     CUDA_TRY(cudaMemsetAsync(P->mbox_alloc, 0, P->mbox_bytes, s));
     TRY(alloc_err(P));
-    CUDA_TRY(cudaMalloc(&P->d_epoch, sizeof(unsigned int) * P->p2p_nslices));
-    CUDA_TRY(cudaMemsetAsync(P->d_epoch, 0, sizeof(unsigned int) * P->p2p_nslices, s));
+    CUDA_TRY(cudaMalloc(&P->d_epoch, sizeof(unsigned int) * P->p2p_nslices * P->rvp));
+    CUDA_TRY(cudaMemsetAsync(P->d_epoch, 0, sizeof(unsigned int) * P->p2p_nslices * P->rvp, s));
     P->p2p = true;
   }
   if (flags & CTRI_FLAG_TIMING) {
@@ -541,8 +560,9 @@ void p2p_fill_rank(const Plan& P, double* x, P2PRank* R, int v = 0) {
   R->yf = P.yf + (int64_t)v * m;
   R->yl = P.yl + (int64_t)v * m;
   R->bt = P.bt + (int64_t)v * m;
-  R->xnext = P.r == 2 ? P.d_xnext2 : P.xt_next + (int64_t)v * m;
-  R->planes4 = P.d_planes4;
+  R->xnext = P.r == 2 ? P.d_xnext2 + (int64_t)v * 2 * m : P.xt_next + (int64_t)v * m;
+  R->planes4 = P.d_planes4 ? P.d_planes4 + (int64_t)v * m : nullptr;  // [4][pstride], row v's segment
+  R->pstride = (P.r == 2 && P.p > 1) ? m * vp : m;
   R->ainv = P.d_ainv;
   R->mbox = reinterpret_cast<unsigned long long*>(P.mbox_alloc) + P.p2p_off + (int64_t)v * P.p2p_vrow_words;
   R->epoch = P.d_epoch + (int64_t)v * P.p2p_nslices;
@@ -560,10 +580,12 @@ void p2p_fill_rank(const Plan& P, double* x, P2PRank* R, int v = 0) {
     R->ag0[r] = P.ainv[(size_t)P.rank * P.p + r];
     if (nx < P.p || P.cyclic) R->ag1[r] = P.ainv[(size_t)(nx % P.p) * P.p + r];
   }
-  R->ppcr = P.d_ppcr;
+  R->ppcr = P.d_ppcr ? P.d_ppcr + (size_t)v * 12 * P.ppcr_steps : nullptr;
   if (P.r == 2) {
-    for (int s = 0; s < kMaxP2PSteps; ++s)
-      R->step[s] = s < (int)P.pstep.size() ? P.pstep[s] : P2PStep{1.0, 0.0, 0.0, -1, -1, -1, -1, 0, 0};
+    for (int s = 0; s < kMaxP2PSteps; ++s) {
+      const size_t k = (size_t)v * kMaxP2PSteps + s;
+      R->step[s] = k < P.pstep.size() ? P.pstep[k] : P2PStep{1.0, 0.0, 0.0, -1, -1, -1, -1, 0, 0};
+    }
     return;
   }
   const Schedule& sc = P.sched;
@@ -893,15 +915,17 @@ ctri_status penta_solve_group(std::vector<Plan*>& G, const double* const* b, dou
   if (P0.p > 1) {
     P2PArgs A;
     p2p_args(P0, &A);
-    const int grid = A.nslices * (int)G.size();
+    const int nrows = (int)G.size() * P0.rvp;  // block rows launched together (ranks x virtual rows)
+    const int grid = A.nslices * nrows;
     if (!P0.ev.empty() && !P0.d_trace) {  // per-round stamps (CTRI_FLAG_TIMING)
       CUDA_TRY(cudaMalloc(&P0.d_trace, sizeof(unsigned long long) * kP2PTrace * grid));
       CUDA_TRY(cudaMemsetAsync(P0.d_trace, 0, sizeof(unsigned long long) * kP2PTrace * grid, s));
       P0.trace_ctas = grid;
     }
     A.trace = P0.d_trace;
-    for (size_t r = 0; r < G.size(); ++r) p2p_fill_rank(*G[r], x[r], &A.rk[r]);
-    cudaError_t e = P0.ppcr ? launch_reduced_penta_pcr(A, (int)G.size(), s)
+    for (size_t r = 0; r < G.size(); ++r)
+      for (int v = 0; v < P0.rvp; ++v) p2p_fill_rank(*G[r], x[r], &A.rk[r * P0.rvp + v], v);
+    cudaError_t e = P0.ppcr ? launch_reduced_penta_pcr(A, nrows, s)
                             : launch_reduced_allgather_r2(A, (int)G.size(), s);
     if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, std::string("penta reduced: ") + cudaGetErrorString(e));
     record(P0, EV_XX, s);

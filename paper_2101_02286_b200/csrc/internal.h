@@ -194,7 +194,8 @@ struct P2PRank {
   unsigned long long* peer_mbox[kMaxP2PRanks];  // every rank's mailbox as addressable here
   P2PStep step[kMaxP2PSteps];
   double ag0[kMaxAG], ag1[kMaxAG];  // all-gather mode: rows i and i+1 of A^{-1} (zeros past p)
-  const double* planes4;         // pentadiagonal all-gather: [4][m] c0 | c1 | w0 | w1
+  const double* planes4;         // pentadiagonal: c0 | c1 | w0 | w1 of this row, plane k at k * pstride
+  int64_t pstride;               // pentadiagonal: plane stride (m, or m * vp with virtual rows)
   const double* ainv;            // pentadiagonal all-gather: [2p][2p] reduced inverse
   const double* ppcr;            // pentadiagonal pairwise: this rank's [step][8] A0 | A1, fold [4]
 };

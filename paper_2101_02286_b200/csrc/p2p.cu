@@ -535,9 +535,9 @@ __global__ void __launch_bounds__(kP2PThreads, 1)
     pw0[i] = pw1[i] = pc0[i] = pc1[i] = 0.0;
     if (i < nc) {
       pc0[i] = R.planes4[col[i]];
-      pc1[i] = R.planes4[m + col[i]];
-      pw0[i] = R.planes4[2 * m + col[i]];
-      pw1[i] = R.planes4[3 * m + col[i]];
+      pc1[i] = R.planes4[R.pstride + col[i]];
+      pw0[i] = R.planes4[2 * R.pstride + col[i]];
+      pw1[i] = R.planes4[3 * R.pstride + col[i]];
     }
   }
   if (right >= 0) {

@@ -413,10 +413,12 @@ ctri_status penta_plan_tables(Plan* P, cudaStream_t s, std::string* why) {
   if (P->p == 1 && P->vp > 1 &&
       cudaMalloc(&P->d_planes4, sizeof(double) * 4 * m * P->vp) != cudaSuccess)
     return CTRI_ERR_OOM;
-  if (P->p > 1) {
-    if (cudaMalloc(&P->d_planes4, sizeof(double) * 4 * m) != cudaSuccess) return CTRI_ERR_OOM;
-    if (cudaMalloc(&P->d_xnext2, sizeof(double) * 2 * m) != cudaSuccess) return CTRI_ERR_OOM;
-    if (cudaMemsetAsync(P->d_xnext2, 0, sizeof(double) * 2 * m, s) != cudaSuccess) return CTRI_ERR_CUDA;
+  if (P->p > 1) {  // per virtual row: planes [4][m * vp], x~ of the next block row [vp][2][m]
+    if (P->d_xnext2) cudaFree(P->d_xnext2);
+    P->d_xnext2 = nullptr;
+    if (cudaMalloc(&P->d_planes4, sizeof(double) * 4 * m * P->vp) != cudaSuccess) return CTRI_ERR_OOM;
+    if (cudaMalloc(&P->d_xnext2, sizeof(double) * 2 * m * P->vp) != cudaSuccess) return CTRI_ERR_OOM;
+    if (cudaMemsetAsync(P->d_xnext2, 0, sizeof(double) * 2 * m * P->vp, s) != cudaSuccess) return CTRI_ERR_CUDA;
   }
   return CTRI_OK;
 }
@@ -460,7 +462,7 @@ cudaError_t launch_penta_window(const Plan& P, double* x, cudaStream_t s) {
   PentaWinArgs A;
   A.x = x;
   A.SR = P.d_pSR;
-  A.next = P.p > 1 ? P.d_xnext2 : nullptr;
+  A.next = P.p > 1 ? P.d_xnext2 + (int64_t)(P.vp - 1) * 2 * P.lay.m() : nullptr;  // the last row's
   A.outer = P.lay.outer;
   A.n = P.tlay.n;
   A.inner = P.lay.inner;

@@ -127,6 +127,23 @@ def main():
                                  "kernel": st["local_kernel"], "path": st["reduced_path"],
                                  "detached": st["detached_rows"]}
         assert st["local_kernel"] == 4 and st["reduced_path"] == 1, st
+    # pentadiagonal with 2048-row slabs: two on-chip partitions per GPU as virtual rows of the
+    # 2x2-block reduced system (2 * world block rows; rows of one GPU through its own mailbox)
+    pdims = (2048 * world, 1, 64)
+    b = workloads.uniform(pdims, 97)
+    plan = pdist.plan_from_process_group(pdims, 0, pb2, True)
+    bl = torch.from_numpy(workloads.slab(b, 0, world, rank)).to(dev)
+    xl = torch.empty_like(bl)
+    plan.solve(bl, xl)
+    torch.cuda.synchronize()
+    st = plan.stats()
+    x = pdist.gather_to_rank0(xl, 0)
+    plan.close()
+    if rank == 0:
+        results["penta_vrows"] = {"err": rel_err(x.cpu().numpy(), oracle.penta_solve(b, 0, pb2, True), 0),
+                                  "kernel": st["local_kernel"], "path": st["reduced_path"],
+                                  "rows": st["reduced_rows"]}
+        assert st["local_kernel"] == 4 and st["vparts"] == 2 and st["reduced_rows"] == 2 * world, st
     # staggered sixth-order interpolation through ctri_compact_apply
     from paper_2101_02286_b200 import ctri
     plan = pdist.plan_from_process_group(dims, 0, ctri.staggered_interp_bands(), True, flags=CTRI_FLAG_DERIV)

@@ -219,14 +219,54 @@ def test_penta_cfg2_grid_full_size(p):
 
 @pytest.mark.parametrize("p", [2, 4])
 @pytest.mark.parametrize("cyclic", [True, False])
-def test_penta_on_chip_2048_row_slabs(p, cyclic):
-    """Slabs of 2048 rows per rank (the cfg2 grid at 4 GPUs): the on-chip solve with clusters of
-    8 (64 chunk heads per column, 2x2-block PCR through shared memory), then the reduced system
+@pytest.mark.parametrize("vp", [1, 2])
+def test_penta_on_chip_2048_row_slabs(p, cyclic, vp, monkeypatch):
+    """Slabs of 2048 rows per rank (the cfg2 grid at 4 GPUs): vp = 1, the on-chip solve with
+    clusters of 8 (64 chunk heads per column, 2x2-block PCR through shared memory); vp = 2, two
+    1024-row partitions per rank as virtual rows of the reduced system; then the reduced system
     over the P2P path and the window pass; vs the oracle."""
+    monkeypatch.setenv("CTRI_VPARTS", str(vp))
     b = workloads.uniform((2048 * p, 1, 64), 170 + p)
     for bands in BANDS:
         x, st = penta_gpu(b, 0, p, bands, cyclic, return_stats=True)
         assert st["local_kernel"] == 4 and st["device_error"] == 0
+        assert st["vparts"] == vp and st["reduced_rows"] == p * vp
         ref = oracle.penta_solve(b, 0, bands, cyclic)
         assert rel_err(x, ref, 0) < TOL_REL
         assert penta_residual(x, b, 0, bands, cyclic) < 1e-13
+
+
+@pytest.mark.parametrize("p,n", [(2, 4096), (3, 2048), (3, 4096), (4, 2048), (2, 2048)])
+@pytest.mark.parametrize("cyclic", [True, False])
+def test_penta_virtual_rows_multi_partition(p, n, cyclic):
+    """nparts > 1 with slabs longer than 1024 rows: every slab solved on chip as n / 1024
+    partitions, the reduced 2x2-block system over nparts * vp block rows on the P2P path
+    (pairwise block PCR; block detach / reattach when the count is not a power of two),
+    then the window pass; vs the oracle for the three band sets."""
+    vp = n // 1024
+    b = workloads.uniform((n * p, 1, 32), 190 + p + n // 1024)
+    for bands in BANDS:
+        x, st = penta_gpu(b, 0, p, bands, cyclic, return_stats=True)
+        assert st["local_kernel"] == 4 and st["device_error"] == 0
+        assert st["vparts"] == vp and st["reduced_rows"] == p * vp, st
+        pr = p * vp
+        if cyclic and pr & (pr - 1):
+            assert st["detached_rows"] == pr - 2 ** int(math.floor(math.log2(pr)))
+        ref = oracle.penta_solve(b, 0, bands, cyclic)
+        assert rel_err(x, ref, 0) < TOL_REL
+        assert penta_residual(x, b, 0, bands, cyclic) < 1e-13
+
+
+@pytest.mark.parametrize("r", [0, 1, 2, 1022, 1023, 1024, 1025, 2047, 2048, 2049, 3071, 3072, 3073, 4095])
+def test_penta_virtual_rows_delta_at_edges(r):
+    """Unit impulses on and next to the virtual-row interfaces (every 1024 rows) and the rank
+    interfaces (2048) of p = 2 slabs of 2048 rows (4 block rows in the reduced system)."""
+    N, p = 4096, 2
+    b = np.zeros((N, 1, 32))
+    b[r] = 1.0
+    for bands in BANDS:
+        for cyclic in (True, False):
+            x, st = penta_gpu(b, 0, p, bands, cyclic, return_stats=True)
+            assert st["vparts"] == 2 and st["reduced_rows"] == 4
+            ref = oracle.penta_solve(b, 0, bands, cyclic)
+            assert np.max(np.abs(x - ref)) < 1e-14 * max(1.0, np.max(np.abs(ref)))
