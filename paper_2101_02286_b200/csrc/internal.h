@@ -100,6 +100,7 @@ struct TileArgs {
   const double* halo_hi;  // [2][m]: rows 0, 1 of the slab below
   unsigned long long* trace;  // measurement only (CTRI_TILE_TRACE=<cta>)
   int trace_cta;              // the CTA whose tiles are stamped
+  int trace_off;              // its first stamped tile (CTRI_TILE_TRACE_OFF)
   int vc_dbg;                 // experiment knob CTRI_VC_DBG, compiled in with -DCTRI_VC_EXPERIMENTS
                               // (bit 0: no window finalisation; bits 2, 3: finalisation without its
                               // stores / loads -- wrong results, timing only)

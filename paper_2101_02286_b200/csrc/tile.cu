@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(NT, MINB)
   // [2][kVcFin][NT] pairs of window values in flight (16-byte cp.async, double-buffered)
   double* vc_buf = reinterpret_cast<double*>(
       smem_raw + ((reinterpret_cast<unsigned char*>(vc_gtab + 8) - smem_raw + 15) & ~(ptrdiff_t)15));
-  double** vc_bptr = reinterpret_cast<double**>(vc_buf + 8 * NT);  // [NT]: the block in flight
+  double** vc_bptr = reinterpret_cast<double**>(vc_buf + 8 * NT);  // [2][NT]: the blocks in flight
 
   const int tid = threadIdx.x;
   // strided axis: lanes run over the C columns of a tile row (coalesced rows);
@@ -254,11 +254,11 @@ __global__ void __launch_bounds__(NT, MINB)
 
   // measurement only (CTRI_TILE_TRACE): CTA 0 stamps its first 64 tiles' phases
   unsigned long long* tr = (A.trace && (int)blockIdx.x == A.trace_cta) ? A.trace : nullptr;
-  auto stamp = [&](int it_, int k) {
-    if (tr && tid == 0 && it_ < 64) {
+  auto stamp = [&](int it_, int k) {  // tiles trace_off .. trace_off + 63
+    if (tr && tid == 0 && it_ >= A.trace_off && it_ < A.trace_off + 64) {
       unsigned long long tt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
-      tr[it_ * 16 + k] = tt;
+      tr[(it_ - A.trace_off) * 16 + k] = tt;
     }
   };
   int it = 0;
@@ -673,9 +673,20 @@ __global__ void __launch_bounds__(NT, MINB)
         dev::mbar_wait(dev::smem_u32(mbar_red + par), (uint32_t)(((vc_gi - 1) >> 1) & 1));
         vc_solve(par);
       }
+      // start loading the next tile's target (stored >= vp tiles ago and acquired since); it
+      // is finalised in the x~ shadow of the next tile, so the loads have a whole tile to land
+      // (issued after this tile's stores they queued behind them: 0.5 us waits per tile)
       int fg, fq;
-      dev::cp_async_wait_all();  // this thread's window rows of this tile's target (loaded a tile ago)
-      if (vc_target(vc_gi, vc_q, &fg, &fq)) vc_store(vc_bptr[tid], fg, fq, it & 1);
+      stamp(it, 12);
+      const int nq = vc_q + 1 < vcp ? vc_q + 1 : 0, ngi = vc_q + 1 < vcp ? vc_gi : vc_gi + 1;
+      if (vc_target(ngi, nq, &fg, &fq)) {
+        double* blk = vc_block(fg, fq);
+        vc_bptr[((it + 1) & 1) * NT + tid] = blk;  // (this thread's own slot)
+        vc_load(blk, (it + 1) & 1);
+      } else {
+        dev::cp_async_commit();  // (an empty group keeps the group count per tile)
+      }
+      stamp(it, 7);
     }
     // ---- owner: head system b^_c (Eq. bi_hat at chunk level), then PCR stages ----
     {
@@ -725,15 +736,13 @@ __global__ void __launch_bounds__(NT, MINB)
       dev::st_async_f64(rmap(rx_b + holder_tid(ocm), (uint32_t)(ocm / CPC)), xt,
                         rmap(mbar_rx, (uint32_t)(ocm / CPC)));
     }
-    if (VC) {  // in the shadow of the x~ return: start loading the next tile's target (stored
-               // >= vp tiles ago and acquired since)
+    if (VC) {  // in the shadow of the x~ return: finalise this tile's target (loaded a tile ago;
+               // the group just issued for the next tile may stay in flight)
       int fg, fq;
-      const int nq = vq + 1 < vcp ? vq + 1 : 0, ngi = vq + 1 < vcp ? vgi : vgi + 1;
-      if (vc_target(ngi, nq, &fg, &fq)) {
-        double* blk = vc_block(fg, fq);
-        vc_bptr[tid] = blk;  // (this thread's own slot: read back by it one tile later)
-        vc_load(blk, (it + 1) & 1);
-      }
+      stamp(it, 14);
+      dev::cp_async_wait_group<1>();
+      if (vc_target(vc_gi, vc_q, &fg, &fq)) vc_store(vc_bptr[(it & 1) * NT + tid], fg, fq, it & 1);
+      stamp(it, 13);
     }
     dev::mbar_wait(dev::smem_u32(mbar_rx), (uint32_t)it & 1u);
     stamp(it, 5);
@@ -790,7 +799,7 @@ __global__ void __launch_bounds__(NT, MINB)
     dev::cp_async_wait_all();
     int fg, fq;
     if (vc_target(vgi, 0, &fg, &fq))  // loaded by the last tile (into buffer it & 1)
-      vc_store(vc_bptr[tid], fg, fq, it & 1);
+      vc_store(vc_bptr[(it & 1) * NT + tid], fg, fq, it & 1);
     if (vc_solver) {
       const int par = gl & 1;
       dev::mbar_wait(dev::smem_u32(mbar_red + par), (uint32_t)((gl >> 1) & 1));
@@ -1160,7 +1169,7 @@ static bool tile_configure_variant(Plan& P, int vi, std::string* why) {
       L.n * L.inner < ((int64_t)1 << 31)) {                           // 32-bit row offsets
     tc.smem_vc = tc.smem_bytes + 128 +
                  (int)(sizeof(double) * ((2 * 8 + 2 * 8 + 2 * 9) * (size_t)(V.C / G) + 2 * (2 * (size_t)P.vwindow + 1) +
-                                         72 + 6 + 9 * (size_t)V.NT));
+                                         72 + 6 + 10 * (size_t)V.NT));  // vc_buf 8 NT, vc_bptr 2 NT
     std::string w2;
     std::swap(w2, *why);
     tc.vc_ok = setup(P.p > 1 ? 5 : 4, tc.smem_vc, &tc.grid_vc);
@@ -1264,11 +1273,15 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   }
   A.uinv = tc.pcr.inv[0];
   A.trace = nullptr;
+  A.trace_off = 0;
   if (knob_tile_trace()) {  // measurement only
     static unsigned long long* d_tr = nullptr;
     if (!d_tr) cudaMalloc(&d_tr, 64 * 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(d_tr, 0, 64 * 16 * sizeof(unsigned long long), s);
     A.trace = d_tr;
     A.trace_cta = std::atoi(std::getenv("CTRI_TILE_TRACE"));  // which CTA stamps (0 if not a number)
+    const char* off = std::getenv("CTRI_TILE_TRACE_OFF");        // its first stamped tile
+    A.trace_off = off ? std::atoi(off) : 0;
   }
   static const int vc_dbg = [] {  // experiment knob, read once per process
     const char* e = std::getenv("CTRI_VC_DBG");
@@ -1383,6 +1396,18 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
       std::fprintf(stderr, "[tile trace] fused finalise (ns): LL %.0f reduce %.0f correct+store %.0f "
                    "(correct %.0f fence %.0f sync %.0f)\n",
                    fw[0] / fcnt, fw[1] / fcnt, fw[2] / fcnt, fz[0] / fcnt, fz[1] / fcnt, fz[2] / fcnt);
+    double vw[3] = {0, 0, 0};
+    int vcnt = 0;
+    for (int i = 4; i < 60; ++i)  // chain: exchange shadow (heads + solver, next loads), x~ shadow
+      if (h[i * 16 + 12] && h[i * 16 + 7] && h[i * 16 + 13] && h[i * 16 + 14]) {
+        vw[0] += (double)(h[i * 16 + 12] - h[i * 16 + 2]);
+        vw[1] += (double)(h[i * 16 + 7] - h[i * 16 + 12]);
+        vw[2] += (double)(h[i * 16 + 13] - h[i * 16 + 14]);
+        ++vcnt;
+      }
+    if (vcnt)
+      std::fprintf(stderr, "[tile trace] chain (ns): heads+solver %.0f next-block loads %.0f (exchange shadow); "
+                   "wait+finalise %.0f (x~ shadow)\n", vw[0] / vcnt, vw[1] / vcnt, vw[2] / vcnt);
     if (cnt)
       std::fprintf(stderr,
                    "[tile trace] per tile (ns): ring_wait+lds %.0f thomas %.0f ex_wait %.0f pcr %.0f "
