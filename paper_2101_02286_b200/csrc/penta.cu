@@ -21,6 +21,7 @@
 #include <cstring>
 
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace ctri {
 
@@ -332,6 +333,49 @@ __global__ void __launch_bounds__(256) k_penta_window(const PentaWinArgs A) {
     }
 }
 
+// strided axis with an even row length: a thread owns a PAIR of adjacent columns (16-byte
+// loads and stores) and kPentaRows consecutive window rows, all loads in flight before the
+// first store (as k_window_pairs)
+__global__ void __launch_bounds__(256) k_penta_window_pairs(const PentaWinArgs A) {
+  const int64_t j = 2 * (blockIdx.x * 256ll + threadIdx.x);  // first column of the pair
+  const int64_t m = A.outer * A.inner;
+  if (j >= m) return;
+  const int64_t o = j / A.inner, c = j - o * A.inner, st = A.inner;
+  const int s = blockIdx.z;  // partition of the slab
+  double* xc = A.x + (o * A.vp + s) * A.n * st + c;
+  const double2 a0 = *reinterpret_cast<const double2*>(xc);
+  const double2 a1 = *reinterpret_cast<const double2*>(xc + st);
+  double2 n0 = make_double2(0.0, 0.0), n1 = make_double2(0.0, 0.0);
+  if (s + 1 < A.vp) {  // x~ of the next partition on this GPU
+    n0 = *reinterpret_cast<const double2*>(xc + A.n * st);
+    n1 = *reinterpret_cast<const double2*>(xc + (A.n + 1) * st);
+  } else if (A.next) {
+    n0 = *reinterpret_cast<const double2*>(A.next + j);
+    n1 = *reinterpret_cast<const double2*>(A.next + m + j);
+  } else if (A.wrap) {  // the first partition of the slab (itself when vp == 1)
+    const double* x0 = A.x + o * A.vp * A.n * st + c;
+    n0 = *reinterpret_cast<const double2*>(x0);
+    n1 = *reinterpret_cast<const double2*>(x0 + st);
+  }
+  const int64_t r0 = (int64_t)blockIdx.y * kPentaRows;
+  double2 v[kPentaRows];
+  double* pr[kPentaRows];
+#pragma unroll
+  for (int t = 0; t < kPentaRows; ++t) {
+    pr[t] = xc + (penta_row(A, r0 + t) + 2) * st;
+    if (r0 + t < A.rows) v[t] = *reinterpret_cast<const double2*>(pr[t]);
+  }
+#pragma unroll
+  for (int t = 0; t < kPentaRows; ++t)
+    if (r0 + t < A.rows) {
+      const int64_t k = penta_row(A, r0 + t);
+      const double s0 = __ldg(A.SR + k), s1 = __ldg(A.SR + A.N + k);
+      const double q0 = __ldg(A.SR + 2 * A.N + k), q1 = __ldg(A.SR + 3 * A.N + k);
+      dev::st_global_cs_v2(pr[t], v[t].x - (s0 * a0.x + s1 * a1.x) - (q0 * n0.x + q1 * n1.x),
+                           v[t].y - (s0 * a0.y + s1 * a1.y) - (q0 * n0.y + q1 * n1.y));
+    }
+}
+
 // contiguous solve axis: one warp per column, lanes along the rows
 __global__ void __launch_bounds__(256) k_penta_window_contig(const PentaWinArgs A) {
   const int64_t w = blockIdx.x * 8ll + (threadIdx.x >> 5);
@@ -477,9 +521,12 @@ cudaError_t launch_penta_window(const Plan& P, double* x, cudaStream_t s) {
     k_penta_window_contig<<<(unsigned)((A.outer + 7) / 8), 256, 0, s>>>(A);
   } else {
     const int64_t m = P.lay.m();
-    dim3 grid((unsigned)((m + 255) / 256), (unsigned)((A.rows + kPentaRows - 1) / kPentaRows),
+    const bool pairs = (A.inner % 2) == 0;
+    const int64_t cpb = pairs ? 512 : 256;  // columns per block
+    dim3 grid((unsigned)((m + cpb - 1) / cpb), (unsigned)((A.rows + kPentaRows - 1) / kPentaRows),
               (unsigned)A.vp);
-    k_penta_window<<<grid, 256, 0, s>>>(A);
+    if (pairs) k_penta_window_pairs<<<grid, 256, 0, s>>>(A);
+    else k_penta_window<<<grid, 256, 0, s>>>(A);
   }
   return cudaGetLastError();
 }
