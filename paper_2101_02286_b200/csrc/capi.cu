@@ -953,8 +953,10 @@ ctri_status deriv_group(std::vector<Plan*>& G, const double* const* f, double* c
   const Stencil5 st = make_stencil5(coef);
   bool fused = true;
   for (Plan* P : G) fused = fused && P->local_kernel == 1 && P->tile.deriv_ok;
-  const bool need_pack = (G[0]->p == 1 && fused) || (G[0]->p > 1 && !G[0]->p2p);
-  if (need_pack) {  // halo planes (with one partition: the slab's own wrap rows)
+  // halo planes for the host-issued exchange (with one partition the fused kernel loads the
+  // slab's own wrap rows by TMA, and the unfused stencil wraps by itself)
+  const bool need_pack = G[0]->p > 1 && !G[0]->p2p;
+  if (need_pack) {
     for (size_t r = 0; r < G.size(); ++r) {
       cudaError_t e = launch_pack_halo(*G[r], f[r], s);
       if (e != cudaSuccess) return fail(CTRI_ERR_CUDA, cudaGetErrorString(e));

@@ -215,10 +215,13 @@ __global__ void __launch_bounds__(NT, MINB)
     dev::mbar_expect_tx(bar, kSubBytes);
     for (int r = 0; r < SR; r += boxr)
       dev::tma_load_3d(dev::smem_u32(dst + (size_t)(r + HALO) * C), &tmap, col0, r0 + r, o, bar, pol);
-    if (DERIV) {  // stencil halo rows row0-2, row0-1 and row0+ROWS, +1 (zero-filled outside the slab)
-      dev::tma_load_3d(dev::smem_u32(dst), &hmap, col0, row0 - HALO, o, bar, pol);
-      dev::tma_load_3d(dev::smem_u32(dst + (size_t)(ROWS + HALO) * C), &hmap, col0, row0 + ROWS, o,
-                       bar, pol);
+    if (DERIV) {  // stencil halo rows row0-2, row0-1 and row0+ROWS, +1: zero-filled outside the
+                  // slab (and then taken from the halo planes), or with one partition the
+                  // periodic wrap rows n-2, n-1 / 0, 1 of the same column tile
+      const int lo = (A.halo_wrap && g == 0) ? (int)A.lay.n - HALO : row0 - HALO;
+      const int hi = (A.halo_wrap && (int)g == G - 1) ? 0 : row0 + ROWS;
+      dev::tma_load_3d(dev::smem_u32(dst), &hmap, col0, lo, o, bar, pol);
+      dev::tma_load_3d(dev::smem_u32(dst + (size_t)(ROWS + HALO) * C), &hmap, col0, hi, o, bar, pol);
     }
   };
   const int hsub = cl / CPS, lc = cl - (cl / CPS) * CPS;  // my sub-tile and chunk within it
@@ -526,7 +529,7 @@ __global__ void __launch_bounds__(NT, MINB)
     }
     dev::mbar_wait(dev::smem_u32(mbar + s), (uint32_t)(seq / SLOTS) & 1u);
     double* tile = ring + (size_t)s * RING;
-    if (DERIV) {
+    if (DERIV && !A.halo_wrap) {
       // slab-edge CTAs: the halo rows outside the slab come from the neighbour slabs (halo planes)
       const int64_t oo = t / A.tiles_per_outer;
       const int64_t cc0 = (t - oo * A.tiles_per_outer) * C;
@@ -1299,6 +1302,8 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   // partition they are this slab's own rows (periodic wrap), packed into send_hi / send_lo
   A.halo_lo = (P.p == 1) ? P.send_hi : P.halo_lo;
   A.halo_hi = (P.p == 1) ? P.send_lo : P.halo_hi;
+  // one partition: the periodic wrap rows come straight from the slab by TMA (no halo planes)
+  A.halo_wrap = (P.p == 1) ? 1 : 0;
   const bool fused = !deriv && P.fused;
   const bool vchain = !deriv && P.vchain;
   // nparts > 1 without the chain: the window rows are stored with an L2 evict-last hint so the
