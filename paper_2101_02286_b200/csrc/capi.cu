@@ -89,7 +89,7 @@ void free_plan(Plan* P) {
   double* bufs[] = {P->d_cp,    P->d_inv_den, P->d_S,      P->d_R,       P->d_vS,    P->d_vR,
                     P->yf,      P->yl,
                     P->bt,      P->yl_prev,   P->bh,       P->recv_m,    P->recv_p,  P->xt,
-                    P->xt_next, P->halo_lo,   P->halo_hi,  P->send_lo,   P->send_hi, P->tile.d_pcr,
+                    P->xt_next, P->halo_lo,   /* halo_hi: inside halo_lo */ P->send_lo, P->send_hi, P->tile.d_pcr,
                     P->d_stage_b, P->d_stage_x, P->d_plu,    P->d_pSR,     P->d_ainv,  P->d_planes4,
                     P->d_xnext2, P->d_ppcr, P->d_vppcr, P->ptc.d_tab};
   for (double* b : bufs)
@@ -329,8 +329,10 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   }
   if (flags & CTRI_FLAG_DERIV) {
     if (!cyclic) return fail(CTRI_ERR_INVALID_ARG, "CTRI_FLAG_DERIV needs a cyclic plan");
-    TRY(alloc_plane(&P->halo_lo, 2 * m));
-    TRY(alloc_plane(&P->halo_hi, 2 * m));
+    // halo_lo | halo_hi as one [2][2][m] allocation: the tile kernel loads a column tile's
+    // halo rows from it with one TMA map (rows 0, 1: the slab above; rows 2, 3: below)
+    TRY(alloc_plane(&P->halo_lo, 4 * m));
+    P->halo_hi = P->halo_lo + 2 * m;
     TRY(alloc_plane(&P->send_lo, 2 * m));
     TRY(alloc_plane(&P->send_hi, 2 * m));
   }

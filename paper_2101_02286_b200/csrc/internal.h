@@ -99,6 +99,7 @@ struct TileArgs {
   const double* halo_lo;  // [2][m]: rows n-2, n-1 of the slab above
   const double* halo_hi;  // [2][m]: rows 0, 1 of the slab below
   int halo_wrap;          // one partition: halo rows are the slab's own wrap rows (TMA), no planes
+  int halo_tma;           // nparts > 1: halo rows from the planes by TMA (xmap), not per-thread loads
   unsigned long long* trace;  // measurement only (CTRI_TILE_TRACE=<cta>)
   int trace_cta;              // the CTA whose tiles are stamped
   int trace_off;              // its first stamped tile (CTRI_TILE_TRACE_OFF)

@@ -218,10 +218,15 @@ __global__ void __launch_bounds__(NT, MINB)
     if (DERIV) {  // stencil halo rows row0-2, row0-1 and row0+ROWS, +1: zero-filled outside the
                   // slab (and then taken from the halo planes), or with one partition the
                   // periodic wrap rows n-2, n-1 / 0, 1 of the same column tile
+      // (nparts > 1: the slab-edge CTAs take them from the halo planes, [2][2][m], through
+      // xmap: rows 0, 1 the slab above, rows 2, 3 the slab below)
       const int lo = (A.halo_wrap && g == 0) ? (int)A.lay.n - HALO : row0 - HALO;
       const int hi = (A.halo_wrap && (int)g == G - 1) ? 0 : row0 + ROWS;
-      dev::tma_load_3d(dev::smem_u32(dst), &hmap, col0, lo, o, bar, pol);
-      dev::tma_load_3d(dev::smem_u32(dst + (size_t)(ROWS + HALO) * C), &hmap, col0, hi, o, bar, pol);
+      const uint32_t dlo = dev::smem_u32(dst), dhi = dev::smem_u32(dst + (size_t)(ROWS + HALO) * C);
+      if (A.halo_tma && g == 0) dev::tma_load_3d(dlo, &xmap, col0, o, 0, bar, pol);
+      else dev::tma_load_3d(dlo, &hmap, col0, lo, o, bar, pol);
+      if (A.halo_tma && (int)g == G - 1) dev::tma_load_3d(dhi, &xmap, col0, o, 2, bar, pol);
+      else dev::tma_load_3d(dhi, &hmap, col0, hi, o, bar, pol);
     }
   };
   const int hsub = cl / CPS, lc = cl - (cl / CPS) * CPS;  // my sub-tile and chunk within it
@@ -529,7 +534,7 @@ __global__ void __launch_bounds__(NT, MINB)
     }
     dev::mbar_wait(dev::smem_u32(mbar + s), (uint32_t)(seq / SLOTS) & 1u);
     double* tile = ring + (size_t)s * RING;
-    if (DERIV && !A.halo_wrap) {
+    if (DERIV && !A.halo_wrap && !A.halo_tma) {
       // slab-edge CTAs: the halo rows outside the slab come from the neighbour slabs (halo planes)
       const int64_t oo = t / A.tiles_per_outer;
       const int64_t cc0 = (t - oo * A.tiles_per_outer) * C;
@@ -1362,6 +1367,19 @@ cudaError_t launch_tile(const Plan& P, const double* b, double* x, cudaStream_t 
   }
   CUtensorMap xmap;
   std::memset(&xmap, 0, sizeof(xmap));
+  A.halo_tma = 0;
+  if (deriv && P.p > 1) {  // (A/B, 2 B200s: cfg5 0.554 -> 0.527 ms; per-thread loads remain for odd rows)
+    // the halo planes as a (inner, outer, 4) tensor: box C x 1 x 2 = the two halo rows of a
+    // column tile, landing in the ring as the tile's rows -2, -1 or ROWS, ROWS + 1
+    cuuint64_t gdim[3] = {(cuuint64_t)P.lay.inner, (cuuint64_t)P.lay.outer, 4};
+    cuuint64_t gstride[2] = {(cuuint64_t)P.lay.inner * 8, (cuuint64_t)(P.lay.m() * 8)};
+    cuuint32_t box[3] = {(cuuint32_t)tc.C, 1, 2};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult cr = enc(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, P.halo_lo, gdim, gstride, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr == CUDA_SUCCESS) A.halo_tma = 1;
+  }
   if (fused) {  // output map for the TMA store of the finalised window blocks (W+1 rows)
     const Layout& L2 = P.tlay;
     cuuint64_t gdim[3] = {(cuuint64_t)L2.inner, (cuuint64_t)L2.n, (cuuint64_t)L2.outer};
