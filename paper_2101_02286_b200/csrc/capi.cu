@@ -892,8 +892,11 @@ ctri_status penta_solve_group(std::vector<Plan*>& G, const double* const* b, dou
                               cudaStream_t s) {
   Plan& P0 = *G[0];
   TRY(check_poisoned(G));
-  for (size_t r = 0; r < G.size(); ++r)
+  for (size_t r = 0; r < G.size(); ++r) {
     if (!b[r] || !x[r]) return fail(CTRI_ERR_INVALID_ARG, "NULL b or x");
+    if (((uintptr_t)b[r] | (uintptr_t)x[r]) & 15)  // TMA tiles, 16-byte window pairs
+      return fail(CTRI_ERR_INVALID_ARG, "b and x must be 16-byte aligned");
+  }
   for (Plan* P : G) P->solves++;
   record(P0, EV_START, s);
   for (size_t r = 0; r < G.size(); ++r) {

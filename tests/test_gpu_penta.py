@@ -270,3 +270,24 @@ def test_penta_virtual_rows_delta_at_edges(r):
             assert st["vparts"] == 2 and st["reduced_rows"] == 4
             ref = oracle.penta_solve(b, 0, bands, cyclic)
             assert np.max(np.abs(x - ref)) < 1e-14 * max(1.0, np.max(np.abs(ref)))
+
+
+def test_misaligned_slabs_rejected():
+    """The tile kernels stream b by TMA and the window passes move 16-byte column pairs: a slab
+    pointer that is only 8-byte aligned is refused with INVALID_ARG (tridiagonal and
+    pentadiagonal plans), never run."""
+    import torch
+
+    from paper_2101_02286_b200 import ctri
+    dims = (2048, 1, 32)
+    n = 2048 * 32
+    buf = torch.zeros(n + 1, dtype=torch.float64, device="cuda:0")
+    ok = torch.zeros(n, dtype=torch.float64, device="cuda:0")
+    for bands in [(1 / 3, 1.0, 1 / 3), BANDS[2]]:
+        plan = ctri.Plan(dims, 0, 1, 0, bands)
+        with pytest.raises(ctri.CtriError, match="INVALID_ARG"):
+            plan.solve(buf[1:], ok)
+        with pytest.raises(ctri.CtriError, match="INVALID_ARG"):
+            plan.solve(ok, buf[1:])
+        plan.solve(ok, buf[:n])  # (aligned: runs)
+        plan.close()
