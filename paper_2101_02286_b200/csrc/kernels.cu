@@ -238,6 +238,58 @@ __global__ void __launch_bounds__(256) k_window_contig(const WindowArgs A) {
   }
 }
 
+// contiguous axis, window of at most 96 rows per partition (the usual case): persistent warps
+// walk the (column, partition) units; a lane's rows, their offsets and their S, R are the same
+// for every unit, so they are computed once, and two units are loaded before either is
+// corrected (the per-unit version spent its issue slots on index arithmetic: ncu cfg4 index 2,
+// 56% issue-busy at 3.2 TB/s)
+constexpr int kWinUnitRows = 3;  // rows per lane: 96 >= the window
+__global__ void __launch_bounds__(256) k_window_contig_units(const WindowArgs A) {
+  const int lane = threadIdx.x & 31;
+  const int64_t units = A.outer * A.vp;
+  const int64_t nw = (int64_t)gridDim.x * 8;
+  const int vsh = __ffs(A.vp) - 1;  // vp is a power of two
+  int64_t roff[kWinUnitRows];
+  double sv[kWinUnitRows], rv[kWinUnitRows];
+  bool act[kWinUnitRows];
+#pragma unroll
+  for (int u = 0; u < kWinUnitRows; ++u) {
+    const int64_t ry = lane + 32 * u;
+    act[u] = ry < A.rows;
+    roff[u] = act[u] ? window_row(A, ry) : 0;
+    sv[u] = act[u] ? __ldg(A.S + roff[u] - 1) : 0.0;
+    rv[u] = act[u] ? __ldg(A.R + roff[u] - 1) : 0.0;
+  }
+  for (int64_t w0 = blockIdx.x * 8ll + (threadIdx.x >> 5); w0 < units; w0 += 2 * nw) {
+    double v[2][kWinUnitRows], xa[2], xn[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int64_t w = w0 + q * nw;
+      xa[q] = xn[q] = 0.0;
+      if (w >= units) continue;
+      const int64_t o = w >> vsh;
+      const int sp = (int)(w - (o << vsh));
+      const double* xs = A.x + w * A.nv;
+      xa[q] = xs[0];
+      if (sp + 1 < A.vp) xn[q] = xs[A.nv];
+      else if (A.next) xn[q] = A.next[o];
+      else if (A.wrap) xn[q] = A.x[(o << vsh) * A.nv];
+#pragma unroll
+      for (int u = 0; u < kWinUnitRows; ++u)
+        if (act[u]) v[q][u] = xs[roff[u]];
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int64_t w = w0 + q * nw;
+      if (w >= units) continue;
+      double* xs = A.x + w * A.nv;
+#pragma unroll
+      for (int u = 0; u < kWinUnitRows; ++u)
+        if (act[u]) xs[roff[u]] = v[q][u] - sv[u] * xa[q] - rv[u] * xn[q];
+    }
+  }
+}
+
 cudaError_t launch_window(const Plan& P, double* x, const double* next, cudaStream_t s) {
   WindowArgs A;
   A.x = x;
@@ -256,7 +308,13 @@ cudaError_t launch_window(const Plan& P, double* x, const double* next, cudaStre
   if (A.rows <= 0) return cudaSuccess;
   if (A.inner == 1) {
     const int64_t warps = A.outer * A.vp;
-    k_window_contig<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(A);
+    if (A.rows <= 32 * kWinUnitRows && (A.vp & (A.vp - 1)) == 0) {
+      // persistent: 6 blocks of 8 warps per SM, every warp several units
+      const int64_t blocks = std::min<int64_t>((warps + 15) / 16, (int64_t)P.num_sms * 6);
+      k_window_contig_units<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(A);
+    } else {
+      k_window_contig<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(A);
+    }
   } else {
     const int64_t m = P.lay.m();
     const bool pairs = (A.inner % 2) == 0;  // (ncu, cold: cfg3 slab 18.1 -> 16.7 us, cfg2 N=2 62 -> 57 us)
