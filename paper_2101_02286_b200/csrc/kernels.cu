@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(256) k_window_contig(const WindowArgs A) {
 // corrected (the per-unit version spent its issue slots on index arithmetic: ncu cfg4 index 2,
 // 56% issue-busy at 3.2 TB/s)
 constexpr int kWinUnitRows = 3;  // rows per lane: 96 >= the window
+constexpr int kWinUnroll = 4;    // units per warp in flight
 __global__ void __launch_bounds__(256) k_window_contig_units(const WindowArgs A) {
   const int lane = threadIdx.x & 31;
   const int64_t units = A.outer * A.vp;
@@ -260,10 +261,10 @@ __global__ void __launch_bounds__(256) k_window_contig_units(const WindowArgs A)
     sv[u] = act[u] ? __ldg(A.S + roff[u] - 1) : 0.0;
     rv[u] = act[u] ? __ldg(A.R + roff[u] - 1) : 0.0;
   }
-  for (int64_t w0 = blockIdx.x * 8ll + (threadIdx.x >> 5); w0 < units; w0 += 2 * nw) {
-    double v[2][kWinUnitRows], xa[2], xn[2];
+  for (int64_t w0 = blockIdx.x * 8ll + (threadIdx.x >> 5); w0 < units; w0 += kWinUnroll * nw) {
+    double v[kWinUnroll][kWinUnitRows], xa[kWinUnroll], xn[kWinUnroll];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < kWinUnroll; ++q) {
       const int64_t w = w0 + q * nw;
       xa[q] = xn[q] = 0.0;
       if (w >= units) continue;
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(256) k_window_contig_units(const WindowArgs A)
         if (act[u]) v[q][u] = xs[roff[u]];
     }
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < kWinUnroll; ++q) {
       const int64_t w = w0 + q * nw;
       if (w >= units) continue;
       double* xs = A.x + w * A.nv;
@@ -310,7 +311,7 @@ cudaError_t launch_window(const Plan& P, double* x, const double* next, cudaStre
     const int64_t warps = A.outer * A.vp;
     if (A.rows <= 32 * kWinUnitRows && (A.vp & (A.vp - 1)) == 0) {
       // persistent: 6 blocks of 8 warps per SM, every warp several units
-      const int64_t blocks = std::min<int64_t>((warps + 15) / 16, (int64_t)P.num_sms * 6);
+      const int64_t blocks = std::min<int64_t>((warps + 8 * kWinUnroll - 1) / (8 * kWinUnroll), (int64_t)P.num_sms * 6);
       k_window_contig_units<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(A);
     } else {
       k_window_contig<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(A);
