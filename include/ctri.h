@@ -183,8 +183,13 @@ ctri_status ctri_plan_create_loopback(ctri_plan* plans, int nparts, const int64_
  * for cyclic non-power-of-two nparts, P:271 / P:294 -- the fold, an x~ round) or, with
  * CTRI_FLAG_ALLGATHER, by ONE all-gather round and plan-time rows of its inverse (nparts <= 8).
  * The local solve runs on chip (2x2-block PCR of 32-row chunk heads in thread-block clusters)
- * for strided slabs of 256..2048 rows, and with nparts == 1 for longer slabs as n/1024
- * partitions of one GPU; column-serial otherwise (contiguous axis, other sizes).
+ * for strided slabs of 256..2048 rows, and for longer strided slabs (n a power-of-two multiple
+ * of 1024, at most 8 of them) as n/1024 partitions of one GPU: with nparts == 1 their reduced
+ * system is solved on the GPU, with nparts > 1 (solve index 0, nparts * n/1024 <= 16, not
+ * CTRI_FLAG_ALLGATHER) they become virtual block rows of the distributed reduced system
+ * (rows of one GPU exchange through its own mailbox; ctri_get_stats reports vparts and
+ * reduced_rows); column-serial otherwise (contiguous axis, other sizes).  b and x must be
+ * 16-byte aligned (INVALID_ARG otherwise).
  * The plan is used with ctri_solve / ctri_solve_loopback / ctri_solve_host /
  * ctri_get_stats / ctri_plan_destroy like a tridiagonal one.  Errors: INVALID_ARG (as
  * ctri_plan_create), PARTITION_TOO_SMALL (n < 6 or N % nparts), UNSUPPORTED (nparts > 8,
