@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--penta", action="store_true",
                     help="pentadiagonal system (r = 2, SURVEY N3) on the config's grid: Lele's "
                          "tenth-order compact LHS (1/20, 1/2, 1, 1/2, 1/20)")
+    ap.add_argument("--no-phase-events", action="store_true",
+                    help="measurement: the plan without CTRI_FLAG_TIMING (no per-phase events between "
+                         "the kernels of a solve; comm_us and the live local-kernel time unavailable)")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch every solve from the host instead of replaying one CUDA graph")
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -308,7 +311,11 @@ def main():
         sd = args.sd
         name = f"custom {dims} solve index {sd}"
     deriv = args.config == "cfg5"
-    flags = CTRI_FLAG_TIMING | (CTRI_FLAG_DERIV if deriv else 0)
+    # the timed region runs the plan a user runs: no per-phase events (CTRI_FLAG_TIMING puts an
+    # event node between the kernels of a captured solve, which costs the programmatic launch
+    # overlap: 14-20 us per multi-kernel solve, profiles/r2_events_ab.txt); a second plan with
+    # the events measures the per-kernel times in its own timed pass (roofline, comm_us)
+    flags = CTRI_FLAG_DERIV if deriv else 0
     if world > 1 and args.reduced == "fused":
         flags |= ctri.CTRI_FLAG_FUSED_REDUCED
     elif world > 1 and args.reduced == "allgather":
@@ -328,37 +335,47 @@ def main():
             raise SystemExit("--penta applies to the solve configs (cfg1-cfg4)")
         bands = (1 / 20, 1 / 2, 1.0, 1 / 2, 1 / 20)
         name = f"pentadiagonal (Lele 10th-order LHS, r = 2): {name}"
-    if world > 1:
-        plan = pdist.plan_from_process_group(dims, sd, bands, flags=flags)
-    else:
-        plan = ctri.Plan(dims, sd, 1, 0, bands=bands, flags=flags)
+    def make_plan(fl):
+        if world > 1:
+            return pdist.plan_from_process_group(dims, sd, bands, flags=fl)
+        return ctri.Plan(dims, sd, 1, 0, bands=bands, flags=fl)
+
+    plan = make_plan(flags)
     lshape = plan.local_shape
     b = workloads.device_uniform(lshape, 1000 * 2 + rank, dev)
     x = torch.empty_like(b)
     stream = torch.cuda.current_stream(dev)
     pts_local = b.numel()
 
-    def step():
-        if coef is not None:
-            plan.compact_apply(coef, b, x)
-        elif deriv:
-            plan.deriv(b, x)
-        else:
-            plan.solve(b, x)
+    def solve_with(pl):
+        def step():
+            if coef is not None:
+                pl.compact_apply(coef, b, x)
+            elif deriv:
+                pl.deriv(b, x)
+            else:
+                pl.solve(b, x)
+        return step
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    timed_step = step
-    if not args.no_graph:  # one solve captured as a CUDA graph, replayed once per step
-        graph = torch.cuda.CUDAGraph()
+    def prepare(step):
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        if args.no_graph:
+            return step
+        graph = torch.cuda.CUDAGraph()  # one solve captured as a CUDA graph, replayed per step
         with torch.cuda.graph(graph):
             step()
         torch.cuda.synchronize()
         for _ in range(max(3, args.warmup)):
             graph.replay()
         torch.cuda.synchronize()
-        timed_step = graph.replay
+        prepare.graphs.append(graph)
+        return graph.replay
+
+    prepare.graphs = []
+    step = solve_with(plan)
+    timed_step = prepare(step)
     st0 = plan.stats()
     sampler = None
     if rank == 0:
@@ -394,22 +411,31 @@ def main():
     if world > 1:
         dist.barrier()
     ms_rank = e0.elapsed_time(e1) / args.steps
-    # per-kernel / per-phase device times of the last solve (plan's own events, same stream)
-    st = plan.stats()
-    # average local-kernel duration: re-run a short series with per-solve stats
+    ms = pdist.max_over_ranks(ms_rank, dev) if world > 1 else ms_rank
+    # per-kernel / per-phase device times: a second plan with phase events (CTRI_FLAG_TIMING),
+    # its own timed pass of the same steps (barrier + synchronize, graph replays back to back);
+    # the plan's events around the local kernel in its last solve, and the mean over 50
+    # isolated solves (each after a synchronize) beside it
+    tplan = plan if args.no_phase_events else make_plan(flags | CTRI_FLAG_TIMING)
+    tstep = solve_with(tplan)
+    treplay = prepare(tstep)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        treplay()
+    torch.cuda.synchronize()
+    st = tplan.stats()
     for _ in range(min(50, args.steps)):
-        step()
-        local_us.append(plan.stats()["t_local_us"])
+        tstep()
+        local_us.append(tplan.stats()["t_local_us"])
     if sampler:
         sampler.stop()
-    ms = pdist.max_over_ranks(ms_rank, dev) if world > 1 else ms_rank
-    # the local kernel's duration live inside the timed region: the plan's own events around it
-    # in the last timed solve (back to back with the others, on the solve stream); the mean over
-    # 50 isolated solves (each after a synchronize) is reported beside it
     t_local_iso = statistics.mean(local_us)
     t_local_iso = pdist.max_over_ranks(t_local_iso, dev) if world > 1 else t_local_iso
     t_local = st["t_local_us"] if st["t_local_us"] > 0 else t_local_iso
-    t_src = "CUDA events around the kernel in the last timed solve (graph replay)"
+    t_src = ("CUDA events (the plan's phase events) around the kernel in the last of a second timed "
+             "pass of the same steps with a phase-event plan (graph replay)")
     if one_launch:
         t_local = 1e3 * statistics.mean(a.elapsed_time(b) for a, b in kev)
         t_src = "CUDA events around every timed step (the solve is one kernel launch)"
@@ -512,6 +538,8 @@ def main():
                              "backsub_kernel": back}) if p > 1 else None,
                 "clocks": sampler.summary() if sampler else None}
         print(json.dumps(line), flush=True)
+    if tplan is not plan:
+        tplan.close()
     plan.close()
     if world > 1:
         dist.barrier()
