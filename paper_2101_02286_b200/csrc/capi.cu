@@ -165,7 +165,19 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
                                                   n / (P->lay.inner == 1 ? 2048 : 1024))
                          : 1;
     if (vp_env) want = std::atoi(vp_env);
-    if (want > 1 && want <= 8 && is_pow2(want) && n % want == 0 && n / want >= 512) P->vp = want;
+    if (want > 1 && want <= 8 && is_pow2(want) && n % want == 0 && n / want >= 512 &&
+        (vp_env || is_pow2(n / want))) {
+      P->vp = want;
+    } else if (!vp_env && want > 1 && P->lay.inner >= 16) {
+      // n not a power-of-two multiple of 1024 (e.g. 6144): the most partitions (<= 8) whose
+      // length is a power of two the tile kernel takes; their reduced system (vp not a power of
+      // two) is solved with a plan-time dense inverse in k_reduced_local, without the chain
+      for (int w = std::min(want, 8); w > 1; --w)
+        if (n % w == 0 && is_pow2(n / w) && n / w >= 512) {
+          P->vp = w;
+          break;
+        }
+    }
   }
   // nparts > 1: "virtual rows" -- every rank's slab is solved as vp partitions too and the
   // reduced system has nparts * vp rows, exchanged over the same LL P2P path (rows on the same
@@ -203,7 +215,7 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   // system across the GPUs keeps the paper's one row per rank.
   // (two levels are opt-in, CTRI_TWO_LEVEL=1: measured on 2 and 4 B200s the in-kernel window
   // work cost more than the virtual rows' window pass it saves -- DESIGN.md section 5)
-  P->vchain = tile_ok && !P->tile.contig && P->vp > 1 && P->tile.vc_ok && !knob_no_vchain() &&
+  P->vchain = tile_ok && !P->tile.contig && P->vp > 1 && is_pow2(P->vp) && P->tile.vc_ok && !knob_no_vchain() &&
               !knob_copy_only() && (p == 1 || knob_two_level());
   P->rvp = (p > 1 && P->vchain) ? 1 : P->vp;
   const int64_t rn = n / P->rvp;  // rows per reduced-system row's partition
@@ -238,6 +250,11 @@ ctri_status plan_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, con
   }
   if (P->gpcr.stages > CTRI_MAX_STAGES) return fail(CTRI_ERR_UNSUPPORTED, "too many PCR stages");
   P->inv_closure = P->gpcr.inv[0];
+  // one GPU, a cyclic vp-row system with vp not a power of two: k_reduced_local applies its
+  // plan-time inverse (the reduced matrix of Eqs. Li_hat..Ui_hat, dense Gaussian elimination)
+  if (p == 1 && P->vp > 1 && cyclic && !is_pow2(P->vp) &&
+      !reduced_inverse(pr, true, L, D, U, pivot_threshold(P->bands), &P->ainv, &fe))
+    return fail((ctri_status)fe.code, fe.detail);
   P->window = backsub_window(pt);
   // two levels: the slab's internal interfaces 1..vp-1 as an acyclic vp-row system whose row 0
   // (the GPU interface, not part of D_i) is decoupled: L^ = D^ - 1 = U^ = 0 there, no coupling

@@ -349,6 +349,8 @@ struct LocalRedArgs {
   double l, u;
   const double *S, *R, *yf, *yl, *bt;
   double alpha[4 * 8], gamma[4 * 8], inv[8];  // [stage][row], vp <= 8
+  int dense;                                  // cyclic, vp not a power of two: x~ = A^-1 b^
+  double ainv[8 * 8];                         // [row][row] of the vp-row reduced matrix
 };
 
 __device__ __forceinline__ double bh_get(const double (&bh)[8], int v) {
@@ -372,6 +374,20 @@ __global__ void __launch_bounds__(128) k_reduced_local(const LocalRedArgs A, dou
     const int vl = (v + vp - 1) % vp;
     const double ylp = (A.cyclic || v > 0) ? A.yl[(o * vp + vl) * A.inner + c] : 0.0;
     bh[v] = A.bt[pj] - A.l * ylp - A.u * A.yf[pj];
+  }
+  if (A.dense) {  // x~_v = sum_w (A^-1)_{vw} b^_w (plan-time inverse; no PCR partner pattern
+                  // for a cyclic system of vp rows when vp is not a power of two)
+    double xv[8];
+    for (int v = 0; v < 8; ++v) {
+      if (v >= vp) break;
+      double acc = 0.0;
+      for (int w = 0; w < 8; ++w)
+        if (w < vp) acc += A.ainv[v * vp + w] * bh[w];
+      xv[v] = acc;
+    }
+    for (int v = 0; v < 8; ++v)
+      if (v < vp) x[((o * vp + v) * A.nv) * A.inner + c] = xv[v];
+    return;
   }
   for (int k = 0; k < A.q; ++k) {
     const int s = 1 << k;
@@ -417,12 +433,19 @@ cudaError_t launch_reduced_local(const Plan& P, double* x, cudaStream_t s) {
   A.yl = P.yl;
   A.bt = P.bt;
   for (int i = 0; i < 32; ++i) A.alpha[i] = A.gamma[i] = 0.0;
+  for (int i = 0; i < 64; ++i) A.ainv[i] = 0.0;
+  A.dense = (P.cyclic && (P.vp & (P.vp - 1)) != 0) ? 1 : 0;
+  if (A.dense) {  // (the plan holds A^-1 of the vp-row system; no PCR tables)
+    if (P.ainv.size() != (size_t)P.vp * P.vp) return cudaErrorInvalidValue;
+    A.q = 0;
+    for (int i = 0; i < P.vp * P.vp; ++i) A.ainv[i] = P.ainv[i];
+  }
   for (int kk = 0; kk < A.q && kk < 4; ++kk)
     for (int v = 0; v < P.vp; ++v) {
       A.alpha[kk * 8 + v] = P.gpcr.alpha[(size_t)kk * P.vp + v];
       A.gamma[kk * 8 + v] = P.gpcr.gamma[(size_t)kk * P.vp + v];
     }
-  for (int v = 0; v < 8; ++v) A.inv[v] = v < P.vp ? P.gpcr.inv[v] : 0.0;
+  for (int v = 0; v < 8; ++v) A.inv[v] = (v < P.vp && !A.dense) ? P.gpcr.inv[v] : 0.0;
   const int64_t m = P.lay.m();
   k_reduced_local<<<blocks_for(m, 128), 128, 0, s>>>(A, x);
   return cudaGetLastError();

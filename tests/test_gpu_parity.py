@@ -638,3 +638,19 @@ def test_p2p_deadline_poisons_plan(monkeypatch):
         g.solve(bs, xs)
     assert e.value.name == "CTRI_ERR_CUDA" and "destroy" in str(e.value)
     g.close()
+
+
+@pytest.mark.parametrize("n,vp", [(6144, 6), (5120, 5), (7168, 7), (12288, 6)])
+@pytest.mark.parametrize("bands,cyclic", [(SYM, True), ((0.45, 1.0, 0.45), True), (NONSYM, False)])
+def test_one_gpu_non_power_of_two_partitions(n, vp, bands, cyclic):
+    """One GPU, n not a power-of-two multiple of 1024: the slab is solved on chip as vp
+    partitions of a power-of-two length (6 x 1024, 5 x 1024, 7 x 1024, 6 x 2048) instead of by
+    the column-serial kernel; the cyclic vp-row reduced system (vp not a power of two) by its
+    plan-time inverse, the acyclic one by PCR; then the window pass.  Every element vs the
+    oracle."""
+    b = workloads.uniform((n, 1, 32), 300 + vp)
+    x, st = gpu_solve(b, 0, 1, bands, cyclic, return_stats=True)
+    assert st["local_kernel"] == 1 and st["vparts"] == vp and st["vchain"] == 0, st
+    ref = oracle.cyclic_solve(b, 0, bands) if cyclic else oracle.acyclic_solve(b, 0, bands)
+    assert rel_err(x, ref, 0) < TOL_REL
+    assert residual(x, b, 0, bands, cyclic) < TOL_RES
