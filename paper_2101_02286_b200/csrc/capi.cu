@@ -412,6 +412,12 @@ ctri_status penta_init(Plan* P, const int64_t gd[3], int sd, int p, int rank, co
   if (vp_fit && (p == 1 || (P->lay.outer == 1 && !(flags & CTRI_FLAG_ALLGATHER) &&
                             p * (n / 1024) <= kMaxP2PRanks)))
     P->vp = (int)(n / 1024);
+  if (p == 1 && P->vp == 1 && !vp_fit && P->lay.inner >= 32 && n > 2048 && !knob_penta_serial())
+    for (int w = 8; w > 1; --w)  // e.g. 6144 = 6 x 1024: power-of-two partitions, dense reduced solve
+      if (n % w == 0 && is_pow2(n / w) && n / w >= 256 && n / w <= 2048) {
+        P->vp = w;
+        break;
+      }
   if (const char* e = std::getenv("CTRI_VPARTS"))
     if (*e && P->vp > 1) {
       const int want = std::atoi(e);

@@ -328,6 +328,7 @@ struct Plan {
   PentaPcr vppcr;                  // nparts == 1, vp > 1: 2x2-block PCR over the vp partitions
   double *d_vppcr = nullptr;       // [stages][vp][4] alpha | gamma, [vp][4] fold
   bool ppcr = false;               // pairwise 2x2-block PCR reduced solve (else all-gather)
+  bool pdense = false;             // one GPU, cyclic, vp not a power of two: d_vppcr holds A^-1
   int ppcr_steps = 0;
   double *d_ppcr = nullptr;        // this rank's [step][8] A0 | A1 and fold [4]
   std::vector<P2PStep> pstep;      // this rank's partners per block-PCR step

@@ -428,15 +428,26 @@ ctri_status penta_plan_tables(Plan* P, cudaStream_t s, std::string* why) {
   }
   P->ainv = inv;
   if (P->p == 1) std::memcpy(P->pcinv, inv.data(), sizeof(P->pcinv));
+  P->pdense = false;
   if (P->p == 1 && P->vp > 1) {  // 2x2-block PCR over the vp partitions of this GPU (R20)
-    if (!penta_block_pcr(P->vp, P->cyclic != 0, pt, guard, &P->vppcr, &fe)) {
-      *why = fe.detail;
-      return (ctri_status)fe.code;
-    }
     std::vector<double> t;
-    t.insert(t.end(), P->vppcr.alpha.begin(), P->vppcr.alpha.end());
-    t.insert(t.end(), P->vppcr.gamma.begin(), P->vppcr.gamma.end());
-    t.insert(t.end(), P->vppcr.fold.begin(), P->vppcr.fold.end());
+    if (P->cyclic && (P->vp & (P->vp - 1)) != 0) {
+      // cyclic with vp not a power of two: the plan-time inverse of the 2vp x 2vp block system
+      if (!penta_reduced_inverse(P->vp, true, pt, guard, &t, &fe)) {
+        *why = fe.detail;
+        return (ctri_status)fe.code;
+      }
+      P->vppcr = PentaPcr();
+      P->pdense = true;
+    } else {
+      if (!penta_block_pcr(P->vp, P->cyclic != 0, pt, guard, &P->vppcr, &fe)) {
+        *why = fe.detail;
+        return (ctri_status)fe.code;
+      }
+      t.insert(t.end(), P->vppcr.alpha.begin(), P->vppcr.alpha.end());
+      t.insert(t.end(), P->vppcr.gamma.begin(), P->vppcr.gamma.end());
+      t.insert(t.end(), P->vppcr.fold.begin(), P->vppcr.fold.end());
+    }
     if (P->d_vppcr) cudaFree(P->d_vppcr);
     P->d_vppcr = nullptr;
     ctri_status st = upload_vec(&P->d_vppcr, t, s);
@@ -539,7 +550,7 @@ __global__ void __launch_bounds__(128) k_penta_reduced_local(double* __restrict_
                                                              const double* __restrict__ planes4,
                                                              const double* __restrict__ tab,
                                                              int64_t outer, int64_t nv, int64_t inner,
-                                                             int vp, int stages, int cyclic) {
+                                                             int vp, int stages, int cyclic, int dense) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t m = outer * inner;
   if (j >= m) return;
@@ -552,6 +563,21 @@ __global__ void __launch_bounds__(128) k_penta_reduced_local(double* __restrict_
     const bool lft = cyclic || v > 0;
     b0[v] = planes4[pj] - (lft ? planes4[2 * pm + pl] : 0.0);
     b1[v] = planes4[pm + pj] - (lft ? planes4[3 * pm + pl] : 0.0);
+  }
+  if (dense) {  // cyclic, vp not a power of two: x~ = (A^)^-1 b^ with the plan-time inverse
+                // (block row v, component r at index 2v + r)
+    const int n2 = 2 * vp;
+    for (int v = 0; v < vp; ++v) {
+      double a0 = 0.0, a1 = 0.0;
+      for (int w = 0; w < vp; ++w) {
+        a0 += tab[(2 * v) * n2 + 2 * w] * b0[w] + tab[(2 * v) * n2 + 2 * w + 1] * b1[w];
+        a1 += tab[(2 * v + 1) * n2 + 2 * w] * b0[w] + tab[(2 * v + 1) * n2 + 2 * w + 1] * b1[w];
+      }
+      double* xs = x + (o * vp + v) * nv * inner + c;
+      xs[0] = a0;
+      xs[inner] = a1;
+    }
+    return;
   }
   for (int k = 0; k < stages; ++k) {
     const int sh = 1 << k;
@@ -586,7 +612,8 @@ __global__ void __launch_bounds__(128) k_penta_reduced_local(double* __restrict_
 cudaError_t launch_penta_reduced_local(const Plan& P, double* x, cudaStream_t s) {
   const int64_t m = P.lay.m();
   k_penta_reduced_local<<<(unsigned)((m + 127) / 128), 128, 0, s>>>(
-      x, P.d_planes4, P.d_vppcr, P.lay.outer, P.tlay.n, P.lay.inner, P.vp, P.vppcr.stages, P.cyclic);
+      x, P.d_planes4, P.d_vppcr, P.lay.outer, P.tlay.n, P.lay.inner, P.vp, P.vppcr.stages, P.cyclic,
+      P.pdense ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -291,3 +291,18 @@ def test_misaligned_slabs_rejected():
             plan.solve(ok, buf[1:])
         plan.solve(ok, buf[:n])  # (aligned: runs)
         plan.close()
+
+
+@pytest.mark.parametrize("n,vp", [(6144, 6), (5120, 5), (3072, 6), (7168, 7)])
+@pytest.mark.parametrize("cyclic", [True, False])
+def test_penta_one_gpu_non_power_of_two_partitions(n, vp, cyclic):
+    """One GPU, n not a power-of-two multiple of 1024: vp on-chip partitions of a power-of-two
+    length; the cyclic 2x2-block reduced system (vp not a power of two) by its plan-time
+    inverse, the acyclic one by block PCR; vs the oracle for the three band sets."""
+    b = workloads.uniform((n, 1, 32), 400 + vp)
+    for bands in BANDS:
+        x, st = penta_gpu(b, 0, 1, bands, cyclic, return_stats=True)
+        assert st["local_kernel"] == 4 and st["vparts"] == vp, st
+        ref = oracle.penta_solve(b, 0, bands, cyclic)
+        assert rel_err(x, ref, 0) < TOL_REL
+        assert penta_residual(x, b, 0, bands, cyclic) < 1e-13
